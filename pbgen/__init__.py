@@ -1,0 +1,117 @@
+"""pbgen — seeded, counter-based synthetic inputs shared by the oracle harness
+and the GPU harness (task rule ③: the only code both sides share).
+
+It contains no PolyBench arithmetic. The formula is in ``pbgen_core.h``;
+``gen_numpy`` re-implements it in numpy (tests pin the C host library and the
+CUDA kernel against it bit for bit).
+
+Streams follow SURVEY.md §8(d): A=1, B=2, C=3, D=4, data=5, x/p/y_1=6,
+r/y_2=7, x1=8, x2=9, y=10 (E/F/G for 3mm reuse 11-13).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+SEED = 13170
+U01, INT8, BIN = 0, 1, 2
+SYM = 1 << 8
+STREAM = dict(A=1, B=2, C=3, D=4, data=5, x=6, p=6, y_1=6, r=7, y_2=7, x1=8, x2=9, y=10,
+              E=11, F=12, G=13, tmp=14)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_host = None
+_dev = None
+
+M64 = (1 << 64) - 1
+
+
+def _splitmix64(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def gen_numpy(rows, cols, stream, seed=SEED, mode=U01, scale=1.0, offset=0.0, row0=0, ld=None):
+    """Pure-numpy generator (reference for the C/CUDA versions; small sizes)."""
+    ld = cols if ld is None else ld
+    r = np.arange(row0, row0 + rows, dtype=np.int64)[:, None]
+    c = np.arange(cols, dtype=np.int64)[None, :]
+    i, j = np.broadcast_arrays(r, c)
+    if mode & SYM:
+        i, j = np.maximum(i, j), np.minimum(i, j)
+    idx = (i * ld + j).astype(np.uint64)
+    base_key = np.uint64((seed * 0x9E3779B97F4A7C15 + stream * 0xD1B54A32D192ED03) & M64)
+    with np.errstate(over="ignore"):
+        z = _splitmix64(base_key + idx)
+    m = mode & 0xFF
+    if m == INT8:
+        v = (z >> np.uint64(61)).astype(np.float64)
+    elif m == BIN:
+        v = (z >> np.uint64(63)).astype(np.float64)
+    else:
+        v = (z >> np.uint64(40)).astype(np.float64) * (1.0 / 16777216.0)
+    return (v * scale + offset).astype(np.float32)
+
+
+def _load_host():
+    global _host
+    if _host is None:
+        path = os.path.join(_HERE, "libpbgen_host.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        lib.pbgen_fill_host.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong,
+                                        ctypes.c_longlong, ctypes.c_longlong, ctypes.c_ulonglong,
+                                        ctypes.c_ulonglong, ctypes.c_int, ctypes.c_double,
+                                        ctypes.c_double]
+        lib.pbgen_fill_host.restype = None
+        _host = lib
+    return _host
+
+
+def _load_dev():
+    global _dev
+    if _dev is None:
+        path = os.path.join(_HERE, "libpbgen_dev.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        lib.pbgen_fill_device.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong,
+                                          ctypes.c_longlong, ctypes.c_longlong,
+                                          ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
+        lib.pbgen_fill_device.restype = ctypes.c_int
+        _dev = lib
+    return _dev
+
+
+def gen_host(rows, cols, stream, seed=SEED, mode=U01, scale=1.0, offset=0.0, row0=0, ld=None,
+             out=None):
+    """C/OpenMP host generator; returns a float32 numpy array rows x cols."""
+    ld = cols if ld is None else ld
+    if out is None:
+        out = np.empty((rows, cols), dtype=np.float32)
+    assert out.dtype == np.float32 and out.flags.c_contiguous and out.size == rows * cols
+    _load_host().pbgen_fill_host(out.ctypes.data, row0, row0 + rows, cols, ld, seed, stream,
+                                 mode, float(scale), float(offset))
+    return out
+
+
+def gen_device(t, stream, seed=SEED, mode=U01, scale=1.0, offset=0.0, row0=0, ld=None,
+               cuda_stream=None):
+    """Fill a contiguous float32 CUDA tensor (2-D rows x cols, or 1-D) in place."""
+    import torch
+    assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+    rows, cols = (t.shape[0], t.shape[1]) if t.dim() == 2 else (1, t.shape[0])
+    ld = cols if ld is None else ld
+    s = torch.cuda.current_stream().cuda_stream if cuda_stream is None else cuda_stream
+    rc = _load_dev().pbgen_fill_device(t.data_ptr(), row0, row0 + rows, cols, ld, seed, stream,
+                                       mode, float(scale), float(offset), s)
+    if rc != 0:
+        raise RuntimeError(f"pbgen_fill_device failed: cuda error {rc}")
+    return t
