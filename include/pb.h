@@ -1,0 +1,199 @@
+/* pb.h — C ABI of libpb, the B200-native PolyBench hot path.
+ *
+ * What the boundary is. The paper (arXiv 2312.13170, /root/reference/PAPER.md)
+ * speeds up the SYCL-Bench "polybench" nd-range kernels in which each
+ * work-item runs an inner loop over global memory (§VI-C
+ * "Loop Internalization", Listings 8-9 at PAPER.md:394-428
+ * §VI-B "Detect Reduction"; kernel list PAPER.md:522-526 §VIII). Each entry
+ * point below is one of those kernels; its arguments follow the PolyBench/C 4.2
+ * problem statement (reading R1 in DESIGN.md), i.e. the same argument order as
+ * PolyBench's kernel_<name>(...).
+ *
+ * Conventions (all entry points):
+ *  - Matrices are fp32 IEEE-754, row-major, contiguous (row pitch == #cols).
+ *    Vectors are contiguous fp32.
+ *  - Every float* / const float* is a DEVICE pointer on the current CUDA device
+ *    (cudaPointerGetAttributes must report cudaMemoryTypeDevice), 16-byte
+ *    aligned. Every matrix column count must be a multiple of 4 (TMA and
+ *    128-bit access stride rule); row counts are unrestricted (>= 1).
+ *    Violations -> PB_ERR_UNSUPPORTED (alignment) / PB_ERR_INVALID_ARG.
+ *  - Outputs must not overlap inputs or each other (the paper's alias
+ *    concern, turned into a checked
+ *    precondition) -> PB_ERR_ALIAS. In/out arrays (C of gemm/syrk/syr2k, D of
+ *    2mm, x1/x2 of mvt) are read then written in place.
+ *  - ws / ws_bytes: caller-owned device workspace, at least
+ *    pb_workspace_size(...) bytes, 256-byte aligned; the library allocates
+ *    nothing on the call path -> PB_ERR_WORKSPACE if too small.
+ *  - stream: a cudaStream_t (NULL = legacy default stream). All work is
+ *    enqueued on it; no call synchronises the host. Kernel faults surface at
+ *    the caller's next synchronisation.
+ *  - Validation happens before anything is enqueued: on any error other than
+ *    PB_ERR_CUDA nothing was launched and no output was touched.
+ *  - Reentrant; concurrent calls on different streams are independent.
+ *  - No C++ exception crosses this ABI; pb_last_error() returns a
+ *    thread-local message describing the last failing call.
+ *
+ * Precision: the dense contractions (gemm/2mm/3mm/syrk/syr2k and the X^T X core
+ * of covariance/correlation) run on tcgen05 tensor cores in split 3xTF32
+ * (x = hi + lo, acc += hi*hi + hi*lo + lo*hi, fp32 accumulation), the
+ * matrix-vector kernels and statistics on CUDA cores in fp32/fp64; every
+ * result matches the fp64 oracle within componentwise relative error 1e-4
+ * (DESIGN.md "Tolerance").
+ */
+#ifndef PB_H
+#define PB_H
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PB_OK = 0,
+  PB_ERR_INVALID_ARG = 1,  /* NULL required pointer, dim <= 0, n < 2 for covariance, host pointer */
+  PB_ERR_UNSUPPORTED = 2,  /* pointer not 16-B aligned or a column count not a multiple of 4 */
+  PB_ERR_ALIAS = 3,        /* an output range overlaps another argument's range */
+  PB_ERR_WORKSPACE = 4,    /* ws NULL / misaligned / smaller than pb_workspace_size */
+  PB_ERR_CUDA = 5,         /* a CUDA runtime/driver call or launch failed */
+  PB_ERR_NCCL = 6          /* reserved (collectives run through torch.distributed) */
+} pb_status;
+
+typedef struct CUstream_st* pb_stream; /* == cudaStream_t */
+
+const char* pb_status_str(pb_status s);
+/* Thread-local detail for the last failing call on this thread ("" if none). */
+const char* pb_last_error(void);
+/* libpb version string, e.g. "pb 0.1 sm_100a". */
+const char* pb_version(void);
+
+/* Workspace bytes needed by `kernel` ("gemm", "2mm", "3mm", "syrk", "syr2k",
+ * "covariance", "correlation", "atax", "bicg", "mvt", "gesummv") for the dims
+ * given in that kernel's argument order (e.g. gemm: {ni, nj, nk}; 2mm:
+ * {ni, nj, nk, nl}; 3mm: {ni, nj, nk, nl, nm}; syrk/syr2k: {n, m};
+ * covariance/correlation: {m, n}; atax/bicg: {m, n}; mvt/gesummv: {n}).
+ * Writes *bytes; PB_ERR_INVALID_ARG on unknown kernel or bad dims. */
+pb_status pb_workspace_size(const char* kernel, const long long* dims, int ndims, size_t* bytes);
+
+/* gemm — PAPER.md:394-401 (Listing 8 is alpha=beta=1); PolyBench kernel_gemm.
+ *   C[i][j] = beta*C[i][j] + alpha * sum_{k<nk} A[i][k]*B[k][j]
+ * C ni x nj (in/out), A ni x nk, B nk x nj. */
+pb_status pb_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
+                  const float* B, void* ws, size_t ws_bytes, pb_stream s);
+
+/* 2mm — PolyBench kernel_2mm (LI applies).
+ *   tmp = alpha*A*B;  D = tmp*C + beta*D
+ * A ni x nk, B nk x nj, tmp ni x nj (optional output, NULL = not written),
+ * C nj x nl, D ni x nl (in/out). */
+pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float* tmp,
+                 const float* A, const float* B, const float* C, float* D, void* ws,
+                 size_t ws_bytes, pb_stream s);
+
+/* 3mm — PolyBench kernel_3mm.  E = A*B;  F = C*D;  G = E*F
+ * A ni x nk, B nk x nj, E ni x nj (out), C nj x nm, D nm x nl, F nj x nl (out),
+ * G ni x nl (out). */
+pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* A, const float* B,
+                 float* F, const float* C, const float* D, float* G, void* ws, size_t ws_bytes,
+                 pb_stream s);
+
+/* syrk — PolyBench kernel_syrk, LOWER triangle (reading R3):
+ *   for j <= i: C[i][j] = beta*C[i][j] + alpha * sum_{k<m} A[i][k]*A[j][k];
+ *   strict upper triangle untouched.   C n x n (in/out), A n x m. */
+pb_status pb_syrk(int n, int m, float alpha, float beta, float* C, const float* A, void* ws,
+                  size_t ws_bytes, pb_stream s);
+
+/* syr2k — PolyBench kernel_syr2k, LOWER triangle (reading R3):
+ *   for j <= i: C[i][j] = beta*C[i][j] + alpha*sum_k (A[j][k]*B[i][k] + B[j][k]*A[i][k])
+ * C n x n (in/out), A, B n x m. */
+pb_status pb_syr2k(int n, int m, float alpha, float beta, float* C, const float* A,
+                   const float* B, void* ws, size_t ws_bytes, pb_stream s);
+
+/* covariance — PolyBench kernel_covariance (reading R4; data NOT mutated, R9):
+ *   mean[j] = sum_i data[i][j] / float_n;  X = data - mean
+ *   cov[i][j] = cov[j][i] = sum_k X[k][i]*X[k][j] / (float_n - 1)
+ * data n x m (n observations of m variables), cov m x m (out, exactly
+ * symmetric), mean m (optional out). Requires n >= 2. */
+pb_status pb_covariance(int m, int n, float float_n, const float* data, float* cov, float* mean,
+                        void* ws, size_t ws_bytes, pb_stream s);
+
+/* correlation — PolyBench kernel_correlation (eps rule R5: stddev <= eps -> 1;
+ * diagonal exactly 1.0, R6):
+ *   stddev[j] = sqrt(sum_i (data[i][j]-mean[j])^2 / float_n)
+ *   X = (data - mean) / (sqrt(float_n)*stddev);  corr[i][j] = sum_k X[k][i]*X[k][j]
+ * data n x m, corr m x m (out), mean, stddev m (optional outs). */
+pb_status pb_correlation(int m, int n, float float_n, float eps, const float* data, float* corr,
+                         float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s);
+
+/* atax — PolyBench kernel_atax:  tmp = A*x;  y = A^T * tmp
+ * A m x n, x n, y n (out), tmp m (optional out). */
+pb_status pb_atax(int m, int n, const float* A, const float* x, float* y, float* tmp, void* ws,
+                  size_t ws_bytes, pb_stream s);
+
+/* bicg — PolyBench kernel_bicg:  s = A^T * r;  q = A * p
+ * A n x m, s m (out), q n (out), p m, r n. */
+pb_status pb_bicg(int m, int n, const float* A, float* s_out, float* q, const float* p,
+                  const float* r, void* ws, size_t ws_bytes, pb_stream s);
+
+/* mvt — PolyBench kernel_mvt:  x1 += A*y_1;  x2 += A^T*y_2
+ * A n x n, x1, x2 n (in/out), y_1, y_2 n. */
+pb_status pb_mvt(int n, float* x1, float* x2, const float* y_1, const float* y_2, const float* A,
+                 void* ws, size_t ws_bytes, pb_stream s);
+
+/* gesummv — PolyBench kernel_gesummv:
+ *   tmp = A*x;  y = alpha*tmp + beta*B*x
+ * A, B n x n, x n, y n (out), tmp n (optional out). */
+pb_status pb_gesummv(int n, float alpha, float beta, const float* A, const float* B, float* tmp,
+                     const float* x, float* y, void* ws, size_t ws_bytes, pb_stream s);
+
+/* ------------------------------------------------------------------------
+ * Row-block sharding helpers (multi-GPU, one process per GPU).
+ * Rank g owns output rows [begin, end). triangular != 0 balances the area of a
+ * lower triangle (boundaries ~ rows*sqrt(g/G)); boundaries are multiples of
+ * `align` (except the last, == rows).
+ */
+pb_status pb_row_partition(int rows, int nranks, int rank, int triangular, int align, int* begin,
+                           int* end);
+
+/* Local (per-shard) pieces the Python distributed layer composes with
+ * torch.distributed collectives. Row indices are GLOBAL; C/out pointers point
+ * at the first row of the caller's row block.
+ *
+ * pb_syrk_rows / pb_syr2k_rows: rows [r0, r1) of the lower-triangular update
+ *   (r0 must be a multiple of 128); A, B are the FULL n x m inputs, C points
+ *   to row r0 of C (rows r1-r0, n columns).
+ * pb_gemm_rows: C[r0:r1] = beta*C[r0:r1] + alpha*A[r0:r1]*B (A, C point at row r0).
+ * pb_matvec_partial: for a row block A_blk (rows x cols):
+ *   rowdot[i]  = base_row[i] + sum_j A_blk[i][j]*v[j]   (if v; base_row may be NULL = 0,
+ *                                                         may equal rowdot: in place)
+ *   colpart[j] = base_col[j] + sum_i A_blk[i][j]*w[i]   (if w; w has `rows` entries;
+ *                                                         base_col may be NULL)
+ *   this is the local half of bicg/mvt/atax before the reduce-scatter. */
+pb_status pb_syrk_rows(int n, int m, int r0, int r1, float alpha, float beta, float* C_blk,
+                       const float* A, void* ws, size_t ws_bytes, pb_stream s);
+pb_status pb_syr2k_rows(int n, int m, int r0, int r1, float alpha, float beta, float* C_blk,
+                        const float* A, const float* B, void* ws, size_t ws_bytes, pb_stream s);
+pb_status pb_matvec_partial(int rows, int cols, const float* A_blk, const float* v,
+                            const float* base_row, float* rowdot, const float* w,
+                            const float* base_col, float* colpart, void* ws, size_t ws_bytes,
+                            pb_stream s);
+/* workspace for the two helpers above: kernel names "syrk_rows" {n,m,r0,r1},
+ * "syr2k_rows" {n,m,r0,r1}, "matvec_partial" {rows, cols}. */
+
+/* ------------------------------------------------------------------------
+ * Paper ablation: the GEMM of PAPER.md Listing 8
+ * (variant 0: one thread per C[i][j], k-loop over global memory, C updated in
+ * global memory each iteration) and its loop-internalised form, Listing 9
+ * (variant 1: M x M local tiles, two barriers per tile step, M = 16);
+ * variant 2 = Listing 9 plus detect-reduction (register accumulator,
+ * PAPER.md Listing 5). All plain fp32 SIMT with pb_gemm's semantics.
+ * Variant 3 = the production 3xTF32 tcgen05 path (== pb_gemm).
+ */
+pb_status pb_gemm_variant(int variant, int ni, int nj, int nk, float alpha, float beta, float* C,
+                          const float* A, const float* B, void* ws, size_t ws_bytes, pb_stream s);
+
+/* Number of kernels launched by the last successful pb_* call on this thread. */
+int pb_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PB_H */

@@ -1,0 +1,236 @@
+"""paper_2312_13170_b200 — thin Python binding of libpb (include/pb.h).
+
+Argument marshalling only: every arithmetic step of the PolyBench hot path
+runs in libpb's sm_100a kernels. PyTorch supplies device memory, streams and
+(in ``dist``) process groups. There is no CPU fallback: if ``libpb.so`` is
+missing or a call fails, a ``PBError`` is raised.
+
+Function names and argument order are those of the C ABI; tensors are passed
+where the ABI takes pointers. ``ws`` may be omitted, in which case a workspace
+of ``workspace_size(...)`` bytes is allocated with torch on the tensors'
+device (callers on the hot path should pass a preallocated one).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "PBError", "lib", "workspace_size", "workspace", "pb_gemm", "pb_2mm", "pb_3mm", "pb_syrk",
+    "pb_syr2k", "pb_covariance", "pb_correlation", "pb_atax", "pb_bicg", "pb_mvt", "pb_gesummv",
+    "pb_row_partition", "pb_syrk_rows", "pb_syr2k_rows", "pb_matvec_partial", "pb_gemm_variant",
+    "pb_version", "last_launch_count", "ABI_FUNCTIONS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpb.so")
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_F = ctypes.c_float
+_Z = ctypes.c_size_t
+
+# name -> argtypes, exactly as declared in include/pb.h
+ABI_FUNCTIONS = {
+    "pb_status_str": ([_I], ctypes.c_char_p),
+    "pb_last_error": ([], ctypes.c_char_p),
+    "pb_version": ([], ctypes.c_char_p),
+    "pb_last_launch_count": ([], _I),
+    "pb_workspace_size": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_longlong), _I,
+                           ctypes.POINTER(_Z)], _I),
+    "pb_gemm": ([_I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_2mm": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_3mm": ([_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_syrk": ([_I, _I, _F, _F, _P, _P, _P, _Z, _P], _I),
+    "pb_syr2k": ([_I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_covariance": ([_I, _I, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_correlation": ([_I, _I, _F, _F, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_atax": ([_I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_bicg": ([_I, _I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_mvt": ([_I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_gesummv": ([_I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_row_partition": ([_I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "pb_syrk_rows": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _Z, _P], _I),
+    "pb_syr2k_rows": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_matvec_partial": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_gemm_variant": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+}
+
+_lib = None
+
+
+class PBError(RuntimeError):
+    def __init__(self, fn, status, detail):
+        super().__init__(f"{fn} failed with status {status}: {detail}")
+        self.status = status
+
+
+def lib():
+    """Load libpb.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise PBError("load", -1, f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in ABI_FUNCTIONS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def pb_version():
+    return lib().pb_version().decode()
+
+
+def last_launch_count():
+    return lib().pb_last_launch_count()
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream, ref=None):
+    if stream is None:
+        import torch
+        dev = ref.device if ref is not None and hasattr(ref, "device") else None
+        return torch.cuda.current_stream(dev).cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _check(name, st):
+    if st != 0:
+        raise PBError(name, st, lib().pb_last_error().decode())
+
+
+def workspace_size(kernel: str, dims) -> int:
+    arr = (ctypes.c_longlong * len(dims))(*[int(d) for d in dims])
+    out = ctypes.c_size_t(0)
+    _check("pb_workspace_size", lib().pb_workspace_size(kernel.encode(), arr, len(dims), ctypes.byref(out)))
+    return out.value
+
+
+def workspace(kernel: str, dims, device):
+    import torch
+    n = workspace_size(kernel, dims)
+    return torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+
+
+_ws_cache = {}
+
+
+def _ws(ws, kernel, dims, ref):
+    """Caller's workspace, or a per-device cached one (kept alive across calls so
+    asynchronous kernels never see it freed)."""
+    if ws is None:
+        need = max(workspace_size(kernel, dims), 256)
+        cur = _ws_cache.get(ref.device)
+        if cur is None or cur.numel() < need:
+            import torch
+            if cur is not None:
+                torch.cuda.synchronize(ref.device)  # the old buffer may still be in use
+            cur = torch.empty(need, dtype=torch.uint8, device=ref.device)
+            _ws_cache[ref.device] = cur
+        ws = cur
+    return _ptr(ws), (ws.numel() * ws.element_size() if hasattr(ws, "numel") else 1 << 62), ws
+
+
+def pb_gemm(ni, nj, nk, alpha, beta, C, A, B, ws=None, stream=None):
+    p, n, keep = _ws(ws, "gemm", (ni, nj, nk), C)
+    _check("pb_gemm", lib().pb_gemm(ni, nj, nk, alpha, beta, _ptr(C), _ptr(A), _ptr(B), p, n, _stream(stream, C)))
+
+
+def pb_gemm_variant(variant, ni, nj, nk, alpha, beta, C, A, B, ws=None, stream=None):
+    p, n, keep = _ws(ws, "gemm_variant", (ni, nj, nk), C)
+    _check("pb_gemm_variant", lib().pb_gemm_variant(variant, ni, nj, nk, alpha, beta, _ptr(C), _ptr(A), _ptr(B),
+                                                    p, n, _stream(stream, C)))
+
+
+def pb_2mm(ni, nj, nk, nl, alpha, beta, tmp, A, B, C, D, ws=None, stream=None):
+    p, n, keep = _ws(ws, "2mm", (ni, nj, nk, nl), D)
+    _check("pb_2mm", lib().pb_2mm(ni, nj, nk, nl, alpha, beta, _ptr(tmp), _ptr(A), _ptr(B), _ptr(C), _ptr(D),
+                                  p, n, _stream(stream, D)))
+
+
+def pb_3mm(ni, nj, nk, nl, nm, E, A, B, F, C, D, G, ws=None, stream=None):
+    p, n, keep = _ws(ws, "3mm", (ni, nj, nk, nl, nm), G)
+    _check("pb_3mm", lib().pb_3mm(ni, nj, nk, nl, nm, _ptr(E), _ptr(A), _ptr(B), _ptr(F), _ptr(C), _ptr(D),
+                                  _ptr(G), p, n, _stream(stream, G)))
+
+
+def pb_syrk(n_, m, alpha, beta, C, A, ws=None, stream=None):
+    p, n, keep = _ws(ws, "syrk", (n_, m), C)
+    _check("pb_syrk", lib().pb_syrk(n_, m, alpha, beta, _ptr(C), _ptr(A), p, n, _stream(stream, C)))
+
+
+def pb_syr2k(n_, m, alpha, beta, C, A, B, ws=None, stream=None):
+    p, n, keep = _ws(ws, "syr2k", (n_, m), C)
+    _check("pb_syr2k", lib().pb_syr2k(n_, m, alpha, beta, _ptr(C), _ptr(A), _ptr(B), p, n, _stream(stream, C)))
+
+
+def pb_syrk_rows(n_, m, r0, r1, alpha, beta, C_blk, A, ws=None, stream=None):
+    p, n, keep = _ws(ws, "syrk_rows", (n_, m, r0, r1), A)
+    _check("pb_syrk_rows", lib().pb_syrk_rows(n_, m, r0, r1, alpha, beta, _ptr(C_blk), _ptr(A), p, n,
+                                              _stream(stream, A)))
+
+
+def pb_syr2k_rows(n_, m, r0, r1, alpha, beta, C_blk, A, B, ws=None, stream=None):
+    p, n, keep = _ws(ws, "syr2k_rows", (n_, m, r0, r1), A)
+    _check("pb_syr2k_rows", lib().pb_syr2k_rows(n_, m, r0, r1, alpha, beta, _ptr(C_blk), _ptr(A), _ptr(B), p, n,
+                                                _stream(stream, A)))
+
+
+def pb_covariance(m, n_, float_n, data, cov, mean=None, ws=None, stream=None):
+    p, n, keep = _ws(ws, "covariance", (m, n_), cov)
+    _check("pb_covariance", lib().pb_covariance(m, n_, float_n, _ptr(data), _ptr(cov), _ptr(mean), p, n,
+                                                _stream(stream, cov)))
+
+
+def pb_correlation(m, n_, float_n, eps, data, corr, mean=None, stddev=None, ws=None, stream=None):
+    p, n, keep = _ws(ws, "correlation", (m, n_), corr)
+    _check("pb_correlation", lib().pb_correlation(m, n_, float_n, eps, _ptr(data), _ptr(corr), _ptr(mean),
+                                                  _ptr(stddev), p, n, _stream(stream, corr)))
+
+
+def pb_atax(m, n_, A, x, y, tmp=None, ws=None, stream=None):
+    p, n, keep = _ws(ws, "atax", (m, n_), y)
+    _check("pb_atax", lib().pb_atax(m, n_, _ptr(A), _ptr(x), _ptr(y), _ptr(tmp), p, n, _stream(stream, y)))
+
+
+def pb_bicg(m, n_, A, s, q, p_, r, ws=None, stream=None):
+    p, n, keep = _ws(ws, "bicg", (m, n_), q)
+    _check("pb_bicg", lib().pb_bicg(m, n_, _ptr(A), _ptr(s), _ptr(q), _ptr(p_), _ptr(r), p, n, _stream(stream, q)))
+
+
+def pb_mvt(n_, x1, x2, y_1, y_2, A, ws=None, stream=None):
+    p, n, keep = _ws(ws, "mvt", (n_,), x1)
+    _check("pb_mvt", lib().pb_mvt(n_, _ptr(x1), _ptr(x2), _ptr(y_1), _ptr(y_2), _ptr(A), p, n, _stream(stream, x1)))
+
+
+def pb_gesummv(n_, alpha, beta, A, B, tmp, x, y, ws=None, stream=None):
+    p, n, keep = _ws(ws, "gesummv", (n_,), y)
+    _check("pb_gesummv", lib().pb_gesummv(n_, alpha, beta, _ptr(A), _ptr(B), _ptr(tmp), _ptr(x), _ptr(y), p, n,
+                                          _stream(stream, y)))
+
+
+def pb_matvec_partial(rows, cols, A_blk, v, base_row, rowdot, w, base_col, colpart, ws=None, stream=None):
+    p, n, keep = _ws(ws, "matvec_partial", (rows, cols), A_blk)
+    _check("pb_matvec_partial", lib().pb_matvec_partial(rows, cols, _ptr(A_blk), _ptr(v), _ptr(base_row),
+                                                        _ptr(rowdot), _ptr(w), _ptr(base_col), _ptr(colpart),
+                                                        p, n, _stream(stream, A_blk)))
+
+
+def pb_row_partition(rows, nranks, rank, triangular=False, align=1):
+    b = ctypes.c_int(0)
+    e = ctypes.c_int(0)
+    _check("pb_row_partition", lib().pb_row_partition(rows, nranks, rank, int(triangular), align,
+                                                      ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value

@@ -1,0 +1,221 @@
+// k_matvec.cu — S14-S16 of the hot path: the HBM-bound
+// matrix-vector kernels of atax / bicg / mvt / gesummv.
+//
+// Paper mapping: the SYCL kernels walk a row (or a column) of A per
+// work-item with a loop over global memory (PAPER.md:379 — local memory helps
+// accesses "not conducive to being coalesced"). Here every matrix byte is read
+// exactly once with coalesced 128-bit streaming loads (ld.global.nc,
+// L1::no_allocate); the vector with temporal reuse (x / p / y_1) is kept in
+// registers per thread (the loop-internalised operand), the
+// reductions are register accumulators (detect-reduction)
+// closed by warp shuffles, and the transposed product accumulates per-tile
+// column partials that a second tiny kernel sums in a fixed order
+// (deterministic, no float atomics). bicg and mvt compute both products in ONE
+// pass over A (the paper's future-work kernel fusion).
+#include "pb_device.cuh"
+#include "pb_internal.h"
+
+namespace pb {
+namespace {
+
+// ------------------------------------------------------------------ rowdot
+// y[i] = alpha*(A_i . x) + beta*(B_i . x); tmp[i] = A_i . x.  R rows per CTA.
+template <int R, bool TWO>
+__global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                     const float* __restrict__ x, int rows, int cols, float alpha,
+                                                     float beta, float* __restrict__ y, float* __restrict__ tmp) {
+  const int row0 = blockIdx.x * R;
+  const int cols4 = cols >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* Ar[R];
+  const float4* Br[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int row = min(row0 + r, rows - 1);
+    Ar[r] = reinterpret_cast<const float4*>(A + (long long)row * cols);
+    if (TWO) Br[r] = reinterpret_cast<const float4*>(B + (long long)row * cols);
+  }
+  float acc[R], accb[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) { acc[r] = 0.f; accb[r] = 0.f; }
+
+  int c = threadIdx.x;
+  for (; c + 256 < cols4; c += 512) {  // two column chunks in flight
+    float4 a0[R], a1[R], b0[R], b1[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      a0[r] = ldg_stream(Ar[r] + c);
+      a1[r] = ldg_stream(Ar[r] + c + 256);
+      if (TWO) { b0[r] = ldg_stream(Br[r] + c); b1[r] = ldg_stream(Br[r] + c + 256); }
+    }
+    const float4 xv0 = x4[c], xv1 = x4[c + 256];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      acc[r] += a0[r].x * xv0.x + a0[r].y * xv0.y + a0[r].z * xv0.z + a0[r].w * xv0.w;
+      acc[r] += a1[r].x * xv1.x + a1[r].y * xv1.y + a1[r].z * xv1.z + a1[r].w * xv1.w;
+      if (TWO) {
+        accb[r] += b0[r].x * xv0.x + b0[r].y * xv0.y + b0[r].z * xv0.z + b0[r].w * xv0.w;
+        accb[r] += b1[r].x * xv1.x + b1[r].y * xv1.y + b1[r].z * xv1.z + b1[r].w * xv1.w;
+      }
+    }
+  }
+  for (; c < cols4; c += 256) {
+    const float4 xv = x4[c];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float4 a = ldg_stream(Ar[r] + c);
+      acc[r] += a.x * xv.x + a.y * xv.y + a.z * xv.z + a.w * xv.w;
+      if (TWO) {
+        const float4 b = ldg_stream(Br[r] + c);
+        accb[r] += b.x * xv.x + b.y * xv.y + b.z * xv.z + b.w * xv.w;
+      }
+    }
+  }
+  __shared__ float red[2][8][R];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float s = warp_sum(acc[r]);
+    float sb = TWO ? warp_sum(accb[r]) : 0.f;
+    if (lane == 0) { red[0][warp][r] = s; red[1][warp][r] = sb; }
+  }
+  __syncthreads();
+  if (threadIdx.x < R && row0 + threadIdx.x < rows) {
+    const int r = threadIdx.x;
+    float s = 0.f, sb = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { s += red[0][w][r]; sb += red[1][w][r]; }
+    if (tmp) tmp[row0 + r] = s;
+    if (y) y[row0 + r] = TWO ? alpha * s + beta * sb : alpha * s;
+  }
+}
+
+// ------------------------------------------------------------------ fused mv / mv^T tiles
+constexpr int TC = 512;  // columns per tile: 32 lanes x 4 float4 groups (128 cols apart)
+constexpr int TR = 256;  // rows per tile: 8 warps x 32 rows
+constexpr int G = TC / 128;
+constexpr int RU = 4;    // rows in flight per warp
+
+template <bool DO_ROW, bool DO_COL>
+__global__ void __launch_bounds__(256, 2) mvmt_kernel(const float* __restrict__ A, int rows, int cols,
+                                                      const float* __restrict__ v, const float* __restrict__ w,
+                                                      float* __restrict__ rowpart, float* __restrict__ colpart) {
+  const int ct = blockIdx.x, rt = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = ct * TC;
+  bool cok[G];
+  float4 vv[G], cacc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int c = c0 + g * 128 + lane * 4;
+    cok[g] = c < cols;
+    vv[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (DO_ROW && cok[g]) vv[g] = *reinterpret_cast<const float4*>(v + c);
+    cacc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int r_begin = rt * TR, r_end = min(r_begin + TR, rows);
+  for (int rb = r_begin + warp * RU; rb < r_end; rb += 8 * RU) {
+    float4 a[RU][G];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int r = rb + u;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int c = c0 + g * 128 + lane * 4;
+        a[u][g] = (r < r_end && cok[g]) ? ldg_stream(reinterpret_cast<const float4*>(A + (long long)r * cols + c))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int r = rb + u;
+      if (DO_COL) {
+        const float wr = r < r_end ? w[r] : 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          cacc[g].x += wr * a[u][g].x; cacc[g].y += wr * a[u][g].y;
+          cacc[g].z += wr * a[u][g].z; cacc[g].w += wr * a[u][g].w;
+        }
+      }
+      if (DO_ROW) {
+        float s = 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          s += a[u][g].x * vv[g].x + a[u][g].y * vv[g].y + a[u][g].z * vv[g].z + a[u][g].w * vv[g].w;
+        s = warp_sum(s);
+        if (lane == 0 && r < r_end) rowpart[(long long)ct * rows + r] = s;
+      }
+    }
+  }
+  if (DO_COL) {
+    __shared__ float4 red[8][TC / 4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) red[warp][g * 32 + lane] = cacc[g];
+    __syncthreads();
+    // 256 threads, TC/4 = 128 float4 columns: threads 0..127 each own one float4
+    if (threadIdx.x < TC / 4) {
+      const int f = threadIdx.x;  // float4 index within tile: g*32 + lane
+      const int c = c0 + (f >> 5) * 128 + (f & 31) * 4;
+      float4 s = red[0][f];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) { s.x += red[k][f].x; s.y += red[k][f].y; s.z += red[k][f].z; s.w += red[k][f].w; }
+      if (c < cols) *reinterpret_cast<float4*>(colpart + (long long)rt * cols + c) = s;
+    }
+  }
+}
+
+// out[i] = (base ? base[i] : 0) + sum_{t < nparts} part[t][i]
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restrict__ part, int nparts, int len,
+                                                           const float* __restrict__ base, float* __restrict__ out) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= len) return;
+  float s = 0.f;
+  for (int t = 0; t < nparts; ++t) s += part[(long long)t * len + i];
+  out[i] = base ? base[i] + s : s;
+}
+
+}  // namespace
+
+cudaError_t launch_rowdot(const float* A, const float* B, const float* x, int rows, int cols, float alpha, float beta,
+                          float* y, float* tmp, cudaStream_t s) {
+  if (B) {
+    constexpr int R = 4;
+    rowdot_kernel<R, true><<<(rows + R - 1) / R, 256, 0, s>>>(A, B, x, rows, cols, alpha, beta, y, tmp);
+  } else {
+    constexpr int R = 8;
+    rowdot_kernel<R, false><<<(rows + R - 1) / R, 256, 0, s>>>(A, nullptr, x, rows, cols, alpha, beta, y, tmp);
+  }
+  return cudaGetLastError();
+}
+
+size_t mvmt_ws_bytes(int rows, int cols) {
+  const size_t nct = (cols + TC - 1) / TC, nrt = (rows + TR - 1) / TR;
+  return align_up(nct * rows * 4, 256) + align_up(nrt * cols * 4, 256);
+}
+
+cudaError_t launch_mvmt(const float* A, int rows, int cols, const float* v, const float* w, const float* base_row,
+                        float* out_row, const float* base_col, float* out_col, void* ws, cudaStream_t s,
+                        int* launches) {
+  const int nct = (cols + TC - 1) / TC, nrt = (rows + TR - 1) / TR;
+  float* rowpart = static_cast<float*>(ws);
+  float* colpart = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up((size_t)nct * rows * 4, 256));
+  dim3 grid(nct, nrt);
+  if (v && w)
+    mvmt_kernel<true, true><<<grid, 256, 0, s>>>(A, rows, cols, v, w, rowpart, colpart);
+  else if (v)
+    mvmt_kernel<true, false><<<grid, 256, 0, s>>>(A, rows, cols, v, w, rowpart, colpart);
+  else
+    mvmt_kernel<false, true><<<grid, 256, 0, s>>>(A, rows, cols, v, w, rowpart, colpart);
+  ++*launches;
+  if (v) {
+    reduce_parts_kernel<<<(rows + 255) / 256, 256, 0, s>>>(rowpart, nct, rows, base_row, out_row);
+    ++*launches;
+  }
+  if (w) {
+    reduce_parts_kernel<<<(cols + 255) / 256, 256, 0, s>>>(colpart, nrt, cols, base_col, out_col);
+    ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pb

@@ -1,0 +1,590 @@
+// pb_api.cu — the C ABI of libpb (include/pb.h): argument validation, alias
+// checks, workspace carving and the launch sequence of each PolyBench kernel.
+// Every arithmetic step runs in the kernels of k_*.cu; this file only decides
+// what to launch. There is no CPU fallback: a missing/failed launch returns an
+// error.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/pb.h"
+#include "pb_internal.h"
+
+using namespace pb;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+pb_status fail(pb_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = std::string(pb_status_str(st)) + ": " + buf;
+  return st;
+}
+
+struct Range {
+  const void* p;
+  size_t bytes;
+  bool out;
+  const char* name;
+};
+
+// Validation context for one call: collects pointer ranges, checks placement,
+// alignment and aliasing (outputs may not overlap anything else).
+struct Check {
+  std::vector<Range> r;
+  pb_status st = PB_OK;
+  int dev = -1;
+
+  Check() { cudaGetDevice(&dev); }
+
+  void arr(const void* p, long long rows, long long cols, bool out, const char* name, bool required = true) {
+    if (st != PB_OK) return;
+    if (p == nullptr) {
+      if (required) st = fail(PB_ERR_INVALID_ARG, "%s is NULL", name);
+      return;
+    }
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0) {
+      st = fail(PB_ERR_UNSUPPORTED, "%s is not 16-byte aligned", name);
+      return;
+    }
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      st = fail(PB_ERR_INVALID_ARG, "%s: cudaPointerGetAttributes failed (%s)", name, cudaGetErrorString(e));
+      return;
+    }
+    if (!(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) || at.device != dev) {
+      st = fail(PB_ERR_INVALID_ARG, "%s is not device memory on the current device", name);
+      return;
+    }
+    r.push_back({p, (size_t)(rows * cols) * sizeof(float), out, name});
+  }
+  void cols4(long long cols, const char* name) {
+    if (st == PB_OK && cols % 4 != 0) st = fail(PB_ERR_UNSUPPORTED, "%s: column count %lld not a multiple of 4", name, cols);
+  }
+  void dims(std::initializer_list<long long> ds) {
+    if (st != PB_OK) return;
+    for (long long d : ds)
+      if (d <= 0 || d > (1ll << 30)) {
+        st = fail(PB_ERR_INVALID_ARG, "dimension %lld out of range", d);
+        return;
+      }
+  }
+  pb_status finish() {
+    if (st != PB_OK) return st;
+    for (size_t i = 0; i < r.size(); ++i) {
+      if (!r[i].out) continue;
+      const char* a0 = static_cast<const char*>(r[i].p);
+      const char* a1 = a0 + r[i].bytes;
+      for (size_t j = 0; j < r.size(); ++j) {
+        if (j == i) continue;
+        const char* b0 = static_cast<const char*>(r[j].p);
+        const char* b1 = b0 + r[j].bytes;
+        if (a0 < b1 && b0 < a1) return st = fail(PB_ERR_ALIAS, "%s overlaps %s", r[i].name, r[j].name);
+      }
+    }
+    return PB_OK;
+  }
+};
+
+// Bump allocator over the caller's workspace (256-B aligned slices).
+struct Carve {
+  char* base;
+  size_t cap, off = 0;
+  Carve(void* b, size_t c) : base(static_cast<char*>(b)), cap(c) {}
+  template <class T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+inline size_t fsz(long long rows, long long cols) { return (size_t)rows * (size_t)cols; }
+
+// ---- workspace layouts (shared by pb_workspace_size and the entry points) ----
+struct SplitBuf {
+  float* hi;
+  float* lo;
+  int rows, K, ld;
+  SplitOperand op() const {
+    SplitOperand o;
+    o.hi = hi; o.lo = lo; o.rows = rows; o.K = K; o.ld = ld;
+    return o;
+  }
+};
+SplitBuf take_split(Carve& c, int rows, int K) {
+  SplitBuf b;
+  b.rows = rows;
+  b.K = K;
+  b.ld = round_up(K, 4);
+  b.hi = c.take<float>(fsz(rows, b.ld));
+  b.lo = c.take<float>(fsz(rows, b.ld));
+  return b;
+}
+
+struct WsGemm { SplitBuf a, bt; };
+WsGemm ws_gemm(Carve& c, int ni, int nj, int nk) { return {take_split(c, ni, nk), take_split(c, nj, nk)}; }
+struct Ws2mm { SplitBuf a, bt, ct, tmp; };
+Ws2mm ws_2mm(Carve& c, int ni, int nj, int nk, int nl) {
+  Ws2mm w;
+  w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.ct = take_split(c, nl, nj); w.tmp = take_split(c, ni, nj);
+  return w;
+}
+struct Ws3mm { SplitBuf a, bt, c, dt, e, ft; };
+Ws3mm ws_3mm(Carve& c, int ni, int nj, int nk, int nl, int nm) {
+  Ws3mm w;
+  w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.c = take_split(c, nj, nm);
+  w.dt = take_split(c, nl, nm); w.e = take_split(c, ni, nj); w.ft = take_split(c, nl, nj);
+  return w;
+}
+struct WsStat { SplitBuf xt; double* part; double* mean; double* inv; };
+WsStat ws_stat(Carve& c, int m, int n) {
+  WsStat w;
+  w.xt = take_split(c, m, n);
+  w.part = c.take<double>(stats_part_doubles(m, n));
+  w.mean = c.take<double>(m);
+  w.inv = c.take<double>(m);
+  return w;
+}
+
+pb_status check_ws(const Carve& need, void* ws, size_t ws_bytes) {
+  if (need.off == 0) return PB_OK;
+  if (ws == nullptr) return fail(PB_ERR_WORKSPACE, "workspace is NULL (%zu bytes needed)", need.off);
+  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) return fail(PB_ERR_WORKSPACE, "workspace not 256-byte aligned");
+  if (ws_bytes < need.off) return fail(PB_ERR_WORKSPACE, "workspace %zu bytes < %zu needed", ws_bytes, need.off);
+  return PB_OK;
+}
+
+pb_status cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(PB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return PB_OK;
+}
+
+#define PB_TRY(expr)                       \
+  do {                                     \
+    pb_status _st = (expr);                \
+    if (_st != PB_OK) return _st;          \
+  } while (0)
+#define PB_CUDA(expr) PB_TRY(cuda_check((expr), #expr))
+
+inline cudaStream_t S(pb_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// core sequences (validated arguments) ---------------------------------------
+pb_status run_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A, const float* B,
+                   const WsGemm& w, cudaStream_t s, int* L) {
+  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, s));
+  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, s));
+  *L += 2;
+  GemmDesc d;
+  d.M = ni; d.N = nj; d.K = nk;
+  d.a[0] = w.a.op(); d.b[0] = w.bt.op();
+  d.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
+  d.alpha = alpha; d.beta = beta;
+  d.cin = C; d.ldc = nj; d.out = C; d.ldo = nj;
+  PB_CUDA(launch_umma_gemm(d, s, L));
+  return PB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pb_status_str(pb_status s) {
+  switch (s) {
+    case PB_OK: return "PB_OK";
+    case PB_ERR_INVALID_ARG: return "PB_ERR_INVALID_ARG";
+    case PB_ERR_UNSUPPORTED: return "PB_ERR_UNSUPPORTED";
+    case PB_ERR_ALIAS: return "PB_ERR_ALIAS";
+    case PB_ERR_WORKSPACE: return "PB_ERR_WORKSPACE";
+    case PB_ERR_CUDA: return "PB_ERR_CUDA";
+    case PB_ERR_NCCL: return "PB_ERR_NCCL";
+  }
+  return "PB_ERR_UNKNOWN";
+}
+
+const char* pb_last_error(void) { return g_err.c_str(); }
+const char* pb_version(void) { return "pb 0.1 sm_100a (3xTF32 tcgen05 + HBM-streaming matvec)"; }
+int pb_last_launch_count(void) { return g_launches; }
+
+pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size_t* bytes) {
+  if (!kernel || !bytes || (nd > 0 && !d)) return fail(PB_ERR_INVALID_ARG, "NULL argument");
+  for (int i = 0; i < nd; ++i)
+    if (d[i] <= 0 && !(strstr(kernel, "_rows") && i == 2 && d[i] == 0))
+      return fail(PB_ERR_INVALID_ARG, "dimension %d is %lld", i, d[i]);
+  Carve c(nullptr, 0);
+  std::string k(kernel);
+  auto need = [&](int n) { return nd == n; };
+  if (k == "gemm" && need(3)) ws_gemm(c, d[0], d[1], d[2]);
+  else if (k == "2mm" && need(4)) ws_2mm(c, d[0], d[1], d[2], d[3]);
+  else if (k == "3mm" && need(5)) ws_3mm(c, d[0], d[1], d[2], d[3], d[4]);
+  else if (k == "syrk" && need(2)) take_split(c, d[0], d[1]);
+  else if (k == "syr2k" && need(2)) { take_split(c, d[0], d[1]); take_split(c, d[0], d[1]); }
+  else if ((k == "covariance" || k == "correlation") && need(2)) ws_stat(c, d[0], d[1]);
+  else if (k == "atax" && need(2)) { c.take<char>(mvmt_ws_bytes(d[0], d[1])); c.take<float>(d[0]); }
+  else if (k == "bicg" && need(2)) c.take<char>(mvmt_ws_bytes(d[1], d[0]));
+  else if (k == "mvt" && need(1)) c.take<char>(mvmt_ws_bytes(d[0], d[0]));
+  else if (k == "gesummv" && need(1)) {}
+  else if (k == "syrk_rows" && need(4)) take_split(c, d[3], d[1]);
+  else if (k == "syr2k_rows" && need(4)) { take_split(c, d[3], d[1]); take_split(c, d[3], d[1]); }
+  else if (k == "matvec_partial" && need(2)) c.take<char>(mvmt_ws_bytes(d[0], d[1]));
+  else if (k == "gemm_variant" && need(3)) ws_gemm(c, d[0], d[1], d[2]);
+  else return fail(PB_ERR_INVALID_ARG, "unknown kernel '%s' or wrong number of dims (%d)", kernel, nd);
+  *bytes = align_up(c.off, 256);
+  return PB_OK;
+}
+
+pb_status pb_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A, const float* B,
+                  void* ws, size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({ni, nj, nk});
+  ck.cols4(nj, "C/B"); ck.cols4(nk, "A");
+  ck.arr(C, ni, nj, true, "C"); ck.arr(A, ni, nk, false, "A"); ck.arr(B, nk, nj, false, "B");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  ws_gemm(need, ni, nj, nk);
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  Carve c(ws, ws_bytes);
+  WsGemm w = ws_gemm(c, ni, nj, nk);
+  int L = 0;
+  PB_TRY(run_gemm(ni, nj, nk, alpha, beta, C, A, B, w, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float* tmp, const float* A,
+                 const float* B, const float* C, float* D, void* ws, size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({ni, nj, nk, nl});
+  ck.cols4(nk, "A"); ck.cols4(nj, "B/tmp"); ck.cols4(nl, "C/D");
+  ck.arr(tmp, ni, nj, true, "tmp", false);
+  ck.arr(A, ni, nk, false, "A"); ck.arr(B, nk, nj, false, "B"); ck.arr(C, nj, nl, false, "C");
+  ck.arr(D, ni, nl, true, "D");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  ws_2mm(need, ni, nj, nk, nl);
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  Carve c(ws, ws_bytes);
+  Ws2mm w = ws_2mm(c, ni, nj, nk, nl);
+  cudaStream_t st = S(s);
+  int L = 0;
+  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
+  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
+  PB_CUDA(launch_split_T(C, nj, nl, nl, w.ct.hi, w.ct.lo, w.ct.ld, nullptr, nullptr, st));
+  L += 3;
+  GemmDesc g1;  // tmp = alpha * A * B  (epilogue emits tmp's split = GEMM 2's A operand)
+  g1.M = ni; g1.N = nj; g1.K = nk;
+  g1.a[0] = w.a.op(); g1.b[0] = w.bt.op();
+  g1.flags = EPI_SPLIT | (tmp ? EPI_OUT : 0u);
+  g1.alpha = alpha;
+  g1.out = tmp; g1.ldo = nj;
+  g1.split_hi = w.tmp.hi; g1.split_lo = w.tmp.lo; g1.ld_split = w.tmp.ld;
+  PB_CUDA(launch_umma_gemm(g1, st, &L));
+  GemmDesc g2;  // D = tmp * C + beta * D
+  g2.M = ni; g2.N = nl; g2.K = nj;
+  g2.a[0] = w.tmp.op(); g2.b[0] = w.ct.op();
+  g2.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
+  g2.alpha = 1.f; g2.beta = beta;
+  g2.cin = D; g2.ldc = nl; g2.out = D; g2.ldo = nl;
+  PB_CUDA(launch_umma_gemm(g2, st, &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* A, const float* B, float* F,
+                 const float* C, const float* D, float* G, void* ws, size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({ni, nj, nk, nl, nm});
+  ck.cols4(nk, "A"); ck.cols4(nj, "B/E"); ck.cols4(nm, "C"); ck.cols4(nl, "D/F/G");
+  ck.arr(E, ni, nj, true, "E"); ck.arr(A, ni, nk, false, "A"); ck.arr(B, nk, nj, false, "B");
+  ck.arr(F, nj, nl, true, "F"); ck.arr(C, nj, nm, false, "C"); ck.arr(D, nm, nl, false, "D");
+  ck.arr(G, ni, nl, true, "G");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  ws_3mm(need, ni, nj, nk, nl, nm);
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  Carve c(ws, ws_bytes);
+  Ws3mm w = ws_3mm(c, ni, nj, nk, nl, nm);
+  cudaStream_t st = S(s);
+  int L = 0;
+  PB_CUDA(launch_split(C, nj, nm, nm, w.c.hi, w.c.lo, w.c.ld, st));
+  PB_CUDA(launch_split_T(D, nm, nl, nl, w.dt.hi, w.dt.lo, w.dt.ld, nullptr, nullptr, st));
+  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
+  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
+  L += 4;
+  GemmDesc gf;  // F = C * D; epilogue also emits F^T split (G's K-major B operand)
+  gf.M = nj; gf.N = nl; gf.K = nm;
+  gf.a[0] = w.c.op(); gf.b[0] = w.dt.op();
+  gf.flags = EPI_OUT | EPI_SPLIT_T;
+  gf.out = F; gf.ldo = nl;
+  gf.split_hi = w.ft.hi; gf.split_lo = w.ft.lo; gf.ld_split = w.ft.ld;
+  PB_CUDA(launch_umma_gemm(gf, st, &L));
+  GemmDesc ge;  // E = A * B; epilogue also emits E split (G's A operand)
+  ge.M = ni; ge.N = nj; ge.K = nk;
+  ge.a[0] = w.a.op(); ge.b[0] = w.bt.op();
+  ge.flags = EPI_OUT | EPI_SPLIT;
+  ge.out = E; ge.ldo = nj;
+  ge.split_hi = w.e.hi; ge.split_lo = w.e.lo; ge.ld_split = w.e.ld;
+  PB_CUDA(launch_umma_gemm(ge, st, &L));
+  GemmDesc gg;  // G = E * F
+  gg.M = ni; gg.N = nl; gg.K = nj;
+  gg.a[0] = w.e.op(); gg.b[0] = w.ft.op();
+  gg.flags = EPI_OUT;
+  gg.out = G; gg.ldo = nl;
+  PB_CUDA(launch_umma_gemm(gg, st, &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+static pb_status syrk_core(int n, int m, int r0, int r1, float alpha, float beta, float* C_blk, const float* A,
+                           const float* B, void* ws, size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({n, m});
+  if (ck.st == PB_OK && (r0 < 0 || r1 > n || r0 >= r1 || r0 % 128 != 0))
+    ck.st = fail(PB_ERR_INVALID_ARG, "row range [%d,%d) invalid (r0 multiple of 128, r1 <= n)", r0, r1);
+  ck.cols4(m, "A/B"); ck.cols4(n, "C");
+  ck.arr(C_blk, r1 - r0, n, true, "C"); ck.arr(A, r1, m, false, "A");
+  if (B) ck.arr(B, r1, m, false, "B");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  take_split(need, r1, m);
+  if (B) take_split(need, r1, m);
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  Carve c(ws, ws_bytes);
+  SplitBuf sa = take_split(c, r1, m);
+  SplitBuf sb{};
+  if (B) sb = take_split(c, r1, m);
+  cudaStream_t st = S(s);
+  int L = 0;
+  PB_CUDA(launch_split(A, r1, m, m, sa.hi, sa.lo, sa.ld, st));
+  ++L;
+  if (B) { PB_CUDA(launch_split(B, r1, m, m, sb.hi, sb.lo, sb.ld, st)); ++L; }
+  GemmDesc d;
+  d.M = r1; d.N = r1; d.K = m;
+  if (B) {  // C[i][j] += A[j].B[i] + B[j].A[i]: pair 0 = (B rows i, A rows j), pair 1 = (A rows i, B rows j)
+    d.npairs = 2;
+    d.a[0] = sb.op(); d.b[0] = sa.op();
+    d.a[1] = sa.op(); d.b[1] = sb.op();
+  } else {
+    d.a[0] = sa.op(); d.b[0] = sa.op();
+  }
+  d.flags = EPI_TRI | EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
+  d.alpha = alpha; d.beta = beta;
+  d.cin = C_blk; d.ldc = n; d.out = C_blk; d.ldo = n; d.out_row0 = r0;
+  d.tm0 = r0 / 128; d.tm1 = (r1 + 127) / 128;
+  PB_CUDA(launch_umma_gemm(d, st, &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_syrk(int n, int m, float alpha, float beta, float* C, const float* A, void* ws, size_t ws_bytes,
+                  pb_stream s) {
+  return syrk_core(n, m, 0, n, alpha, beta, C, A, nullptr, ws, ws_bytes, s);
+}
+pb_status pb_syr2k(int n, int m, float alpha, float beta, float* C, const float* A, const float* B, void* ws,
+                   size_t ws_bytes, pb_stream s) {
+  if (!B) return fail(PB_ERR_INVALID_ARG, "B is NULL");
+  return syrk_core(n, m, 0, n, alpha, beta, C, A, B, ws, ws_bytes, s);
+}
+pb_status pb_syrk_rows(int n, int m, int r0, int r1, float alpha, float beta, float* C_blk, const float* A, void* ws,
+                       size_t ws_bytes, pb_stream s) {
+  return syrk_core(n, m, r0, r1, alpha, beta, C_blk, A, nullptr, ws, ws_bytes, s);
+}
+pb_status pb_syr2k_rows(int n, int m, int r0, int r1, float alpha, float beta, float* C_blk, const float* A,
+                        const float* B, void* ws, size_t ws_bytes, pb_stream s) {
+  if (!B) return fail(PB_ERR_INVALID_ARG, "B is NULL");
+  return syrk_core(n, m, r0, r1, alpha, beta, C_blk, A, B, ws, ws_bytes, s);
+}
+
+static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, const float* data, float* out,
+                           float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({m, n});
+  if (ck.st == PB_OK && !corr && n < 2) ck.st = fail(PB_ERR_INVALID_ARG, "covariance needs n >= 2");
+  if (ck.st == PB_OK && !(float_n > 0.f) ) ck.st = fail(PB_ERR_INVALID_ARG, "float_n must be > 0");
+  if (ck.st == PB_OK && !corr && float_n == 1.0f) ck.st = fail(PB_ERR_INVALID_ARG, "float_n - 1 == 0");
+  ck.cols4(m, "data/out");
+  ck.arr(data, n, m, false, "data");
+  ck.arr(out, m, m, true, corr ? "corr" : "cov");
+  ck.arr(mean, 1, m, true, "mean", false);
+  if (corr) ck.arr(stddev, 1, m, true, "stddev", false);
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  ws_stat(need, m, n);
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  Carve c(ws, ws_bytes);
+  WsStat w = ws_stat(c, m, n);
+  cudaStream_t st = S(s);
+  int L = 0;
+  PB_CUDA(launch_colstats(data, n, m, (double)float_n, (double)eps, corr, w.part, w.mean, w.inv, mean,
+                          corr ? stddev : nullptr, st, &L));
+  PB_CUDA(launch_split_T(data, n, m, m, w.xt.hi, w.xt.lo, w.xt.ld, w.mean, corr ? w.inv : nullptr, st));
+  ++L;
+  GemmDesc d;  // Gram core: out[i][j] = alpha * sum_k Xt[i][k] Xt[j][k], lower tiles + mirror
+  d.M = m; d.N = m; d.K = n;
+  d.a[0] = w.xt.op(); d.b[0] = w.xt.op();
+  d.flags = EPI_TRI | EPI_MIRROR | EPI_OUT | (corr ? EPI_DIAG_ONE : 0u);
+  d.alpha = corr ? 1.0f : (float)(1.0 / ((double)float_n - 1.0));
+  d.out = out; d.ldo = m;
+  PB_CUDA(launch_umma_gemm(d, st, &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_covariance(int m, int n, float float_n, const float* data, float* cov, float* mean, void* ws,
+                        size_t ws_bytes, pb_stream s) {
+  return stat_core(false, m, n, float_n, 0.f, data, cov, mean, nullptr, ws, ws_bytes, s);
+}
+pb_status pb_correlation(int m, int n, float float_n, float eps, const float* data, float* corr, float* mean,
+                         float* stddev, void* ws, size_t ws_bytes, pb_stream s) {
+  return stat_core(true, m, n, float_n, eps, data, corr, mean, stddev, ws, ws_bytes, s);
+}
+
+pb_status pb_atax(int m, int n, const float* A, const float* x, float* y, float* tmp, void* ws, size_t ws_bytes,
+                  pb_stream s) {
+  Check ck;
+  ck.dims({m, n});
+  ck.cols4(n, "A");
+  ck.arr(A, m, n, false, "A"); ck.arr(x, 1, n, false, "x"); ck.arr(y, 1, n, true, "y");
+  ck.arr(tmp, 1, m, true, "tmp", false);
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  need.take<char>(mvmt_ws_bytes(m, n));
+  need.take<float>(m);
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  Carve c(ws, ws_bytes);
+  void* mw = c.take<char>(mvmt_ws_bytes(m, n));
+  float* t = c.take<float>(m);
+  if (tmp) t = tmp;
+  cudaStream_t st = S(s);
+  int L = 0;
+  PB_CUDA(launch_rowdot(A, nullptr, x, m, n, 1.f, 0.f, nullptr, t, st));  // tmp = A x
+  ++L;
+  PB_CUDA(launch_mvmt(A, m, n, nullptr, t, nullptr, nullptr, nullptr, y, mw, st, &L));  // y = A^T tmp
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_bicg(int m, int n, const float* A, float* s_out, float* q, const float* p, const float* r, void* ws,
+                  size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({m, n});
+  ck.cols4(m, "A");
+  ck.arr(A, n, m, false, "A"); ck.arr(s_out, 1, m, true, "s"); ck.arr(q, 1, n, true, "q");
+  ck.arr(p, 1, m, false, "p"); ck.arr(r, 1, n, false, "r");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  need.take<char>(mvmt_ws_bytes(n, m));
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  int L = 0;
+  PB_CUDA(launch_mvmt(A, n, m, p, r, nullptr, q, nullptr, s_out, ws, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_mvt(int n, float* x1, float* x2, const float* y_1, const float* y_2, const float* A, void* ws,
+                 size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({n});
+  ck.cols4(n, "A");
+  ck.arr(x1, 1, n, true, "x1"); ck.arr(x2, 1, n, true, "x2");
+  ck.arr(y_1, 1, n, false, "y_1"); ck.arr(y_2, 1, n, false, "y_2"); ck.arr(A, n, n, false, "A");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  need.take<char>(mvmt_ws_bytes(n, n));
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  int L = 0;
+  PB_CUDA(launch_mvmt(A, n, n, y_1, y_2, x1, x1, x2, x2, ws, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_gesummv(int n, float alpha, float beta, const float* A, const float* B, float* tmp, const float* x,
+                     float* y, void* ws, size_t ws_bytes, pb_stream s) {
+  (void)ws; (void)ws_bytes;
+  Check ck;
+  ck.dims({n});
+  ck.cols4(n, "A/B");
+  ck.arr(A, n, n, false, "A"); ck.arr(B, n, n, false, "B"); ck.arr(tmp, 1, n, true, "tmp", false);
+  ck.arr(x, 1, n, false, "x"); ck.arr(y, 1, n, true, "y");
+  PB_TRY(ck.finish());
+  PB_CUDA(launch_rowdot(A, B, x, n, n, alpha, beta, y, tmp, S(s)));
+  g_launches = 1;
+  return PB_OK;
+}
+
+pb_status pb_matvec_partial(int rows, int cols, const float* A_blk, const float* v, const float* base_row,
+                            float* rowdot, const float* w, const float* base_col, float* colpart, void* ws,
+                            size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({rows, cols});
+  ck.cols4(cols, "A_blk");
+  if (ck.st == PB_OK && !v && !w) ck.st = fail(PB_ERR_INVALID_ARG, "neither v nor w given");
+  if (ck.st == PB_OK && ((v == nullptr) != (rowdot == nullptr) || (w == nullptr) != (colpart == nullptr)))
+    ck.st = fail(PB_ERR_INVALID_ARG, "v/rowdot and w/colpart must be given together");
+  ck.arr(A_blk, rows, cols, false, "A_blk");
+  ck.arr(v, 1, cols, false, "v", false);
+  ck.arr(w, 1, rows, false, "w", false);
+  if (rowdot != base_row) ck.arr(base_row, 1, rows, false, "base_row", false);
+  if (colpart != base_col) ck.arr(base_col, 1, cols, false, "base_col", false);
+  ck.arr(rowdot, 1, rows, true, "rowdot", false);
+  ck.arr(colpart, 1, cols, true, "colpart", false);
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  need.take<char>(mvmt_ws_bytes(rows, cols));
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  int L = 0;
+  PB_CUDA(launch_mvmt(A_blk, rows, cols, v, w, base_row, rowdot, base_col, colpart, ws, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_row_partition(int rows, int nranks, int rank, int triangular, int align, int* begin, int* end) {
+  if (rows <= 0 || nranks <= 0 || rank < 0 || rank >= nranks || align <= 0 || !begin || !end)
+    return fail(PB_ERR_INVALID_ARG, "bad partition arguments");
+  auto bound = [&](int g) -> int {
+    if (g <= 0) return 0;
+    if (g >= nranks) return rows;
+    double f = triangular ? std::sqrt((double)g / nranks) : (double)g / nranks;
+    long long b = llround(f * rows / align) * (long long)align;
+    if (b < 0) b = 0;
+    if (b > rows) b = rows;
+    return (int)b;
+  };
+  int b0 = bound(rank), b1 = bound(rank + 1);  // bound() is monotone in g
+  *begin = b0;
+  *end = std::max(b0, b1);
+  return PB_OK;
+}
+
+pb_status pb_gemm_variant(int variant, int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
+                          const float* B, void* ws, size_t ws_bytes, pb_stream s) {
+  if (variant == 3) return pb_gemm(ni, nj, nk, alpha, beta, C, A, B, ws, ws_bytes, s);
+  if (variant < 0 || variant > 3) return fail(PB_ERR_INVALID_ARG, "variant %d", variant);
+  Check ck;
+  ck.dims({ni, nj, nk});
+  ck.cols4(nj, "C/B"); ck.cols4(nk, "A");
+  ck.arr(C, ni, nj, true, "C"); ck.arr(A, ni, nk, false, "A"); ck.arr(B, nk, nj, false, "B");
+  PB_TRY(ck.finish());
+  cudaStream_t st = S(s);
+  if (variant == 0) PB_CUDA(launch_gemm_listing8(ni, nj, nk, alpha, beta, C, A, B, st));
+  if (variant == 1) PB_CUDA(launch_gemm_listing9(ni, nj, nk, alpha, beta, C, A, B, st));
+  if (variant == 2) PB_CUDA(launch_gemm_listing9_reg(ni, nj, nk, alpha, beta, C, A, B, st));
+  g_launches = 1;
+  return PB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// pb_internal.h — host-side interfaces between the C ABI (pb_api.cu) and the
+// kernel translation units. Not installed; not part of the ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace pb {
+
+// ---- 3xTF32 tcgen05 GEMM (k_umma.cu) ---------------------------------------
+// One K-major split operand: hi/lo arrays of `rows` x `K` (row pitch ld floats).
+struct SplitOperand {
+  const float* hi = nullptr;
+  const float* lo = nullptr;
+  int rows = 0;
+  int K = 0;
+  int ld = 0;
+};
+
+enum : uint32_t {
+  EPI_TRI = 1u << 0,       // only tiles/elements with j <= i (lower triangle)
+  EPI_MIRROR = 1u << 1,    // also write out[j][i] (symmetric output)
+  EPI_DIAG_ONE = 1u << 2,  // out[i][i] = 1
+  EPI_CIN = 1u << 3,       // v += beta * Cin[i][j]
+  EPI_OUT = 1u << 4,       // write fp32 out[i][j]
+  EPI_SPLIT = 1u << 5,     // write hi/lo split of v at [i][j] (next GEMM's K-major A operand)
+  EPI_SPLIT_T = 1u << 6,   // write hi/lo split of v at [j][i] (next GEMM's K-major B operand)
+};
+
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;  // output rows (operand-a rows), cols (operand-b rows), contraction
+  int npairs = 1;           // 1, or 2 for syr2k (acc = a0*b0^T + a1*b1^T)
+  SplitOperand a[2], b[2];
+  uint32_t flags = EPI_OUT;
+  float alpha = 1.f, beta = 0.f;
+  const float* cin = nullptr;
+  int ldc = 0;
+  float* out = nullptr;
+  int ldo = 0;
+  int out_row0 = 0;  // out/cin row index = i - out_row0
+  float* split_hi = nullptr;
+  float* split_lo = nullptr;
+  int ld_split = 0;
+  int tm0 = 0, tm1 = -1;  // tile-row range (default all)
+};
+
+cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches);
+
+// ---- split / prep (k_split.cu) ----------------------------------------------
+// hi/lo split of a rows x cols matrix; same layout (ldo = ld of output).
+cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi, float* lo, int ldo,
+                         cudaStream_t s);
+// hi/lo split of the transpose: out (cols x rows), out pitch ldo (>= rows).
+// If mean != nullptr: value = (x - mean[col]) * inv[col] computed in double first
+// (inv == nullptr means 1).
+cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* hiT, float* loT, int ldo,
+                           const double* mean, const double* inv, cudaStream_t s);
+
+// ---- column statistics (k_stats.cu) -----------------------------------------
+// mean[j] = sum_i data[i][j] / float_n (double). If want_sd: sd/inv with eps rule.
+// part: workspace of stats_part_doubles(m, n) doubles.
+size_t stats_part_doubles(int m, int n);
+cudaError_t launch_colstats(const float* data, int n, int m, double float_n, double eps, bool want_sd,
+                            double* part, double* mean, double* inv, float* mean_out, float* sd_out,
+                            cudaStream_t s, int* launches);
+
+// ---- matrix-vector family (k_matvec.cu) -------------------------------------
+// y[i] = alpha * A_i.x + beta * B_i.x (B may be null -> beta ignored); tmp[i] = A_i.x (optional).
+cudaError_t launch_rowdot(const float* A, const float* B, const float* x, int rows, int cols, float alpha,
+                          float beta, float* y, float* tmp, cudaStream_t s);
+// Fused single pass over A (rows x cols):
+//   rowpart[ct][i] = sum_{j in col tile ct} A[i][j]*v[j]        (if v)
+//   colpart[rt][j] = sum_{i in row tile rt} A[i][j]*w[i]        (if w)
+// then out_row[i] = base_row[i] + sum_ct rowpart, out_col[j] = base_col[j] + sum_rt colpart.
+size_t mvmt_ws_bytes(int rows, int cols);
+cudaError_t launch_mvmt(const float* A, int rows, int cols, const float* v, const float* w,
+                        const float* base_row, float* out_row, const float* base_col, float* out_col,
+                        void* ws, cudaStream_t s, int* launches);
+
+// ---- SIMT ablation kernels (k_simt.cu): PAPER.md Listing 8 / Listing 9 -------
+cudaError_t launch_gemm_listing8(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
+                                 const float* B, cudaStream_t s);
+cudaError_t launch_gemm_listing9(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
+                                 const float* B, cudaStream_t s);
+cudaError_t launch_gemm_listing9_reg(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
+                                     const float* B, cudaStream_t s);
+
+inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace pb

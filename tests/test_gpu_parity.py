@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same pbgen inputs. Sizes span several 128x128 tiles with ragged tails; the
+exactness, determinism and precision-discriminator pins (P1, P32, P34 of
+SURVEY.md §8(c)) and the ABI's error behaviour are checked here too.
+Full BASELINE.json-size checks live in test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import paper_2312_13170_b200 as pb  # noqa: E402
+import pbgen  # noqa: E402
+from tests import parity as P  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _ok(r):
+    assert r["ok"], {k: v for k, v in r.items() if k not in ("g", "r")}
+
+
+# ------------------------------------------------------------------ generator
+def test_pbgen_device_matches_host_bitwise():
+    for mode in (pbgen.U01, pbgen.INT8, pbgen.U01 | pbgen.SYM):
+        t = torch.empty(77, 132, device="cuda")
+        pbgen.gen_device(t, 3, mode=mode, scale=0.5, offset=-0.25, row0=5, ld=132)
+        h = pbgen.gen_host(77, 132, 3, mode=mode, scale=0.5, offset=-0.25, row0=5, ld=132)
+        assert np.array_equal(P.host(t).view(np.uint32), h.view(np.uint32))
+
+
+# ------------------------------------------------------------------ gemm family
+@pytest.mark.parametrize("ni,nj,nk", [(128, 128, 32), (128, 128, 128), (7, 4, 4), (129, 132, 260),
+                                      (300, 516, 388), (1000, 1024, 1000), (640, 384, 2052)])
+def test_gemm(ni, nj, nk):
+    _ok(P.check_gemm(ni, nj, nk))
+
+
+@pytest.mark.parametrize("alpha,beta", [(1.5, 0.0), (0.0, 1.2), (-2.0, 0.5), (1.0, 1.0)])
+def test_gemm_alpha_beta(alpha, beta):
+    _ok(P.check_gemm(257, 260, 300, alpha, beta))
+
+
+def test_gemm_integer_inputs_bitwise_P1():
+    """values in {0..7}: hi = x, lo = 0, every product and partial sum exact
+    in fp32 -> the tensor-core path equals the oracle bit for bit."""
+    r = P.check_gemm(384, 260, 1024, alpha=1.5, beta=0.5, mode=pbgen.INT8)
+    assert np.array_equal(r["g"].astype(np.float64), r["r"])
+
+
+def test_gemm_run_to_run_deterministic_P32():
+    A = torch.from_numpy(P.H(512, 516, 1)).cuda()
+    B = torch.from_numpy(P.H(516, 384, 2)).cuda()
+    C0 = torch.from_numpy(P.H(512, 384, 3)).cuda()
+    outs = []
+    for _ in range(3):
+        C = C0.clone()
+        pb.pb_gemm(512, 384, 516, 1.5, 1.2, C, A, B)
+        outs.append(P.host(C))
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+def test_gemm_precision_discriminator_P34():
+    """centred inputs U[-1/2,1/2): 3xTF32 must stay at fp32-level error
+    (<= 2e-6 of |A||B|), which a silent 1xTF32 path (~1e-5) would fail."""
+    for nk in (2048, 4096):
+        A = P.H(256, nk, 1, offset=-0.5)
+        B = P.H(nk, 256, 2, offset=-0.5)
+        C = np.zeros((256, 256), np.float32)
+        dC = P.dev(C)
+        pb.pb_gemm(256, 256, nk, 1.0, 0.0, dC, P.dev(A), P.dev(B))
+        g = P.host(dC)
+        r = oracle.gemm(1.0, 0.0, C, A, B)
+        scale = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64))
+        assert np.max(np.abs(g - r) / scale) <= 2e-6
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_gemm_paper_variants(variant):
+    _ok(P.check_gemm(130, 132, 200, variant=variant))
+
+
+def test_listing8_equals_listing9_bitwise():
+    """loop internalization preserves semantics; our SIMT
+    twins keep the k order, so Listing 8 and Listing 9 agree bit for bit."""
+    a = P.check_gemm(100, 96, 150, variant=0)["g"]
+    b = P.check_gemm(100, 96, 150, variant=1)["g"]
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dims", [(128, 128, 128, 128), (129, 132, 136, 124), (384, 260, 516, 260)])
+def test_2mm(dims):
+    _ok(P.check_2mm(*dims))
+
+
+def test_2mm_chain_identity_P7():
+    ni = nj = nk = nl = 256
+    A, B, D = P.H(ni, nk, 1), P.H(nk, nj, 2), P.H(ni, nl, 4)
+    C = np.eye(nj, dtype=np.float32)
+    dD = P.dev(D)
+    pb.pb_2mm(ni, nj, nk, nl, 1.5, 1.2, None, P.dev(A), P.dev(B), P.dev(C), dD)
+    r = oracle.gemm(1.5, 1.2, D, A, B)
+    s = oracle.gemm(1.5, 1.2, D, A, B, absmode=True)
+    assert P.cerr(P.host(dD), r, s) <= P.TOL
+
+
+@pytest.mark.parametrize("dims", [(128, 128, 128, 128, 128), (129, 132, 136, 124, 260), (260, 388, 132, 256, 300)])
+def test_3mm(dims):
+    _ok(P.check_3mm(*dims))
+
+
+@pytest.mark.parametrize("n,m", [(128, 128), (132, 136), (260, 388), (512, 1028), (1000, 300)])
+def test_syrk(n, m):
+    _ok(P.check_syrk(n, m))
+
+
+@pytest.mark.parametrize("n,m", [(128, 128), (132, 136), (388, 260), (516, 1024)])
+def test_syr2k(n, m):
+    _ok(P.check_syr2k(n, m))
+
+
+def test_syr2k_equals_syrk_doubled_P12():
+    n, m = 260, 300
+    A = P.H(n, m, 1, mode=pbgen.INT8)
+    C = P.H(n, n, 3, mode=pbgen.INT8 | pbgen.SYM)
+    c1, c2 = P.dev(C), P.dev(C)
+    dA = P.dev(A)
+    pb.pb_syr2k(n, m, 1.5, 0.5, c1, dA, dA)
+    pb.pb_syrk(n, m, 3.0, 0.5, c2, dA)
+    assert np.array_equal(P.host(c1), P.host(c2))
+
+
+def test_syrk_integer_bitwise_P1():
+    n, m = 260, 1024
+    A = P.H(n, m, 1, mode=pbgen.INT8)
+    C = P.H(n, n, 3, mode=pbgen.INT8 | pbgen.SYM)
+    dC = P.dev(C)
+    pb.pb_syrk(n, m, 1.5, 0.5, dC, P.dev(A))
+    assert np.array_equal(P.host(dC).astype(np.float64), oracle.syrk(1.5, 0.5, C, A))
+
+
+@pytest.mark.parametrize("m,n", [(128, 128), (132, 137), (260, 517), (516, 2048)])
+def test_covariance(m, n):
+    _ok(P.check_covariance(m, n))
+
+
+@pytest.mark.parametrize("m,n", [(128, 128), (132, 137), (260, 517), (516, 2048)])
+def test_correlation(m, n):
+    _ok(P.check_correlation(m, n))
+
+
+def test_covariance_unstructured_ragged():
+    _ok(P.check_covariance(388, 301, structured=False))
+
+
+# ------------------------------------------------------------------ matrix-vector
+@pytest.mark.parametrize("m,n", [(1, 4), (7, 8), (257, 516), (1000, 2052), (4096, 4096), (3001, 5000)])
+def test_atax(m, n):
+    _ok(P.check_atax(m, n))
+
+
+@pytest.mark.parametrize("m,n", [(4, 1), (8, 7), (516, 257), (2052, 1000), (4096, 4096), (5000, 3001)])
+def test_bicg(m, n):
+    _ok(P.check_bicg(m, n))
+
+
+@pytest.mark.parametrize("n", [4, 8, 132, 516, 2052, 4096])
+def test_mvt(n):
+    _ok(P.check_mvt(n))
+
+
+@pytest.mark.parametrize("n", [4, 8, 132, 516, 2052, 4096])
+def test_gesummv(n):
+    _ok(P.check_gesummv(n))
+
+
+def test_matvec_deterministic_P32():
+    n = 4096
+    A, p, r = P.dev(P.H(n, n, 1)), P.dev(P.H(1, n, 6)[0]), P.dev(P.H(1, n, 7)[0])
+    res = []
+    for _ in range(2):
+        s, q = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+        pb.pb_bicg(n, n, A, s, q, p, r)
+        res.append((P.host(s), P.host(q)))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+# ------------------------------------------------------------------ ABI error behaviour
+def test_abi_errors_leave_outputs_untouched():
+    A = torch.ones(64, 64, device="cuda")
+    B = torch.ones(64, 64, device="cuda")
+    C = torch.full((64, 64), 3.0, device="cuda")
+    with pytest.raises(pb.PBError) as e:  # alias: C overlaps A
+        pb.pb_gemm(64, 64, 64, 1.0, 1.0, A, A, B)
+    assert e.value.status == 3
+    with pytest.raises(pb.PBError) as e:  # cols % 4
+        pb.pb_gemm(64, 62, 64, 1.0, 1.0, C, A, B)
+    assert e.value.status == 2
+    with pytest.raises(pb.PBError) as e:  # misaligned pointer
+        pb.pb_gemm(8, 8, 8, 1.0, 1.0, C.view(-1)[1:].data_ptr(), A, B)
+    assert e.value.status == 2
+    with pytest.raises(pb.PBError) as e:  # host pointer
+        pb.pb_gemm(8, 8, 8, 1.0, 1.0, torch.ones(8, 8).data_ptr(), A, B)
+    assert e.value.status == 1
+    ws = torch.empty(256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(pb.PBError) as e:  # workspace too small
+        pb.pb_gemm(64, 64, 64, 1.0, 1.0, C, A, B, ws=ws)
+    assert e.value.status == 4
+    assert bool((C == 3.0).all())
+
+
+def test_row_sharded_pieces_match_full():
+    """Host-side sharding math on one GPU: syrk_rows bands and matvec partials
+    reassemble the single-call results (P33 on one device)."""
+    n, m = 520, 300
+    A = P.dev(P.H(n, m, 1))
+    C0 = P.dev(P.H(n, n, 3, mode=pbgen.SYM))
+    full = C0.clone()
+    pb.pb_syrk(n, m, 1.5, 1.2, full, A)
+    parts = C0.clone()
+    for g in range(3):
+        r0, r1 = pb.pb_row_partition(n, 3, g, triangular=True, align=128)
+        if r1 > r0:
+            pb.pb_syrk_rows(n, m, r0, r1, 1.5, 1.2, parts[r0:r1], A)
+    assert np.array_equal(P.host(full), P.host(parts))
+    rows, cols = 1000, 1028
+    A = P.dev(P.H(rows, cols, 1))
+    v, w = P.dev(P.H(1, cols, 6)[0]), P.dev(P.H(1, rows, 7)[0])
+    rd, cp = torch.empty(rows, device="cuda"), torch.empty(cols, device="cuda")
+    pb.pb_matvec_partial(rows, cols, A, v, None, rd, w, None, cp)
+    s, q = torch.empty(cols, device="cuda"), torch.empty(rows, device="cuda")
+    pb.pb_bicg(cols, rows, A, s, q, v, w)
+    assert np.array_equal(P.host(rd), P.host(q)) and np.array_equal(P.host(cp), P.host(s))
