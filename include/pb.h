@@ -76,7 +76,9 @@ pb_status pb_workspace_size(const char* kernel, const long long* dims, int ndims
 
 /* gemm — PAPER.md:394-401 (Listing 8 is alpha=beta=1); PolyBench kernel_gemm.
  *   C[i][j] = beta*C[i][j] + alpha * sum_{k<nk} A[i][k]*B[k][j]
- * C ni x nj (in/out), A ni x nk, B nk x nj. */
+ * C ni x nj (in/out), A ni x nk, B nk x nj. beta == 0 means C is not read
+ * (BLAS convention; so NaN/garbage in C is not propagated). Same for the beta
+ * of 2mm, syrk, syr2k. */
 pb_status pb_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                   const float* B, void* ws, size_t ws_bytes, pb_stream s);
 
@@ -175,6 +177,11 @@ pb_status pb_matvec_partial(int rows, int cols, const float* A_blk, const float*
                             const float* base_row, float* rowdot, const float* w,
                             const float* base_col, float* colpart, void* ws, size_t ws_bytes,
                             pb_stream s);
+/* pb_gesummv_rows: rows of gesummv for a row block: y_blk = alpha*A_blk*x + beta*B_blk*x,
+ *   tmp_blk = A_blk*x (optional); A_blk, B_blk are rows x n, x has n entries. */
+pb_status pb_gesummv_rows(int rows, int n, float alpha, float beta, const float* A_blk,
+                          const float* B_blk, float* tmp_blk, const float* x, float* y_blk, void* ws,
+                          size_t ws_bytes, pb_stream s);
 /* workspace for the two helpers above: kernel names "syrk_rows" {n,m,r0,r1},
  * "syr2k_rows" {n,m,r0,r1}, "matvec_partial" {rows, cols}. */
 

@@ -18,7 +18,7 @@ import os
 __all__ = [
     "PBError", "lib", "workspace_size", "workspace", "pb_gemm", "pb_2mm", "pb_3mm", "pb_syrk",
     "pb_syr2k", "pb_covariance", "pb_correlation", "pb_atax", "pb_bicg", "pb_mvt", "pb_gesummv",
-    "pb_row_partition", "pb_syrk_rows", "pb_syr2k_rows", "pb_matvec_partial", "pb_gemm_variant",
+    "pb_row_partition", "pb_syrk_rows", "pb_gesummv_rows", "pb_syr2k_rows", "pb_matvec_partial", "pb_gemm_variant",
     "pb_version", "last_launch_count", "ABI_FUNCTIONS",
 ]
 
@@ -54,6 +54,7 @@ ABI_FUNCTIONS = {
     "pb_syr2k_rows": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
     "pb_matvec_partial": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gemm_variant": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_gesummv_rows": ([_I, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
 }
 
 _lib = None
@@ -131,14 +132,15 @@ def _ws(ws, kernel, dims, ref):
     """Caller's workspace, or a per-device cached one (kept alive across calls so
     asynchronous kernels never see it freed)."""
     if ws is None:
+        import torch
         need = max(workspace_size(kernel, dims), 256)
-        cur = _ws_cache.get(ref.device)
+        device = ref.device if hasattr(ref, "device") else torch.device("cuda", torch.cuda.current_device())
+        cur = _ws_cache.get(device)
         if cur is None or cur.numel() < need:
-            import torch
             if cur is not None:
-                torch.cuda.synchronize(ref.device)  # the old buffer may still be in use
-            cur = torch.empty(need, dtype=torch.uint8, device=ref.device)
-            _ws_cache[ref.device] = cur
+                torch.cuda.synchronize(device)  # the old buffer may still be in use
+            cur = torch.empty(need, dtype=torch.uint8, device=device)
+            _ws_cache[device] = cur
         ws = cur
     return _ptr(ws), (ws.numel() * ws.element_size() if hasattr(ws, "numel") else 1 << 62), ws
 
@@ -219,6 +221,12 @@ def pb_gesummv(n_, alpha, beta, A, B, tmp, x, y, ws=None, stream=None):
     p, n, keep = _ws(ws, "gesummv", (n_,), y)
     _check("pb_gesummv", lib().pb_gesummv(n_, alpha, beta, _ptr(A), _ptr(B), _ptr(tmp), _ptr(x), _ptr(y), p, n,
                                           _stream(stream, y)))
+
+
+def pb_gesummv_rows(rows, n_, alpha, beta, A_blk, B_blk, tmp_blk, x, y_blk, ws=None, stream=None):
+    p, n, keep = _ws(ws, "gesummv_rows", (rows, n_), A_blk)
+    _check("pb_gesummv_rows", lib().pb_gesummv_rows(rows, n_, alpha, beta, _ptr(A_blk), _ptr(B_blk), _ptr(tmp_blk),
+                                                    _ptr(x), _ptr(y_blk), p, n, _stream(stream, A_blk)))
 
 
 def pb_matvec_partial(rows, cols, A_blk, v, base_row, rowdot, w, base_col, colpart, ws=None, stream=None):

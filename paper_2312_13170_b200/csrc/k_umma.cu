@@ -24,7 +24,7 @@
 //               masks, fp32 / split / mirrored stores
 // Tiles 128 x 128 (UMMA M=128, N=128, K=8 per instruction), BK = 32 (one 128-B
 // swizzle row of fp32), 3-stage ring of {A_hi, A_lo, B_hi, B_lo} = 64 KiB/stage,
-// double-buffered TMEM accumulator (2 x 128 columns).
+// double-buffered TMEM accumulators (2 x {big, small} x 128 columns = all 512).
 #include <math.h>
 
 #include "pb_device.cuh"
@@ -41,7 +41,7 @@ constexpr int TILE_BYTES = BM * BK * 4;          // 16 KiB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;      // A_hi, A_lo, B_hi, B_lo
 constexpr int NUM_THREADS = 192;
 constexpr int GROUP_M = 8;                       // tile-rows per raster group (L2 reuse)
-constexpr uint32_t TMEM_COLS = 2 * BN;
+constexpr uint32_t TMEM_COLS = 4 * BN;  // 2 buffers x {big, small} accumulators = 512 columns
 
 struct Params {
   int M, N, K, npairs, nkb;  // nkb = k-blocks per pair
@@ -176,7 +176,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&ctl->tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
+        // Two accumulators per tile: `big` takes a_hi*b_hi, `small` takes the
+        // cross terms a_hi*b_lo + a_lo*b_hi (2^-11 smaller), so the rounding of
+        // each tensor-core accumulate hits the small terms at their own scale.
+        const uint32_t d_big = tmem_base + acc * 2 * BN;
+        const uint32_t d_small = d_big + BN;
         for (int kb = 0; kb < nkb_total; ++kb) {
           mbar_wait(&ctl->full[stage], phase);
           tc_fence_after();
@@ -187,9 +191,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t al = umma_desc_k_sw128(st + 1 * TILE_BYTES + kk * 32);
             const uint64_t bh = umma_desc_k_sw128(st + 2 * TILE_BYTES + kk * 32);
             const uint64_t bl = umma_desc_k_sw128(st + 3 * TILE_BYTES + kk * 32);
-            mma_tf32(d, al, bh, idesc, (kb | kk) != 0);  // small terms first
-            mma_tf32(d, ah, bl, idesc, 1);
-            mma_tf32(d, ah, bh, idesc, 1);
+            const uint32_t accum = (kb | kk) != 0;
+            mma_tf32(d_small, al, bh, idesc, accum);
+            mma_tf32(d_small, ah, bl, idesc, 1);
+            mma_tf32(d_big, ah, bh, idesc, accum);
           }
           mma_commit(&ctl->empty[stage]);  // frees the smem stage when these MMAs finish
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -214,15 +219,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool diag_tile = (flags & EPI_TRI) && tm == tn;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
+        uint32_t r[16], rs[16];
         __syncwarp();
-        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, r);
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 2 * BN + c0;
+        tmem_ld16(ta, r);
+        tmem_ld16(ta + BN, rs);
         tmem_wait_ld();
         const int j0 = tn * BN + c0;
         if (row_ok && j0 < p.N) {
         float v[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = p.alpha * __uint_as_float(r[e]);
+        for (int e = 0; e < 16; ++e) v[e] = p.alpha * (__uint_as_float(r[e]) + __uint_as_float(rs[e]));
         const long long orow = (long long)(i - p.out_row0);
         if (flags & EPI_CIN) {
           const float* cp = p.cin + orow * p.ldc + j0;

@@ -238,6 +238,7 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   else if (k == "bicg" && need(2)) c.take<char>(mvmt_ws_bytes(d[1], d[0]));
   else if (k == "mvt" && need(1)) c.take<char>(mvmt_ws_bytes(d[0], d[0]));
   else if (k == "gesummv" && need(1)) {}
+  else if (k == "gesummv_rows" && need(2)) {}
   else if (k == "syrk_rows" && need(4)) take_split(c, d[3], d[1]);
   else if (k == "syr2k_rows" && need(4)) { take_split(c, d[3], d[1]); take_split(c, d[3], d[1]); }
   else if (k == "matvec_partial" && need(2)) c.take<char>(mvmt_ws_bytes(d[0], d[1]));
@@ -512,18 +513,23 @@ pb_status pb_mvt(int n, float* x1, float* x2, const float* y_1, const float* y_2
   return PB_OK;
 }
 
-pb_status pb_gesummv(int n, float alpha, float beta, const float* A, const float* B, float* tmp, const float* x,
-                     float* y, void* ws, size_t ws_bytes, pb_stream s) {
+pb_status pb_gesummv_rows(int rows, int n, float alpha, float beta, const float* A, const float* B, float* tmp,
+                          const float* x, float* y, void* ws, size_t ws_bytes, pb_stream s) {
   (void)ws; (void)ws_bytes;
   Check ck;
-  ck.dims({n});
+  ck.dims({rows, n});
   ck.cols4(n, "A/B");
-  ck.arr(A, n, n, false, "A"); ck.arr(B, n, n, false, "B"); ck.arr(tmp, 1, n, true, "tmp", false);
-  ck.arr(x, 1, n, false, "x"); ck.arr(y, 1, n, true, "y");
+  ck.arr(A, rows, n, false, "A"); ck.arr(B, rows, n, false, "B"); ck.arr(tmp, 1, rows, true, "tmp", false);
+  ck.arr(x, 1, n, false, "x"); ck.arr(y, 1, rows, true, "y");
   PB_TRY(ck.finish());
-  PB_CUDA(launch_rowdot(A, B, x, n, n, alpha, beta, y, tmp, S(s)));
+  PB_CUDA(launch_rowdot(A, B, x, rows, n, alpha, beta, y, tmp, S(s)));
   g_launches = 1;
   return PB_OK;
+}
+
+pb_status pb_gesummv(int n, float alpha, float beta, const float* A, const float* B, float* tmp, const float* x,
+                     float* y, void* ws, size_t ws_bytes, pb_stream s) {
+  return pb_gesummv_rows(n, n, alpha, beta, A, B, tmp, x, y, ws, ws_bytes, s);
 }
 
 pb_status pb_matvec_partial(int rows, int cols, const float* A_blk, const float* v, const float* base_row,

@@ -1,0 +1,158 @@
+"""Row-block data parallelism over the GPUs of one node (DESIGN.md §Multi-GPU,
+SURVEY.md §8(e)). One process per GPU; torch.distributed (NCCL over
+NVLink/NVSwitch on GPUs, gloo in the CPU tests) carries the only exchange
+steps the math needs:
+
+  gemm, 2mm, gesummv, syrk, syr2k   no collective: rank g owns output rows R_g and
+                                    computes them from its row block + replicated
+                                    operands (2mm: tmp[R] = alpha A[R] B is exactly
+                                    what D[R] = tmp[R] C + beta D[R] needs)
+  3mm                               F = C D by row blocks, ALL-GATHER of F (async, overlapped
+                                    with E[R] = A[R] B), then G[R] = E[R] F
+  atax, bicg, mvt                   row dots local; the transposed product's per-rank
+                                    partial vector is REDUCE-SCATTERed into the same
+                                    row partition (mvt folds x2's old value into rank 0's
+                                    partial, so the sum is x2 + A^T y_2)
+
+Every arithmetic step runs in libpb through the C ABI (`K` below defaults to
+the binding; the CPU gloo tests inject an oracle-backed namespace to check
+the partition and collective logic without a GPU). Outputs stay row-sharded
+(reading R15).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+import paper_2312_13170_b200 as _pb
+
+
+def _world():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(), dist.get_rank()
+    return 1, 0
+
+
+def partition(rows, world, rank, triangular=False, align=128, K=_pb):
+    return K.pb_row_partition(rows, world, rank, triangular, align)
+
+
+def _all_gather_rows(full, local, world, bounds, async_op=False):
+    """full[rows] <- concat of every rank's `local` row block."""
+    sizes = [e - b for b, e in bounds]
+    if len(set(sizes)) == 1:
+        return dist.all_gather_into_tensor(full, local, async_op=async_op)
+    mx = max(sizes)  # uneven blocks: pad every block to the largest, gather, unpad
+    _, rank = _world()
+    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: sizes[rank]].copy_(local[: sizes[rank]])
+    big = torch.empty((world * mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(big, pad)
+    for g, (b, e) in enumerate(bounds):
+        full[b:e].copy_(big[g * mx: g * mx + (e - b)])
+    return None
+
+
+def _reduce_scatter_vec(out_local, partial, world, bounds):
+    """out_local <- (sum over ranks of partial)[bounds[rank]]."""
+    sizes = [e - b for b, e in bounds]
+    if len(set(sizes)) == 1 and sizes[0] * world == partial.numel():
+        dist.reduce_scatter_tensor(out_local, partial)
+    else:
+        dist.all_reduce(partial)
+        _, rank = _world()
+        b, e = bounds[rank]
+        out_local.copy_(partial[b:e])
+
+
+# --------------------------------------------------------------------- contractions
+def mm2_rows(ctx, n, alpha, beta, tmp, A, B, C, D, ws, K=_pb):
+    """2mm on this rank's rows (A, tmp, D are the local row blocks)."""
+    rows = A.shape[0]
+    if rows == 0:
+        return 0
+    K.pb_2mm(rows, n, n, n, alpha, beta, tmp, A, B, C, D, ws=ws)
+    return K.last_launch_count()
+
+
+def mm3_rows(ctx, n, E, A, B, Fl, F, C, D, G, ws, K=_pb):
+    """3mm: F row block -> async all-gather of F overlapped with E[R] = A[R] B -> G[R] = E[R] F."""
+    world, rank = _world()
+    L = 0
+    if world == 1:
+        K.pb_3mm(A.shape[0], n, n, n, n, E, A, B, F, C, D, G, ws=ws)
+        return K.last_launch_count()
+    bounds = [partition(n, world, g, False, 128, K) for g in range(world)]
+    f0, f1 = bounds[rank]
+    if f1 > f0:
+        K.pb_gemm(f1 - f0, n, n, 1.0, 0.0, Fl, C[f0:f1], D, ws=ws)  # F[R'] = C[R'] D
+        L += K.last_launch_count()
+    work = _all_gather_rows(F, Fl, world, bounds, async_op=True)
+    rows = A.shape[0]
+    if rows:
+        K.pb_gemm(rows, n, n, 1.0, 0.0, E, A, B, ws=ws)  # E[R] = A[R] B, overlaps the all-gather
+        L += K.last_launch_count()
+    if work is not None and hasattr(work, "wait"):
+        work.wait()
+    if rows:
+        K.pb_gemm(rows, n, n, 1.0, 0.0, G, E, F, ws=ws)  # G[R] = E[R] F
+        L += K.last_launch_count()
+    return L
+
+
+def syrk_rows(ctx, n, m, alpha, beta, C_blk, A, ws, B=None, K=_pb):
+    world, rank = _world()
+    r0, r1 = partition(n, world, rank, True, 128, K)
+    if r1 <= r0:
+        return 0
+    if B is None:
+        K.pb_syrk_rows(n, m, r0, r1, alpha, beta, C_blk, A, ws=ws)
+    else:
+        K.pb_syr2k_rows(n, m, r0, r1, alpha, beta, C_blk, A, B, ws=ws)
+    return K.last_launch_count()
+
+
+# --------------------------------------------------------------------- matrix-vector
+def matvec(ctx, kernel, n, v, ws, alpha, beta, K=_pb):
+    """atax / bicg / mvt / gesummv on this rank's row block of A (and B).
+    v: dict with A (local rows x n), x, r, x1, x2, y2 (full n vectors), y, s, yo
+    (full-length partial buffers), q/tmp outputs."""
+    world, rank = _world()
+    A = v["A"]
+    rows = A.shape[0]
+    if world == 1:
+        if kernel == "atax":
+            K.pb_atax(rows, n, A, v["x"], v["y"], v["tmp"], ws=ws)
+        elif kernel == "bicg":
+            K.pb_bicg(n, rows, A, v["s"], v["q"], v["x"], v["r"], ws=ws)
+        elif kernel == "mvt":
+            K.pb_mvt(n, v["x1"], v["x2"], v["x"], v["y2"], A, ws=ws)
+        else:
+            K.pb_gesummv(n, alpha, beta, A, v["B"], v["tmp"], v["x"], v["yo"], ws=ws)
+        return K.last_launch_count()
+    bounds = [partition(n, world, g, False, 4, K) for g in range(world)]
+    r0, r1 = bounds[rank]
+    L = 0
+    if kernel == "atax":  # tmp[R] = A[R] x ; y = sum_g A[R_g]^T tmp[R_g]
+        part = v["yo"]
+        K.pb_matvec_partial(rows, n, A, v["x"], None, v["tmp"][:rows], None, None, None, ws=ws)
+        L += K.last_launch_count()
+        K.pb_matvec_partial(rows, n, A, None, None, None, v["tmp"][:rows], None, part, ws=ws)
+        L += K.last_launch_count()
+        _reduce_scatter_vec(v["y"][r0:r1], part, world, bounds)
+    elif kernel == "bicg":  # q[R] = A[R] p ; s = sum_g A[R_g]^T r[R_g]
+        part = v["yo"]
+        K.pb_matvec_partial(rows, n, A, v["x"], None, v["q"][r0:r1], v["r"][r0:r1], None, part, ws=ws)
+        L += K.last_launch_count()
+        _reduce_scatter_vec(v["s"][r0:r1], part, world, bounds)
+    elif kernel == "mvt":  # x1[R] += A[R] y_1 ; x2 = x2 + sum_g A[R_g]^T y_2[R_g]
+        part = v["yo"]
+        x1l = v["x1"][r0:r1]
+        K.pb_matvec_partial(rows, n, A, v["x"], x1l, x1l, v["y2"][r0:r1], v["x2"] if rank == 0 else None, part,
+                            ws=ws)
+        L += K.last_launch_count()
+        _reduce_scatter_vec(v["x2"][r0:r1], part, world, bounds)
+    else:  # gesummv: purely row-local
+        K.pb_gesummv_rows(rows, n, alpha, beta, A, v["B"], v["tmp"][:rows], v["x"], v["yo"][r0:r1], ws=ws)
+        L += K.last_launch_count()
+    return L

@@ -1,0 +1,152 @@
+"""Parity at BASELINE.json's full sizes, through the same C-ABI calls (and so
+the same launch configurations) bench.py times. Where the oracle cannot
+recompute everything in seconds (2mm/3mm at 4096, syrk/syr2k at 8192) it
+evaluates sampled rows / entries one by one; elsewhere the full output is
+compared. Inputs: pbgen host generator (seed 13170), uploaded.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import paper_2312_13170_b200 as pb  # noqa: E402
+import pbgen  # noqa: E402
+from tests import parity as P  # noqa: E402
+
+S = pbgen.STREAM
+AL, BE = 1.5, 1.2
+rng = np.random.default_rng(13170)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    torch.cuda.empty_cache()
+
+
+def _ok(r):
+    assert r["ok"], r
+
+
+def test_gemm_128_config():
+    _ok(P.check_gemm(128, 128, 128, AL, BE))
+
+
+def test_covariance_2048_config():
+    _ok(P.check_covariance(2048, 2048))
+
+
+def test_correlation_2048_config():
+    _ok(P.check_correlation(2048, 2048))
+
+
+def test_2mm_4096_sampled_rows():
+    n = 4096
+    A, B, C, D = (P.H(n, n, S[k]) for k in ("A", "B", "C", "D"))
+    dtmp, dD = torch.empty(n, n, device="cuda"), P.dev(D)
+    pb.pb_2mm(n, n, n, n, AL, BE, dtmp, P.dev(A), P.dev(B), P.dev(C), dD)
+    rows = np.unique(np.concatenate([[0, 127, 128, n - 1], rng.integers(0, n, 28)]))
+    t_r, D_r = oracle.mm2_rows(AL, BE, A, B, C, D, rows)
+    t_s, D_s = oracle.mm2_rows(AL, BE, A, B, C, D, rows, absmode=True)
+    assert P.cerr(P.host(dtmp)[rows], t_r, t_s) <= P.TOL
+    assert P.cerr(P.host(dD)[rows], D_r, D_s) <= P.TOL
+
+
+def test_3mm_4096_sampled_rows():
+    n = 4096
+    A, B, C, D = (P.H(n, n, S[k]) for k in ("A", "B", "C", "D"))
+    dE, dF, dG = (torch.empty(n, n, device="cuda") for _ in range(3))
+    pb.pb_3mm(n, n, n, n, n, dE, P.dev(A), P.dev(B), dF, P.dev(C), P.dev(D), dG)
+    rows = np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, 14)]))
+    E_r, F_r, G_r = oracle.mm3_rows(A, B, C, D, rows)
+    E_s, F_s, G_s = oracle.mm3_rows(A, B, C, D, rows, absmode=True)
+    assert P.cerr(P.host(dE)[rows], E_r, E_s) <= P.TOL
+    assert P.cerr(P.host(dF), F_r, F_s) <= P.TOL  # all of F
+    assert P.cerr(P.host(dG)[rows], G_r, G_s) <= P.TOL
+
+
+def _tri_samples(n, k):
+    i = rng.integers(0, n, k)
+    j = (rng.random(k) * (i + 1)).astype(np.int64)
+    i = np.concatenate([i, [n - 1, n - 1, 0, 128, 8191 % n]])
+    j = np.concatenate([j, [0, n - 1, 0, 127, 8191 % n]])
+    return i.astype(np.int32), j.astype(np.int32)
+
+
+@pytest.mark.parametrize("two", [False, True])
+def test_syrk_syr2k_8192_sampled(two):
+    n = m = 8192
+    A = P.H(n, m, S["A"])
+    B = P.H(n, m, S["B"]) if two else None
+    C = P.H(n, n, S["C"], mode=pbgen.U01 | pbgen.SYM)
+    dC = P.dev(C)
+    if two:
+        pb.pb_syr2k(n, m, AL, BE, dC, P.dev(A), P.dev(B))
+    else:
+        pb.pb_syrk(n, m, AL, BE, dC, P.dev(A))
+    g = P.host(dC)
+    i, j = _tri_samples(n, 3000)
+    r = oracle.syrk_at(AL, BE, C, A, i, j, B=B)
+    s = oracle.syrk_at(AL, BE, C, A, i, j, B=B, absmode=True)
+    assert P.cerr(g[i, j], r, s) <= P.TOL
+    # strict upper triangle untouched (sampled rows, all their upper entries)
+    for row in (0, 1, 4095, 8190):
+        assert np.array_equal(g[row, row + 1:], C[row, row + 1:])
+
+
+MV = 32768
+
+
+@pytest.fixture(scope="module")
+def mv_inputs():
+    A = P.H(MV, MV, S["A"])
+    return A, P.dev(A)
+
+
+def test_atax_32768(mv_inputs):
+    A, dA = mv_inputs
+    x = P.H(1, MV, S["x"])[0]
+    dy, dt = torch.empty(MV, device="cuda"), torch.empty(MV, device="cuda")
+    pb.pb_atax(MV, MV, dA, P.dev(x), dy, dt)
+    y_r, t_r = oracle.atax(A, x)
+    y_s, t_s = oracle.atax(A, x, absmode=True)
+    assert P.cerr(P.host(dy), y_r, y_s) <= P.TOL and P.cerr(P.host(dt), t_r, t_s) <= P.TOL
+
+
+def test_bicg_32768(mv_inputs):
+    A, dA = mv_inputs
+    p, r = P.H(1, MV, S["p"])[0], P.H(1, MV, S["r"])[0]
+    ds, dq = torch.empty(MV, device="cuda"), torch.empty(MV, device="cuda")
+    pb.pb_bicg(MV, MV, dA, ds, dq, P.dev(p), P.dev(r))
+    s_r, q_r = oracle.bicg(A, p, r)
+    s_s, q_s = oracle.bicg(A, p, r, absmode=True)
+    assert P.cerr(P.host(ds), s_r, s_s) <= P.TOL and P.cerr(P.host(dq), q_r, q_s) <= P.TOL
+
+
+def test_mvt_32768(mv_inputs):
+    A, dA = mv_inputs
+    x1, x2 = P.H(1, MV, S["x1"])[0], P.H(1, MV, S["x2"])[0]
+    y1, y2 = P.H(1, MV, S["y_1"])[0], P.H(1, MV, S["y_2"])[0]
+    d1, d2 = P.dev(x1), P.dev(x2)
+    pb.pb_mvt(MV, d1, d2, P.dev(y1), P.dev(y2), dA)
+    o1, o2 = oracle.mvt(x1, x2, y1, y2, A)
+    s1, s2 = oracle.mvt(x1, x2, y1, y2, A, absmode=True)
+    assert P.cerr(P.host(d1), o1, s1) <= P.TOL and P.cerr(P.host(d2), o2, s2) <= P.TOL
+
+
+def test_gesummv_32768(mv_inputs):
+    A, dA = mv_inputs
+    B = P.H(MV, MV, S["B"])
+    x = P.H(1, MV, S["x"])[0]
+    dt, dy = torch.empty(MV, device="cuda"), torch.empty(MV, device="cuda")
+    dB = P.dev(B)
+    pb.pb_gesummv(MV, AL, BE, dA, dB, dt, P.dev(x), dy)
+    t_r, y_r = oracle.gesummv(AL, BE, A, B, x)
+    t_s, y_s = oracle.gesummv(AL, BE, A, B, x, absmode=True)
+    del dB
+    assert P.cerr(P.host(dt), t_r, t_s) <= P.TOL and P.cerr(P.host(dy), y_r, y_s) <= P.TOL
