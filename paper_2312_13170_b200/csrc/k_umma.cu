@@ -24,7 +24,9 @@
 //               masks, fp32 / split / mirrored stores
 // Tiles 128 x 128 (UMMA M=128, N=128, K=8 per instruction), BK = 32 (one 128-B
 // swizzle row of fp32), 3-stage ring of {A_hi, A_lo, B_hi, B_lo} = 64 KiB/stage,
-// double-buffered TMEM accumulators (2 x {big, small} x 128 columns = all 512).
+// two TMEM accumulator slots (2 x {big, small} x 128 columns = all 512) that
+// alternate per 512-wide K chunk; the epilogue promotes each chunk into fp32
+// registers (RN) so the tensor core's truncating accumulate cannot bias long K.
 #include <math.h>
 
 #include "pb_device.cuh"
@@ -41,7 +43,8 @@ constexpr int TILE_BYTES = BM * BK * 4;          // 16 KiB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;      // A_hi, A_lo, B_hi, B_lo
 constexpr int NUM_THREADS = 192;
 constexpr int GROUP_M = 8;                       // tile-rows per raster group (L2 reuse)
-constexpr uint32_t TMEM_COLS = 4 * BN;  // 2 buffers x {big, small} accumulators = 512 columns
+constexpr uint32_t TMEM_COLS = 4 * BN;  // 2 slots x {big, small} accumulators = 512 columns
+constexpr int CHUNK_KB = 16;            // k-blocks (16 x 32 = 512 of K) per TMEM partial sum
 
 struct Params {
   int M, N, K, npairs, nkb;  // nkb = k-blocks per pair
@@ -166,139 +169,156 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
+    // The k-loop of a tile is cut into chunks of CHUNK_KB k-blocks. Each chunk
+    // accumulates into one of two TMEM slots; the epilogue warps drain a
+    // finished slot into fp32 registers (round-to-nearest adds) while the next
+    // chunk runs in the other slot. The tensor-core accumulate truncates, so
+    // this bounds the truncation bias to one chunk.
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(BM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&ctl->tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
-        tc_fence_after();
-        // Two accumulators per tile: `big` takes a_hi*b_hi, `small` takes the
-        // cross terms a_hi*b_lo + a_lo*b_hi (2^-11 smaller), so the rounding of
-        // each tensor-core accumulate hits the small terms at their own scale.
-        const uint32_t d_big = tmem_base + acc * 2 * BN;
-        const uint32_t d_small = d_big + BN;
-        for (int kb = 0; kb < nkb_total; ++kb) {
-          mbar_wait(&ctl->full[stage], phase);
+      int chunk_it = 0;
+      for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int kb0 = 0; kb0 < nkb_total; kb0 += CHUNK_KB, ++chunk_it) {
+          const int slot = chunk_it & 1;
+          const uint32_t slot_phase = (chunk_it >> 1) & 1;
+          mbar_wait(&ctl->tempty[slot], slot_phase ^ 1);  // epilogue drained this slot
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
+          // `big` takes a_hi*b_hi, `small` the cross terms a_hi*b_lo + a_lo*b_hi
+          // (2^-11 smaller): the small terms are rounded at their own scale.
+          const uint32_t d_big = tmem_base + slot * 2 * BN;
+          const uint32_t d_small = d_big + BN;
+          const int kb1 = min(kb0 + CHUNK_KB, nkb_total);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&ctl->full[stage], phase);
+            tc_fence_after();
+            const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t ah = umma_desc_k_sw128(st + 0 * TILE_BYTES + kk * 32);
-            const uint64_t al = umma_desc_k_sw128(st + 1 * TILE_BYTES + kk * 32);
-            const uint64_t bh = umma_desc_k_sw128(st + 2 * TILE_BYTES + kk * 32);
-            const uint64_t bl = umma_desc_k_sw128(st + 3 * TILE_BYTES + kk * 32);
-            const uint32_t accum = (kb | kk) != 0;
-            mma_tf32(d_small, al, bh, idesc, accum);
-            mma_tf32(d_small, ah, bl, idesc, 1);
-            mma_tf32(d_big, ah, bh, idesc, accum);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t ah = umma_desc_k_sw128(st + 0 * TILE_BYTES + kk * 32);
+              const uint64_t al = umma_desc_k_sw128(st + 1 * TILE_BYTES + kk * 32);
+              const uint64_t bh = umma_desc_k_sw128(st + 2 * TILE_BYTES + kk * 32);
+              const uint64_t bl = umma_desc_k_sw128(st + 3 * TILE_BYTES + kk * 32);
+              const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
+              mma_tf32(d_small, al, bh, idesc, accum);
+              mma_tf32(d_small, ah, bl, idesc, 1);
+              mma_tf32(d_big, ah, bh, idesc, accum);
+            }
+            mma_commit(&ctl->empty[stage]);  // frees the smem stage when these MMAs finish
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&ctl->empty[stage]);  // frees the smem stage when these MMAs finish
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          mma_commit(&ctl->tfull[slot]);  // chunk partial sums ready for the epilogue
         }
-        mma_commit(&ctl->tfull[acc]);  // accumulator ready for the epilogue
       }
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t flags = p.flags;
-    int it = 0;
-    for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    int chunk_it = 0;
+    for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int tm, tn;
       tile_coords(p, t, tm, tn);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&ctl->tfull[acc], acc_phase);
-      tc_fence_after();
+      float acc[BN];  // this thread's output row of the tile, fp32 registers
+#pragma unroll
+      for (int c = 0; c < BN; ++c) acc[c] = 0.f;
+      for (int kb0 = 0; kb0 < nkb_total; kb0 += CHUNK_KB, ++chunk_it) {
+        const int slot = chunk_it & 1;
+        const uint32_t slot_phase = (chunk_it >> 1) & 1;
+        mbar_wait(&ctl->tfull[slot], slot_phase);
+        tc_fence_after();
+        __syncwarp();
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + slot * 2 * BN;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t r[16], rs[16];
+          tmem_ld16(ta + c0, r);
+          tmem_ld16(ta + BN + c0, rs);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(r[e]) + __uint_as_float(rs[e]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->tempty[slot]);
+      }
       const int i = tm * BM + q * 32 + lane;  // output row (operand-a space)
       const bool row_ok = i < p.M;
       const bool diag_tile = (flags & EPI_TRI) && tm == tn;
-#pragma unroll 1
+      const long long orow = (long long)(i - p.out_row0);
+#pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16], rs[16];
-        __syncwarp();
-        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 2 * BN + c0;
-        tmem_ld16(ta, r);
-        tmem_ld16(ta + BN, rs);
-        tmem_wait_ld();
         const int j0 = tn * BN + c0;
         if (row_ok && j0 < p.N) {
-        float v[16];
+          float v[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = p.alpha * (__uint_as_float(r[e]) + __uint_as_float(rs[e]));
-        const long long orow = (long long)(i - p.out_row0);
-        if (flags & EPI_CIN) {
-          const float* cp = p.cin + orow * p.ldc + j0;
-#pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            if (j0 + e < p.N) {
-              float4 c = *reinterpret_cast<const float4*>(cp + e);
-              v[e] += p.beta * c.x; v[e + 1] += p.beta * c.y; v[e + 2] += p.beta * c.z; v[e + 3] += p.beta * c.w;
-            }
-          }
-        }
-        if (flags & EPI_DIAG_ONE) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (j0 + e == i) v[e] = 1.0f;
-        }
-        if (!diag_tile) {
-          if (flags & EPI_OUT) {
-            float* op = p.out + orow * p.ldo + j0;
-#pragma unroll
-            for (int e = 0; e < 16; e += 4)
-              if (j0 + e < p.N) store4(op + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
-          }
-          if (flags & EPI_SPLIT) {
-            float* hp = p.split_hi + (long long)i * p.ld_split + j0;
-            float* lp = p.split_lo + (long long)i * p.ld_split + j0;
+          for (int e = 0; e < 16; ++e) v[e] = p.alpha * acc[c0 + e];
+          if (flags & EPI_CIN) {
+            const float* cp = p.cin + orow * p.ldc + j0;
 #pragma unroll
             for (int e = 0; e < 16; e += 4) {
               if (j0 + e < p.N) {
-                float h[4], l[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) split3x(v[e + u], h[u], l[u]);
-                store4(hp + e, h[0], h[1], h[2], h[3]);
-                store4(lp + e, l[0], l[1], l[2], l[3]);
+                float4 c = *reinterpret_cast<const float4*>(cp + e);
+                v[e] += p.beta * c.x; v[e + 1] += p.beta * c.y; v[e + 2] += p.beta * c.z; v[e + 3] += p.beta * c.w;
               }
             }
           }
-        } else {  // lower-triangular diagonal tile: element mask j <= i
-          if (flags & EPI_OUT) {
-            float* op = p.out + orow * p.ldo + j0;
+          if (flags & EPI_DIAG_ONE) {
 #pragma unroll
             for (int e = 0; e < 16; ++e)
-              if (j0 + e < p.N && j0 + e <= i) op[e] = v[e];
+              if (j0 + e == i) v[e] = 1.0f;
           }
-        }
-        if (flags & EPI_MIRROR) {  // out[j][i] = v for j < i (j <= i on diagonal tiles handled above)
+          if (!diag_tile) {
+            if (flags & EPI_OUT) {
+              float* op = p.out + orow * p.ldo + j0;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int j = j0 + e;
-            if (j < p.N && j < i) p.out[(long long)(j - p.out_row0) * p.ldo + i] = v[e];
+              for (int e = 0; e < 16; e += 4)
+                if (j0 + e < p.N) store4(op + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+            }
+            if (flags & EPI_SPLIT) {
+              float* hp = p.split_hi + (long long)i * p.ld_split + j0;
+              float* lp = p.split_lo + (long long)i * p.ld_split + j0;
+#pragma unroll
+              for (int e = 0; e < 16; e += 4) {
+                if (j0 + e < p.N) {
+                  float h[4], l[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) split3x(v[e + u], h[u], l[u]);
+                  store4(hp + e, h[0], h[1], h[2], h[3]);
+                  store4(lp + e, l[0], l[1], l[2], l[3]);
+                }
+              }
+            }
+          } else {  // lower-triangular diagonal tile: element mask j <= i
+            if (flags & EPI_OUT) {
+              float* op = p.out + orow * p.ldo + j0;
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (j0 + e < p.N && j0 + e <= i) op[e] = v[e];
+            }
           }
-        }
-        if (flags & EPI_SPLIT_T) {
+          if (flags & EPI_MIRROR) {  // out[j][i] = v for j < i
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int j = j0 + e;
-            if (j < p.N) {
-              float h, l;
-              split3x(v[e], h, l);
-              p.split_hi[(long long)j * p.ld_split + i] = h;
-              p.split_lo[(long long)j * p.ld_split + i] = l;
+            for (int e = 0; e < 16; ++e) {
+              const int j = j0 + e;
+              if (j < p.N && j < i) p.out[(long long)(j - p.out_row0) * p.ldo + i] = v[e];
+            }
+          }
+          if (flags & EPI_SPLIT_T) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int j = j0 + e;
+              if (j < p.N) {
+                float h, l;
+                split3x(v[e], h, l);
+                p.split_hi[(long long)j * p.ld_split + i] = h;
+                p.split_lo[(long long)j * p.ld_split + i] = l;
+              }
             }
           }
         }
-        }  // row_ok && j0 < N
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->tempty[acc]);
     }
   }
 

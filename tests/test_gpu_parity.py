@@ -82,6 +82,16 @@ def test_gemm_precision_discriminator_P34():
         assert np.max(np.abs(g - r) / scale) <= 2e-6
 
 
+@pytest.mark.parametrize("nk", [8192, 16384])
+def test_gemm_long_k_no_truncation_bias(nk):
+    """U[0,1) data, long K: the tensor-core accumulate truncates, so without
+    chunked promotion the result is biased low by ~(K/8)*2^-24 (1e-4 at K=16k).
+    With 512-wide chunks promoted to fp32 registers the error stays ~1e-6."""
+    r = P.check_gemm(256, 128, nk, 1.0, 0.0)
+    assert r["err"] <= 1e-5, r["err"]
+    assert abs(np.mean((r["g"] - r["r"]) / r["r"])) <= 5e-6  # no systematic bias
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_gemm_paper_variants(variant):
     _ok(P.check_gemm(130, 132, 200, variant=variant))
