@@ -174,7 +174,181 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
   out[i] = base ? base[i] + s : s;
 }
 
+// ------------------------------------------------------------------ atax, single pass
+// y = A^T (A x) reading A ONCE (S16). A 2-CTA cluster owns a contiguous block of
+// rows; CTA `rank` holds the column slice [c0, c0 + w) of every row. Per row b:
+//   dot  : the slice arrives in an smem stage by 1-D bulk copy (TMA engine);
+//          512 threads dot it with their registers of x -> CTA partial -> written
+//          into BOTH CTAs' smem (DSMEM) and announced by a cluster-scope mbarrier
+//          arrive (release), so neither CTA blocks on the other;
+//   axpy : once both partials of row b are in (acquire), tmp_b = p0 + p1 (fixed
+//          order, identical in both CTAs) and y_acc += tmp_b * A[b][slice] from the
+//          SAME smem stage — the row is never re-read from HBM or L2.
+// dot(b+1) is issued before axpy(b), hiding the DSMEM round trip. y_acc (the
+// loop-carried reduction) lives in registers; the per-cluster
+// partial y vectors are summed by reduce_parts_kernel in a fixed order.
+constexpr int AX_THREADS = 512;
+constexpr int AX_V = 8;                               // float4 per thread per slice
+constexpr int AX_SLICE = AX_THREADS * AX_V * 4;       // 16384 floats = 64 KiB
+constexpr int AX_STAGES = 3;
+constexpr int AX_RED = 4;  // partial slots: a peer's dot(b+4) can only start after our axpy(b)
+
+struct __align__(16) AxCtl {
+  uint64_t full[AX_STAGES];
+  uint64_t red[AX_RED];
+  float part[AX_RED][2];
+  float wred[AX_THREADS / 32];
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
+    atax_onepass_kernel(const float* __restrict__ A, const float* __restrict__ x, int m, int n, int w0,
+                        float* __restrict__ tmp, float* __restrict__ ypart) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* stage_buf = reinterpret_cast<float*>(sm);
+  AxCtl* ctl = reinterpret_cast<AxCtl*>(sm + (size_t)AX_STAGES * AX_SLICE * 4);
+  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int c0 = rank ? w0 : 0;
+  const int w = rank ? n - w0 : w0;
+  const int w4 = w >> 2;
+  const int r0 = (int)((long long)m * cl / ncl), r1 = (int)((long long)m * (cl + 1) / ncl);
+  const int nb = r1 - r0;
+
+  if (tid == 0) {
+    for (int s = 0; s < AX_STAGES; ++s) mbar_init(&ctl->full[s], 1);
+    for (int s = 0; s < AX_RED; ++s) mbar_init(&ctl->red[s], 2);
+    fence_mbar_init();
+  }
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
+
+  float4 xv[AX_V], yacc[AX_V];
+  const float4* x4 = reinterpret_cast<const float4*>(x + c0);
+#pragma unroll
+  for (int v = 0; v < AX_V; ++v) {
+    const int idx = tid + v * AX_THREADS;
+    xv[v] = idx < w4 ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    yacc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  auto issue = [&](int b) {  // thread 0: row b's slice -> stage b % STAGES
+    const int s = b % AX_STAGES;
+    mbar_arrive_expect_tx(&ctl->full[s], (uint32_t)w * 4u);
+    if (w > 0) bulk_g2s(stage_buf + (size_t)s * AX_SLICE, A + (long long)(r0 + b) * n + c0, (uint32_t)w * 4u,
+                        &ctl->full[s]);
+  };
+  if (tid == 0)
+    for (int b = 0; b < AX_STAGES && b < nb; ++b) issue(b);
+
+  const uint32_t red0 = smem_u32(&ctl->red[0]);
+  const uint32_t part0 = smem_u32(&ctl->part[0][0]);
+  auto dot = [&](int b) {
+    const int s = b % AX_STAGES;
+    mbar_wait(&ctl->full[s], (uint32_t)(b / AX_STAGES) & 1u);
+    const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)s * AX_SLICE);
+    float p = 0.f;
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const int idx = tid + v * AX_THREADS;
+      if (idx < w4) {
+        const float4 a = row[idx];
+        p += a.x * xv[v].x + a.y * xv[v].y + a.z * xv[v].z + a.w * xv[v].w;
+      }
+    }
+    p = warp_sum(p);
+    if (lane == 0) ctl->wred[warp] = p;
+    __syncthreads();
+    if (tid == 0) {
+      float q = 0.f;
+#pragma unroll
+      for (int k = 0; k < AX_THREADS / 32; ++k) q += ctl->wred[k];
+      const int slot = b % AX_RED;
+      const uint32_t poff = (uint32_t)(slot * 2 + rank) * 4u;
+      const uint32_t roff = (uint32_t)slot * 8u;
+      st_cluster_f32(map_peer(part0 + poff, rank), q);
+      st_cluster_f32(map_peer(part0 + poff, peer), q);
+      mbar_arrive_cluster(map_peer(red0 + roff, rank));
+      mbar_arrive_cluster(map_peer(red0 + roff, peer));
+    }
+  };
+  auto axpy = [&](int b) {
+    const int slot = b % AX_RED;
+    mbar_wait_cluster(&ctl->red[slot], (uint32_t)(b / AX_RED) & 1u);
+    const float t = ctl->part[slot][0] + ctl->part[slot][1];
+    if (tmp && rank == 0 && tid == 0) tmp[r0 + b] = t;
+    const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)(b % AX_STAGES) * AX_SLICE);
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const int idx = tid + v * AX_THREADS;
+      if (idx < w4) {
+        const float4 a = row[idx];
+        yacc[v].x += t * a.x; yacc[v].y += t * a.y; yacc[v].z += t * a.z; yacc[v].w += t * a.w;
+      }
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0 && b + AX_STAGES < nb) issue(b + AX_STAGES);
+  };
+
+  if (nb > 0) dot(0);
+  for (int b = 0; b < nb; ++b) {
+    if (b + 1 < nb) dot(b + 1);
+    axpy(b);
+  }
+  float4* yp = reinterpret_cast<float4*>(ypart + (long long)cl * n + c0);
+#pragma unroll
+  for (int v = 0; v < AX_V; ++v) {
+    const int idx = tid + v * AX_THREADS;
+    if (idx < w4) yp[idx] = yacc[v];
+  }
+  cluster_sync_all();  // no CTA leaves while its peer may still touch its smem
+}
+
 }  // namespace
+
+size_t atax_ws_bytes(int m, int n) {
+  const size_t onepass = align_up((size_t)74 * n * 4, 256);
+  const size_t twopass = mvmt_ws_bytes(m, n);
+  return (onepass > twopass ? onepass : twopass) + align_up((size_t)m * 4, 256);
+}
+
+cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, float* tmp, void* ws,
+                        cudaStream_t s, int* launches) {
+  float* t = reinterpret_cast<float*>(static_cast<char*>(ws) + (atax_ws_bytes(m, n) - align_up((size_t)m * 4, 256)));
+  if (!tmp) tmp = t;
+  if (n >= 1024 && n <= 2 * AX_SLICE && m >= 2 * 74) {
+    static int ncl = 0;
+    const size_t smem = (size_t)AX_STAGES * AX_SLICE * 4 + sizeof(AxCtl);
+    if (!ncl) {
+      cudaError_t e = cudaFuncSetAttribute(atax_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(148);
+      cfg.blockDim = dim3(AX_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 2; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, atax_onepass_kernel, &cfg) != cudaSuccess || nc <= 0) {
+        cudaGetLastError();
+        nc = 74;
+      }
+      ncl = nc < 74 ? nc : 74;
+    }
+    const int w0 = ((n / 4 + 1) / 2) * 4;
+    float* ypart = static_cast<float*>(ws);
+    atax_onepass_kernel<<<2 * ncl, AX_THREADS, smem, s>>>(A, x, m, n, w0, tmp, ypart);
+    reduce_parts_kernel<<<(n + 255) / 256, 256, 0, s>>>(ypart, ncl, n, nullptr, y);
+    *launches += 2;
+    return cudaGetLastError();
+  }
+  // two passes: tmp = A x, then y = A^T tmp
+  cudaError_t e = launch_rowdot(A, nullptr, x, m, n, 1.f, 0.f, nullptr, tmp, s);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  return launch_mvmt(A, m, n, nullptr, tmp, nullptr, nullptr, nullptr, y, ws, s, launches);
+}
 
 cudaError_t launch_rowdot(const float* A, const float* B, const float* x, int rows, int cols, float alpha, float beta,
                           float* y, float* tmp, cudaStream_t s) {

@@ -234,7 +234,7 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   else if (k == "syrk" && need(2)) take_split(c, d[0], d[1]);
   else if (k == "syr2k" && need(2)) { take_split(c, d[0], d[1]); take_split(c, d[0], d[1]); }
   else if ((k == "covariance" || k == "correlation") && need(2)) ws_stat(c, d[0], d[1]);
-  else if (k == "atax" && need(2)) { c.take<char>(mvmt_ws_bytes(d[0], d[1])); c.take<float>(d[0]); }
+  else if (k == "atax" && need(2)) c.take<char>(atax_ws_bytes(d[0], d[1]));
   else if (k == "bicg" && need(2)) c.take<char>(mvmt_ws_bytes(d[1], d[0]));
   else if (k == "mvt" && need(1)) c.take<char>(mvmt_ws_bytes(d[0], d[0]));
   else if (k == "gesummv" && need(1)) {}
@@ -463,18 +463,10 @@ pb_status pb_atax(int m, int n, const float* A, const float* x, float* y, float*
   ck.arr(tmp, 1, m, true, "tmp", false);
   PB_TRY(ck.finish());
   Carve need(nullptr, 0);
-  need.take<char>(mvmt_ws_bytes(m, n));
-  need.take<float>(m);
+  need.take<char>(atax_ws_bytes(m, n));
   PB_TRY(check_ws(need, ws, ws_bytes));
-  Carve c(ws, ws_bytes);
-  void* mw = c.take<char>(mvmt_ws_bytes(m, n));
-  float* t = c.take<float>(m);
-  if (tmp) t = tmp;
-  cudaStream_t st = S(s);
   int L = 0;
-  PB_CUDA(launch_rowdot(A, nullptr, x, m, n, 1.f, 0.f, nullptr, t, st));  // tmp = A x
-  ++L;
-  PB_CUDA(launch_mvmt(A, m, n, nullptr, t, nullptr, nullptr, nullptr, y, mw, st, &L));  // y = A^T tmp
+  PB_CUDA(launch_atax(A, x, m, n, y, tmp, ws, S(s), &L));
   g_launches = L;
   return PB_OK;
 }

@@ -78,6 +78,12 @@ cudaError_t launch_mvmt(const float* A, int rows, int cols, const float* v, cons
                         const float* base_row, float* out_row, const float* base_col, float* out_col,
                         void* ws, cudaStream_t s, int* launches);
 
+// atax: single pass (2-CTA cluster, row slice in smem, DSMEM partial-dot exchange)
+// when 1024 <= n <= 32768, else two passes. ws: atax_ws_bytes(m, n).
+size_t atax_ws_bytes(int m, int n);
+cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, float* tmp, void* ws,
+                        cudaStream_t s, int* launches);
+
 // ---- SIMT ablation kernels (k_simt.cu): PAPER.md Listing 8 / Listing 9 -------
 cudaError_t launch_gemm_listing8(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                  const float* B, cudaStream_t s);

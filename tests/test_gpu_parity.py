@@ -171,7 +171,8 @@ def test_covariance_unstructured_ragged():
 
 
 # ------------------------------------------------------------------ matrix-vector
-@pytest.mark.parametrize("m,n", [(1, 4), (7, 8), (257, 516), (1000, 2052), (4096, 4096), (3001, 5000)])
+@pytest.mark.parametrize("m,n", [(1, 4), (7, 8), (257, 516), (1000, 2052), (4096, 4096), (3001, 5000),
+                                 (150, 32768), (5000, 1024), (148, 1028), (2000, 32764)])
 def test_atax(m, n):
     _ok(P.check_atax(m, n))
 
@@ -189,6 +190,17 @@ def test_mvt(n):
 @pytest.mark.parametrize("n", [4, 8, 132, 516, 2052, 4096])
 def test_gesummv(n):
     _ok(P.check_gesummv(n))
+
+
+def test_atax_onepass_deterministic_and_tmp_optional():
+    m, n = 3000, 8192
+    A, x = P.dev(P.H(m, n, 1)), P.dev(P.H(1, n, 6)[0])
+    ys = []
+    for tmp in (None, torch.empty(m, device="cuda")):
+        y = torch.empty(n, device="cuda")
+        pb.pb_atax(m, n, A, x, y, tmp)
+        ys.append(P.host(y))
+    assert np.array_equal(ys[0], ys[1])
 
 
 def test_matvec_deterministic_P32():
