@@ -31,34 +31,55 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X,
 }
 
 // out[c][r] = split(f(X[r][c])) with f(x) = ((double)x - mean[c]) * inv[c] when mean != null.
+// 64 x 64 tile per CTA: float4 loads of X rows, padded smem transpose, float4
+// stores of the hi / lo rows (output pitch ldo is a multiple of 4).
 __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ X, int rows, int cols, int ldx,
                                                       float* __restrict__ hiT, float* __restrict__ loT, int ldo,
                                                       const double* __restrict__ mean,
                                                       const double* __restrict__ inv) {
-  __shared__ float tile[32][33];
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
-  for (int k = ty; k < 32; k += 8) {
-    const int r = r0 + k, c = c0 + tx;
-    float v = 0.f;
+  __shared__ float tile[64][65];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int c = c0 + 4 * tx;
+  double mu[4] = {0, 0, 0, 0}, sc[4] = {1, 1, 1, 1};
+  if (mean && c < cols) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      mu[u] = mean[c + u];
+      if (inv) sc[u] = inv[c + u];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int rl = ty + 16 * k, r = r0 + rl;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < rows && c < cols) {
-      v = X[(long long)r * ldx + c];
+      v = *reinterpret_cast<const float4*>(X + (long long)r * ldx + c);
       if (mean) {
-        double d = (double)v - mean[c];
-        if (inv) d *= inv[c];
-        v = (float)d;
+        v.x = (float)(((double)v.x - mu[0]) * sc[0]);
+        v.y = (float)(((double)v.y - mu[1]) * sc[1]);
+        v.z = (float)(((double)v.z - mu[2]) * sc[2]);
+        v.w = (float)(((double)v.w - mu[3]) * sc[3]);
       }
     }
-    tile[k][tx] = v;
+    tile[rl][4 * tx + 0] = v.x;
+    tile[rl][4 * tx + 1] = v.y;
+    tile[rl][4 * tx + 2] = v.z;
+    tile[rl][4 * tx + 3] = v.w;
   }
   __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int c = c0 + k, r = r0 + tx;  // output row c, output col r
-    if (c < cols && r < rows) {
-      float h, l;
-      split3x(tile[tx][k], h, l);
-      hiT[(long long)c * ldo + r] = h;
-      loT[(long long)c * ldo + r] = l;
+  const int r = r0 + 4 * tx;  // first of 4 output columns (input rows) of this thread
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int cl = ty + 16 * k;  // output row within the tile (input column)
+    if (c0 + cl < cols && r < rows) {
+      float4 h, l;
+      split3x(tile[4 * tx + 0][cl], h.x, l.x);
+      split3x(tile[4 * tx + 1][cl], h.y, l.y);
+      split3x(tile[4 * tx + 2][cl], h.z, l.z);
+      split3x(tile[4 * tx + 3][cl], h.w, l.w);
+      *reinterpret_cast<float4*>(hiT + (long long)(c0 + cl) * ldo + r) = h;
+      *reinterpret_cast<float4*>(loT + (long long)(c0 + cl) * ldo + r) = l;
     }
   }
 }
@@ -78,7 +99,7 @@ cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi,
 
 cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* hiT, float* loT, int ldo,
                            const double* mean, const double* inv, cudaStream_t s) {
-  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  dim3 grid((cols + 63) / 64, (rows + 63) / 64);
   split_t_kernel<<<grid, 256, 0, s>>>(X, rows, cols, ldx, hiT, loT, ldo, mean, inv);
   return cudaGetLastError();
 }
