@@ -198,8 +198,8 @@ constexpr int AX_WARPS = AX_THREADS / 32;
 struct __align__(16) AxCtl {
   uint64_t full[AX_STAGES];   // slice landed (tx bytes)
   uint64_t empty[AX_STAGES];  // 16 compute warps done with the slice
-  uint64_t dotb[AX_RED];      // 16 warp partials of row b written
   uint64_t red[AX_RED];       // both CTAs' partials of row b written (cluster scope)
+  unsigned cnt[AX_RED];       // warps that have posted their partial of row b
   float part[AX_RED][2];
   float wred[AX_RED][AX_WARPS];
 };
@@ -225,8 +225,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_BLOCK, 1)
       mbar_init(&ctl->empty[s], AX_WARPS);
     }
     for (int s = 0; s < AX_RED; ++s) {
-      mbar_init(&ctl->dotb[s], AX_WARPS);
       mbar_init(&ctl->red[s], 2);
+      ctl->cnt[s] = 0;
     }
     fence_mbar_init();
   }
@@ -271,20 +271,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_BLOCK, 1)
       }
       p = warp_sum(p);
       if (lane == 0) {
-        ctl->wred[slot][warp] = p;
-        mbar_arrive(&ctl->dotb[slot]);
-      }
-      if (tid == 0) {  // CTA partial -> both CTAs of the pair
-        mbar_wait(&ctl->dotb[slot], (uint32_t)(b / AX_RED) & 1u);
-        float q = 0.f;
+        // The LAST warp to post its partial forms the CTA partial (no warp waits).
+        volatile float* wr = ctl->wred[slot];
+        wr[warp] = p;
+        __threadfence_block();
+        if (atomicAdd(&ctl->cnt[slot], 1u) == AX_WARPS - 1) {
+          __threadfence_block();
+          atomicExch(&ctl->cnt[slot], 0u);  // before this row's send, hence before any post of row b+4
+          float q = 0.f;
 #pragma unroll
-        for (int k = 0; k < AX_WARPS; ++k) q += ctl->wred[slot][k];
-        const uint32_t poff = (uint32_t)(slot * 2 + rank) * 4u;
-        const uint32_t roff = (uint32_t)slot * 8u;
-        st_cluster_f32(map_peer(part0 + poff, rank), q);
-        st_cluster_f32(map_peer(part0 + poff, peer), q);
-        mbar_arrive_cluster(map_peer(red0 + roff, rank));
-        mbar_arrive_cluster(map_peer(red0 + roff, peer));
+          for (int k = 0; k < AX_WARPS; ++k) q += wr[k];  // fixed order
+          const uint32_t poff = (uint32_t)(slot * 2 + rank) * 4u;
+          const uint32_t roff = (uint32_t)slot * 8u;
+          st_cluster_f32(map_peer(part0 + poff, rank), q);
+          st_cluster_f32(map_peer(part0 + poff, peer), q);
+          mbar_arrive_cluster(map_peer(red0 + roff, rank));
+          mbar_arrive_cluster(map_peer(red0 + roff, peer));
+        }
       }
     };
     auto axpy = [&](int b) {

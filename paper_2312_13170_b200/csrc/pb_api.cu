@@ -183,6 +183,9 @@ pb_status cuda_check(cudaError_t e, const char* what) {
 
 inline cudaStream_t S(pb_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Below this many multiply-adds pb_gemm runs the single-launch SIMT kernel.
+constexpr long long SMALL_GEMM_MACS = 1ll << 21;
+
 // core sequences (validated arguments) ---------------------------------------
 pb_status run_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A, const float* B,
                    const WsGemm& w, cudaStream_t s, int* L) {
@@ -258,6 +261,14 @@ pb_status pb_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, con
   Carve need(nullptr, 0);
   ws_gemm(need, ni, nj, nk);
   PB_TRY(check_ws(need, ws, ws_bytes));
+  if ((long long)ni * nj * nk <= SMALL_GEMM_MACS) {
+    // Launch-latency regime (e.g. the N = 128 config: 2 MFMA): one launch of the
+    // paper's own loop-internalised kernel (Listing 9 + register accumulation)
+    // beats split + tensor-core GEMM (3 launches). DESIGN.md §8.
+    PB_CUDA(launch_gemm_listing9_reg(ni, nj, nk, alpha, beta, C, A, B, S(s)));
+    g_launches = 1;
+    return PB_OK;
+  }
   Carve c(ws, ws_bytes);
   WsGemm w = ws_gemm(c, ni, nj, nk);
   int L = 0;

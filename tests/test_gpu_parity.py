@@ -37,7 +37,7 @@ def test_pbgen_device_matches_host_bitwise():
 
 
 # ------------------------------------------------------------------ gemm family
-@pytest.mark.parametrize("ni,nj,nk", [(128, 128, 32), (128, 128, 128), (7, 4, 4), (129, 132, 260),
+@pytest.mark.parametrize("ni,nj,nk", [(128, 128, 32), (128, 128, 128), (7, 4, 4), (129, 132, 260), (130, 132, 128),
                                       (300, 516, 388), (1000, 1024, 1000), (640, 384, 2052)])
 def test_gemm(ni, nj, nk):
     _ok(P.check_gemm(ni, nj, nk))
