@@ -187,24 +187,20 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
 // dot(b+1) is issued before axpy(b), hiding the DSMEM round trip. y_acc (the
 // loop-carried reduction) lives in registers; the per-cluster
 // partial y vectors are summed by reduce_parts_kernel in a fixed order.
-constexpr int AX_THREADS = 512;                       // compute threads (16 warps)
-constexpr int AX_BLOCK = AX_THREADS + 32;             // + 1 producer warp
+constexpr int AX_THREADS = 512;
 constexpr int AX_V = 8;                               // float4 per thread per slice
 constexpr int AX_SLICE = AX_THREADS * AX_V * 4;       // 16384 floats = 64 KiB
 constexpr int AX_STAGES = 3;
 constexpr int AX_RED = 4;  // partial slots: a peer's dot(b+4) can only start after our axpy(b)
-constexpr int AX_WARPS = AX_THREADS / 32;
 
 struct __align__(16) AxCtl {
-  uint64_t full[AX_STAGES];   // slice landed (tx bytes)
-  uint64_t empty[AX_STAGES];  // 16 compute warps done with the slice
-  uint64_t red[AX_RED];       // both CTAs' partials of row b written (cluster scope)
-  unsigned cnt[AX_RED];       // warps that have posted their partial of row b
+  uint64_t full[AX_STAGES];
+  uint64_t red[AX_RED];
   float part[AX_RED][2];
-  float wred[AX_RED][AX_WARPS];
+  float wred[AX_THREADS / 32];
 };
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_BLOCK, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
     atax_onepass_kernel(const float* __restrict__ A, const float* __restrict__ x, int m, int n, int w0,
                         float* __restrict__ tmp, float* __restrict__ ypart) {
   extern __shared__ __align__(128) uint8_t sm[];
@@ -220,107 +216,89 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_BLOCK, 1)
   const int nb = r1 - r0;
 
   if (tid == 0) {
-    for (int s = 0; s < AX_STAGES; ++s) {
-      mbar_init(&ctl->full[s], 1);
-      mbar_init(&ctl->empty[s], AX_WARPS);
-    }
-    for (int s = 0; s < AX_RED; ++s) {
-      mbar_init(&ctl->red[s], 2);
-      ctl->cnt[s] = 0;
-    }
+    for (int s = 0; s < AX_STAGES; ++s) mbar_init(&ctl->full[s], 1);
+    for (int s = 0; s < AX_RED; ++s) mbar_init(&ctl->red[s], 2);
     fence_mbar_init();
   }
   cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
 
-  if (warp == AX_WARPS) {
-    // ---------------- producer warp: 1-D bulk copies of row slices into the ring
-    if (lane == 0) {
-      for (int b = 0; b < nb; ++b) {
-        const int s = b % AX_STAGES;
-        if (b >= AX_STAGES) mbar_wait(&ctl->empty[s], (uint32_t)(b / AX_STAGES - 1) & 1u);
-        mbar_arrive_expect_tx(&ctl->full[s], (uint32_t)w * 4u);
-        if (w > 0)
-          bulk_g2s(stage_buf + (size_t)s * AX_SLICE, A + (long long)(r0 + b) * n + c0, (uint32_t)w * 4u,
-                   &ctl->full[s]);
-      }
-    }
-  } else {
-    // ---------------- 16 compute warps
-    float4 xv[AX_V], yacc[AX_V];
-    const float4* x4 = reinterpret_cast<const float4*>(x + c0);
+  float4 xv[AX_V], yacc[AX_V];
+  const float4* x4 = reinterpret_cast<const float4*>(x + c0);
 #pragma unroll
-    for (int v = 0; v < AX_V; ++v) {
-      const int idx = tid + v * AX_THREADS;
-      xv[v] = idx < w4 ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
-      yacc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    const uint32_t red0 = smem_u32(&ctl->red[0]);
-    const uint32_t part0 = smem_u32(&ctl->part[0][0]);
-    auto dot = [&](int b) {
-      const int s = b % AX_STAGES, slot = b % AX_RED;
-      mbar_wait(&ctl->full[s], (uint32_t)(b / AX_STAGES) & 1u);
-      const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)s * AX_SLICE);
-      float p = 0.f;
-#pragma unroll
-      for (int v = 0; v < AX_V; ++v) {
-        const int idx = tid + v * AX_THREADS;
-        if (idx < w4) {
-          const float4 a = row[idx];
-          p += a.x * xv[v].x + a.y * xv[v].y + a.z * xv[v].z + a.w * xv[v].w;
-        }
-      }
-      p = warp_sum(p);
-      if (lane == 0) {
-        // The LAST warp to post its partial forms the CTA partial (no warp waits).
-        volatile float* wr = ctl->wred[slot];
-        wr[warp] = p;
-        __threadfence_block();
-        if (atomicAdd(&ctl->cnt[slot], 1u) == AX_WARPS - 1) {
-          __threadfence_block();
-          atomicExch(&ctl->cnt[slot], 0u);  // before this row's send, hence before any post of row b+4
-          float q = 0.f;
-#pragma unroll
-          for (int k = 0; k < AX_WARPS; ++k) q += wr[k];  // fixed order
-          const uint32_t poff = (uint32_t)(slot * 2 + rank) * 4u;
-          const uint32_t roff = (uint32_t)slot * 8u;
-          st_cluster_f32(map_peer(part0 + poff, rank), q);
-          st_cluster_f32(map_peer(part0 + poff, peer), q);
-          mbar_arrive_cluster(map_peer(red0 + roff, rank));
-          mbar_arrive_cluster(map_peer(red0 + roff, peer));
-        }
-      }
-    };
-    auto axpy = [&](int b) {
-      const int slot = b % AX_RED;
-      mbar_wait_cluster(&ctl->red[slot], (uint32_t)(b / AX_RED) & 1u);
-      const float t = ctl->part[slot][0] + ctl->part[slot][1];  // same order in both CTAs
-      if (tmp && rank == 0 && tid == 0) tmp[r0 + b] = t;
-      const int s = b % AX_STAGES;
-      const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)s * AX_SLICE);
-#pragma unroll
-      for (int v = 0; v < AX_V; ++v) {
-        const int idx = tid + v * AX_THREADS;
-        if (idx < w4) {
-          const float4 a = row[idx];
-          yacc[v].x += t * a.x; yacc[v].y += t * a.y; yacc[v].z += t * a.z; yacc[v].w += t * a.w;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->empty[s]);  // this warp is done with the slice
-    };
-    if (nb > 0) dot(0);
-    for (int b = 0; b < nb; ++b) {
-      if (b + 1 < nb) dot(b + 1);
-      axpy(b);
-    }
-    float4* yp = reinterpret_cast<float4*>(ypart + (long long)cl * n + c0);
-#pragma unroll
-    for (int v = 0; v < AX_V; ++v) {
-      const int idx = tid + v * AX_THREADS;
-      if (idx < w4) yp[idx] = yacc[v];
-    }
+  for (int v = 0; v < AX_V; ++v) {
+    const int idx = tid + v * AX_THREADS;
+    xv[v] = idx < w4 ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    yacc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  __syncwarp();
+  auto issue = [&](int b) {  // thread 0: row b's slice -> stage b % STAGES
+    const int s = b % AX_STAGES;
+    mbar_arrive_expect_tx(&ctl->full[s], (uint32_t)w * 4u);
+    if (w > 0) bulk_g2s(stage_buf + (size_t)s * AX_SLICE, A + (long long)(r0 + b) * n + c0, (uint32_t)w * 4u,
+                        &ctl->full[s]);
+  };
+  if (tid == 0)
+    for (int b = 0; b < AX_STAGES && b < nb; ++b) issue(b);
+
+  const uint32_t red0 = smem_u32(&ctl->red[0]);
+  const uint32_t part0 = smem_u32(&ctl->part[0][0]);
+  auto dot = [&](int b) {
+    const int s = b % AX_STAGES;
+    mbar_wait(&ctl->full[s], (uint32_t)(b / AX_STAGES) & 1u);
+    const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)s * AX_SLICE);
+    float p = 0.f;
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const int idx = tid + v * AX_THREADS;
+      if (idx < w4) {
+        const float4 a = row[idx];
+        p += a.x * xv[v].x + a.y * xv[v].y + a.z * xv[v].z + a.w * xv[v].w;
+      }
+    }
+    p = warp_sum(p);
+    if (lane == 0) ctl->wred[warp] = p;
+    __syncthreads();
+    if (tid == 0) {
+      float q = 0.f;
+#pragma unroll
+      for (int k = 0; k < AX_THREADS / 32; ++k) q += ctl->wred[k];
+      const int slot = b % AX_RED;
+      const uint32_t poff = (uint32_t)(slot * 2 + rank) * 4u;
+      const uint32_t roff = (uint32_t)slot * 8u;
+      st_cluster_f32(map_peer(part0 + poff, rank), q);
+      st_cluster_f32(map_peer(part0 + poff, peer), q);
+      mbar_arrive_cluster(map_peer(red0 + roff, rank));
+      mbar_arrive_cluster(map_peer(red0 + roff, peer));
+    }
+  };
+  auto axpy = [&](int b) {
+    const int slot = b % AX_RED;
+    mbar_wait_cluster(&ctl->red[slot], (uint32_t)(b / AX_RED) & 1u);
+    const float t = ctl->part[slot][0] + ctl->part[slot][1];
+    if (tmp && rank == 0 && tid == 0) tmp[r0 + b] = t;
+    const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)(b % AX_STAGES) * AX_SLICE);
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const int idx = tid + v * AX_THREADS;
+      if (idx < w4) {
+        const float4 a = row[idx];
+        yacc[v].x += t * a.x; yacc[v].y += t * a.y; yacc[v].z += t * a.z; yacc[v].w += t * a.w;
+      }
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0 && b + AX_STAGES < nb) issue(b + AX_STAGES);
+  };
+
+  if (nb > 0) dot(0);
+  for (int b = 0; b < nb; ++b) {
+    if (b + 1 < nb) dot(b + 1);
+    axpy(b);
+  }
+  float4* yp = reinterpret_cast<float4*>(ypart + (long long)cl * n + c0);
+#pragma unroll
+  for (int v = 0; v < AX_V; ++v) {
+    const int idx = tid + v * AX_THREADS;
+    if (idx < w4) yp[idx] = yacc[v];
+  }
   cluster_sync_all();  // no CTA leaves while its peer may still touch its smem
 }
 
@@ -344,7 +322,7 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
       if (e != cudaSuccess) return e;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(148);
-      cfg.blockDim = dim3(AX_BLOCK);
+      cfg.blockDim = dim3(AX_THREADS);
       cfg.dynamicSmemBytes = smem;
       cudaLaunchAttribute at;
       at.id = cudaLaunchAttributeClusterDimension;
@@ -360,7 +338,7 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
     }
     const int w0 = ((n / 4 + 1) / 2) * 4;
     float* ypart = static_cast<float*>(ws);
-    atax_onepass_kernel<<<2 * ncl, AX_BLOCK, smem, s>>>(A, x, m, n, w0, tmp, ypart);
+    atax_onepass_kernel<<<2 * ncl, AX_THREADS, smem, s>>>(A, x, m, n, w0, tmp, ypart);
     reduce_parts_kernel<<<(n + 255) / 256, 256, 0, s>>>(ypart, ncl, n, nullptr, y);
     *launches += 2;
     return cudaGetLastError();
