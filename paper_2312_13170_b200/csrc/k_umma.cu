@@ -17,6 +17,12 @@
 // Precision: x = hi + lo with hi = tf32_rna(x), lo = tf32_rna(x - hi) (split
 // done by k_split.cu); acc += a_hi*b_hi + a_hi*b_lo + a_lo*b_hi (lo*lo dropped).
 //
+// Two variants (template CG): CG = 1, one CTA per 128x128 tile; CG = 2, an SM
+// pair (2-CTA cluster, tcgen05 cta_group::2) per 256x128 tile: each CTA stages
+// its 128 rows of A and HALF of B (64 rows), the leader CTA issues M=256 MMAs
+// that read both CTAs' smem, and each CTA's TMEM holds its 128 output rows.
+// Per-SM operand traffic drops from 64 KiB to 48 KiB per k-block.
+//
 // CTA layout (192 threads, 1 CTA/SM, persistent over tiles):
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocator + MMA issuer (one lane)
@@ -28,6 +34,10 @@
 // alternate per 512-wide K chunk; the epilogue promotes each chunk into fp32
 // registers (RN) so the tensor core's truncating accumulate cannot bias long K.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "pb_device.cuh"
 #include "pb_internal.h"
@@ -35,16 +45,31 @@
 namespace pb {
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 128;
+constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;
-constexpr int STAGES = 3;
-constexpr int TILE_BYTES = BM * BK * 4;          // 16 KiB per operand tile
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;      // A_hi, A_lo, B_hi, B_lo
-constexpr int NUM_THREADS = 192;
-constexpr int GROUP_M = 8;                       // tile-rows per raster group (L2 reuse)
-constexpr uint32_t TMEM_COLS = 4 * BN;  // 2 slots x {big, small} accumulators = 512 columns
-constexpr int CHUNK_KB = 16;            // k-blocks (16 x 32 = 512 of K) per TMEM partial sum
+constexpr int GROUP_M = 8;  // tile-rows per raster group (L2 reuse)
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int A_TILE = BM * BK * 4;  // 16 KiB
+constexpr int EPI_COLS = 128;        // accumulator columns (fp32 registers) per epilogue thread
+
+// Tile configurations. BN = MMA N (output columns per tile). With BN = 128 each
+// slot holds separate `big` (a_hi b_hi) and `small` (cross terms) accumulators;
+// with BN = 256 a slot is one 256-column accumulator (TMEM is 512 columns) and
+// chunks are shorter. Smem read demand per MMA flop halves from BN=128 to 256,
+// which is what bounds the tf32 SS-MMA rate.
+template <int CG, int BN>
+struct Cfg {
+  static constexpr int B_ROWS = BN / CG;                  // B rows staged by each CTA
+  static constexpr int B_TILE = B_ROWS * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+  static constexpr int STAGES = (196 * 1024) / STAGE_BYTES;
+  static constexpr int PAIR_M = BM * CG;                  // output rows per tile
+  static constexpr bool SPLIT_ACC = BN == 128;            // separate big / small accumulators
+  static constexpr int SLOT_COLS = SPLIT_ACC ? 2 * BN : BN;
+  static constexpr int CHUNK_KB = SPLIT_ACC ? 16 : 8;     // k-blocks per TMEM partial sum (512 / 256 of K)
+  static constexpr int EPI_WARPS = 4 * (BN / EPI_COLS);
+  static constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+};
 
 struct Params {
   int M, N, K, npairs, nkb;  // nkb = k-blocks per pair
@@ -58,48 +83,45 @@ struct Params {
   float* split_hi;
   float* split_lo;
   int ld_split;
-  int tm0, tm1, tiles_n;
+  int tm0, tm1, tiles_n, ratio;  // ratio = tile rows / BN (CG)
   long long num_tiles;
 };
 
 struct __align__(8) Ctl {
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
+  uint64_t full[8];
+  uint64_t empty[8];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ long long tri_count(long long r) { return r * (r + 1) / 2; }
+// number of column tiles in tile-row tm (lower triangle: tiles touching j <= i)
+__device__ __forceinline__ int row_tiles(const Params& p, int tm) {
+  if (!(p.flags & EPI_TRI)) return p.tiles_n;
+  return min(p.ratio * (tm + 1), p.tiles_n);
+}
 
 // Tile t of the persistent schedule -> (tm, tn). Raster: groups of GROUP_M
 // tile-rows; inside a group tn is the outer index so CTAs running together
-// share B panels (and the GROUP_M A panels) in L2.
+// share B panels (and the group's A panels) in L2. In the lower-triangle mode
+// column tn holds the rows tm >= tn / ratio of the group.
 __device__ void tile_coords(const Params& p, long long t, int& tm, int& tn) {
-  const bool tri = (p.flags & EPI_TRI) != 0;
   int g0 = p.tm0;
   for (;;) {
-    int g1 = min(g0 + GROUP_M, p.tm1);
-    long long cnt = tri ? (tri_count(g1) - tri_count(g0)) : (long long)(g1 - g0) * p.tiles_n;
+    const int g1 = min(g0 + GROUP_M, p.tm1);
+    long long cnt = 0;
+    for (int r = g0; r < g1; ++r) cnt += row_tiles(p, r);
     if (t < cnt || g1 >= p.tm1) {
-      int gs = g1 - g0;
-      if (!tri) {
-        tn = (int)(t / gs);
-        tm = g0 + (int)(t % gs);
-      } else if (t < (long long)g0 * gs) {  // columns left of the group's diagonal block: full height
-        tn = (int)(t / gs);
-        tm = g0 + (int)(t % gs);
-      } else {                              // diagonal block: column c has rows [c, g1)
-        t -= (long long)g0 * gs;
-        int c = g0;
-        while (t >= g1 - c) {
-          t -= g1 - c;
-          ++c;
+      for (int c = 0;; ++c) {
+        const int first = (p.flags & EPI_TRI) ? max(g0, c / p.ratio) : g0;
+        const int rows = g1 - first;
+        if (t < rows) {
+          tn = c;
+          tm = first + (int)t;
+          return;
         }
-        tn = c;
-        tm = c + (int)t;
+        t -= rows;
       }
-      return;
     }
     t -= cnt;
     g0 = g1;
@@ -110,18 +132,83 @@ __device__ __forceinline__ void store4(float* p, float a, float b, float c, floa
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
 }
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// ---- cta_group-specific PTX
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* dst, uint32_t ncols) {
+  if constexpr (CG == 1) {
+    tmem_alloc(dst, ncols);
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) {
+  if constexpr (CG == 1)
+    tmem_dealloc(taddr, ncols);
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void mma_cg(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (CG == 1) {
+    mma_tf32(d, a, b, idesc, acc);
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+// Commit this thread's MMAs to `bar` (CG=2: the barrier at the same offset in both CTAs).
+template <int CG>
+__device__ __forceinline__ void commit_cg(uint64_t* bar) {
+  if constexpr (CG == 1) {
+    mma_commit(bar);
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  }
+}
+// TMA tile load; CG=2: completion is counted on the LEADER CTA's barrier.
+template <int CG>
+__device__ __forceinline__ void tma_load_cg(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1) {
+  if constexpr (CG == 1) {
+    tma_load_2d(m, bar, dst, c0, c1);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+  }
+}
+
+template <int CG, int BN>
+__global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     umma3x_kernel(const __grid_constant__ CUtensorMap a0h, const __grid_constant__ CUtensorMap a0l,
                   const __grid_constant__ CUtensorMap b0h, const __grid_constant__ CUtensorMap b0l,
                   const __grid_constant__ CUtensorMap a1h, const __grid_constant__ CUtensorMap a1l,
                   const __grid_constant__ CUtensorMap b1h, const __grid_constant__ CUtensorMap b1l,
                   const Params p) {
+  using C = Cfg<CG, BN>;
+  constexpr int STAGES = C::STAGES, STAGE_BYTES = C::STAGE_BYTES, B_TILE = C::B_TILE;
+  constexpr int CHUNK_KB = C::CHUNK_KB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + STAGES * STAGE_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const long long tile0 = blockIdx.x / CG, tile_step = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -130,7 +217,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&ctl->tfull[s], 1);
-      mbar_init(&ctl->tempty[s], 4);  // one arrive per epilogue warp
+      mbar_init(&ctl->tempty[s], C::EPI_WARPS * CG);  // one arrive per epilogue warp of every CTA
     }
     fence_mbar_init();
   }
@@ -138,57 +225,62 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&a0h); tma_prefetch(&a0l); tma_prefetch(&b0h); tma_prefetch(&b0l);
     if (p.npairs > 1) { tma_prefetch(&a1h); tma_prefetch(&a1l); tma_prefetch(&b1h); tma_prefetch(&b1l); }
   }
-  if (warp == 1) tmem_alloc(&ctl->tmem_base, TMEM_COLS);
+  if (warp == 1) tmem_alloc_cg<CG>(&ctl->tmem_base, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = ctl->tmem_base;
   const int nkb_total = p.nkb * p.npairs;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (every CTA loads its own A rows and B half)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (long long t = tile0; t < p.num_tiles; t += tile_step) {
         int tm, tn;
         tile_coords(p, t, tm, tn);
+        const int arow = tm * C::PAIR_M + (int)rank * BM;
+        const int brow = tn * BN + (int)rank * C::B_ROWS;
         for (int kb = 0; kb < nkb_total; ++kb) {
           mbar_wait(&ctl->empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           const int pair = kb >= p.nkb;
           const int k = (kb - pair * p.nkb) * BK;
-          mbar_arrive_expect_tx(&ctl->full[stage], STAGE_BYTES);
-          tma_load_2d(pair ? &a1h : &a0h, &ctl->full[stage], st + 0 * TILE_BYTES, k, tm * BM);
-          tma_load_2d(pair ? &a1l : &a0l, &ctl->full[stage], st + 1 * TILE_BYTES, k, tm * BM);
-          tma_load_2d(pair ? &b1h : &b0h, &ctl->full[stage], st + 2 * TILE_BYTES, k, tn * BN);
-          tma_load_2d(pair ? &b1l : &b0l, &ctl->full[stage], st + 3 * TILE_BYTES, k, tn * BN);
+          if (leader) mbar_arrive_expect_tx(&ctl->full[stage], CG * STAGE_BYTES);
+          tma_load_cg<CG>(pair ? &a1h : &a0h, &ctl->full[stage], st, k, arow);
+          tma_load_cg<CG>(pair ? &a1l : &a0l, &ctl->full[stage], st + A_TILE, k, arow);
+          tma_load_cg<CG>(pair ? &b1h : &b0h, &ctl->full[stage], st + 2 * A_TILE, k, brow);
+          tma_load_cg<CG>(pair ? &b1l : &b0l, &ctl->full[stage], st + 2 * A_TILE + B_TILE, k, brow);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (leader CTA) =====================
     // The k-loop of a tile is cut into chunks of CHUNK_KB k-blocks. Each chunk
     // accumulates into one of two TMEM slots; the epilogue warps drain a
     // finished slot into fp32 registers (round-to-nearest adds) while the next
     // chunk runs in the other slot. The tensor-core accumulate truncates, so
     // this bounds the truncation bias to one chunk.
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(BM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int chunk_it = 0;
-      for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (long long t = tile0; t < p.num_tiles; t += tile_step) {
         for (int kb0 = 0; kb0 < nkb_total; kb0 += CHUNK_KB, ++chunk_it) {
           const int slot = chunk_it & 1;
           const uint32_t slot_phase = (chunk_it >> 1) & 1;
-          mbar_wait(&ctl->tempty[slot], slot_phase ^ 1);  // epilogue drained this slot
+          if constexpr (CG == 2)  // every epilogue (both CTAs) drained this slot
+            mbar_wait_cluster(&ctl->tempty[slot], slot_phase ^ 1);
+          else
+            mbar_wait(&ctl->tempty[slot], slot_phase ^ 1);
           tc_fence_after();
-          // `big` takes a_hi*b_hi, `small` the cross terms a_hi*b_lo + a_lo*b_hi
-          // (2^-11 smaller): the small terms are rounded at their own scale.
-          const uint32_t d_big = tmem_base + slot * 2 * BN;
-          const uint32_t d_small = d_big + BN;
+          // BN=128: `big` takes a_hi*b_hi, `small` the cross terms a_hi*b_lo +
+          // a_lo*b_hi (2^-11 smaller), rounded at their own scale.
+          const uint32_t d_big = tmem_base + slot * C::SLOT_COLS;
+          const uint32_t d_small = C::SPLIT_ACC ? d_big + BN : d_big;
           const int kb1 = min(kb0 + CHUNK_KB, nkb_total);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&ctl->full[stage], phase);
@@ -196,60 +288,75 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t ah = umma_desc_k_sw128(st + 0 * TILE_BYTES + kk * 32);
-              const uint64_t al = umma_desc_k_sw128(st + 1 * TILE_BYTES + kk * 32);
-              const uint64_t bh = umma_desc_k_sw128(st + 2 * TILE_BYTES + kk * 32);
-              const uint64_t bl = umma_desc_k_sw128(st + 3 * TILE_BYTES + kk * 32);
+              const uint64_t ah = umma_desc_k_sw128(st + kk * 32);
+              const uint64_t al = umma_desc_k_sw128(st + A_TILE + kk * 32);
+              const uint64_t bh = umma_desc_k_sw128(st + 2 * A_TILE + kk * 32);
+              const uint64_t bl = umma_desc_k_sw128(st + 2 * A_TILE + B_TILE + kk * 32);
               const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
-              mma_tf32(d_small, al, bh, idesc, accum);
-              mma_tf32(d_small, ah, bl, idesc, 1);
-              mma_tf32(d_big, ah, bh, idesc, accum);
+              mma_cg<CG>(d_small, al, bh, idesc, accum);
+              mma_cg<CG>(d_small, ah, bl, idesc, 1);
+              mma_cg<CG>(d_big, ah, bh, idesc, C::SPLIT_ACC ? accum : 1u);
             }
-            mma_commit(&ctl->empty[stage]);  // frees the smem stage when these MMAs finish
+            commit_cg<CG>(&ctl->empty[stage]);  // frees the stage (in both CTAs) when these MMAs finish
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&ctl->tfull[slot]);  // chunk partial sums ready for the epilogue
+          commit_cg<CG>(&ctl->tfull[slot]);  // chunk partial sums ready for the epilogues
         }
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // ===================== epilogue (warps 2..5 of every CTA) =====================
+    const int q = warp & 3;                    // TMEM lane quarter this warp may access
+    const int ch = (warp - 2) / 4;             // which EPI_COLS-wide column half of the tile
+    const int cbase = ch * EPI_COLS;
     const uint32_t flags = p.flags;
     int chunk_it = 0;
-    for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (long long t = tile0; t < p.num_tiles; t += tile_step) {
       int tm, tn;
       tile_coords(p, t, tm, tn);
-      float acc[BN];  // this thread's output row of the tile, fp32 registers
+      float acc[EPI_COLS];  // this thread's row x column-half of the tile, fp32 registers
 #pragma unroll
-      for (int c = 0; c < BN; ++c) acc[c] = 0.f;
+      for (int c = 0; c < EPI_COLS; ++c) acc[c] = 0.f;
       for (int kb0 = 0; kb0 < nkb_total; kb0 += CHUNK_KB, ++chunk_it) {
         const int slot = chunk_it & 1;
         const uint32_t slot_phase = (chunk_it >> 1) & 1;
         mbar_wait(&ctl->tfull[slot], slot_phase);
         tc_fence_after();
         __syncwarp();
-        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + slot * 2 * BN;
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + slot * C::SLOT_COLS + cbase;
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t r[16], rs[16];
+        for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
+          uint32_t r[16];
           tmem_ld16(ta + c0, r);
-          tmem_ld16(ta + BN + c0, rs);
-          tmem_wait_ld();
+          if constexpr (C::SPLIT_ACC) {
+            uint32_t rs[16];
+            tmem_ld16(ta + BN + c0, rs);
+            tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(r[e]) + __uint_as_float(rs[e]);
+            for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(r[e]) + __uint_as_float(rs[e]);
+          } else {
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(r[e]);
+          }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ctl->tempty[slot]);
+        if (lane == 0) {
+          if constexpr (CG == 2)
+            mbar_arrive_cluster(map_peer(smem_u32(&ctl->tempty[slot]), 0));  // leader's barrier
+          else
+            mbar_arrive(&ctl->tempty[slot]);
+        }
       }
-      const int i = tm * BM + q * 32 + lane;  // output row (operand-a space)
+      const int row0 = tm * C::PAIR_M + (int)rank * BM;  // first output row of this CTA
+      const int i = row0 + q * 32 + lane;                // this thread's output row
       const bool row_ok = i < p.M;
-      const bool diag_tile = (flags & EPI_TRI) && tm == tn;
+      const bool diag_tile = (flags & EPI_TRI) && (tn * BN + BN - 1 > row0);  // tile crosses j > i
       const long long orow = (long long)(i - p.out_row0);
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        const int j0 = tn * BN + c0;
+      for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
+        const int j0 = tn * BN + cbase + c0;
         if (row_ok && j0 < p.N) {
           float v[16];
 #pragma unroll
@@ -290,7 +397,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
               }
             }
-          } else {  // lower-triangular diagonal tile: element mask j <= i
+          } else {  // tile crosses the diagonal: element mask j <= i
             if (flags & EPI_OUT) {
               float* op = p.out + orow * p.ldo + j0;
 #pragma unroll
@@ -323,10 +430,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc_cg<CG>(tmem_base, TMEM_COLS);
   }
 }
 
@@ -347,13 +454,13 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// K-major operand (rows x K, pitch ld floats), box = 32 (K) x 128 (rows), 128-B swizzle.
-bool make_map(CUtensorMap* m, const float* base, int rows, int K, int ld) {
+// K-major operand (rows x K, pitch ld floats), box = 32 (K) x box_rows, 128-B swizzle.
+bool make_map(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -370,6 +477,58 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+template <int CG, int BN>
+cudaError_t launch_cg(const GemmDesc& d, Params p, cudaStream_t s, int* launches) {
+  using C = Cfg<CG, BN>;
+  const int tiles_m = (d.M + C::PAIR_M - 1) / C::PAIR_M;
+  p.tiles_n = (d.N + BN - 1) / BN;
+  p.ratio = C::PAIR_M / BN;
+  p.tm0 = d.tm0 * 128 / C::PAIR_M;  // d.tm0 is in 128-row units
+  p.tm1 = d.tm1 < 0 ? tiles_m : (d.tm1 * 128 + C::PAIR_M - 1) / C::PAIR_M;
+  if (p.tm1 > tiles_m) p.tm1 = tiles_m;
+  if (p.tm1 <= p.tm0) return cudaSuccess;
+  long long nt = 0;
+  for (int tm = p.tm0; tm < p.tm1; ++tm)
+    nt += (d.flags & EPI_TRI) ? std::min(p.ratio * (tm + 1), p.tiles_n) : p.tiles_n;
+  p.num_tiles = nt;
+  CUtensorMap maps[8];
+  for (int q = 0; q < 2; ++q) {
+    const SplitOperand& A = d.a[q < d.npairs ? q : 0];
+    const SplitOperand& B = d.b[q < d.npairs ? q : 0];
+    if (!make_map(&maps[4 * q + 0], A.hi, A.rows, A.K, A.ld, BM) ||
+        !make_map(&maps[4 * q + 1], A.lo, A.rows, A.K, A.ld, BM) ||
+        !make_map(&maps[4 * q + 2], B.hi, B.rows, B.K, B.ld, C::B_ROWS) ||
+        !make_map(&maps[4 * q + 3], B.lo, B.rows, B.K, B.ld, C::B_ROWS))
+      return cudaErrorInvalidValue;
+  }
+  const size_t smem = C::STAGES * C::STAGE_BYTES + 1024 + sizeof(Ctl) + 64;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(umma3x_kernel<CG, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const long long max_units = num_sms() / CG;
+  const long long units = p.num_tiles < max_units ? p.num_tiles : max_units;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * CG));
+  cfg.blockDim = dim3(C::NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, umma3x_kernel<CG, BN>, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+                                     maps[6], maps[7], p);
+  if (launches) ++*launches;
+  if (getenv("PB_TRACE"))
+    fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld grid=%lld\n", CG, BN, d.M, d.N, d.K,
+            d.npairs, d.flags, p.num_tiles, units * CG);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
@@ -392,36 +551,22 @@ cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
   p.split_hi = d.split_hi;
   p.split_lo = d.split_lo;
   p.ld_split = d.ld_split;
-  const int tiles_m = (d.M + BM - 1) / BM;
-  p.tiles_n = (d.N + BN - 1) / BN;
-  p.tm0 = d.tm0;
-  p.tm1 = d.tm1 < 0 ? tiles_m : d.tm1;
-  if (p.tm1 <= p.tm0) return cudaSuccess;
-  if (d.flags & EPI_TRI) {
-    p.num_tiles = (long long)p.tm1 * (p.tm1 + 1) / 2 - (long long)p.tm0 * (p.tm0 + 1) / 2;
-  } else {
-    p.num_tiles = (long long)(p.tm1 - p.tm0) * p.tiles_n;
+  // Tile choice: 2-CTA 256x256 tiles (half the smem read traffic per MMA flop)
+  // when they still give >= ~2 waves over the SM pairs; otherwise 2-CTA 256x128;
+  // problems under 256 rows (or odd 128-row band starts) use 1-CTA 128x128.
+  static const int force = getenv("PB_UMMA_TILE") ? atoi(getenv("PB_UMMA_TILE")) : 0;
+  const int rows = d.tm1 < 0 ? d.M : (d.tm1 - d.tm0) * 128;
+  const bool pair_ok = rows >= 256 && (d.tm0 % 2) == 0;
+  long long tiles256 = 0;
+  if (pair_ok) {
+    const int tm = (rows + 255) / 256, tn = (d.N + 255) / 256;
+    tiles256 = (d.flags & EPI_TRI) ? (long long)tm * (tm + 1) / 2 : (long long)tm * tn;
   }
-  CUtensorMap maps[8];
-  for (int q = 0; q < 2; ++q) {
-    const SplitOperand& A = d.a[q < d.npairs ? q : 0];
-    const SplitOperand& B = d.b[q < d.npairs ? q : 0];
-    if (!make_map(&maps[4 * q + 0], A.hi, A.rows, A.K, A.ld) || !make_map(&maps[4 * q + 1], A.lo, A.rows, A.K, A.ld) ||
-        !make_map(&maps[4 * q + 2], B.hi, B.rows, B.K, B.ld) || !make_map(&maps[4 * q + 3], B.lo, B.rows, B.K, B.ld))
-      return cudaErrorInvalidValue;
-  }
-  const size_t smem = STAGES * STAGE_BYTES + 1024 + sizeof(Ctl) + 64;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(umma3x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  long long grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
-  umma3x_kernel<<<(unsigned)grid, NUM_THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
-                                                          maps[6], maps[7], p);
-  if (launches) ++*launches;
-  return cudaGetLastError();
+  int choice = !pair_ok ? 1 : (tiles256 >= 2 * (num_sms() / 2) ? 3 : 2);
+  if (force >= 1 && force <= 3 && (force == 1 || pair_ok)) choice = force;
+  if (choice == 3) return launch_cg<2, 256>(d, p, s, launches);
+  if (choice == 2) return launch_cg<2, 128>(d, p, s, launches);
+  return launch_cg<1, 128>(d, p, s, launches);
 }
 
 }  // namespace pb

@@ -102,7 +102,7 @@ def mm3_rows(ctx, n, E, A, B, Fl, F, C, D, G, ws, K=_pb):
 
 def syrk_rows(ctx, n, m, alpha, beta, C_blk, A, ws, B=None, K=_pb):
     world, rank = _world()
-    r0, r1 = partition(n, world, rank, True, 128, K)
+    r0, r1 = partition(n, world, rank, True, 256, K)
     if r1 <= r0:
         return 0
     if B is None:
