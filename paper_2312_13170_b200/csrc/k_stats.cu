@@ -1,15 +1,9 @@
-// k_stats.cu — S10/S11 of the hot path: column means and standard
+// k_stats.cu — S10-S12 of the hot path: column means and standard
 // deviations for covariance / correlation ("array reduction" opportunities,
 // PAPER.md:542; detect-reduction PAPER.md:344-374: each column sum is a
-// register accumulator, written once per row chunk).
-//
-// Pass  : part[rc][j] = (sum_{i in chunk rc} x[i][j], sum x^2)   fp64, one read of data
-//         (thread = 4 adjacent columns, float4 loads, whole chunk unrolled)
-// Final : one warp per column: lane c sums chunks c, c+32, ... then a fixed
-//         butterfly -> mean[j] = S/float_n;
-//         var[j] = (Q - S*S/float_n)/float_n  (fp64; reading R17 in DESIGN.md)
-//         sd[j] = sqrt(var); sd <= eps -> 1 (reading R5); inv[j] = 1/(sqrt(float_n)*sd)
-// Deterministic (no atomics): every sum has a fixed order.
+// register accumulator) fused with the centring / normalisation and the TF32
+// split of the Gram operand. Variance: (sum x^2 - (sum x) mu) / float_n in fp64
+// (reading R17 in DESIGN.md). Deterministic: every sum has a fixed order.
 #include <math.h>
 
 #include "pb_device.cuh"
@@ -18,88 +12,109 @@
 namespace pb {
 namespace {
 
-constexpr int RC = 16;    // rows per chunk (all loads of a chunk in flight together)
-constexpr int TPB = 256;  // threads per CTA; 4 columns each -> 1024 columns per CTA
+// ------------------------------------------------------------------ fused prep
+// One CTA owns PC = 16 columns of data (n x m) and all n rows:
+//  pass 1: fp64 sums (and sums of squares) of its columns -> mean, stddev (eps
+//          rule), inv = 1/(sqrt(float_n)*sd) (correlation) or 1 (covariance);
+//  pass 2: Xt[c][r] = split(((double)x - mean[c]) * inv[c]) written transposed
+//          (m x ldo, K-major for the Gram core) from 4x4 register transposes, so
+//          every store is a 16-byte piece of a contiguous Xt row.
+// The CTA's 16 x n slab (128 KiB at n = 2048) is re-read in pass 2 from L1/L2.
+constexpr int PC = 16;
+constexpr int PT = 256;
 
-template <bool SQ>
-__global__ void __launch_bounds__(TPB) colsum_kernel(const float* __restrict__ data, int n, int m,
-                                                     double* __restrict__ psum, double* __restrict__ psq) {
-  const int j = (blockIdx.x * TPB + threadIdx.x) * 4;
-  const int r0 = blockIdx.y * RC;
-  if (j >= m) return;
-  const int r1 = min(r0 + RC, n);
-  float4 v[RC];
+template <bool CORR>
+__global__ void __launch_bounds__(PT) stats_split_kernel(const float* __restrict__ data, int n, int m, double float_n,
+                                                         double eps, float* __restrict__ hiT, float* __restrict__ loT,
+                                                         int ldo, float* __restrict__ mean_out,
+                                                         float* __restrict__ sd_out) {
+  __shared__ double red_s[PT / 4][PC], red_q[CORR ? PT / 4 : 1][PC];
+  __shared__ double mu_s[PC], inv_s[PC];
+  const int c0 = blockIdx.x * PC;
+  const int t = threadIdx.x;
+  // ---- pass 1: thread = (column quad cq, row lane rl); rows rl, rl + 64, ...
+  {
+    const int cq = t & 3, rl = t >> 2;
+    const int c = c0 + 4 * cq;
+    double s[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0};
+    if (c < m) {
+#pragma unroll 8
+      for (int r = rl; r < n; r += PT / 4) {
+        const float4 v = *reinterpret_cast<const float4*>(data + (long long)r * m + c);
+        const double a = v.x, b = v.y, cc = v.z, d = v.w;
+        s[0] += a; s[1] += b; s[2] += cc; s[3] += d;
+        if (CORR) { q[0] += a * a; q[1] += b * b; q[2] += cc * cc; q[3] += d * d; }
+      }
+    }
 #pragma unroll
-  for (int k = 0; k < RC; ++k)
-    v[k] = (r0 + k < r1) ? *reinterpret_cast<const float4*>(data + (long long)(r0 + k) * m + j)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-  double s[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int k = 0; k < RC; ++k) {
-    const double a = v[k].x, b = v[k].y, c = v[k].z, d = v[k].w;
-    s[0] += a; s[1] += b; s[2] += c; s[3] += d;
-    if (SQ) { q[0] += a * a; q[1] += b * b; q[2] += c * c; q[3] += d * d; }
+    for (int u = 0; u < 4; ++u) {
+      red_s[rl][4 * cq + u] = s[u];
+      if (CORR) red_q[rl][4 * cq + u] = q[u];
+    }
   }
-  double* ps = psum + (long long)blockIdx.y * m + j;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) ps[u] = s[u];
-  if (SQ) {
-    double* pq = psq + (long long)blockIdx.y * m + j;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) pq[u] = q[u];
+  __syncthreads();
+  if (t < PC) {  // fixed-order column reduction and the per-column statistics
+    double S = 0.0, Q = 0.0;
+    for (int k = 0; k < PT / 4; ++k) {
+      S += red_s[k][t];
+      if (CORR) Q += red_q[k][t];
+    }
+    const double mu = S / float_n;
+    double inv = 1.0;
+    if (c0 + t < m) {
+      if (mean_out) mean_out[c0 + t] = (float)mu;
+      if (CORR) {
+        double var = (Q - S * mu) / float_n;
+        if (var < 0.0) var = 0.0;
+        double sd = sqrt(var);
+        if (sd <= eps) sd = 1.0;
+        inv = 1.0 / (sqrt(float_n) * sd);
+        if (sd_out) sd_out[c0 + t] = (float)sd;
+      }
+    }
+    mu_s[t] = mu;
+    inv_s[t] = inv;
   }
-}
-
-template <bool SQ>
-__global__ void __launch_bounds__(256) finalize_kernel(const double* __restrict__ psum, const double* __restrict__ psq,
-                                                       int nchunks, int m, double float_n, double eps,
-                                                       double* __restrict__ mean, double* __restrict__ inv,
-                                                       float* __restrict__ mean_out, float* __restrict__ sd_out) {
-  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (j >= m) return;
-  double s = 0.0, q = 0.0;
-  for (int c = lane; c < nchunks; c += 32) {
-    s += psum[(long long)c * m + j];
-    if (SQ) q += psq[(long long)c * m + j];
-  }
-  s = warp_sum_d(s);
-  if (SQ) q = warp_sum_d(q);
-  if (lane == 0) {
-    const double mu = s / float_n;
-    mean[j] = mu;
-    if (mean_out) mean_out[j] = (float)mu;
-    if (SQ) {
-      double var = (q - s * mu) / float_n;
-      if (var < 0.0) var = 0.0;
-      double sd = sqrt(var);
-      if (sd <= eps) sd = 1.0;
-      inv[j] = 1.0 / (sqrt(float_n) * sd);
-      if (sd_out) sd_out[j] = (float)sd;
+  __syncthreads();
+  // ---- pass 2: 4x4 blocks (4 rows x 4 columns); lanes walk consecutive row quads
+  const int nrq = (n + 3) / 4;
+  const int nblk = nrq * (PC / 4);
+  for (int b = t; b < nblk; b += PT) {
+    const int cq = b / nrq, rq = b - cq * nrq;
+    const int c = c0 + 4 * cq, r = 4 * rq;
+    if (c >= m) continue;
+    float x[4][4];  // x[row u][col v]
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r + u < n) v = *reinterpret_cast<const float4*>(data + (long long)(r + u) * m + c);
+      x[u][0] = v.x; x[u][1] = v.y; x[u][2] = v.z; x[u][3] = v.w;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double mu = mu_s[4 * cq + v], inv = inv_s[4 * cq + v];
+      float h[4], l[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float val = (r + u < n) ? (float)(((double)x[u][v] - mu) * inv) : 0.f;
+        split3x(val, h[u], l[u]);
+      }
+      const long long o = (long long)(c + v) * ldo + r;
+      *reinterpret_cast<float4*>(hiT + o) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(loT + o) = make_float4(l[0], l[1], l[2], l[3]);
     }
   }
 }
 
 }  // namespace
 
-size_t stats_part_doubles(int m, int n) { return 2 * (size_t)((n + RC - 1) / RC) * (size_t)m; }
-
-cudaError_t launch_colstats(const float* data, int n, int m, double float_n, double eps, bool want_sd,
-                            double* part, double* mean, double* inv, float* mean_out, float* sd_out,
-                            cudaStream_t s, int* launches) {
-  const int nchunks = (n + RC - 1) / RC;
-  double* psum = part;
-  double* psq = part + (size_t)nchunks * m;
-  dim3 grid((m / 4 + TPB - 1) / TPB, nchunks);
-  dim3 fgrid((m + 7) / 8);
-  if (want_sd) {
-    colsum_kernel<true><<<grid, TPB, 0, s>>>(data, n, m, psum, psq);
-    finalize_kernel<true><<<fgrid, 256, 0, s>>>(psum, psq, nchunks, m, float_n, eps, mean, inv, mean_out, sd_out);
-  } else {
-    colsum_kernel<false><<<grid, TPB, 0, s>>>(data, n, m, psum, psq);
-    finalize_kernel<false><<<fgrid, 256, 0, s>>>(psum, psq, nchunks, m, float_n, eps, mean, inv, mean_out, sd_out);
-  }
-  *launches += 2;
+cudaError_t launch_stats_split(const float* data, int n, int m, double float_n, double eps, bool corr, float* hiT,
+                               float* loT, int ldo, float* mean_out, float* sd_out, cudaStream_t s) {
+  const int grid = (m + PC - 1) / PC;
+  if (corr)
+    stats_split_kernel<true><<<grid, PT, 0, s>>>(data, n, m, float_n, eps, hiT, loT, ldo, mean_out, sd_out);
+  else
+    stats_split_kernel<false><<<grid, PT, 0, s>>>(data, n, m, float_n, eps, hiT, loT, ldo, mean_out, sd_out);
   return cudaGetLastError();
 }
 

@@ -85,6 +85,9 @@ struct Params {
   int ld_split;
   int tm0, tm1, tiles_n, ratio;  // ratio = tile rows / BN (CG)
   long long num_tiles;
+  int ksplit;                    // K splits per tile (split-K); work unit = (tile, split)
+  float* part;                   // split-K partial tiles [unit][CG][128][BN]
+  unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
 };
 
 struct __align__(8) Ctl {
@@ -93,6 +96,7 @@ struct __align__(8) Ctl {
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
+  uint32_t last_flag;
 };
 
 // number of column tiles in tile-row tm (lower triangle: tiles touching j <= i)
@@ -231,18 +235,21 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = ctl->tmem_base;
   const int nkb_total = p.nkb * p.npairs;
+  const long long num_units = p.num_tiles * p.ksplit;
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA loads its own A rows and B half)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (long long t = tile0; t < p.num_tiles; t += tile_step) {
+      for (long long u = tile0; u < num_units; u += tile_step) {
         int tm, tn;
-        tile_coords(p, t, tm, tn);
+        tile_coords(p, u / p.ksplit, tm, tn);
         const int arow = tm * C::PAIR_M + (int)rank * BM;
         const int brow = tn * BN + (int)rank * C::B_ROWS;
-        for (int kb = 0; kb < nkb_total; ++kb) {
+        const int ks = (int)(u % p.ksplit);
+        const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
+        for (int kb = kbA; kb < kbB; ++kb) {
           mbar_wait(&ctl->empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           const int pair = kb >= p.nkb;
@@ -268,8 +275,10 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int chunk_it = 0;
-      for (long long t = tile0; t < p.num_tiles; t += tile_step) {
-        for (int kb0 = 0; kb0 < nkb_total; kb0 += CHUNK_KB, ++chunk_it) {
+      for (long long u = tile0; u < num_units; u += tile_step) {
+        const int ks = (int)(u % p.ksplit);
+        const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
+        for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
           const int slot = chunk_it & 1;
           const uint32_t slot_phase = (chunk_it >> 1) & 1;
           if constexpr (CG == 2)  // every epilogue (both CTAs) drained this slot
@@ -281,7 +290,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           // a_lo*b_hi (2^-11 smaller), rounded at their own scale.
           const uint32_t d_big = tmem_base + slot * C::SLOT_COLS;
           const uint32_t d_small = C::SPLIT_ACC ? d_big + BN : d_big;
-          const int kb1 = min(kb0 + CHUNK_KB, nkb_total);
+          const int kb1 = min(kb0 + CHUNK_KB, kbB);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&ctl->full[stage], phase);
             tc_fence_after();
@@ -311,13 +320,16 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     const int cbase = ch * EPI_COLS;
     const uint32_t flags = p.flags;
     int chunk_it = 0;
-    for (long long t = tile0; t < p.num_tiles; t += tile_step) {
+    for (long long u = tile0; u < num_units; u += tile_step) {
+      const long long t = u / p.ksplit;
+      const int ks = (int)(u % p.ksplit);
+      const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
       int tm, tn;
       tile_coords(p, t, tm, tn);
       float acc[EPI_COLS];  // this thread's row x column-half of the tile, fp32 registers
 #pragma unroll
       for (int c = 0; c < EPI_COLS; ++c) acc[c] = 0.f;
-      for (int kb0 = 0; kb0 < nkb_total; kb0 += CHUNK_KB, ++chunk_it) {
+      for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
         const int slot = chunk_it & 1;
         const uint32_t slot_phase = (chunk_it >> 1) & 1;
         mbar_wait(&ctl->tfull[slot], slot_phase);
@@ -347,6 +359,42 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
             mbar_arrive_cluster(map_peer(smem_u32(&ctl->tempty[slot]), 0));  // leader's barrier
           else
             mbar_arrive(&ctl->tempty[slot]);
+        }
+      }
+      if (p.ksplit > 1) {
+        // Split-K: post this unit's partial tile, count arrivals; the LAST unit of
+        // the tile to arrive sums all partials in split order (deterministic,
+        // no waiting) and runs the epilogue; the others are done with the tile.
+        const int rl = q * 32 + lane;
+        float* mine = p.part + (((u * CG + rank) * BM + rl) * (long long)BN + cbase);
+#pragma unroll
+        for (int c = 0; c < EPI_COLS; c += 4) store4(mine + c, acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"r"(C::EPI_WARPS * 32) : "memory");
+        if (warp == 2 && lane == 0) {
+          unsigned* cnt = p.counters + t * CG + rank;
+          const unsigned prev = atomicAdd(cnt, 1u);
+          const uint32_t last = prev == (unsigned)(p.ksplit - 1);
+          if (last) atomicExch(cnt, 0u);
+          ctl->last_flag = last;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(C::EPI_WARPS * 32) : "memory");
+        if (!ctl->last_flag) continue;
+        __threadfence();
+        // sum partials 0..ksplit-1 in order (own partial re-read from L2: same order
+        // whichever unit arrives last)
+        for (int k2 = 0; k2 < p.ksplit; ++k2) {
+          const float4* o = reinterpret_cast<const float4*>(
+              p.part + ((((t * p.ksplit + k2) * CG + rank) * BM + rl) * (long long)BN + cbase));
+#pragma unroll
+          for (int c = 0; c < EPI_COLS; c += 4) {
+            const float4 v = __ldcg(o + c / 4);
+            if (k2 == 0) {
+              acc[c] = v.x; acc[c + 1] = v.y; acc[c + 2] = v.z; acc[c + 3] = v.w;
+            } else {
+              acc[c] += v.x; acc[c + 1] += v.y; acc[c + 2] += v.z; acc[c + 3] += v.w;
+            }
+          }
         }
       }
       const int row0 = tm * C::PAIR_M + (int)rank * BM;  // first output row of this CTA
@@ -480,7 +528,7 @@ int num_sms() {
 }
 
 template <int CG, int BN>
-cudaError_t launch_cg(const GemmDesc& d, Params p, cudaStream_t s, int* launches) {
+cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, int* launches) {
   using C = Cfg<CG, BN>;
   const int tiles_m = (d.M + C::PAIR_M - 1) / C::PAIR_M;
   p.tiles_n = (d.N + BN - 1) / BN;
@@ -493,6 +541,13 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, cudaStream_t s, int* launches
   for (int tm = p.tm0; tm < p.tm1; ++tm)
     nt += (d.flags & EPI_TRI) ? std::min(p.ratio * (tm + 1), p.tiles_n) : p.tiles_n;
   p.num_tiles = nt;
+  p.ksplit = ksplit;
+  p.part = d.part;
+  p.counters = d.counters;
+  if (ksplit > 1) {
+    cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)nt * CG * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+  }
   CUtensorMap maps[8];
   for (int q = 0; q < 2; ++q) {
     const SplitOperand& A = d.a[q < d.npairs ? q : 0];
@@ -511,7 +566,8 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, cudaStream_t s, int* launches
     attr_set = true;
   }
   const long long max_units = num_sms() / CG;
-  const long long units = p.num_tiles < max_units ? p.num_tiles : max_units;
+  const long long work = p.num_tiles * p.ksplit;
+  const long long units = work < max_units ? work : max_units;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
   cfg.blockDim = dim3(C::NUM_THREADS);
@@ -526,8 +582,8 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, cudaStream_t s, int* launches
                                      maps[6], maps[7], p);
   if (launches) ++*launches;
   if (getenv("PB_TRACE"))
-    fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld grid=%lld\n", CG, BN, d.M, d.N, d.K,
-            d.npairs, d.flags, p.num_tiles, units * CG);
+    fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld ksplit=%d grid=%lld\n", CG, BN,
+            d.M, d.N, d.K, d.npairs, d.flags, p.num_tiles, p.ksplit, units * CG);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -551,22 +607,50 @@ cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
   p.split_hi = d.split_hi;
   p.split_lo = d.split_lo;
   p.ld_split = d.ld_split;
-  // Tile choice: 2-CTA 256x256 tiles (half the smem read traffic per MMA flop)
-  // when they still give >= ~2 waves over the SM pairs; otherwise 2-CTA 256x128;
-  // problems under 256 rows (or odd 128-row band starts) use 1-CTA 128x128.
+  const UmmaPlan pl = umma_plan(d);
+  int ks = pl.ksplit;
+  if (ks > 1 && (d.part == nullptr || d.counters == nullptr)) ks = 1;
+  if (pl.cfg == 3) return launch_cg<2, 256>(d, p, ks, s, launches);
+  if (pl.cfg == 2) return launch_cg<2, 128>(d, p, ks, s, launches);
+  return launch_cg<1, 128>(d, p, ks, s, launches);
+}
+
+// Tile configuration and split-K factor: a pure function of the shape (tuned
+// for 148 SMs = 74 pairs) so pb_workspace_size can reserve the partials.
+//   cfg 3: 2-CTA 256x256 tiles (half the smem reads per MMA flop)
+//   cfg 2: 2-CTA 256x128;  cfg 1: 1-CTA 128x128 (under 256 rows / odd band start)
+// ksplit in 1..4 maximises wave efficiency x (1 - 3% per extra split), keeping
+// >= 8 k-blocks per split.
+UmmaPlan umma_plan(const GemmDesc& d) {
   static const int force = getenv("PB_UMMA_TILE") ? atoi(getenv("PB_UMMA_TILE")) : 0;
+  static const int force_ks = getenv("PB_UMMA_KSPLIT") ? atoi(getenv("PB_UMMA_KSPLIT")) : 0;
+  UmmaPlan pl;
   const int rows = d.tm1 < 0 ? d.M : (d.tm1 - d.tm0) * 128;
   const bool pair_ok = rows >= 256 && (d.tm0 % 2) == 0;
-  long long tiles256 = 0;
-  if (pair_ok) {
-    const int tm = (rows + 255) / 256, tn = (d.N + 255) / 256;
-    tiles256 = (d.flags & EPI_TRI) ? (long long)tm * (tm + 1) / 2 : (long long)tm * tn;
+  pl.cfg = pair_ok ? 3 : 1;
+  if (force >= 1 && force <= 3 && (force == 1 || pair_ok)) pl.cfg = force;
+  const int pm = pl.cfg == 1 ? 128 : 256, bn = pl.cfg == 3 ? 256 : 128, cg = pl.cfg == 1 ? 1 : 2;
+  const int tm0 = d.tm0 * 128 / pm;
+  const int tiles_m = (d.M + pm - 1) / pm;
+  const int tm1 = d.tm1 < 0 ? tiles_m : std::min(tiles_m, (d.tm1 * 128 + pm - 1) / pm);
+  const int tiles_n = (d.N + bn - 1) / bn, ratio = pm / bn;
+  long long nt = 0;
+  for (int tm = tm0; tm < tm1; ++tm) nt += (d.flags & EPI_TRI) ? std::min(ratio * (tm + 1), tiles_n) : tiles_n;
+  pl.tiles = nt;
+  const int nkb_total = ((d.K + BK - 1) / BK) * d.npairs;
+  const int units = 148 / cg;
+  double best = -1.0;
+  pl.ksplit = 1;
+  for (int ks = 1; ks <= 4; ++ks) {
+    if (ks > 1 && nkb_total / ks < 8) break;
+    const long long w = nt * ks;
+    const double eff = (double)w / ((double)units * ((w + units - 1) / units)) * (1.0 - 0.03 * (ks - 1));
+    if (eff > best + 1e-9) { best = eff; pl.ksplit = ks; }
   }
-  int choice = !pair_ok ? 1 : (tiles256 >= 2 * (num_sms() / 2) ? 3 : 2);
-  if (force >= 1 && force <= 3 && (force == 1 || pair_ok)) choice = force;
-  if (choice == 3) return launch_cg<2, 256>(d, p, s, launches);
-  if (choice == 2) return launch_cg<2, 128>(d, p, s, launches);
-  return launch_cg<1, 128>(d, p, s, launches);
+  if (force_ks >= 1 && force_ks <= 8 && nkb_total / force_ks >= 1) pl.ksplit = force_ks;
+  pl.part_bytes = pl.ksplit > 1 ? (size_t)nt * pl.ksplit * cg * 128 * bn * sizeof(float) : 0;
+  pl.counter_bytes = pl.ksplit > 1 ? (size_t)nt * cg * sizeof(unsigned) : 0;
+  return pl;
 }
 
 }  // namespace pb

@@ -136,28 +136,67 @@ SplitBuf take_split(Carve& c, int rows, int K) {
   return b;
 }
 
-struct WsGemm { SplitBuf a, bt; };
-WsGemm ws_gemm(Carve& c, int ni, int nj, int nk) { return {take_split(c, ni, nk), take_split(c, nj, nk)}; }
-struct Ws2mm { SplitBuf a, bt, ct, tmp; };
+// Split-K scratch shared by the GEMMs of one call (they run in stream order).
+struct SplitK {
+  float* part = nullptr;
+  unsigned* counters = nullptr;
+  void attach(GemmDesc& d) const { d.part = part; d.counters = counters; }
+};
+GemmDesc shape(int M, int N, int K, int npairs = 1, uint32_t flags = EPI_OUT, int tm0 = 0, int tm1 = -1) {
+  GemmDesc d;
+  d.M = M; d.N = N; d.K = K; d.npairs = npairs; d.flags = flags; d.tm0 = tm0; d.tm1 = tm1;
+  return d;
+}
+SplitK take_splitk(Carve& c, std::initializer_list<GemmDesc> gemms) {
+  size_t part = 0, cnt = 0;
+  for (const GemmDesc& g : gemms) {
+    const UmmaPlan pl = umma_plan(g);
+    part = std::max(part, pl.part_bytes);
+    cnt = std::max(cnt, pl.counter_bytes);
+  }
+  SplitK k;
+  if (part) {
+    k.part = c.take<float>(part / sizeof(float));
+    k.counters = c.take<unsigned>(cnt / sizeof(unsigned));
+  }
+  return k;
+}
+
+struct WsGemm { SplitBuf a, bt; SplitK sk; };
+WsGemm ws_gemm(Carve& c, int ni, int nj, int nk) {
+  WsGemm w;
+  w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk);
+  w.sk = take_splitk(c, {shape(ni, nj, nk)});
+  return w;
+}
+struct Ws2mm { SplitBuf a, bt, ct, tmp; SplitK sk; };
 Ws2mm ws_2mm(Carve& c, int ni, int nj, int nk, int nl) {
   Ws2mm w;
   w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.ct = take_split(c, nl, nj); w.tmp = take_split(c, ni, nj);
+  w.sk = take_splitk(c, {shape(ni, nj, nk), shape(ni, nl, nj)});
   return w;
 }
-struct Ws3mm { SplitBuf a, bt, c, dt, e, ft; };
+struct Ws3mm { SplitBuf a, bt, c, dt, e, ft; SplitK sk; };
 Ws3mm ws_3mm(Carve& c, int ni, int nj, int nk, int nl, int nm) {
   Ws3mm w;
   w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.c = take_split(c, nj, nm);
   w.dt = take_split(c, nl, nm); w.e = take_split(c, ni, nj); w.ft = take_split(c, nl, nj);
+  w.sk = take_splitk(c, {shape(nj, nl, nm), shape(ni, nj, nk), shape(ni, nl, nj)});
   return w;
 }
-struct WsStat { SplitBuf xt; double* part; double* mean; double* inv; };
+struct WsStat { SplitBuf xt; SplitK sk; };
 WsStat ws_stat(Carve& c, int m, int n) {
   WsStat w;
   w.xt = take_split(c, m, n);
-  w.part = c.take<double>(stats_part_doubles(m, n));
-  w.mean = c.take<double>(m);
-  w.inv = c.take<double>(m);
+  w.sk = take_splitk(c, {shape(m, m, n, 1, EPI_TRI)});
+  return w;
+}
+struct WsSyrk { SplitBuf a, b; SplitK sk; };
+WsSyrk ws_syrk(Carve& c, int n, int m, int r0, int r1, bool two) {
+  WsSyrk w;
+  w.a = take_split(c, r1, m);
+  if (two) w.b = take_split(c, r1, m);
+  w.sk = take_splitk(c, {shape(r1, r1, m, two ? 2 : 1, EPI_TRI, r0 / 128, (r1 + 127) / 128)});
   return w;
 }
 
@@ -198,6 +237,7 @@ pb_status run_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, co
   d.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
   d.alpha = alpha; d.beta = beta;
   d.cin = C; d.ldc = nj; d.out = C; d.ldo = nj;
+  w.sk.attach(d);
   PB_CUDA(launch_umma_gemm(d, s, L));
   return PB_OK;
 }
@@ -234,16 +274,16 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   if (k == "gemm" && need(3)) ws_gemm(c, d[0], d[1], d[2]);
   else if (k == "2mm" && need(4)) ws_2mm(c, d[0], d[1], d[2], d[3]);
   else if (k == "3mm" && need(5)) ws_3mm(c, d[0], d[1], d[2], d[3], d[4]);
-  else if (k == "syrk" && need(2)) take_split(c, d[0], d[1]);
-  else if (k == "syr2k" && need(2)) { take_split(c, d[0], d[1]); take_split(c, d[0], d[1]); }
+  else if (k == "syrk" && need(2)) ws_syrk(c, d[0], d[1], 0, d[0], false);
+  else if (k == "syr2k" && need(2)) ws_syrk(c, d[0], d[1], 0, d[0], true);
   else if ((k == "covariance" || k == "correlation") && need(2)) ws_stat(c, d[0], d[1]);
   else if (k == "atax" && need(2)) c.take<char>(atax_ws_bytes(d[0], d[1]));
   else if (k == "bicg" && need(2)) c.take<char>(mvmt_ws_bytes(d[1], d[0]));
   else if (k == "mvt" && need(1)) c.take<char>(mvmt_ws_bytes(d[0], d[0]));
   else if (k == "gesummv" && need(1)) {}
   else if (k == "gesummv_rows" && need(2)) {}
-  else if (k == "syrk_rows" && need(4)) take_split(c, d[3], d[1]);
-  else if (k == "syr2k_rows" && need(4)) { take_split(c, d[3], d[1]); take_split(c, d[3], d[1]); }
+  else if (k == "syrk_rows" && need(4)) ws_syrk(c, d[0], d[1], d[2], d[3], false);
+  else if (k == "syr2k_rows" && need(4)) ws_syrk(c, d[0], d[1], d[2], d[3], true);
   else if (k == "matvec_partial" && need(2)) c.take<char>(mvmt_ws_bytes(d[0], d[1]));
   else if (k == "gemm_variant" && need(3)) ws_gemm(c, d[0], d[1], d[2]);
   else return fail(PB_ERR_INVALID_ARG, "unknown kernel '%s' or wrong number of dims (%d)", kernel, nd);
@@ -304,6 +344,7 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
   g1.alpha = alpha;
   g1.out = tmp; g1.ldo = nj;
   g1.split_hi = w.tmp.hi; g1.split_lo = w.tmp.lo; g1.ld_split = w.tmp.ld;
+  w.sk.attach(g1);
   PB_CUDA(launch_umma_gemm(g1, st, &L));
   GemmDesc g2;  // D = tmp * C + beta * D
   g2.M = ni; g2.N = nl; g2.K = nj;
@@ -311,6 +352,7 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
   g2.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
   g2.alpha = 1.f; g2.beta = beta;
   g2.cin = D; g2.ldc = nl; g2.out = D; g2.ldo = nl;
+  w.sk.attach(g2);
   PB_CUDA(launch_umma_gemm(g2, st, &L));
   g_launches = L;
   return PB_OK;
@@ -343,6 +385,7 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   gf.flags = EPI_OUT | EPI_SPLIT_T;
   gf.out = F; gf.ldo = nl;
   gf.split_hi = w.ft.hi; gf.split_lo = w.ft.lo; gf.ld_split = w.ft.ld;
+  w.sk.attach(gf);
   PB_CUDA(launch_umma_gemm(gf, st, &L));
   GemmDesc ge;  // E = A * B; epilogue also emits E split (G's A operand)
   ge.M = ni; ge.N = nj; ge.K = nk;
@@ -350,12 +393,14 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   ge.flags = EPI_OUT | EPI_SPLIT;
   ge.out = E; ge.ldo = nj;
   ge.split_hi = w.e.hi; ge.split_lo = w.e.lo; ge.ld_split = w.e.ld;
+  w.sk.attach(ge);
   PB_CUDA(launch_umma_gemm(ge, st, &L));
   GemmDesc gg;  // G = E * F
   gg.M = ni; gg.N = nl; gg.K = nj;
   gg.a[0] = w.e.op(); gg.b[0] = w.ft.op();
   gg.flags = EPI_OUT;
   gg.out = G; gg.ldo = nl;
+  w.sk.attach(gg);
   PB_CUDA(launch_umma_gemm(gg, st, &L));
   g_launches = L;
   return PB_OK;
@@ -372,13 +417,11 @@ static pb_status syrk_core(int n, int m, int r0, int r1, float alpha, float beta
   if (B) ck.arr(B, r1, m, false, "B");
   PB_TRY(ck.finish());
   Carve need(nullptr, 0);
-  take_split(need, r1, m);
-  if (B) take_split(need, r1, m);
+  ws_syrk(need, n, m, r0, r1, B != nullptr);
   PB_TRY(check_ws(need, ws, ws_bytes));
   Carve c(ws, ws_bytes);
-  SplitBuf sa = take_split(c, r1, m);
-  SplitBuf sb{};
-  if (B) sb = take_split(c, r1, m);
+  WsSyrk w = ws_syrk(c, n, m, r0, r1, B != nullptr);
+  SplitBuf sa = w.a, sb = w.b;
   cudaStream_t st = S(s);
   int L = 0;
   PB_CUDA(launch_split(A, r1, m, m, sa.hi, sa.lo, sa.ld, st));
@@ -397,6 +440,7 @@ static pb_status syrk_core(int n, int m, int r0, int r1, float alpha, float beta
   d.alpha = alpha; d.beta = beta;
   d.cin = C_blk; d.ldc = n; d.out = C_blk; d.ldo = n; d.out_row0 = r0;
   d.tm0 = r0 / 128; d.tm1 = (r1 + 127) / 128;
+  w.sk.attach(d);
   PB_CUDA(launch_umma_gemm(d, st, &L));
   g_launches = L;
   return PB_OK;
@@ -441,9 +485,8 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
   WsStat w = ws_stat(c, m, n);
   cudaStream_t st = S(s);
   int L = 0;
-  PB_CUDA(launch_colstats(data, n, m, (double)float_n, (double)eps, corr, w.part, w.mean, w.inv, mean,
-                          corr ? stddev : nullptr, st, &L));
-  PB_CUDA(launch_split_T(data, n, m, m, w.xt.hi, w.xt.lo, w.xt.ld, w.mean, corr ? w.inv : nullptr, st));
+  PB_CUDA(launch_stats_split(data, n, m, (double)float_n, (double)eps, corr, w.xt.hi, w.xt.lo, w.xt.ld, mean,
+                             corr ? stddev : nullptr, st));
   ++L;
   GemmDesc d;  // Gram core: out[i][j] = alpha * sum_k Xt[i][k] Xt[j][k], lower tiles + mirror
   d.M = m; d.N = m; d.K = n;
@@ -451,6 +494,7 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
   d.flags = EPI_TRI | EPI_MIRROR | EPI_OUT | (corr ? EPI_DIAG_ONE : 0u);
   d.alpha = corr ? 1.0f : (float)(1.0 / ((double)float_n - 1.0));
   d.out = out; d.ldo = m;
+  w.sk.attach(d);
   PB_CUDA(launch_umma_gemm(d, st, &L));
   g_launches = L;
   return PB_OK;

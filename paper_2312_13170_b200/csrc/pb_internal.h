@@ -42,9 +42,18 @@ struct GemmDesc {
   float* split_hi = nullptr;
   float* split_lo = nullptr;
   int ld_split = 0;
-  int tm0 = 0, tm1 = -1;  // tile-row range (default all)
+  int tm0 = 0, tm1 = -1;  // tile-row range in 128-row units (default all)
+  float* part = nullptr;       // split-K partials (umma_plan(d).part_bytes)
+  unsigned* counters = nullptr;  // split-K counters (umma_plan(d).counter_bytes)
 };
 
+struct UmmaPlan {
+  int cfg = 1;     // 1: 1-CTA 128x128, 2: 2-CTA 256x128, 3: 2-CTA 256x256
+  int ksplit = 1;  // split-K factor
+  long long tiles = 0;
+  size_t part_bytes = 0, counter_bytes = 0;
+};
+UmmaPlan umma_plan(const GemmDesc& d);
 cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches);
 
 // ---- split / prep (k_split.cu) ----------------------------------------------
@@ -58,12 +67,10 @@ cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* h
                            const double* mean, const double* inv, cudaStream_t s);
 
 // ---- column statistics (k_stats.cu) -----------------------------------------
-// mean[j] = sum_i data[i][j] / float_n (double). If want_sd: sd/inv with eps rule.
-// part: workspace of stats_part_doubles(m, n) doubles.
-size_t stats_part_doubles(int m, int n);
-cudaError_t launch_colstats(const float* data, int n, int m, double float_n, double eps, bool want_sd,
-                            double* part, double* mean, double* inv, float* mean_out, float* sd_out,
-                            cudaStream_t s, int* launches);
+// Fused covariance/correlation prep: column mean (+ stddev, eps rule) and the
+// centred (normalised) data written transposed as a hi/lo split (m x ldo).
+cudaError_t launch_stats_split(const float* data, int n, int m, double float_n, double eps, bool corr, float* hiT,
+                               float* loT, int ldo, float* mean_out, float* sd_out, cudaStream_t s);
 
 // ---- matrix-vector family (k_matvec.cu) -------------------------------------
 // y[i] = alpha * A_i.x + beta * B_i.x (B may be null -> beta ignored); tmp[i] = A_i.x (optional).

@@ -242,16 +242,16 @@ def test_row_sharded_pieces_match_full():
     """Host-side sharding math on one GPU: syrk_rows bands and matvec partials
     reassemble the single-call results (P33 on one device)."""
     n, m = 520, 300
-    A = P.dev(P.H(n, m, 1))
-    C0 = P.dev(P.H(n, n, 3, mode=pbgen.SYM))
-    full = C0.clone()
-    pb.pb_syrk(n, m, 1.5, 1.2, full, A)
-    parts = C0.clone()
-    for g in range(3):
+    Ah, Ch = P.H(n, m, 1), P.H(n, n, 3, mode=pbgen.SYM)
+    A = P.dev(Ah)
+    parts = P.dev(Ch)
+    for g in range(3):  # bands may run different tile configs: compare with the oracle
         r0, r1 = pb.pb_row_partition(n, 3, g, triangular=True, align=128)
         if r1 > r0:
             pb.pb_syrk_rows(n, m, r0, r1, 1.5, 1.2, parts[r0:r1], A)
-    assert np.array_equal(P.host(full), P.host(parts))
+    r = oracle.syrk(1.5, 1.2, Ch, Ah)
+    s = oracle.syrk(1.5, 1.2, Ch, Ah, absmode=True)
+    assert P.cerr(P.host(parts), r, s) <= P.TOL
     rows, cols = 1000, 1028
     A = P.dev(P.H(rows, cols, 1))
     v, w = P.dev(P.H(1, cols, 6)[0]), P.dev(P.H(1, rows, 7)[0])
