@@ -21,10 +21,10 @@ namespace {
 //          every store is a 16-byte piece of a contiguous Xt row.
 // The CTA's 16 x n slab (128 KiB at n = 2048) is re-read in pass 2 from L1/L2.
 constexpr int PC = 16;
-constexpr int PT = 256;
+constexpr int PT = 512;
 
 template <bool CORR>
-__global__ void __launch_bounds__(PT) stats_split_kernel(const float* __restrict__ data, int n, int m, double float_n,
+__global__ void __launch_bounds__(PT, 1) stats_split_kernel(const float* __restrict__ data, int n, int m, double float_n,
                                                          double eps, float* __restrict__ hiT, float* __restrict__ loT,
                                                          int ldo, float* __restrict__ mean_out,
                                                          float* __restrict__ sd_out) {

@@ -1,0 +1,70 @@
+#!/usr/bin/env python
+"""Quick device timing of single C-ABI calls (tuning aid; not the bench).
+
+usage: python scripts/time_calls.py <kernel> [n] [reps]
+Prints the median CUDA-event time of the call (captured into a CUDA graph so
+host overhead is excluded). Env PB_UMMA_TILE / PB_UMMA_KSPLIT steer the GEMM
+plan.
+"""
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2312_13170_b200 as pb  # noqa: E402
+import pbgen  # noqa: E402
+
+
+def main():
+    k = sys.argv[1]
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+    dev = torch.device("cuda", 0)
+
+    def g(r, c, s):
+        t = torch.empty(r, c, device=dev)
+        pbgen.gen_device(t, s)
+        return t
+
+    if k in ("covariance", "correlation"):
+        data, out = g(n, n, 5), torch.empty(n, n, device=dev)
+        ws = pb.workspace(k, (n, n), dev)
+        f = (lambda: pb.pb_covariance(n, n, float(n), data, out, None, ws=ws)) if k == "covariance" else \
+            (lambda: pb.pb_correlation(n, n, float(n), 0.1, data, out, None, None, ws=ws))
+        flops = n * n * (n + 1)
+    elif k == "gemm":
+        A, B, C = g(n, n, 1), g(n, n, 2), g(n, n, 3)
+        ws = pb.workspace("gemm", (n, n, n), dev)
+        f = lambda: pb.pb_gemm(n, n, n, 1.5, 1.2, C, A, B, ws=ws)  # noqa: E731
+        flops = 2 * n ** 3
+    elif k == "syrk":
+        A, C = g(n, n, 1), g(n, n, 3)
+        ws = pb.workspace("syrk", (n, n), dev)
+        f = lambda: pb.pb_syrk(n, n, 1.5, 1.2, C, A, ws=ws)  # noqa: E731
+        flops = n * (n + 1) * n
+    else:
+        raise SystemExit(f"unknown kernel {k}")
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        f()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    print(f"{k} n={n} tile={os.environ.get('PB_UMMA_TILE', '-')} ks={os.environ.get('PB_UMMA_KSPLIT', '-')}: "
+          f"{ms * 1e3:.1f} us  {flops / ms / 1e9:.1f} TFLOP/s useful")
+
+
+if __name__ == "__main__":
+    main()
