@@ -38,6 +38,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "pb_device.cuh"
 #include "pb_internal.h"
@@ -66,7 +67,7 @@ struct Cfg {
   static constexpr int PAIR_M = BM * CG;                  // output rows per tile
   static constexpr bool SPLIT_ACC = BN == 128;            // separate big / small accumulators
   static constexpr int SLOT_COLS = SPLIT_ACC ? 2 * BN : BN;
-  static constexpr int CHUNK_KB = SPLIT_ACC ? 16 : 8;     // k-blocks per TMEM partial sum (512 / 256 of K)
+  static constexpr int CHUNK_KB = 16;                     // k-blocks per TMEM partial sum (512 of K)
   static constexpr int EPI_WARPS = 4 * (BN / EPI_COLS);
   static constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 };
@@ -88,7 +89,20 @@ struct Params {
   int ksplit;                    // K splits per tile (split-K); work unit = (tile, split)
   float* part;                   // split-K partial tiles [unit][CG][128][BN]
   unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
+  int dbg;                       // PB_UMMA_DEBUG (tuning only): 1 = skip partial exchange
+  unsigned long long* tstamp;    // PB_UMMA_TIMING (tuning only): [cta][unit<16][8] globaltimer stamps
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TSTAMP(unit_local, ev)                                                                         \
+  do {                                                                                                 \
+    if (p.tstamp && (unit_local) < 16)                                                                 \
+      p.tstamp[((unsigned long long)blockIdx.x * 16 + (unit_local)) * 8 + (ev)] = gtimer();            \
+  } while (0)
 
 struct __align__(8) Ctl {
   uint64_t full[8];
@@ -244,10 +258,10 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       uint32_t phase = 0;
       for (long long u = tile0; u < num_units; u += tile_step) {
         int tm, tn;
-        tile_coords(p, u / p.ksplit, tm, tn);
+        tile_coords(p, u % p.num_tiles, tm, tn);
         const int arow = tm * C::PAIR_M + (int)rank * BM;
         const int brow = tn * BN + (int)rank * C::B_ROWS;
-        const int ks = (int)(u % p.ksplit);
+        const int ks = (int)(u / p.num_tiles);
         const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
         for (int kb = kbA; kb < kbB; ++kb) {
           mbar_wait(&ctl->empty[stage], phase ^ 1);
@@ -275,9 +289,11 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int chunk_it = 0;
-      for (long long u = tile0; u < num_units; u += tile_step) {
-        const int ks = (int)(u % p.ksplit);
+      int ul = 0;
+      for (long long u = tile0; u < num_units; u += tile_step, ++ul) {
+        const int ks = (int)(u / p.num_tiles);
         const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
+        TSTAMP(ul, 0);
         for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
           const int slot = chunk_it & 1;
           const uint32_t slot_phase = (chunk_it >> 1) & 1;
@@ -311,6 +327,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           }
           commit_cg<CG>(&ctl->tfull[slot]);  // chunk partial sums ready for the epilogues
         }
+        TSTAMP(ul, 1);
       }
     }
   } else {
@@ -320,9 +337,10 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     const int cbase = ch * EPI_COLS;
     const uint32_t flags = p.flags;
     int chunk_it = 0;
-    for (long long u = tile0; u < num_units; u += tile_step) {
-      const long long t = u / p.ksplit;
-      const int ks = (int)(u % p.ksplit);
+    int ul = 0;
+    for (long long u = tile0; u < num_units; u += tile_step, ++ul) {
+      const long long t = u % p.num_tiles;  // split-major order: a tile's splits run apart in time
+      const int ks = (int)(u / p.num_tiles);
       const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
       int tm, tn;
       tile_coords(p, t, tm, tn);
@@ -334,6 +352,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         const uint32_t slot_phase = (chunk_it >> 1) & 1;
         mbar_wait(&ctl->tfull[slot], slot_phase);
         tc_fence_after();
+        if (kb0 == kbA && warp == 2 && lane == 0) TSTAMP(ul, 2);
         __syncwarp();
         const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + slot * C::SLOT_COLS + cbase;
 #pragma unroll
@@ -361,14 +380,17 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
             mbar_arrive(&ctl->tempty[slot]);
         }
       }
-      if (p.ksplit > 1) {
+      if (warp == 2 && lane == 0) TSTAMP(ul, 3);
+      if (p.ksplit > 1 && p.dbg != 1) {
         // Split-K: post this unit's partial tile, count arrivals; the LAST unit of
         // the tile to arrive sums all partials in split order (deterministic,
         // no waiting) and runs the epilogue; the others are done with the tile.
+        // partial layout [unit][rank][col half][c/4][row 0..127][4]: lanes (rows) write
+        // consecutive 16-byte pieces, every access is a coalesced 512-byte line set
         const int rl = q * 32 + lane;
-        float* mine = p.part + (((u * CG + rank) * BM + rl) * (long long)BN + cbase);
+        float4* mine = reinterpret_cast<float4*>(p.part) + ((u * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
 #pragma unroll
-        for (int c = 0; c < EPI_COLS; c += 4) store4(mine + c, acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        for (int c = 0; c < EPI_COLS; c += 4) mine[(c / 4) * BM] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"r"(C::EPI_WARPS * 32) : "memory");
         if (warp == 2 && lane == 0) {
@@ -384,11 +406,11 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         // sum partials 0..ksplit-1 in order (own partial re-read from L2: same order
         // whichever unit arrives last)
         for (int k2 = 0; k2 < p.ksplit; ++k2) {
-          const float4* o = reinterpret_cast<const float4*>(
-              p.part + ((((t * p.ksplit + k2) * CG + rank) * BM + rl) * (long long)BN + cbase));
+          const float4* o = reinterpret_cast<const float4*>(p.part) +
+                            (((k2 * p.num_tiles + t) * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
 #pragma unroll
           for (int c = 0; c < EPI_COLS; c += 4) {
-            const float4 v = __ldcg(o + c / 4);
+            const float4 v = __ldcg(o + (c / 4) * BM);
             if (k2 == 0) {
               acc[c] = v.x; acc[c + 1] = v.y; acc[c + 2] = v.z; acc[c + 3] = v.w;
             } else {
@@ -397,6 +419,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           }
         }
       }
+      if (warp == 2 && lane == 0) TSTAMP(ul, 4);
       const int row0 = tm * C::PAIR_M + (int)rank * BM;  // first output row of this CTA
       const int i = row0 + q * 32 + lane;                // this thread's output row
       const bool row_ok = i < p.M;
@@ -474,6 +497,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           }
         }
       }
+      if (warp == 2 && lane == 0) TSTAMP(ul, 5);
     }
   }
 
@@ -542,6 +566,13 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
     nt += (d.flags & EPI_TRI) ? std::min(p.ratio * (tm + 1), p.tiles_n) : p.tiles_n;
   p.num_tiles = nt;
   p.ksplit = ksplit;
+  static const int dbg = getenv("PB_UMMA_DEBUG") ? atoi(getenv("PB_UMMA_DEBUG")) : 0;
+  p.dbg = dbg;
+  static const bool timing = getenv("PB_UMMA_TIMING") != nullptr;
+  static unsigned long long* tbuf = nullptr;
+  if (timing && !tbuf) cudaMalloc(&tbuf, 148 * 16 * 8 * sizeof(unsigned long long));  // debug only
+  p.tstamp = timing ? tbuf : nullptr;
+  if (timing) cudaMemsetAsync(tbuf, 0, 148 * 16 * 8 * sizeof(unsigned long long), s);
   p.part = d.part;
   p.counters = d.counters;
   if (ksplit > 1) {
@@ -581,6 +612,28 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
   cudaError_t e = cudaLaunchKernelEx(&cfg, umma3x_kernel<CG, BN>, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
                                      maps[6], maps[7], p);
   if (launches) ++*launches;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (p.tstamp) cudaStreamIsCapturing(s, &cap);
+  if (p.tstamp && cap == cudaStreamCaptureStatusNone) {  // debug: per-phase durations (us), medians over CTAs/units
+    std::vector<unsigned long long> h(148 * 16 * 8);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), p.tstamp, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    std::vector<double> mma, drain_lag, split, store;
+    for (int c = 0; c < (int)(units * CG); ++c)
+      for (int u = 0; u < 16; ++u) {
+        const unsigned long long* e = &h[((size_t)c * 16 + u) * 8];
+        for (int k = 0; k < 6; ++k)
+          if (e[k]) { t0 = std::min(t0, e[k]); t1 = std::max(t1, e[k]); }
+        if (e[0] && e[1]) mma.push_back((e[1] - e[0]) / 1e3);
+        if (e[1] && e[3]) drain_lag.push_back(((long long)e[3] - (long long)e[1]) / 1e3);
+        if (e[3] && e[4]) split.push_back((e[4] - e[3]) / 1e3);
+        if (e[4] && e[5]) store.push_back((e[5] - e[4]) / 1e3);
+      }
+    auto med = [](std::vector<double> v) { if (v.empty()) return 0.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+    fprintf(stderr, "[pb timing] span %.1f us | per unit median: mma %.1f, mma-end->drained %.1f, split-exchange %.1f, "
+            "stores %.1f us (n=%zu)\n", (t1 - t0) / 1e3, med(mma), med(drain_lag), med(split), med(store), mma.size());
+  }
   if (getenv("PB_TRACE"))
     fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld ksplit=%d grid=%lld\n", CG, BN,
             d.M, d.N, d.K, d.npairs, d.flags, p.num_tiles, p.ksplit, units * CG);
