@@ -14,6 +14,7 @@ namespace {
 
 __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X, int rows, int cols4, int ldx,
                                                     float* __restrict__ hi, float* __restrict__ lo, int ldo) {
+  pdl_wait();
   const long long total = (long long)rows * cols4;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -38,6 +39,7 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
                                                       const double* __restrict__ mean,
                                                       const double* __restrict__ inv) {
   __shared__ float tile[64][65];
+  pdl_wait();
   const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int c = c0 + 4 * tx;
@@ -93,15 +95,13 @@ cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi,
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  split_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, rows, cols4, ldx, hi, lo, ldo);
-  return cudaGetLastError();
+  return launch_pdl(split_kernel, dim3((unsigned)blocks), dim3(256), 0, s, X, rows, cols4, ldx, hi, lo, ldo);
 }
 
 cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* hiT, float* loT, int ldo,
                            const double* mean, const double* inv, cudaStream_t s) {
   dim3 grid((cols + 63) / 64, (rows + 63) / 64);
-  split_t_kernel<<<grid, 256, 0, s>>>(X, rows, cols, ldx, hiT, loT, ldo, mean, inv);
-  return cudaGetLastError();
+  return launch_pdl(split_t_kernel, grid, dim3(256), 0, s, X, rows, cols, ldx, hiT, loT, ldo, mean, inv);
 }
 
 }  // namespace pb

@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
+  pdl_wait();  // the setup above overlapped the producer kernel's tail (PDL)
   const uint32_t tmem_base = ctl->tmem_base;
   const int nkb_total = p.nkb * p.npairs;
   const long long num_units = p.num_tiles * p.ksplit;
@@ -381,6 +382,13 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         }
       }
       if (warp == 2 && lane == 0) TSTAMP(ul, 3);
+      if (p.ksplit > 1 && (flags & EPI_PARTIAL)) {  // partials only; launch_gram_combine finishes
+        const int rl = q * 32 + lane;
+        float4* mine = reinterpret_cast<float4*>(p.part) + ((u * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
+#pragma unroll
+        for (int c = 0; c < EPI_COLS; c += 4) mine[(c / 4) * BM] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        continue;
+      }
       if (p.ksplit > 1 && p.dbg != 1) {
         // Split-K: post this unit's partial tile, count arrivals; the LAST unit of
         // the tile to arrive sums all partials in split order (deterministic,
@@ -604,11 +612,13 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
   cfg.blockDim = dim3(C::NUM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CG; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, umma3x_kernel<CG, BN>, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
                                      maps[6], maps[7], p);
   if (launches) ++*launches;
@@ -640,7 +650,91 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// Gram combine (EPI_PARTIAL): one CTA per (tile, rank, 32-row block). Partials
+// (layout [unit][rank][half][c4][row][4]) are read with lanes on rows (coalesced),
+// summed in split order (deterministic), scaled, staged in padded smem, then written
+// row-major with lanes on columns and mirrored with lanes on rows (both coalesced).
+template <int CG, int BN>
+__global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int diag_one) {
+  constexpr int PAIR_M = BM * CG, C4 = BN / 4;
+  __shared__ float tile[32][BN + 1];
+  pdl_wait();
+  const int blk = blockIdx.x;
+  const long long t = blk / (CG * 4);
+  const int rank = (blk / 4) % CG, rb = blk % 4;
+  int tm, tn;
+  tile_coords(p, t, tm, tn);
+  const int row_base = tm * PAIR_M + rank * BM + rb * 32;  // first output row of this block
+  const int col_base = tn * BN;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // 8 warps
+  // read + sum: warp w handles c4 = w, w+8, ...; lane = row within the block. All
+  // C4/8 loads of one split are issued before any is used (memory-level parallelism).
+  constexpr int NC = C4 / 8;
+  float4 acc[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < p.ksplit; ++s) {
+    const float4* base = reinterpret_cast<const float4*>(p.part) +
+                         (((s * p.num_tiles + t) * CG + rank) * (long long)BN) * (BM / 4) + rb * 32 + lane;
+    float4 v[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) v[k] = __ldcg(base + (long long)(w + 8 * k) * BM);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      acc[k].x += v[k].x; acc[k].y += v[k].y; acc[k].z += v[k].z; acc[k].w += v[k].w;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int c4 = w + 8 * k;
+    tile[lane][4 * c4 + 0] = p.alpha * acc[k].x;
+    tile[lane][4 * c4 + 1] = p.alpha * acc[k].y;
+    tile[lane][4 * c4 + 2] = p.alpha * acc[k].z;
+    tile[lane][4 * c4 + 3] = p.alpha * acc[k].w;
+  }
+  __syncthreads();
+  // direct lower part out[i][j], j <= i: lanes on columns
+  for (int r = w; r < 32; r += 8) {
+    const int i = row_base + r;
+    if (i >= p.M) break;
+    for (int c = lane; c < BN; c += 32) {
+      const int j = col_base + c;
+      if (j > i || j >= p.N) break;
+      p.out[(long long)i * p.ldo + j] = (diag_one && j == i) ? 1.0f : tile[r][c];
+    }
+  }
+  // mirror out[j][i] = v for j < i: lanes on rows i
+  const int i = row_base + lane;
+  if (i < p.M) {
+    for (int c = w; c < BN; c += 8) {
+      const int j = col_base + c;
+      if (j >= p.N) break;
+      if (j < i) p.out[(long long)j * p.ldo + i] = tile[lane][c];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, cudaStream_t s, int* launches) {
+  if (pl.ksplit <= 1) return cudaSuccess;
+  Params p{};
+  p.M = d.M; p.N = d.N; p.flags = d.flags; p.alpha = d.alpha; p.out = d.out; p.ldo = d.ldo;
+  p.part = d.part; p.ksplit = pl.ksplit; p.num_tiles = pl.tiles;
+  const int pm = pl.cfg == 1 ? 128 : 256, bn = pl.cfg == 3 ? 256 : 128;
+  p.tm0 = 0;
+  p.tm1 = (d.M + pm - 1) / pm;
+  p.tiles_n = (d.N + bn - 1) / bn;
+  p.ratio = pm / bn;
+  const unsigned grid = (unsigned)(pl.tiles * (pm / 128) * 4);  // (tile, rank, 32-row block)
+  const int dg = diag_one ? 1 : 0;
+  cudaError_t e;
+  if (pl.cfg == 3) e = launch_pdl(gram_combine_kernel<2, 256>, dim3(grid), dim3(256), 0, s, p, dg);
+  else if (pl.cfg == 2) e = launch_pdl(gram_combine_kernel<2, 128>, dim3(grid), dim3(256), 0, s, p, dg);
+  else e = launch_pdl(gram_combine_kernel<1, 128>, dim3(grid), dim3(256), 0, s, p, dg);
+  if (launches) ++*launches;
+  return e;
+}
 
 cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
   Params p{};

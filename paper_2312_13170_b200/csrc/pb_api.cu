@@ -495,7 +495,10 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
   d.alpha = corr ? 1.0f : (float)(1.0 / ((double)float_n - 1.0));
   d.out = out; d.ldo = m;
   w.sk.attach(d);
+  const UmmaPlan pl = umma_plan(d);
+  if (pl.ksplit > 1 && w.sk.part) d.flags |= EPI_PARTIAL;  // split-K: partials + combine kernel
   PB_CUDA(launch_umma_gemm(d, st, &L));
+  if (d.flags & EPI_PARTIAL) PB_CUDA(launch_gram_combine(d, pl, corr, st, &L));
   g_launches = L;
   return PB_OK;
 }

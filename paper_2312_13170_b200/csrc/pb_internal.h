@@ -26,6 +26,7 @@ enum : uint32_t {
   EPI_OUT = 1u << 4,       // write fp32 out[i][j]
   EPI_SPLIT = 1u << 5,     // write hi/lo split of v at [i][j] (next GEMM's K-major A operand)
   EPI_SPLIT_T = 1u << 6,   // write hi/lo split of v at [j][i] (next GEMM's K-major B operand)
+  EPI_PARTIAL = 1u << 7,   // split-K: only write the per-split partial tiles (a combine kernel finishes)
 };
 
 struct GemmDesc {
@@ -55,6 +56,9 @@ struct UmmaPlan {
 };
 UmmaPlan umma_plan(const GemmDesc& d);
 cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches);
+// Gram finish for EPI_PARTIAL launches (plan pl): out[i][j] = alpha * sum_s partial_s for
+// j <= i, mirrored to out[j][i]; diag_one -> out[i][i] = 1.
+cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, cudaStream_t s, int* launches);
 
 // ---- split / prep (k_split.cu) ----------------------------------------------
 // hi/lo split of a rows x cols matrix; same layout (ldo = ld of output).
@@ -98,6 +102,25 @@ cudaError_t launch_gemm_listing9(int ni, int nj, int nk, float alpha, float beta
                                  const float* B, cudaStream_t s);
 cudaError_t launch_gemm_listing9_reg(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                      const float* B, cudaStream_t s);
+
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled
+// while its predecessor drains; every kernel launched this way calls pdl_wait()
+// before it touches data the predecessor produced.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
