@@ -79,7 +79,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
@@ -222,10 +222,15 @@ def run_ours(args):
     if world != args.gpus:
         if rank == 0:
             print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    if os.environ.get("PB_SHARE_GPU"):  # test aid: every rank on cuda:0 (gloo), e.g. 2 ranks on 1 GPU
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("PB_SHARE_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     kernels = KERNELS if args.kernels == "all" else args.kernels.split(",")
     suite = Suite(rank, world, dev, kernels)
     W = work()
@@ -233,7 +238,10 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize(dev)
 
     launches_of = {}
@@ -292,11 +300,12 @@ def run_ours(args):
     total_ms = t0.elapsed_time(t1)
     per_k = {k: statistics.mean(e[k][0].elapsed_time(e[k][1]) for e in ev) for k in kernels}
     if world > 1:
-        tt = torch.tensor([total_ms] + [per_k[k] for k in kernels], device=dev, dtype=torch.float64)
+        cdev = dev if dist.get_backend() == "nccl" else "cpu"
+        tt = torch.tensor([total_ms] + [per_k[k] for k in kernels], device=cdev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt[0])
         per_k = {k: float(tt[i + 1]) for i, k in enumerate(kernels)}
-        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+        lt = torch.tensor([launches], device=cdev, dtype=torch.int64)
         dist.all_reduce(lt)
         launches = int(lt[0])
 
@@ -408,7 +417,10 @@ def measure_e2e(suite, kernels, W, steps, dev, world, local):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
     torch.cuda.synchronize(dev)
     t0.record(stream)
     for _ in range(steps):
@@ -424,7 +436,7 @@ def measure_e2e(suite, kernels, W, steps, dev, world, local):
     torch.cuda.synchronize(dev)
     ms = t0.elapsed_time(t1) / steps
     if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tt = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
     flops = sum(W[k][0] for k in kernels)

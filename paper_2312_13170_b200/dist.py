@@ -37,9 +37,26 @@ def partition(rows, world, rank, triangular=False, align=128, K=_pb):
     return K.pb_row_partition(rows, world, rank, triangular, align)
 
 
+def _staged():
+    """gloo carries CUDA tensors only through host copies (multi-rank tests on one
+    GPU); NCCL moves them device to device over NVLink."""
+    return dist.get_backend() != "nccl"
+
+
 def _all_gather_rows(full, local, world, bounds, async_op=False):
     """full[rows] <- concat of every rank's `local` row block."""
     sizes = [e - b for b, e in bounds]
+    if _staged() and full.is_cuda:
+        parts = [torch.empty((e - b,) + tuple(local.shape[1:]), dtype=local.dtype) for b, e in bounds]
+        _, rank = _world()
+        mx = max(sizes)
+        pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype)
+        pad[: sizes[rank]].copy_(local[: sizes[rank]].cpu())
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad)
+        for g, (b, e) in enumerate(bounds):
+            full[b:e].copy_(bufs[g][: e - b])
+        return None
     if len(set(sizes)) == 1:
         return dist.all_gather_into_tensor(full, local, async_op=async_op)
     mx = max(sizes)  # uneven blocks: pad every block to the largest, gather, unpad
@@ -56,6 +73,13 @@ def _all_gather_rows(full, local, world, bounds, async_op=False):
 def _reduce_scatter_vec(out_local, partial, world, bounds):
     """out_local <- (sum over ranks of partial)[bounds[rank]]."""
     sizes = [e - b for b, e in bounds]
+    if _staged() and partial.is_cuda:
+        h = partial.cpu()
+        dist.all_reduce(h)
+        _, rank = _world()
+        b, e = bounds[rank]
+        out_local.copy_(h[b:e])
+        return
     if len(set(sizes)) == 1 and sizes[0] * world == partial.numel():
         dist.reduce_scatter_tensor(out_local, partial)
     else:

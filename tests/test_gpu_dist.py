@@ -1,0 +1,146 @@
+"""The row-block data-parallel layer (paper_2312_13170_b200.dist) with the REAL
+libpb kernels: two ranks share cuda:0 over gloo (collectives staged through
+the host), each computes its row shard through the C ABI, and the reassembled
+results must match the single-process oracle. This exercises every N>1 code
+path of the kernels' sharded entry points on the one GPU this build has; the
+NCCL transport itself is only exercised on a multi-GPU box.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import pbgen  # noqa: E402
+from tests import parity as P  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_2312_13170_b200 as pb
+    from paper_2312_13170_b200 import dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", 0)
+    H = lambda r, c, s, **kw: torch.from_numpy(pbgen.gen_host(r, c, s, **kw)).to(dev)  # noqa: E731
+    res = {}
+    try:
+        # 3mm: F row blocks + all-gather, E/G local rows
+        n = 512
+        r0, r1 = D.partition(n, world, rank, False, 128)
+        A, B, C, Dm = H(n, n, 1), H(n, n, 2), H(n, n, 3), H(n, n, 4)
+        E, G, F = (torch.empty(r1 - r0, n, device=dev), torch.empty(r1 - r0, n, device=dev),
+                   torch.empty(n, n, device=dev))
+        Fl = torch.empty(r1 - r0, n, device=dev)
+        ws = pb.workspace("3mm", (n, n, n, n, n), dev)
+        D.mm3_rows(None, n, E, A[r0:r1].contiguous(), B, Fl, F, C, Dm, G, ws)
+        # 2mm: row-local
+        tmp = torch.empty(r1 - r0, n, device=dev)
+        D2 = Dm[r0:r1].clone()
+        D.mm2_rows(None, n, 1.5, 1.2, tmp, A[r0:r1].contiguous(), B, C, D2, pb.workspace("2mm", (n,) * 4, dev))
+        torch.cuda.synchronize()
+        res["3mm"] = (r0, r1, G.cpu().numpy(), F.cpu().numpy())
+        res["2mm"] = (r0, r1, D2.cpu().numpy())
+        # syrk / syr2k triangular bands
+        n2, m2 = 768, 260
+        s0, s1 = D.partition(n2, world, rank, True, 256)
+        A2, B2 = H(n2, m2, 1), H(n2, m2, 2)
+        Cf = H(n2, n2, 3, mode=pbgen.SYM)
+        Cb, Cb2 = Cf[s0:s1].clone(), Cf[s0:s1].clone()
+        wsy = pb.workspace("syr2k_rows", (n2, m2, 0, n2), dev)
+        D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb, A2, wsy)
+        D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb2, A2, wsy, B=B2)
+        torch.cuda.synchronize()
+        res["syrk"] = (s0, s1, Cb.cpu().numpy())
+        res["syr2k"] = (s0, s1, Cb2.cpu().numpy())
+        # matvec family
+        nv = 2048
+        v0, v1 = D.partition(nv, world, rank, False, 4)
+        Av, Bv = H(nv, nv, 1), H(nv, nv, 2)
+        vec = {k: H(1, nv, s).view(-1) for k, s in (("x", 6), ("r", 7), ("y2", 7), ("x1", 8), ("x2", 9))}
+        wsm = pb.workspace("atax", (nv, nv), dev)
+        for kern in ("atax", "bicg", "mvt", "gesummv"):
+            v = dict(A=Av[v0:v1].contiguous(), B=Bv[v0:v1].contiguous(), x=vec["x"].clone(), r=vec["r"].clone(),
+                     y2=vec["y2"].clone(), x1=vec["x1"].clone(), x2=vec["x2"].clone(),
+                     y=torch.zeros(nv, device=dev), s=torch.zeros(nv, device=dev), q=torch.zeros(nv, device=dev),
+                     yo=torch.zeros(nv, device=dev), tmp=torch.zeros(v1 - v0, device=dev))
+            D.matvec(None, kern, nv, v, wsm, 1.5, 1.2)
+            torch.cuda.synchronize()
+            out = {"atax": v["y"], "bicg": v["s"], "mvt": v["x2"], "gesummv": v["yo"]}[kern]
+            extra = {"bicg": v["q"], "mvt": v["x1"], "atax": v["tmp"], "gesummv": v["yo"]}[kern]
+            res[kern] = (v0, v1, out.cpu().numpy()[v0:v1], extra.cpu().numpy())
+        q.put((rank, res))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, {"error": repr(e)}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_two_ranks_one_gpu_real_kernels():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert "error" not in out[r], out[r]
+    n = 512
+    A, B, C, Dm = (pbgen.gen_host(n, n, s) for s in (1, 2, 3, 4))
+    E_r, F_r, G_r = oracle.mm3(A, B, C, Dm)
+    _, _, G_s = oracle.mm3(A, B, C, Dm, absmode=True)
+    F_s = oracle.mm3(A, B, C, Dm, absmode=True)[1]
+    t_r, D_r = oracle.mm2(1.5, 1.2, A, B, C, Dm)
+    t_s, D_s = oracle.mm2(1.5, 1.2, A, B, C, Dm, absmode=True)
+    G = np.zeros((n, n))
+    Dg = np.zeros((n, n))
+    for r in range(world):
+        r0, r1, g, f = out[r]["3mm"]
+        G[r0:r1] = g
+        assert P.cerr(f, F_r, F_s) <= P.TOL  # all-gather delivered all of F
+        r0, r1, d = out[r]["2mm"]
+        Dg[r0:r1] = d
+    assert P.cerr(G, G_r, G_s) <= P.TOL and P.cerr(Dg, D_r, D_s) <= P.TOL
+    n2, m2 = 768, 260
+    A2, B2 = pbgen.gen_host(n2, m2, 1), pbgen.gen_host(n2, m2, 2)
+    Cf = pbgen.gen_host(n2, n2, 3, mode=pbgen.SYM)
+    for name, ref, sc in (("syrk", oracle.syrk(1.5, 1.2, Cf, A2), oracle.syrk(1.5, 1.2, Cf, A2, absmode=True)),
+                          ("syr2k", oracle.syr2k(1.5, 1.2, Cf, A2, B2),
+                           oracle.syr2k(1.5, 1.2, Cf, A2, B2, absmode=True))):
+        got = np.zeros((n2, n2))
+        for r in range(world):
+            s0, s1, blk = out[r][name]
+            got[s0:s1] = blk
+        assert P.cerr(got, ref, sc) <= P.TOL, name
+    nv = 2048
+    Av, Bv = pbgen.gen_host(nv, nv, 1), pbgen.gen_host(nv, nv, 2)
+    x, rr, y2, x1, x2 = (pbgen.gen_host(1, nv, s)[0] for s in (6, 7, 7, 8, 9))
+    refs = {"atax": oracle.atax(Av, x)[0], "bicg": oracle.bicg(Av, x, rr)[0],
+            "mvt": oracle.mvt(x1, x2, x, y2, Av)[1], "gesummv": oracle.gesummv(1.5, 1.2, Av, Bv, x)[1]}
+    for k, ref in refs.items():
+        got = np.zeros(nv)
+        for r in range(world):
+            v0, v1, blk, _ = out[r][k]
+            got[v0:v1] = blk
+        assert np.max(np.abs(got - ref) / np.abs(ref)) <= P.TOL, k
