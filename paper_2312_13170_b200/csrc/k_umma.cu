@@ -86,7 +86,8 @@ struct Params {
   int ld_split;
   int tm0, tm1, tiles_n, ratio;  // ratio = tile rows / BN (CG)
   long long num_tiles;
-  int ksplit;                    // K splits per tile (split-K); work unit = (tile, split)
+  int ksplit;                    // K splits of each split tile (split-K)
+  long long split_tiles;         // tiles [0, split_tiles) are split; units of split tiles come first
   float* part;                   // split-K partial tiles [unit][CG][128][BN]
   unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
   int dbg;                       // PB_UMMA_DEBUG (tuning only): 1 = skip partial exchange
@@ -148,6 +149,32 @@ __device__ void tile_coords(const Params& p, long long t, int& tm, int& tn) {
 
 __device__ __forceinline__ void store4(float* p, float a, float b, float c, float d) {
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+
+// Work unit u -> (tile, split, k-block range). Units [0, split_tiles*ksplit) are
+// the K-splits of the split tiles (split-major); the rest are whole tiles. Split
+// tiles go first so their fixup overlaps the whole tiles that follow.
+struct Unit {
+  long long t;
+  int ks, kbA, kbB;
+  bool split;
+};
+__device__ __forceinline__ Unit unit_of(const Params& p, long long u, int nkb_total) {
+  Unit r;
+  const long long rs = p.split_tiles * p.ksplit;
+  if (u < rs) {
+    r.t = u % p.split_tiles;
+    r.ks = (int)(u / p.split_tiles);
+    r.split = p.ksplit > 1;
+  } else {
+    r.t = p.split_tiles + (u - rs);
+    r.ks = 0;
+    r.split = false;
+  }
+  const int S = r.split ? p.ksplit : 1;
+  r.kbA = (int)((long long)nkb_total * r.ks / S);
+  r.kbB = (int)((long long)nkb_total * (r.ks + 1) / S);
+  return r;
 }
 
 // ---- cta_group-specific PTX
@@ -250,7 +277,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   pdl_wait();  // the setup above overlapped the producer kernel's tail (PDL)
   const uint32_t tmem_base = ctl->tmem_base;
   const int nkb_total = p.nkb * p.npairs;
-  const long long num_units = p.num_tiles * p.ksplit;
+  const long long num_units = p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles);
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA loads its own A rows and B half)
@@ -258,13 +285,12 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (long long u = tile0; u < num_units; u += tile_step) {
+        const Unit un = unit_of(p, u, nkb_total);
         int tm, tn;
-        tile_coords(p, u % p.num_tiles, tm, tn);
+        tile_coords(p, un.t, tm, tn);
         const int arow = tm * C::PAIR_M + (int)rank * BM;
         const int brow = tn * BN + (int)rank * C::B_ROWS;
-        const int ks = (int)(u / p.num_tiles);
-        const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
-        for (int kb = kbA; kb < kbB; ++kb) {
+        for (int kb = un.kbA; kb < un.kbB; ++kb) {
           mbar_wait(&ctl->empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           const int pair = kb >= p.nkb;
@@ -292,8 +318,8 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       int chunk_it = 0;
       int ul = 0;
       for (long long u = tile0; u < num_units; u += tile_step, ++ul) {
-        const int ks = (int)(u / p.num_tiles);
-        const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
+        const Unit un = unit_of(p, u, nkb_total);
+        const int kbA = un.kbA, kbB = un.kbB;
         TSTAMP(ul, 0);
         for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
           const int slot = chunk_it & 1;
@@ -340,9 +366,9 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     int chunk_it = 0;
     int ul = 0;
     for (long long u = tile0; u < num_units; u += tile_step, ++ul) {
-      const long long t = u % p.num_tiles;  // split-major order: a tile's splits run apart in time
-      const int ks = (int)(u / p.num_tiles);
-      const int kbA = (int)((long long)nkb_total * ks / p.ksplit), kbB = (int)((long long)nkb_total * (ks + 1) / p.ksplit);
+      const Unit un = unit_of(p, u, nkb_total);
+      const long long t = un.t;
+      const int kbA = un.kbA, kbB = un.kbB;
       int tm, tn;
       tile_coords(p, t, tm, tn);
       float acc[EPI_COLS];  // this thread's row x column-half of the tile, fp32 registers
@@ -382,14 +408,14 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         }
       }
       if (warp == 2 && lane == 0) TSTAMP(ul, 3);
-      if (p.ksplit > 1 && (flags & EPI_PARTIAL)) {  // partials only; launch_gram_combine finishes
+      if (un.split && (flags & EPI_PARTIAL)) {  // partials only; launch_gram_combine finishes
         const int rl = q * 32 + lane;
         float4* mine = reinterpret_cast<float4*>(p.part) + ((u * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
 #pragma unroll
         for (int c = 0; c < EPI_COLS; c += 4) mine[(c / 4) * BM] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
         continue;
       }
-      if (p.ksplit > 1 && p.dbg != 1) {
+      if (un.split && p.dbg != 1) {
         // Split-K: post this unit's partial tile, count arrivals; the LAST unit of
         // the tile to arrive sums all partials in split order (deterministic,
         // no waiting) and runs the epilogue; the others are done with the tile.
@@ -415,7 +441,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         // whichever unit arrives last)
         for (int k2 = 0; k2 < p.ksplit; ++k2) {
           const float4* o = reinterpret_cast<const float4*>(p.part) +
-                            (((k2 * p.num_tiles + t) * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
+                            (((k2 * p.split_tiles + t) * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
 #pragma unroll
           for (int c = 0; c < EPI_COLS; c += 4) {
             const float4 v = __ldcg(o + (c / 4) * BM);
@@ -560,7 +586,7 @@ int num_sms() {
 }
 
 template <int CG, int BN>
-cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, int* launches) {
+cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_tiles, cudaStream_t s, int* launches) {
   using C = Cfg<CG, BN>;
   const int tiles_m = (d.M + C::PAIR_M - 1) / C::PAIR_M;
   p.tiles_n = (d.N + BN - 1) / BN;
@@ -574,6 +600,7 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
     nt += (d.flags & EPI_TRI) ? std::min(p.ratio * (tm + 1), p.tiles_n) : p.tiles_n;
   p.num_tiles = nt;
   p.ksplit = ksplit;
+  p.split_tiles = ksplit > 1 ? split_tiles : 0;
   static const int dbg = getenv("PB_UMMA_DEBUG") ? atoi(getenv("PB_UMMA_DEBUG")) : 0;
   p.dbg = dbg;
   static const bool timing = getenv("PB_UMMA_TIMING") != nullptr;
@@ -584,7 +611,7 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
   p.part = d.part;
   p.counters = d.counters;
   if (ksplit > 1) {
-    cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)nt * CG * sizeof(unsigned), s);
+    cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)p.split_tiles * CG * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
   }
   CUtensorMap maps[8];
@@ -605,7 +632,7 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
     attr_set = true;
   }
   const long long max_units = num_sms() / CG;
-  const long long work = p.num_tiles * p.ksplit;
+  const long long work = p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles);
   const long long units = work < max_units ? work : max_units;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
@@ -645,8 +672,8 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, cudaStream_t s, i
             "stores %.1f us (n=%zu)\n", (t1 - t0) / 1e3, med(mma), med(drain_lag), med(split), med(store), mma.size());
   }
   if (getenv("PB_TRACE"))
-    fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld ksplit=%d grid=%lld\n", CG, BN,
-            d.M, d.N, d.K, d.npairs, d.flags, p.num_tiles, p.ksplit, units * CG);
+    fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld split %lldx%d grid=%lld\n", CG,
+            BN, d.M, d.N, d.K, d.npairs, d.flags, p.num_tiles, p.split_tiles, p.ksplit, units * CG);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -675,7 +702,7 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
   for (int k = 0; k < NC; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = 0; s < p.ksplit; ++s) {
     const float4* base = reinterpret_cast<const float4*>(p.part) +
-                         (((s * p.num_tiles + t) * CG + rank) * (long long)BN) * (BM / 4) + rb * 32 + lane;
+                         (((s * p.split_tiles + t) * CG + rank) * (long long)BN) * (BM / 4) + rb * 32 + lane;
     float4 v[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) v[k] = __ldcg(base + (long long)(w + 8 * k) * BM);
@@ -720,13 +747,13 @@ cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag
   if (pl.ksplit <= 1) return cudaSuccess;
   Params p{};
   p.M = d.M; p.N = d.N; p.flags = d.flags; p.alpha = d.alpha; p.out = d.out; p.ldo = d.ldo;
-  p.part = d.part; p.ksplit = pl.ksplit; p.num_tiles = pl.tiles;
+  p.part = d.part; p.ksplit = pl.ksplit; p.num_tiles = pl.tiles; p.split_tiles = pl.split_tiles;
   const int pm = pl.cfg == 1 ? 128 : 256, bn = pl.cfg == 3 ? 256 : 128;
   p.tm0 = 0;
   p.tm1 = (d.M + pm - 1) / pm;
   p.tiles_n = (d.N + bn - 1) / bn;
   p.ratio = pm / bn;
-  const unsigned grid = (unsigned)(pl.tiles * (pm / 128) * 4);  // (tile, rank, 32-row block)
+  const unsigned grid = (unsigned)(pl.split_tiles * (pm / 128) * 4);  // (split tile, rank, 32-row block)
   const int dg = diag_one ? 1 : 0;
   cudaError_t e;
   if (pl.cfg == 3) e = launch_pdl(gram_combine_kernel<2, 256>, dim3(grid), dim3(256), 0, s, p, dg);
@@ -757,9 +784,9 @@ cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
   const UmmaPlan pl = umma_plan(d);
   int ks = pl.ksplit;
   if (ks > 1 && (d.part == nullptr || d.counters == nullptr)) ks = 1;
-  if (pl.cfg == 3) return launch_cg<2, 256>(d, p, ks, s, launches);
-  if (pl.cfg == 2) return launch_cg<2, 128>(d, p, ks, s, launches);
-  return launch_cg<1, 128>(d, p, ks, s, launches);
+  if (pl.cfg == 3) return launch_cg<2, 256>(d, p, ks, pl.split_tiles, s, launches);
+  if (pl.cfg == 2) return launch_cg<2, 128>(d, p, ks, pl.split_tiles, s, launches);
+  return launch_cg<1, 128>(d, p, ks, pl.split_tiles, s, launches);
 }
 
 // Tile configuration and split-K factor: a pure function of the shape (tuned
@@ -785,18 +812,19 @@ UmmaPlan umma_plan(const GemmDesc& d) {
   for (int tm = tm0; tm < tm1; ++tm) nt += (d.flags & EPI_TRI) ? std::min(ratio * (tm + 1), tiles_n) : tiles_n;
   pl.tiles = nt;
   const int nkb_total = ((d.K + BK - 1) / BK) * d.npairs;
-  const int units = 148 / cg;
-  double best = -1.0;
-  pl.ksplit = 1;
-  for (int ks = 1; ks <= 4; ++ks) {
-    if (ks > 1 && nkb_total / ks < 8) break;
-    const long long w = nt * ks;
-    const double eff = (double)w / ((double)units * ((w + units - 1) / units)) * (1.0 - 0.03 * (ks - 1));
-    if (eff > best + 1e-9) { best = eff; pl.ksplit = ks; }
-  }
-  if (force_ks >= 1 && force_ks <= 8 && nkb_total / force_ks >= 1) pl.ksplit = force_ks;
-  pl.part_bytes = pl.ksplit > 1 ? (size_t)nt * pl.ksplit * cg * 128 * bn * sizeof(float) : 0;
-  pl.counter_bytes = pl.ksplit > 1 ? (size_t)nt * cg * sizeof(unsigned) : 0;
+  const long long units = 148 / cg;
+  // Data-parallel + split-K hybrid: whole tiles fill floor(T / units) waves; the
+  // R = T mod units remainder tiles are split S ways (S <= units / R, <= 4, and
+  // >= 8 k-blocks per split) so the last partial wave is ~full of 1/S-size units.
+  long long R = nt < units ? nt : nt % units;
+  int S = R > 0 ? (int)std::min<long long>(4, units / R) : 1;
+  while (S > 1 && nkb_total / S < 8) --S;
+  if (force_ks >= 1 && force_ks <= 8 && nkb_total / force_ks >= 1) { S = force_ks; R = nt; }
+  if (S <= 1) { S = 1; R = 0; }
+  pl.ksplit = S;
+  pl.split_tiles = R;
+  pl.part_bytes = S > 1 ? (size_t)R * S * cg * 128 * bn * sizeof(float) : 0;
+  pl.counter_bytes = S > 1 ? (size_t)R * cg * sizeof(unsigned) : 0;
   return pl;
 }
 

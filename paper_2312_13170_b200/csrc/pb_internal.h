@@ -50,8 +50,9 @@ struct GemmDesc {
 
 struct UmmaPlan {
   int cfg = 1;     // 1: 1-CTA 128x128, 2: 2-CTA 256x128, 3: 2-CTA 256x256
-  int ksplit = 1;  // split-K factor
+  int ksplit = 1;  // split-K factor of the split tiles
   long long tiles = 0;
+  long long split_tiles = 0;  // tiles [0, split_tiles) are split ksplit ways
   size_t part_bytes = 0, counter_bytes = 0;
 };
 UmmaPlan umma_plan(const GemmDesc& d);
