@@ -315,7 +315,11 @@ def run_ours(args):
 
     if rank == 0:
         hbm, bf16, bf16s, src = peaks()
-        tf32 = bf16 * 0.5  # kind::tf32 runs at half the kind::f16 rate (nominal 1.1 vs 2.25 PF)
+        # Kernels are timed inside a long step (K steps of the whole suite, power-capped):
+        # the sustained bf16 figure is the denominator (B200_PROFILING.md); the burst-basis
+        # fraction is reported beside it.
+        useful_burst = bf16 * 0.5 / 3.0
+        tf32 = bf16s * 0.5  # kind::tf32 runs at half the kind::f16 rate (nominal 1.1 vs 2.25 PF)
         useful = tf32 / 3.0  # three TF32 MMAs per fp32-accurate FMA (3xTF32)
         ms = total_ms / args.steps
         flops = sum(W[k][0] for k in kernels)
@@ -326,6 +330,8 @@ def run_ours(args):
             kern[k] = {"ms": round(per_k[k], 4), "gflops": round(f / t / 1e9, 1), "gbs": round(b / t / 1e9, 1),
                        "bound": BOUND[k],
                        "frac": round((b / t / 1e9) / hbm if BOUND[k] == "hbm" else (f / t / 1e12) / useful, 4)}
+            if BOUND[k] == "tensor":
+                kern[k]["frac_burst"] = round((f / t / 1e12) / useful_burst, 4)
         dom = max(kernels, key=lambda k: per_k[k])
         f, b = W[dom]
         t = per_k[dom] * 1e-3
@@ -336,7 +342,8 @@ def run_ours(args):
         else:
             roof = {"bound": "tensor", "achieved": round(f / t / 1e12, 2), "peak": round(useful, 1),
                     "unit": "TFLOP/s", "frac": round(f / t / 1e12 / useful, 4), "traffic": None, "kernel": dom,
-                    "peak_source": f"{src} bf16 burst {bf16} TF/s x 0.5 (tf32/bf16 nominal ratio) / 3 (3xTF32)"}
+                    "peak_source": f"{src} bf16 sustained {bf16s} TF/s x 0.5 (tf32/bf16 nominal ratio) / 3 (3xTF32)",
+                    "peak_burst": round(useful_burst, 1), "frac_burst": round(f / t / 1e12 / useful_burst, 4)}
         tr = load_traffic(dom)
         if tr is not None:
             roof["traffic"] = tr

@@ -165,7 +165,7 @@ __device__ __forceinline__ Unit unit_of(const Params& p, long long u, int nkb_to
   if (u < rs) {
     r.t = u % p.split_tiles;
     r.ks = (int)(u / p.split_tiles);
-    r.split = p.ksplit > 1;
+    r.split = true;
   } else {
     r.t = p.split_tiles + (u - rs);
     r.ks = 0;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         for (int c = 0; c < EPI_COLS; c += 4) mine[(c / 4) * BM] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
         continue;
       }
-      if (un.split && p.dbg != 1) {
+      if (un.split && p.ksplit > 1 && p.dbg != 1) {
         // Split-K: post this unit's partial tile, count arrivals; the LAST unit of
         // the tile to arrive sums all partials in split order (deterministic,
         // no waiting) and runs the epilogue; the others are done with the tile.
@@ -600,7 +600,7 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
     nt += (d.flags & EPI_TRI) ? std::min(p.ratio * (tm + 1), p.tiles_n) : p.tiles_n;
   p.num_tiles = nt;
   p.ksplit = ksplit;
-  p.split_tiles = ksplit > 1 ? split_tiles : 0;
+  p.split_tiles = (ksplit > 1 || (d.flags & EPI_PARTIAL)) ? split_tiles : 0;
   static const int dbg = getenv("PB_UMMA_DEBUG") ? atoi(getenv("PB_UMMA_DEBUG")) : 0;
   p.dbg = dbg;
   static const bool timing = getenv("PB_UMMA_TIMING") != nullptr;
@@ -610,7 +610,7 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
   if (timing) cudaMemsetAsync(tbuf, 0, 148 * 16 * 8 * sizeof(unsigned long long), s);
   p.part = d.part;
   p.counters = d.counters;
-  if (ksplit > 1) {
+  if (ksplit > 1 && !(d.flags & EPI_PARTIAL)) {
     cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)p.split_tiles * CG * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
   }
@@ -679,12 +679,28 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
 
 // Gram combine (EPI_PARTIAL): one CTA per (tile, rank, 32-row block). Partials
 // (layout [unit][rank][half][c4][row][4]) are read with lanes on rows (coalesced),
-// summed in split order (deterministic), scaled, staged in padded smem, then written
+// summed in split order (deterministic), staged in padded smem, then written
 // row-major with lanes on columns and mirrored with lanes on rows (both coalesced).
+// With band statistics (banded prep, reading R18) it adds the between-band scatter
+//   sum_b n_b (mu_b - c)_i (mu_b - c)_j,   c = sum_b n_b mu_b / float_n,
+// and for correlation scales by inv_i inv_j, inv = 1/(sqrt(float_n) sd), sd from
+// (sum_b M2_b + sum_b n_b (mu_b - c)^2) / float_n with the eps rule (fp64).
+struct CombineStats {
+  const double* band_mean;
+  const double* band_m2;
+  int nbands, n, corr;
+  double float_n, eps;
+  float* mean_out;
+  float* sd_out;
+};
+constexpr int MAXB = 8;
+
 template <int CG, int BN>
-__global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int diag_one) {
-  constexpr int PAIR_M = BM * CG, C4 = BN / 4;
+__global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int diag_one, const CombineStats cs) {
+  constexpr int PAIR_M = BM * CG, C4 = BN / 4, NCOL = 32 + BN;
   __shared__ float tile[32][BN + 1];
+  __shared__ float dev_s[MAXB][NCOL];  // mu_b - c (fp32 is ample: the term is summed in fp64) for rows, columns
+  __shared__ double inv_s[NCOL];
   pdl_wait();
   const int blk = blockIdx.x;
   const long long t = blk / (CG * 4);
@@ -694,6 +710,42 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
   const int row_base = tm * PAIR_M + rank * BM + rb * 32;  // first output row of this block
   const int col_base = tn * BN;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // 8 warps
+  const bool banded = cs.band_mean != nullptr;
+  if (banded) {
+    for (int e = threadIdx.x; e < NCOL; e += 256) {
+      const int col = e < 32 ? row_base + e : col_base + (e - 32);
+      double S = 0.0, M2 = 0.0, mu[MAXB];
+      int nb[MAXB];
+      for (int b = 0; b < cs.nbands; ++b) {
+        nb[b] = min(256, cs.n - 256 * b);
+        mu[b] = col < p.N ? cs.band_mean[(long long)b * p.N + col] : 0.0;
+        S += nb[b] * mu[b];
+      }
+      const double c = S / cs.float_n;
+      double between = 0.0;
+      for (int b = cs.nbands; b < MAXB; ++b) dev_s[b][e] = 0.f;
+      for (int b = 0; b < cs.nbands; ++b) {
+        const double d = mu[b] - c;
+        dev_s[b][e] = (float)d;
+        between += nb[b] * d * d;
+        if (cs.corr && col < p.N) M2 += cs.band_m2[(long long)b * p.N + col];
+      }
+      double inv = 1.0;
+      double sd = 0.0;
+      if (cs.corr) {
+        sd = sqrt((M2 + between) / cs.float_n);
+        if (sd <= cs.eps) sd = 1.0;
+        inv = 1.0 / (sqrt(cs.float_n) * sd);
+      }
+      inv_s[e] = inv;
+      // column statistics outputs: written once, by the diagonal tile's first block
+      if (e >= 32 && col < p.N && rank == 0 && rb == 0 && tm == tn / p.ratio) {
+        if (cs.mean_out) cs.mean_out[col] = (float)c;
+        if (cs.corr && cs.sd_out) cs.sd_out[col] = (float)sd;
+      }
+    }
+    __syncthreads();
+  }
   // read + sum: warp w handles c4 = w, w+8, ...; lane = row within the block. All
   // C4/8 loads of one split are issued before any is used (memory-level parallelism).
   constexpr int NC = C4 / 8;
@@ -711,13 +763,34 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
       acc[k].x += v[k].x; acc[k].y += v[k].y; acc[k].z += v[k].z; acc[k].w += v[k].w;
     }
   }
+  // between-band term for row `lane`: er[b] = n_b (mu_b - c)_row (registers); the column
+  // factors come from smem as warp-wide broadcasts; 8 fp32 FMAs per element.
+  float er[MAXB];
+  float rinv = 1.f;
+  if (banded) {
+#pragma unroll
+    for (int b = 0; b < MAXB; ++b) er[b] = b < cs.nbands ? (float)min(256, cs.n - 256 * b) * dev_s[b][lane] : 0.f;
+    rinv = (float)inv_s[lane];
+  }
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int c4 = w + 8 * k;
-    tile[lane][4 * c4 + 0] = p.alpha * acc[k].x;
-    tile[lane][4 * c4 + 1] = p.alpha * acc[k].y;
-    tile[lane][4 * c4 + 2] = p.alpha * acc[k].z;
-    tile[lane][4 * c4 + 3] = p.alpha * acc[k].w;
+    const float g[4] = {acc[k].x, acc[k].y, acc[k].z, acc[k].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int cc = 4 * c4 + e;
+      float v = g[e];
+      if (banded) {
+        float between = 0.f;
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) between = fmaf(er[b], dev_s[b][32 + cc], between);
+        v += between;
+        v = cs.corr ? v * rinv * (float)inv_s[32 + cc] : p.alpha * v;
+      } else {
+        v = p.alpha * v;
+      }
+      tile[lane][cc] = v;
+    }
   }
   __syncthreads();
   // direct lower part out[i][j], j <= i: lanes on columns
@@ -743,8 +816,14 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
 
 }  // namespace
 
-cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, cudaStream_t s, int* launches) {
-  if (pl.ksplit <= 1) return cudaSuccess;
+cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, const GramStats& st,
+                                cudaStream_t s, int* launches) {
+  if (pl.split_tiles <= 0) return cudaSuccess;
+  if (st.nbands > MAXB) return cudaErrorInvalidValue;
+  CombineStats cs;
+  cs.band_mean = st.band_mean; cs.band_m2 = st.band_m2; cs.nbands = st.nbands; cs.n = st.n;
+  cs.corr = st.band_m2 != nullptr; cs.float_n = st.float_n; cs.eps = st.eps;
+  cs.mean_out = st.mean_out; cs.sd_out = st.sd_out;
   Params p{};
   p.M = d.M; p.N = d.N; p.flags = d.flags; p.alpha = d.alpha; p.out = d.out; p.ldo = d.ldo;
   p.part = d.part; p.ksplit = pl.ksplit; p.num_tiles = pl.tiles; p.split_tiles = pl.split_tiles;
@@ -756,9 +835,9 @@ cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag
   const unsigned grid = (unsigned)(pl.split_tiles * (pm / 128) * 4);  // (split tile, rank, 32-row block)
   const int dg = diag_one ? 1 : 0;
   cudaError_t e;
-  if (pl.cfg == 3) e = launch_pdl(gram_combine_kernel<2, 256>, dim3(grid), dim3(256), 0, s, p, dg);
-  else if (pl.cfg == 2) e = launch_pdl(gram_combine_kernel<2, 128>, dim3(grid), dim3(256), 0, s, p, dg);
-  else e = launch_pdl(gram_combine_kernel<1, 128>, dim3(grid), dim3(256), 0, s, p, dg);
+  if (pl.cfg == 3) e = launch_pdl(gram_combine_kernel<2, 256>, dim3(grid), dim3(256), 0, s, p, dg, cs);
+  else if (pl.cfg == 2) e = launch_pdl(gram_combine_kernel<2, 128>, dim3(grid), dim3(256), 0, s, p, dg, cs);
+  else e = launch_pdl(gram_combine_kernel<1, 128>, dim3(grid), dim3(256), 0, s, p, dg, cs);
   if (launches) ++*launches;
   return e;
 }
@@ -784,6 +863,7 @@ cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
   const UmmaPlan pl = umma_plan(d);
   int ks = pl.ksplit;
   if (ks > 1 && (d.part == nullptr || d.counters == nullptr)) ks = 1;
+  if ((d.flags & EPI_PARTIAL) && d.part == nullptr) return cudaErrorInvalidValue;
   if (pl.cfg == 3) return launch_cg<2, 256>(d, p, ks, pl.split_tiles, s, launches);
   if (pl.cfg == 2) return launch_cg<2, 128>(d, p, ks, pl.split_tiles, s, launches);
   return launch_cg<1, 128>(d, p, ks, pl.split_tiles, s, launches);
@@ -821,10 +901,11 @@ UmmaPlan umma_plan(const GemmDesc& d) {
   while (S > 1 && nkb_total / S < 8) --S;
   if (force_ks >= 1 && force_ks <= 8 && nkb_total / force_ks >= 1) { S = force_ks; R = nt; }
   if (S <= 1) { S = 1; R = 0; }
+  if (d.flags & EPI_PARTIAL) R = nt;  // every tile through partials (the combine finishes all)
   pl.ksplit = S;
   pl.split_tiles = R;
-  pl.part_bytes = S > 1 ? (size_t)R * S * cg * 128 * bn * sizeof(float) : 0;
-  pl.counter_bytes = S > 1 ? (size_t)R * cg * sizeof(unsigned) : 0;
+  pl.part_bytes = R > 0 ? (size_t)R * S * cg * 128 * bn * sizeof(float) : 0;
+  pl.counter_bytes = (S > 1 && !(d.flags & EPI_PARTIAL)) ? (size_t)R * cg * sizeof(unsigned) : 0;
   return pl;
 }
 

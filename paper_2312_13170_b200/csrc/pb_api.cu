@@ -184,11 +184,21 @@ Ws3mm ws_3mm(Carve& c, int ni, int nj, int nk, int nl, int nm) {
   w.sk = take_splitk(c, {shape(nj, nl, nm), shape(ni, nj, nk), shape(ni, nl, nj)});
   return w;
 }
-struct WsStat { SplitBuf xt; SplitK sk; };
+// covariance/correlation: n <= MAX_BANDED rows use the banded single-pass prep
+// (band-centred operand + between-band scatter in the combine, reading R18);
+// longer columns use the exact two-phase prep (mean first, then centre).
+constexpr int MAX_BANDED = 8 * 256;
+inline bool banded_stats(int n) { return n <= MAX_BANDED; }
+struct WsStat { SplitBuf xt; SplitK sk; double* band_mean = nullptr; double* band_m2 = nullptr; };
 WsStat ws_stat(Carve& c, int m, int n) {
   WsStat w;
   w.xt = take_split(c, m, n);
-  w.sk = take_splitk(c, {shape(m, m, n, 1, EPI_TRI)});
+  const bool banded = banded_stats(n);
+  w.sk = take_splitk(c, {shape(m, m, n, 1, EPI_TRI | (banded ? EPI_PARTIAL : 0u))});
+  if (banded) {
+    w.band_mean = c.take<double>((size_t)band_count(n) * m);
+    w.band_m2 = c.take<double>((size_t)band_count(n) * m);
+  }
   return w;
 }
 struct WsSyrk { SplitBuf a, b; SplitK sk; };
@@ -485,20 +495,37 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
   WsStat w = ws_stat(c, m, n);
   cudaStream_t st = S(s);
   int L = 0;
-  PB_CUDA(launch_stats_split(data, n, m, (double)float_n, (double)eps, corr, w.xt.hi, w.xt.lo, w.xt.ld, mean,
-                             corr ? stddev : nullptr, st));
+  const bool banded = banded_stats(n);
+  GramStats gs;
+  if (banded) {  // one pass: band-centred split + per-band column statistics
+    PB_CUDA(launch_band_prep(data, n, m, corr, w.xt.hi, w.xt.lo, w.xt.ld, w.band_mean, corr ? w.band_m2 : nullptr, st));
+    gs.band_mean = w.band_mean;
+    gs.band_m2 = corr ? w.band_m2 : nullptr;
+    gs.nbands = band_count(n);
+    gs.n = n;
+    gs.float_n = (double)float_n;
+    gs.eps = (double)eps;
+    gs.mean_out = mean;
+    gs.sd_out = corr ? stddev : nullptr;
+  } else {  // exact mean first, then centre (and normalise) into the split operand
+    PB_CUDA(launch_stats_split(data, n, m, (double)float_n, (double)eps, corr, w.xt.hi, w.xt.lo, w.xt.ld, mean,
+                               corr ? stddev : nullptr, st));
+  }
   ++L;
   GemmDesc d;  // Gram core: out[i][j] = alpha * sum_k Xt[i][k] Xt[j][k], lower tiles + mirror
   d.M = m; d.N = m; d.K = n;
   d.a[0] = w.xt.op(); d.b[0] = w.xt.op();
-  d.flags = EPI_TRI | EPI_MIRROR | EPI_OUT | (corr ? EPI_DIAG_ONE : 0u);
-  d.alpha = corr ? 1.0f : (float)(1.0 / ((double)float_n - 1.0));
+  d.flags = EPI_TRI | EPI_MIRROR | EPI_OUT | (corr ? EPI_DIAG_ONE : 0u) | (banded ? EPI_PARTIAL : 0u);
+  d.alpha = (corr && !banded) ? 1.0f : (float)(1.0 / ((double)float_n - 1.0));
   d.out = out; d.ldo = m;
   w.sk.attach(d);
-  const UmmaPlan pl = umma_plan(d);
-  if (pl.ksplit > 1 && w.sk.part) d.flags |= EPI_PARTIAL;  // split-K: partials + combine kernel
+  UmmaPlan pl = umma_plan(d);
+  if (!banded && pl.ksplit > 1 && w.sk.part) {  // split-K: partials + combine kernel
+    d.flags |= EPI_PARTIAL;
+    pl = umma_plan(d);
+  }
   PB_CUDA(launch_umma_gemm(d, st, &L));
-  if (d.flags & EPI_PARTIAL) PB_CUDA(launch_gram_combine(d, pl, corr, st, &L));
+  if (d.flags & EPI_PARTIAL) PB_CUDA(launch_gram_combine(d, pl, corr, gs, st, &L));
   g_launches = L;
   return PB_OK;
 }

@@ -26,7 +26,7 @@ enum : uint32_t {
   EPI_OUT = 1u << 4,       // write fp32 out[i][j]
   EPI_SPLIT = 1u << 5,     // write hi/lo split of v at [i][j] (next GEMM's K-major A operand)
   EPI_SPLIT_T = 1u << 6,   // write hi/lo split of v at [j][i] (next GEMM's K-major B operand)
-  EPI_PARTIAL = 1u << 7,   // split-K: only write the per-split partial tiles (a combine kernel finishes)
+  EPI_PARTIAL = 1u << 7,   // every tile only writes (per-split) partials; launch_gram_combine finishes
 };
 
 struct GemmDesc {
@@ -57,9 +57,20 @@ struct UmmaPlan {
 };
 UmmaPlan umma_plan(const GemmDesc& d);
 cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches);
+// Statistics the Gram combine needs (nullptr band_mean: the operand was centred exactly).
+struct GramStats {
+  const double* band_mean = nullptr;  // [nbands][m]
+  const double* band_m2 = nullptr;    // [nbands][m] (correlation)
+  int nbands = 0, n = 0;
+  double float_n = 0.0, eps = 0.0;
+  float* mean_out = nullptr;
+  float* sd_out = nullptr;
+};
+
 // Gram finish for EPI_PARTIAL launches (plan pl): out[i][j] = alpha * sum_s partial_s for
 // j <= i, mirrored to out[j][i]; diag_one -> out[i][i] = 1.
-cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, cudaStream_t s, int* launches);
+cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, const GramStats& st,
+                                cudaStream_t s, int* launches);
 
 // ---- split / prep (k_split.cu) ----------------------------------------------
 // hi/lo split of a rows x cols matrix; same layout (ldo = ld of output).
@@ -77,6 +88,11 @@ cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* h
 cudaError_t launch_stats_split(const float* data, int n, int m, double float_n, double eps, bool corr, float* hiT,
                                float* loT, int ldo, float* mean_out, float* sd_out, cudaStream_t s);
 
+// Banded single-pass prep (n <= 8 * 256): band-centred split + per-band column
+// means (and M2 for correlation), fp64 [band_count(n)][m].
+int band_count(int n);
+cudaError_t launch_band_prep(const float* data, int n, int m, bool corr, float* hiT, float* loT, int ldo,
+                             double* band_mean, double* band_m2, cudaStream_t s);
 // ---- matrix-vector family (k_matvec.cu) -------------------------------------
 // y[i] = alpha * A_i.x + beta * B_i.x (B may be null -> beta ignored); tmp[i] = A_i.x (optional).
 cudaError_t launch_rowdot(const float* A, const float* B, const float* x, int rows, int cols, float alpha,

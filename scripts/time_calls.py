@@ -39,6 +39,11 @@ def main():
         ws = pb.workspace("gemm", (n, n, n), dev)
         f = lambda: pb.pb_gemm(n, n, n, 1.5, 1.2, C, A, B, ws=ws)  # noqa: E731
         flops = 2 * n ** 3
+    elif k == "2mm":
+        A, B, C, Dm, tmp = g(n, n, 1), g(n, n, 2), g(n, n, 3), g(n, n, 4), torch.empty(n, n, device=dev)
+        ws = pb.workspace("2mm", (n,) * 4, dev)
+        f = lambda: pb.pb_2mm(n, n, n, n, 1.5, 1.2, tmp, A, B, C, Dm, ws=ws)  # noqa: E731
+        flops = 4 * n ** 3
     elif k == "syrk":
         A, C = g(n, n, 1), g(n, n, 3)
         ws = pb.workspace("syrk", (n, n), dev)
