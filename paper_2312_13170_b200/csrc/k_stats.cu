@@ -13,6 +13,7 @@ namespace pb {
 namespace {
 
 // ------------------------------------------------------------------ fused prep
+// Used for long columns (n > 2048; shorter ones take the banded prep below).
 // One CTA owns PC = 16 columns of data (n x m) and all n rows:
 //  pass 1: fp64 sums (and sums of squares) of its columns -> mean, stddev (eps
 //          rule), inv = 1/(sqrt(float_n)*sd) (correlation) or 1 (covariance);
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(PT, 1) stats_split_kernel(const float* __restr
     const int c = c0 + 4 * cq;
     double s[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0};
     if (c < m) {
-      constexpr int U = 16;  // rows in flight per thread
+      constexpr int U = 8;  // rows in flight per thread
       for (int r0 = rl; r0 < n; r0 += U * (PT / 4)) {
         float4 v[U];
 #pragma unroll
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(PT, 1) stats_split_kernel(const float* __restr
   // ---- pass 2: 4x4 blocks (4 rows x 4 columns); lanes walk consecutive row quads
   const int nrq = (n + 3) / 4;
   const int nblk = nrq * (PC / 4);
-  constexpr int B = 4;  // 4x4 blocks whose loads are in flight together
+  constexpr int B = 2;  // 4x4 blocks whose loads are in flight together
   for (int b0 = t; b0 < nblk; b0 += B * PT) {
     float x[B][4][4];  // x[block][row u][col v]
 #pragma unroll
@@ -124,125 +125,6 @@ __global__ void __launch_bounds__(PT, 1) stats_split_kernel(const float* __restr
     }
     }
   }
-}
-
-// ------------------------------------------------------------------ fused prep, cluster form
-// For n <= 2048: an 8-CTA cluster owns 64 columns; CTA r of the cluster holds rows
-// [r*R, (r+1)*R) (R <= 256) of those columns in REGISTERS (4x4 blocks, 4 per thread),
-// posts its fp64 column sums (and sums of squares) into every peer's smem through
-// DSMEM, and after one cluster barrier each CTA reduces the 8 posts in rank order
-// (deterministic, identical in every CTA), then centres / normalises / splits its
-// blocks from registers and writes them transposed. Data is read exactly once.
-constexpr int CL_CTAS = 8, CL_COLS = 64, CL_T = 256, CL_B = 4;
-
-template <bool CORR>
-__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_T, 2)
-    stats_split_cluster_kernel(const float* __restrict__ data, int n, int m, double float_n, double eps,
-                               float* __restrict__ hiT, float* __restrict__ loT, int ldo,
-                               float* __restrict__ mean_out, float* __restrict__ sd_out) {
-  __shared__ double post_s[CL_CTAS][CL_COLS], post_q[CL_CTAS][CL_COLS];
-  __shared__ double red_s[CL_T / 16][CL_COLS], red_q[CORR ? CL_T / 16 : 1][CL_COLS];
-  __shared__ double mu_s[CL_COLS], inv_s[CL_COLS];
-  pdl_wait();
-  const uint32_t rank = cluster_rank();
-  const int t = threadIdx.x;
-  const int c0 = (blockIdx.x / CL_CTAS) * CL_COLS;
-  const int rows_per = ((n + CL_CTAS - 1) / CL_CTAS + 3) / 4 * 4;
-  const int r_begin = (int)rank * rows_per;
-  // thread -> (column quad cq in 0..15, row-quad lane rq0 in 0..15); blocks rq0 + 16*k
-  const int rq0 = t & 15, cq = t >> 4;  // lanes on row quads: the transposed stores are coalesced
-  const int c = c0 + 4 * cq;
-  float x[CL_B][4][4];
-  double s[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int k = 0; k < CL_B; ++k) {
-    const int r = r_begin + 4 * (rq0 + 16 * k);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (c < m && r + u < n && r + u < r_begin + rows_per)
-        v = *reinterpret_cast<const float4*>(data + (long long)(r + u) * m + c);
-      x[k][u][0] = v.x; x[k][u][1] = v.y; x[k][u][2] = v.z; x[k][u][3] = v.w;
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < CL_B; ++k)
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const double a = x[k][u][v];
-        s[v] += a;
-        if (CORR) q[v] += a * a;
-      }
-  // CTA reduction over the 16 row lanes (fixed order)
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    red_s[rq0][4 * cq + v] = s[v];
-    if (CORR) red_q[rq0][4 * cq + v] = q[v];
-  }
-  __syncthreads();
-  if (t < CL_COLS) {
-    double S = 0.0, Q = 0.0;
-    for (int k = 0; k < CL_T / 16; ++k) {
-      S += red_s[k][t];
-      if (CORR) Q += red_q[k][t];
-    }
-    // post into every CTA of the cluster (including this one)
-    const uint32_t ps = smem_u32(&post_s[rank][t]), pq = smem_u32(&post_q[rank][t]);
-    for (int d = 0; d < CL_CTAS; ++d) {
-      const uint32_t a = map_peer(ps, d);
-      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(S) : "memory");
-      if (CORR) {
-        const uint32_t b = map_peer(pq, d);
-        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(b), "d"(Q) : "memory");
-      }
-    }
-  }
-  cluster_sync_all();
-  if (t < CL_COLS) {
-    double S = 0.0, Q = 0.0;
-    for (int d = 0; d < CL_CTAS; ++d) {  // rank order: identical in every CTA
-      S += post_s[d][t];
-      if (CORR) Q += post_q[d][t];
-    }
-    const double mu = S / float_n;
-    double inv = 1.0;
-    const bool writer = rank == 0 && c0 + t < m;
-    if (writer && mean_out) mean_out[c0 + t] = (float)mu;
-    if (CORR) {
-      double var = (Q - S * mu) / float_n;
-      if (var < 0.0) var = 0.0;
-      double sd = sqrt(var);
-      if (sd <= eps) sd = 1.0;
-      inv = 1.0 / (sqrt(float_n) * sd);
-      if (writer && sd_out) sd_out[c0 + t] = (float)sd;
-    }
-    mu_s[t] = mu;
-    inv_s[t] = inv;
-  }
-  __syncthreads();
-  if (c < m) {
-#pragma unroll
-    for (int k = 0; k < CL_B; ++k) {
-      const int r = r_begin + 4 * (rq0 + 16 * k);
-      if (r >= n || r >= r_begin + rows_per) continue;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const double mu = mu_s[4 * cq + v], inv = inv_s[4 * cq + v];
-        float h[4], l[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float val = (r + u < n) ? (float)(((double)x[k][u][v] - mu) * inv) : 0.f;
-          split3x(val, h[u], l[u]);
-        }
-        const long long o = (long long)(c + v) * ldo + r;
-        *reinterpret_cast<float4*>(hiT + o) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(loT + o) = make_float4(l[0], l[1], l[2], l[3]);
-      }
-    }
-  }
-  cluster_sync_all();  // peers may still be posting into this CTA's smem until here
 }
 
 // ------------------------------------------------------------------ banded single-pass prep (n <= 2048)
@@ -362,22 +244,6 @@ cudaError_t launch_band_prep(const float* data, int n, int m, bool corr, float* 
 
 cudaError_t launch_stats_split(const float* data, int n, int m, double float_n, double eps, bool corr, float* hiT,
                                float* loT, int ldo, float* mean_out, float* sd_out, cudaStream_t s) {
-  if (n <= CL_CTAS * 4 * 16 * CL_B && n >= 64) {  // n <= 2048: cluster form, data held in registers
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(((m + CL_COLS - 1) / CL_COLS) * CL_CTAS);
-    cfg.blockDim = dim3(CL_T);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (corr)
-      return cudaLaunchKernelEx(&cfg, stats_split_cluster_kernel<true>, data, n, m, float_n, eps, hiT, loT, ldo,
-                                mean_out, sd_out);
-    return cudaLaunchKernelEx(&cfg, stats_split_cluster_kernel<false>, data, n, m, float_n, eps, hiT, loT, ldo,
-                              mean_out, sd_out);
-  }
   const int grid = (m + PC - 1) / PC;
   if (corr)
     return launch_pdl(stats_split_kernel<true>, dim3(grid), dim3(PT), 0, s, data, n, m, float_n, eps, hiT, loT, ldo,

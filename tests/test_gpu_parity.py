@@ -170,6 +170,20 @@ def test_covariance_unstructured_ragged():
     _ok(P.check_covariance(388, 301, structured=False))
 
 
+@pytest.mark.parametrize("m,n", [(132, 2049), (68, 3001)])
+def test_cov_corr_long_columns_exact_mean_path(m, n):
+    """n > 2048 rows: the exact-mean prep path (not the banded one)."""
+    _ok(P.check_covariance(m, n))
+    _ok(P.check_correlation(m, n))
+
+
+@pytest.mark.parametrize("m,n", [(132, 255), (132, 257), (260, 1999), (64, 2048)])
+def test_cov_corr_band_edges(m, n):
+    """banded prep: ragged last band, single band, exactly 8 bands."""
+    _ok(P.check_covariance(m, n))
+    _ok(P.check_correlation(m, n))
+
+
 # ------------------------------------------------------------------ matrix-vector
 @pytest.mark.parametrize("m,n", [(1, 4), (7, 8), (257, 516), (1000, 2052), (4096, 4096), (3001, 5000),
                                  (150, 32768), (5000, 1024), (148, 1028), (2000, 32764)])
