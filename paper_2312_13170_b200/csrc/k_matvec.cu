@@ -12,6 +12,8 @@
 // column partials that a second tiny kernel sums in a fixed order
 // (deterministic, no float atomics). bicg and mvt compute both products in ONE
 // pass over A (the paper's future-work kernel fusion).
+#include <stdlib.h>
+
 #include "pb_device.cuh"
 #include "pb_internal.h"
 
@@ -302,6 +304,145 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
   cluster_sync_all();  // no CTA leaves while its peer may still touch its smem
 }
 
+// ------------------------------------------------------------------ atax, single pass, register rows
+// Variant of the kernel above: each thread copies ITS float4s of row b from the
+// smem stage into registers and the stage is handed back to the TMA engine at
+// once (one CTA barrier per row), so stage reuse no longer waits for the DSMEM
+// partial-dot exchange; x lives in smem, row b-1 stays in registers until its
+// tmp arrives, the CTA partial is formed by the last warp to post (no barrier).
+constexpr int AR_STAGES = 2;
+
+struct __align__(16) ArCtl {
+  uint64_t full[AR_STAGES];
+  uint64_t red[AX_RED];
+  unsigned cnt[AX_RED];
+  float part[AX_RED][2];
+  float wred[AX_RED][AX_THREADS / 32];
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
+    atax_reg_kernel(const float* __restrict__ A, const float* __restrict__ x, int m, int n, int w0,
+                    float* __restrict__ tmp, float* __restrict__ ypart) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* xs = reinterpret_cast<float*>(sm);                          // AX_SLICE floats
+  float* stage_buf = xs + AX_SLICE;                                  // AR_STAGES x AX_SLICE
+  ArCtl* ctl = reinterpret_cast<ArCtl*>(stage_buf + (size_t)AR_STAGES * AX_SLICE);
+  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = AX_THREADS / 32;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int c0 = rank ? w0 : 0;
+  const int w = rank ? n - w0 : w0;
+  const int w4 = w >> 2;
+  const int r0 = (int)((long long)m * cl / ncl), r1 = (int)((long long)m * (cl + 1) / ncl);
+  const int nb = r1 - r0;
+
+  if (tid == 0) {
+    for (int s = 0; s < AR_STAGES; ++s) mbar_init(&ctl->full[s], 1);
+    for (int s = 0; s < AX_RED; ++s) {
+      mbar_init(&ctl->red[s], 2);
+      ctl->cnt[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  {
+    const float4* x4 = reinterpret_cast<const float4*>(x + c0);
+    float4* xs4 = reinterpret_cast<float4*>(xs);
+    for (int i = tid; i < w4; i += AX_THREADS) xs4[i] = x4[i];
+  }
+  cluster_sync_all();  // barriers exist in both CTAs; x slice staged
+  auto issue = [&](int b) {
+    const int s = b % AR_STAGES;
+    mbar_arrive_expect_tx(&ctl->full[s], (uint32_t)w * 4u);
+    if (w > 0) bulk_g2s(stage_buf + (size_t)s * AX_SLICE, A + (long long)(r0 + b) * n + c0, (uint32_t)w * 4u,
+                        &ctl->full[s]);
+  };
+  if (tid == 0)
+    for (int b = 0; b < AR_STAGES && b < nb; ++b) issue(b);
+  float4 yacc[AX_V];
+#pragma unroll
+  for (int v = 0; v < AX_V; ++v) yacc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t red0 = smem_u32(&ctl->red[0]);
+  const uint32_t part0 = smem_u32(&ctl->part[0][0]);
+  const float4* xs4 = reinterpret_cast<const float4*>(xs);
+
+  // row b: load into `cur`, free the stage, dot, post; then finish row b-1 from `prev`
+  auto step = [&](int b, float4(&cur)[AX_V], float4(&prev)[AX_V]) {
+    const int s = b % AR_STAGES, slot = b % AX_RED;
+    mbar_wait(&ctl->full[s], (uint32_t)(b / AR_STAGES) & 1u);
+    const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)s * AX_SLICE);
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const int idx = tid + v * AX_THREADS;
+      cur[v] = idx < w4 ? row[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();  // every thread holds its part of row b: the stage can be refilled
+    if (tid == 0 && b + AR_STAGES < nb) issue(b + AR_STAGES);
+    float p = 0.f;
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const int idx = tid + v * AX_THREADS;
+      if (idx < w4) {
+        const float4 xv = xs4[idx];
+        p += cur[v].x * xv.x + cur[v].y * xv.y + cur[v].z * xv.z + cur[v].w * xv.w;
+      }
+    }
+    p = warp_sum(p);
+    if (lane == 0) {
+      volatile float* wr = ctl->wred[slot];
+      wr[warp] = p;
+      __threadfence_block();
+      if (atomicAdd(&ctl->cnt[slot], 1u) == NW - 1) {  // last warp forms the CTA partial
+        __threadfence_block();
+        atomicExch(&ctl->cnt[slot], 0u);
+        float q = 0.f;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) q += wr[k];
+        const uint32_t poff = (uint32_t)(slot * 2 + rank) * 4u, roff = (uint32_t)slot * 8u;
+        st_cluster_f32(map_peer(part0 + poff, rank), q);
+        st_cluster_f32(map_peer(part0 + poff, peer), q);
+        mbar_arrive_cluster(map_peer(red0 + roff, rank));
+        mbar_arrive_cluster(map_peer(red0 + roff, peer));
+      }
+    }
+    if (b >= 1) {  // axpy of row b-1 (its partials had the whole dot of row b to arrive)
+      const int ps = (b - 1) % AX_RED;
+      mbar_wait_cluster(&ctl->red[ps], (uint32_t)((b - 1) / AX_RED) & 1u);
+      const float t = ctl->part[ps][0] + ctl->part[ps][1];
+      if (tmp && rank == 0 && tid == 0) tmp[r0 + b - 1] = t;
+#pragma unroll
+      for (int v = 0; v < AX_V; ++v) {
+        yacc[v].x += t * prev[v].x; yacc[v].y += t * prev[v].y; yacc[v].z += t * prev[v].z; yacc[v].w += t * prev[v].w;
+      }
+    }
+  };
+  float4 ra[AX_V], rb[AX_V];
+  int b = 0;
+  for (; b + 1 < nb; b += 2) {
+    step(b, ra, rb);
+    step(b + 1, rb, ra);
+  }
+  if (b < nb) step(b, ra, rb);
+  if (nb > 0) {  // last row's axpy
+    const int last = nb - 1, ps = last % AX_RED;
+    float4(&lr)[AX_V] = (last & 1) ? rb : ra;
+    mbar_wait_cluster(&ctl->red[ps], (uint32_t)(last / AX_RED) & 1u);
+    const float t = ctl->part[ps][0] + ctl->part[ps][1];
+    if (tmp && rank == 0 && tid == 0) tmp[r0 + last] = t;
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      yacc[v].x += t * lr[v].x; yacc[v].y += t * lr[v].y; yacc[v].z += t * lr[v].z; yacc[v].w += t * lr[v].w;
+    }
+  }
+  float4* yp = reinterpret_cast<float4*>(ypart + (long long)cl * n + c0);
+#pragma unroll
+  for (int v = 0; v < AX_V; ++v) {
+    const int idx = tid + v * AX_THREADS;
+    if (idx < w4) yp[idx] = yacc[v];
+  }
+  cluster_sync_all();
+}
+
 }  // namespace
 
 size_t atax_ws_bytes(int m, int n) {
@@ -338,7 +479,19 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
     }
     const int w0 = ((n / 4 + 1) / 2) * 4;
     float* ypart = static_cast<float*>(ws);
-    atax_onepass_kernel<<<2 * ncl, AX_THREADS, smem, s>>>(A, x, m, n, w0, tmp, ypart);
+    static const int variant = getenv("PB_ATAX_VARIANT") ? atoi(getenv("PB_ATAX_VARIANT")) : 2;
+    if (variant == 2) {
+      const size_t smem2 = (size_t)(1 + AR_STAGES) * AX_SLICE * 4 + sizeof(ArCtl);
+      static bool set2 = false;
+      if (!set2) {
+        cudaError_t e = cudaFuncSetAttribute(atax_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        if (e != cudaSuccess) return e;
+        set2 = true;
+      }
+      atax_reg_kernel<<<2 * ncl, AX_THREADS, smem2, s>>>(A, x, m, n, w0, tmp, ypart);
+    } else {
+      atax_onepass_kernel<<<2 * ncl, AX_THREADS, smem, s>>>(A, x, m, n, w0, tmp, ypart);
+    }
     reduce_parts_kernel<<<(n + 255) / 256, 256, 0, s>>>(ypart, ncl, n, nullptr, y);
     *launches += 2;
     return cudaGetLastError();
