@@ -8,7 +8,7 @@ CSRC      := $(PKG)/csrc
 KSRC      := $(CSRC)/pb_api.cu $(CSRC)/k_umma.cu $(CSRC)/k_split.cu $(CSRC)/k_stats.cu \
              $(CSRC)/k_matvec.cu $(CSRC)/k_simt.cu
 KOBJ      := $(patsubst $(CSRC)/%.cu,build/%.o,$(KSRC))
-HDRS      := include/pb.h $(CSRC)/pb_internal.h $(CSRC)/pb_device.cuh
+HDRS      := include/pb.h $(CSRC)/pb_internal.h $(CSRC)/pb_device.cuh $(CSRC)/pb_band_prep.cuh
 
 all: $(PKG)/libpb.so oracle/libpb_oracle.so pbgen/libpbgen_host.so pbgen/libpbgen_dev.so
 

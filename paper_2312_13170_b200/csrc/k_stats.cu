@@ -6,6 +6,7 @@
 // (reading R17 in DESIGN.md). Deterministic: every sum has a fixed order.
 #include <math.h>
 
+#include "pb_band_prep.cuh"
 #include "pb_device.cuh"
 #include "pb_internal.h"
 
@@ -128,106 +129,18 @@ __global__ void __launch_bounds__(PT, 1) stats_split_kernel(const float* __restr
 }
 
 // ------------------------------------------------------------------ banded single-pass prep (n <= 2048)
-// CTA (column block cb of 64 columns, row band b of <= 256 rows) holds its band in
-// registers, computes the band's column means mu_b and (correlation) M2_b =
-// sum (x - mu_b)^2 exactly in fp64 (two passes over registers), writes them, and
-// emits the BAND-centred data split + transposed. No grid-wide dependency: the
-// Gram of band-centred data plus the between-band scatter
-//   sum_b n_b (mu_b - mu)(mu_b - mu)^T      (Chan et al.'s pairwise update)
-// is exactly X_c^T X_c, and gram_combine adds that term (reading R18).
-constexpr int BAND = 256, BCOLS = 64, BT = 256, BB = 4;
-
+// Standalone kernel around band_prep_block (pb_band_prep.cuh): one CTA per
+// (64-column block, 256-row band). The Gram of band-centred data plus the
+// between-band scatter sum_b n_b (mu_b - mu)(mu_b - mu)^T (Chan et al.) is
+// exactly X_c^T X_c; gram_combine adds that term (reading R18).
 template <bool CORR>
 __global__ void __launch_bounds__(BT, 2)
     band_prep_kernel(const float* __restrict__ data, int n, int m, float* __restrict__ hiT, float* __restrict__ loT,
                      int ldo, double* __restrict__ band_mean, double* __restrict__ band_m2) {
-  __shared__ double red[BT / 16][BCOLS];
-  __shared__ double mu_s[BCOLS];
+  __shared__ BandScratch sc;
   pdl_wait();
-  const int t = threadIdx.x;
-  const int c0 = blockIdx.x * BCOLS, b = blockIdx.y;
-  const int r_begin = b * BAND, r_end = min(r_begin + BAND, n);
-  const double nb = (double)(r_end - r_begin);
-  const int rq0 = t & 15, cq = t >> 4;  // lanes on row quads: coalesced transposed stores
-  const int c = c0 + 4 * cq;
-  float x[BB][4][4];
-#pragma unroll
-  for (int k = 0; k < BB; ++k) {
-    const int r = r_begin + 4 * (rq0 + 16 * k);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (c < m && r + u < r_end) v = *reinterpret_cast<const float4*>(data + (long long)(r + u) * m + c);
-      x[k][u][0] = v.x; x[k][u][1] = v.y; x[k][u][2] = v.z; x[k][u][3] = v.w;
-    }
-  }
-  // band column sums -> mu_b
-  {
-    double sv[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < BB; ++k)
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) sv[v] += (double)x[k][u][v];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) red[rq0][4 * cq + v] = sv[v];
-  }
-  __syncthreads();
-  if (t < BCOLS) {
-    double S = 0.0;
-    for (int k = 0; k < BT / 16; ++k) S += red[k][t];
-    const double mu = S / nb;
-    mu_s[t] = mu;
-    if (c0 + t < m) band_mean[(long long)b * m + c0 + t] = mu;
-  }
-  __syncthreads();
-  double mu[4];
-#pragma unroll
-  for (int v = 0; v < 4; ++v) mu[v] = mu_s[4 * cq + v];
-  if (CORR) {  // M2_b = sum (x - mu_b)^2, second pass over the registers
-    double qv[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < BB; ++k) {
-      const int r = r_begin + 4 * (rq0 + 16 * k);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-          if (r + u < r_end) {
-            const double d = (double)x[k][u][v] - mu[v];
-            qv[v] += d * d;
-          }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int v = 0; v < 4; ++v) red[rq0][4 * cq + v] = qv[v];
-    __syncthreads();
-    if (t < BCOLS && c0 + t < m) {
-      double Q = 0.0;
-      for (int k = 0; k < BT / 16; ++k) Q += red[k][t];
-      band_m2[(long long)b * m + c0 + t] = Q;
-    }
-  }
-  if (c < m) {
-#pragma unroll
-    for (int k = 0; k < BB; ++k) {
-      const int r = r_begin + 4 * (rq0 + 16 * k);
-      if (r >= r_end) continue;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        float h[4], l[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float val = (r + u < r_end) ? (float)((double)x[k][u][v] - mu[v]) : 0.f;
-          split3x(val, h[u], l[u]);
-        }
-        const long long o = (long long)(c + v) * ldo + r;
-        *reinterpret_cast<float4*>(hiT + o) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(loT + o) = make_float4(l[0], l[1], l[2], l[3]);
-      }
-    }
-  }
+  band_prep_block<CORR, CtaSync>(data, n, m, hiT, loT, ldo, band_mean, band_m2, blockIdx.x, blockIdx.y, threadIdx.x,
+                                 sc);
 }
 
 }  // namespace
