@@ -1,0 +1,36 @@
+"""Every GEMM tile configuration / split-K factor and the atax variants against
+the oracle: each case runs in a subprocess with the tuning environment set
+(PB_UMMA_TILE: 1 = 1-CTA 128x128, 2 = 2-CTA 256x128, 3 = 2-CTA 256x256;
+PB_UMMA_KSPLIT: forced split-K on every tile; PB_ATAX_VARIANT: 1 = smem rows,
+2 = register rows), since the library reads them once per process."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = [
+    ({"PB_UMMA_TILE": "1"}, "gemm or 2mm or 3mm or syrk or syr2k or cov or corr"),
+    ({"PB_UMMA_TILE": "2"}, "gemm or 2mm or 3mm or syrk or syr2k or cov or corr"),
+    ({"PB_UMMA_TILE": "3", "PB_UMMA_KSPLIT": "3"}, "gemm or 2mm or 3mm or syrk or syr2k or cov or corr"),
+    ({"PB_UMMA_TILE": "2", "PB_UMMA_KSPLIT": "2"}, "gemm or syr2k or cov"),
+    ({"PB_ATAX_VARIANT": "1"}, "atax"),
+]
+
+
+@pytest.mark.parametrize("env,sel", CASES, ids=[",".join(f"{k}={v}" for k, v in e.items()) for e, _ in CASES])
+def test_config_parity(env, sel):
+    pytest.importorskip("torch")
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    # row_sharded mixes tile configs across bands by design; precision/ablation tests
+    # pin the default plan
+    sel = f"({sel}) and not row_sharded and not discriminator and not listing8 and not variants"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", sel],
+                       cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
