@@ -14,6 +14,7 @@ namespace {
 
 __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X, int rows, int cols4, int ldx,
                                                     float* __restrict__ hi, float* __restrict__ lo, int ldo) {
+  pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
   const long long total = (long long)rows * cols4;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -39,6 +40,7 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
                                                       const double* __restrict__ mean,
                                                       const double* __restrict__ inv) {
   __shared__ float tile[64][65];
+  pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
   const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;

@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(PT, 1) stats_split_kernel(const float* __restr
                                                          float* __restrict__ sd_out) {
   __shared__ double red_s[PT / 4][PC], red_q[CORR ? PT / 4 : 1][PC];
   __shared__ double mu_s[PC], inv_s[PC];
+  pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
   const int c0 = blockIdx.x * PC;
   const int t = threadIdx.x;
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(BT, 2)
     band_prep_kernel(const float* __restrict__ data, int n, int m, float* __restrict__ hiT, float* __restrict__ loT,
                      int ldo, double* __restrict__ band_mean, double* __restrict__ band_m2) {
   __shared__ BandScratch sc;
+  pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
   band_prep_block<CORR, CtaSync>(data, n, m, hiT, loT, ldo, band_mean, band_m2, blockIdx.x, blockIdx.y, threadIdx.x,
                                  sc);

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();  // the setup above overlapped the producer kernel's tail (PDL)
   const uint32_t tmem_base = ctl->tmem_base;
   const int nkb_total = p.nkb * p.npairs;
@@ -698,9 +699,11 @@ constexpr int MAXB = 8;
 template <int CG, int BN>
 __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int diag_one, const CombineStats cs) {
   constexpr int PAIR_M = BM * CG, C4 = BN / 4, NCOL = 32 + BN;
-  __shared__ float tile[32][BN + 1];
-  __shared__ float dev_s[MAXB][NCOL];  // mu_b - c (fp32 is ample: the term is summed in fp64) for rows, columns
-  __shared__ double inv_s[NCOL];
+  // tile: padded [32][BN+1] on the general path, XOR-swizzled [32][BN] float4 quads on the fast path
+  __shared__ __align__(16) float tile_raw[32 * (BN + 1)];
+  __shared__ __align__(16) float dev_s[MAXB][NCOL];  // mu_b - c (fp32 is ample: the term is summed in fp64)
+  __shared__ __align__(16) float inv_s[NCOL];        // 1/(sqrt(float_n) sd) for rows, columns (1 for covariance)
+  pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
   const int blk = blockIdx.x;
   const long long t = blk / (CG * 4);
@@ -714,21 +717,26 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
   if (banded) {
     for (int e = threadIdx.x; e < NCOL; e += 256) {
       const int col = e < 32 ? row_base + e : col_base + (e - 32);
-      double S = 0.0, M2 = 0.0, mu[MAXB];
+      // all band loads issued before any is used (unrolled over MAXB, predicated)
+      double S = 0.0, M2 = 0.0, mu[MAXB], m2[MAXB];
       int nb[MAXB];
-      for (int b = 0; b < cs.nbands; ++b) {
-        nb[b] = min(256, cs.n - 256 * b);
-        mu[b] = col < p.N ? cs.band_mean[(long long)b * p.N + col] : 0.0;
-        S += nb[b] * mu[b];
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        const bool in = b < cs.nbands && col < p.N;
+        nb[b] = b < cs.nbands ? min(256, cs.n - 256 * b) : 0;
+        mu[b] = in ? cs.band_mean[(long long)b * p.N + col] : 0.0;
+        m2[b] = in && cs.corr ? cs.band_m2[(long long)b * p.N + col] : 0.0;
       }
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) S += nb[b] * mu[b];
       const double c = S / cs.float_n;
       double between = 0.0;
-      for (int b = cs.nbands; b < MAXB; ++b) dev_s[b][e] = 0.f;
-      for (int b = 0; b < cs.nbands; ++b) {
-        const double d = mu[b] - c;
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        const double d = b < cs.nbands ? mu[b] - c : 0.0;
         dev_s[b][e] = (float)d;
         between += nb[b] * d * d;
-        if (cs.corr && col < p.N) M2 += cs.band_m2[(long long)b * p.N + col];
+        M2 += m2[b];
       }
       double inv = 1.0;
       double sd = 0.0;
@@ -737,7 +745,7 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
         if (sd <= cs.eps) sd = 1.0;
         inv = 1.0 / (sqrt(cs.float_n) * sd);
       }
-      inv_s[e] = inv;
+      inv_s[e] = (float)inv;
       // column statistics outputs: written once, by the diagonal tile's first block
       if (e >= 32 && col < p.N && rank == 0 && rb == 0 && tm == tn / p.ratio) {
         if (cs.mean_out) cs.mean_out[col] = (float)c;
@@ -764,33 +772,76 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
     }
   }
   // between-band term for row `lane`: er[b] = n_b (mu_b - c)_row (registers); the column
-  // factors come from smem as warp-wide broadcasts; 8 fp32 FMAs per element.
+  // factors are float4 warp-wide broadcasts from smem; 8 fp32 FMAs per element.
   float er[MAXB];
   float rinv = 1.f;
   if (banded) {
 #pragma unroll
     for (int b = 0; b < MAXB; ++b) er[b] = b < cs.nbands ? (float)min(256, cs.n - 256 * b) * dev_s[b][lane] : 0.f;
-    rinv = (float)inv_s[lane];
+    rinv = inv_s[lane];
   }
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int c4 = w + 8 * k;
-    const float g[4] = {acc[k].x, acc[k].y, acc[k].z, acc[k].w};
+    float4 v = acc[k];
+    if (banded) {
+      float4 bt = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int cc = 4 * c4 + e;
-      float v = g[e];
-      if (banded) {
-        float between = 0.f;
-#pragma unroll
-        for (int b = 0; b < MAXB; ++b) between = fmaf(er[b], dev_s[b][32 + cc], between);
-        v += between;
-        v = cs.corr ? v * rinv * (float)inv_s[32 + cc] : p.alpha * v;
-      } else {
-        v = p.alpha * v;
+      for (int b = 0; b < MAXB; ++b) {
+        const float4 f = *reinterpret_cast<const float4*>(&dev_s[b][32 + 4 * c4]);
+        bt.x = fmaf(er[b], f.x, bt.x); bt.y = fmaf(er[b], f.y, bt.y);
+        bt.z = fmaf(er[b], f.z, bt.z); bt.w = fmaf(er[b], f.w, bt.w);
       }
-      tile[lane][cc] = v;
+      v.x += bt.x; v.y += bt.y; v.z += bt.z; v.w += bt.w;
+      if (cs.corr) {
+        const float4 ic = *reinterpret_cast<const float4*>(&inv_s[32 + 4 * c4]);
+        v.x *= rinv * ic.x; v.y *= rinv * ic.y; v.z *= rinv * ic.z; v.w *= rinv * ic.w;
+      } else {
+        v.x *= p.alpha; v.y *= p.alpha; v.z *= p.alpha; v.w *= p.alpha;
+      }
+    } else {
+      v.x *= p.alpha; v.y *= p.alpha; v.z *= p.alpha; v.w *= p.alpha;
     }
+    acc[k] = v;
+  }
+  // Fast path: a full 32 x BN block strictly below the diagonal (every j < i), 16-byte
+  // aligned rows. Mirror out[j][i] straight from registers (lanes = consecutive i: one
+  // 128 B segment per store); direct out[i][j] through a swizzled tile (quad c4 of row r
+  // at quad c4 ^ (r & 7): both the STS.128 and LDS.128 below are bank-conflict free)
+  // as 16-byte stores, 512 B per warp instruction.
+  const bool fast = row_base + 32 <= p.M && col_base + BN <= p.N && col_base + BN <= row_base &&
+                    (p.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+  if (fast) {
+    float* mo = p.out + (long long)col_base * p.ldo + row_base + lane;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c4 = w + 8 * k;
+      float* q = mo + (long long)(4 * c4) * p.ldo;
+      q[0] = acc[k].x;
+      q[p.ldo] = acc[k].y;
+      q[2 * (long long)p.ldo] = acc[k].z;
+      q[3 * (long long)p.ldo] = acc[k].w;
+      *reinterpret_cast<float4*>(&tile_raw[lane * BN + 4 * (c4 ^ (lane & 7))]) = acc[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int r = w + 8 * rr;
+      float* o = p.out + (long long)(row_base + r) * p.ldo + col_base;
+#pragma unroll
+      for (int h = 0; h < BN / 128; ++h) {
+        const int q4 = lane + 32 * h;
+        *reinterpret_cast<float4*>(o + 4 * q4) = *reinterpret_cast<const float4*>(&tile_raw[r * BN + 4 * (q4 ^ (r & 7))]);
+      }
+    }
+    return;
+  }
+  // General path (diagonal and ragged blocks): padded tile, per-element bounds.
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int c4 = w + 8 * k;
+    float* tr = &tile_raw[lane * (BN + 1) + 4 * c4];
+    tr[0] = acc[k].x; tr[1] = acc[k].y; tr[2] = acc[k].z; tr[3] = acc[k].w;
   }
   __syncthreads();
   // direct lower part out[i][j], j <= i: lanes on columns
@@ -800,7 +851,7 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
     for (int c = lane; c < BN; c += 32) {
       const int j = col_base + c;
       if (j > i || j >= p.N) break;
-      p.out[(long long)i * p.ldo + j] = (diag_one && j == i) ? 1.0f : tile[r][c];
+      p.out[(long long)i * p.ldo + j] = (diag_one && j == i) ? 1.0f : tile_raw[r * (BN + 1) + c];
     }
   }
   // mirror out[j][i] = v for j < i: lanes on rows i
@@ -809,7 +860,7 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
     for (int c = w; c < BN; c += 8) {
       const int j = col_base + c;
       if (j >= p.N) break;
-      if (j < i) p.out[(long long)j * p.ldo + i] = tile[lane][c];
+      if (j < i) p.out[(long long)j * p.ldo + i] = tile_raw[lane * (BN + 1) + c];
     }
   }
 }

@@ -1,5 +1,5 @@
 # ncu evidence for profiles/: launch list of the bench command + full captures of the hot kernels
-TAG=${1:-r02}
+TAG=${1:-r03}
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --graphs 0 > gpurun_out/${TAG}_ncu_bench.log 2>&1
 cap() {  # name kernel-regex skip bench-kernels
@@ -12,5 +12,6 @@ cap atax atax 3 atax
 cap bicg mvmt 3 bicg
 cap gesummv rowdot 3 gesummv
 cap cov_gram umma3x 3 covariance
-cap cov_prep stats_split 3 covariance
+cap cov_prep band_prep 3 covariance
+cap cov_combine gram_combine 3 covariance
 ls gpurun_out | grep $TAG

@@ -4,7 +4,7 @@
 usage: python scripts/time_calls.py <kernel> [n] [reps]
 Prints the median CUDA-event time of the call (captured into a CUDA graph so
 host overhead is excluded). Env PB_UMMA_TILE / PB_UMMA_KSPLIT steer the GEMM
-plan.
+plan; PB_FLUSH=1 writes a 256 MB buffer before each replay (cold L2).
 """
 import os
 import statistics
@@ -58,8 +58,11 @@ def main():
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=s):
         f()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if os.environ.get("PB_FLUSH") else None
     ts = []
     for _ in range(reps):
+        if flush is not None:
+            flush.fill_(1)  # evict the inputs from the 126 MB L2 (cold-input timing)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         graph.replay()
