@@ -21,6 +21,8 @@ the partition and collective logic without a GPU). Outputs stay row-sharded
 """
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -31,6 +33,13 @@ def _world():
     if dist.is_available() and dist.is_initialized():
         return dist.get_world_size(), dist.get_rank()
     return 1, 0
+
+
+def _single(world):
+    """True when the unsharded single-GPU entry points apply. PB_FORCE_DIST=1 (test
+    aid) keeps a world-size-1 process group on the sharded path, so one GPU runs
+    every N>1 call, NCCL collectives included."""
+    return world == 1 and not os.environ.get("PB_FORCE_DIST")
 
 
 def partition(rows, world, rank, triangular=False, align=128, K=_pb):
@@ -103,7 +112,7 @@ def mm3_rows(ctx, n, E, A, B, Fl, F, C, D, G, ws, K=_pb):
     """3mm: F row block -> async all-gather of F overlapped with E[R] = A[R] B -> G[R] = E[R] F."""
     world, rank = _world()
     L = 0
-    if world == 1:
+    if _single(world):
         K.pb_3mm(A.shape[0], n, n, n, n, E, A, B, F, C, D, G, ws=ws)
         return K.last_launch_count()
     bounds = [partition(n, world, g, False, 128, K) for g in range(world)]
@@ -144,7 +153,7 @@ def matvec(ctx, kernel, n, v, ws, alpha, beta, K=_pb):
     world, rank = _world()
     A = v["A"]
     rows = A.shape[0]
-    if world == 1:
+    if _single(world):
         if kernel == "atax":
             K.pb_atax(rows, n, A, v["x"], v["y"], v["tmp"], ws=ws)
         elif kernel == "bicg":

@@ -27,14 +27,18 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, backend="gloo"):
     import torch.distributed as dist
 
     import paper_2312_13170_b200 as pb
     from paper_2312_13170_b200 import dist as D
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":  # world size 1 kept on the sharded path: NCCL collectives on device tensors
+        os.environ["PB_FORCE_DIST"] = "1"
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     dev = torch.device("cuda", 0)
     H = lambda r, c, s, **kw: torch.from_numpy(pbgen.gen_host(r, c, s, **kw)).to(dev)  # noqa: E731
     res = {}
@@ -90,15 +94,18 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_dist_two_ranks_one_gpu_real_kernels():
+@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1)])
+def test_dist_ranks_one_gpu_real_kernels(backend, world):
+    """gloo: two ranks share cuda:0 (host-staged collectives). nccl: one rank with
+    PB_FORCE_DIST, i.e. the N>1 code path (partition, partial kernels,
+    all_gather_into_tensor / reduce_scatter_tensor on device tensors) end to end."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    world = 2
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=600) for _ in range(world))
@@ -144,3 +151,21 @@ def test_dist_two_ranks_one_gpu_real_kernels():
             v0, v1, blk, _ = out[r][k]
             got[v0:v1] = blk
         assert np.max(np.abs(got - ref) / np.abs(ref)) <= P.TOL, k
+
+
+def test_bench_forced_sharded_nccl():
+    """bench.py on the sharded path over a world-size-1 NCCL group: one JSON line,
+    every kernel timed, e2e included."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PB_FORCE_DIST="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "1", "--warmup", "3", "--no-cpu"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
+    assert all(v["ms"] > 0 for v in line["kernels"].values())
