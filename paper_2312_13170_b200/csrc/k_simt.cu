@@ -58,7 +58,62 @@ __global__ void listing9_kernel(int ni, int nj, int nk, float alpha, float beta,
   if (REG_ACC && ok) *c = acc;
 }
 
+// Small-problem GEMM (pb_gemm below SMALL_GEMM_MACS, e.g. the N = 128 config, where
+// a launch costs more than the math). Loop internalization with the whole K strip
+// (up to KC = 128) as the local tile: one global round trip per strip instead of one
+// per 16-wide tile step, all float4 loads in flight together; detect-reduction into
+// four register accumulators (exact fp32 FMAs, fixed order: deterministic). C is
+// read before the strip loads only when beta != 0 (BLAS convention, include/pb.h).
+constexpr int ST = 16, KC = 128;
+
+__global__ void __launch_bounds__(256) small_gemm_kernel(int ni, int nj, int nk, float alpha, float beta, float* C,
+                                                         const float* __restrict__ A, const float* __restrict__ B) {
+  __shared__ __align__(16) float As[ST][KC + 4];
+  __shared__ __align__(16) float Bs[KC][ST];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = blockIdx.y * ST, j0 = blockIdx.x * ST;
+  const int i = i0 + ty, j = j0 + tx;
+  const bool ok = i < ni && j < nj;
+  const float cin = (ok && beta != 0.f) ? C[(long long)i * nj + j] : 0.f;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = 0; k0 < nk; k0 += KC) {  // nk % 4 == 0 and nj % 4 == 0 (validated): whole float4s
+#pragma unroll
+    for (int e = threadIdx.x; e < ST * KC / 4; e += 256) {
+      const int r = e / (KC / 4), c4 = e % (KC / 4);
+      const int gi = i0 + r, gk = k0 + 4 * c4;
+      *reinterpret_cast<float4*>(&As[r][4 * c4]) =
+          (gi < ni && gk < nk) ? *reinterpret_cast<const float4*>(A + (long long)gi * nk + gk) : zero;
+    }
+#pragma unroll
+    for (int e = threadIdx.x; e < KC * ST / 4; e += 256) {
+      const int k = e / (ST / 4), c4 = e % (ST / 4);
+      const int gk = k0 + k, gj = j0 + 4 * c4;
+      *reinterpret_cast<float4*>(&Bs[k][4 * c4]) =
+          (gk < nk && gj < nj) ? *reinterpret_cast<const float4*>(B + (long long)gk * nj + gj) : zero;
+    }
+    __syncthreads();
+    const int kc = min(KC, nk - k0);
+    for (int k = 0; k < kc; k += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fmaf(As[ty][k + u], Bs[k + u][tx], acc[u]);
+    }
+    __syncthreads();
+  }
+  if (ok) {
+    const float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    C[(long long)i * nj + j] = beta != 0.f ? alpha * sum + beta * cin : alpha * sum;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_gemm_small(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
+                              const float* B, cudaStream_t s) {
+  dim3 grid((nj + ST - 1) / ST, (ni + ST - 1) / ST);
+  small_gemm_kernel<<<grid, 256, 0, s>>>(ni, nj, nk, alpha, beta, C, A, B);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gemm_listing8(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                  const float* B, cudaStream_t s) {

@@ -312,10 +312,10 @@ pb_status pb_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, con
   ws_gemm(need, ni, nj, nk);
   PB_TRY(check_ws(need, ws, ws_bytes));
   if ((long long)ni * nj * nk <= SMALL_GEMM_MACS) {
-    // Launch-latency regime (e.g. the N = 128 config: 2 MFMA): one launch of the
-    // paper's own loop-internalised kernel (Listing 9 + register accumulation)
-    // beats split + tensor-core GEMM (3 launches). DESIGN.md §8.
-    PB_CUDA(launch_gemm_listing9_reg(ni, nj, nk, alpha, beta, C, A, B, S(s)));
+    // Launch-latency regime (e.g. the N = 128 config: 2 M multiply-adds): one launch
+    // of the whole-K-strip SIMT kernel (loop internalization + register accumulation,
+    // exact fp32) beats split + tensor-core GEMM (3 launches). DESIGN.md §8.
+    PB_CUDA(launch_gemm_small(ni, nj, nk, alpha, beta, C, A, B, S(s)));
     g_launches = 1;
     return PB_OK;
   }

@@ -117,6 +117,8 @@ cudaError_t launch_gemm_listing8(int ni, int nj, int nk, float alpha, float beta
                                  const float* B, cudaStream_t s);
 cudaError_t launch_gemm_listing9(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                  const float* B, cudaStream_t s);
+cudaError_t launch_gemm_small(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
+                              const float* B, cudaStream_t s);
 cudaError_t launch_gemm_listing9_reg(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                      const float* B, cudaStream_t s);
 

@@ -48,6 +48,24 @@ def test_gemm_alpha_beta(alpha, beta):
     _ok(P.check_gemm(257, 260, 300, alpha, beta))
 
 
+# small-problem path (ni*nj*nk <= 2^21: one SIMT launch): ragged tiles, several K strips + tail
+@pytest.mark.parametrize("ni,nj,nk,alpha,beta", [(100, 36, 260, 1.5, 1.2), (33, 20, 12, 1.5, 1.2), (1, 4, 4, 2.0, 0.5),
+                                                 (17, 128, 516, -1.0, 0.0), (128, 128, 128, 0.0, 1.2)])
+def test_gemm_small_path(ni, nj, nk, alpha, beta):
+    _ok(P.check_gemm(ni, nj, nk, alpha, beta))
+
+
+def test_gemm_small_path_beta0_ignores_C():
+    """beta == 0: C is write-only (include/pb.h), so NaN in C must not propagate."""
+    import paper_2312_13170_b200 as pb
+    A, B = pbgen.gen_host(64, 96, 1), pbgen.gen_host(96, 32, 2)
+    C = P.dev(np.full((64, 32), np.nan, dtype=np.float32))
+    pb.pb_gemm(64, 32, 96, 1.5, 0.0, C, P.dev(A), P.dev(B))
+    r = oracle.gemm(1.5, 0.0, np.zeros((64, 32), np.float32), A, B)
+    g = P.host(C)
+    assert np.isfinite(g).all() and np.max(np.abs(g - r) / np.abs(r)) <= P.TOL
+
+
 def test_gemm_integer_inputs_bitwise_P1():
     """values in {0..7}: hi = x, lo = 0, every product and partial sum exact
     in fp32 -> the tensor-core path equals the oracle bit for bit."""
