@@ -6,9 +6,9 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall
 PKG       := paper_2312_13170_b200
 CSRC      := $(PKG)/csrc
 KSRC      := $(CSRC)/pb_api.cu $(CSRC)/k_umma.cu $(CSRC)/k_split.cu $(CSRC)/k_stats.cu \
-             $(CSRC)/k_matvec.cu $(CSRC)/k_simt.cu
+             $(CSRC)/k_matvec.cu $(CSRC)/k_simt.cu $(CSRC)/pb_dist.cu
 KOBJ      := $(patsubst $(CSRC)/%.cu,build/%.o,$(KSRC))
-HDRS      := include/pb.h $(CSRC)/pb_internal.h $(CSRC)/pb_device.cuh $(CSRC)/pb_band_prep.cuh
+HDRS      := include/pb.h $(CSRC)/pb_internal.h $(CSRC)/pb_check.h $(CSRC)/pb_device.cuh $(CSRC)/pb_band_prep.cuh
 
 all: $(PKG)/libpb.so oracle/libpb_oracle.so pbgen/libpbgen_host.so pbgen/libpbgen_dev.so
 
@@ -17,7 +17,7 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
 
 $(PKG)/libpb.so: $(KOBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(KOBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(KOBJ) -ldl
 
 # The oracle: plain C++, fp64, no FMA contraction, no fast-math (test infrastructure only).
 oracle/libpb_oracle.so: oracle/pb_oracle.cpp

@@ -172,6 +172,10 @@ class Suite:
         out = [("gemm", (GEMM_N,) * 3), ("covariance", (STAT_N, STAT_N)), ("2mm", (MM_N,) * 4),
                ("3mm", (MM_N,) * 5), ("gemm", (MM_N,) * 3), ("syr2k_rows", (SY_N, SY_N, 0, SY_N)),
                ("matvec_partial", (MV_N, MV_N)), ("atax", (MV_N, MV_N))]
+        if self.D.comm() is not None:  # pb_<k>_dist entry points: dims + (nranks, rank)
+            G = (self.world, self.rank)
+            out += [("2mm_dist", (MM_N,) * 4 + G), ("3mm_dist", (MM_N,) * 5 + G), ("syr2k_dist", (SY_N, SY_N) + G),
+                    ("atax_dist", (MV_N, MV_N) + G), ("bicg_dist", (MV_N, MV_N) + G), ("mvt_dist", (MV_N,) + G)]
         return out
 
     def run(self, k, stream=None):
@@ -237,6 +241,8 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+            import paper_2312_13170_b200.dist as D
+            D.init_comm()  # libpb's own NCCL communicator: the pb_<k>_dist entry points
     kernels = KERNELS if args.kernels == "all" else args.kernels.split(",")
     suite = Suite(rank, world, dev, kernels)
     W = work()
@@ -384,6 +390,9 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline(kernels, budget_s=args.cpu_budget)
         print(json.dumps(line), flush=True)
     if sharded:
+        import paper_2312_13170_b200.dist as D
+        torch.cuda.synchronize(dev)
+        D.close_comm()
         dist.destroy_process_group()
 
 

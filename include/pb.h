@@ -55,7 +55,7 @@ typedef enum {
   PB_ERR_ALIAS = 3,        /* an output range overlaps another argument's range */
   PB_ERR_WORKSPACE = 4,    /* ws NULL / misaligned / smaller than pb_workspace_size */
   PB_ERR_CUDA = 5,         /* a CUDA runtime/driver call or launch failed */
-  PB_ERR_NCCL = 6          /* reserved (collectives run through torch.distributed) */
+  PB_ERR_NCCL = 6          /* libnccl.so.2 not loadable, or an NCCL call failed */
 } pb_status;
 
 typedef struct CUstream_st* pb_stream; /* == cudaStream_t */
@@ -162,7 +162,6 @@ pb_status pb_row_partition(int rows, int nranks, int rank, int triangular, int a
  * pb_syrk_rows / pb_syr2k_rows: rows [r0, r1) of the lower-triangular update
  *   (r0 must be a multiple of 128); A, B are the FULL n x m inputs, C points
  *   to row r0 of C (rows r1-r0, n columns).
- * pb_gemm_rows: C[r0:r1] = beta*C[r0:r1] + alpha*A[r0:r1]*B (A, C point at row r0).
  * pb_matvec_partial: for a row block A_blk (rows x cols):
  *   rowdot[i]  = base_row[i] + sum_j A_blk[i][j]*v[j]   (if v; base_row may be NULL = 0,
  *                                                         may equal rowdot: in place)
@@ -184,6 +183,79 @@ pb_status pb_gesummv_rows(int rows, int n, float alpha, float beta, const float*
                           size_t ws_bytes, pb_stream s);
 /* workspace for the two helpers above: kernel names "syrk_rows" {n,m,r0,r1},
  * "syr2k_rows" {n,m,r0,r1}, "matvec_partial" {rows, cols}. */
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU entry points. One process per
+ * GPU; every kernel shards by OUTPUT ROW BLOCKS and has at most one exchange
+ * step, run with NCCL (NVLink/NVSwitch) inside libpb:
+ *   gemm, 2mm, syrk, syr2k, gesummv   no exchange
+ *   3mm                               all-gather of F (overlapped with E = A B
+ *                                     on the comm's own stream)
+ *   atax, bicg, mvt                   reduce-scatter of the transposed-product
+ *                                     partial vector
+ * libnccl.so.2 is resolved with dlopen at the first pb_comm_* call (env
+ * PB_NCCL_LIB overrides the name), so libpb loads without NCCL; PB_ERR_NCCL if
+ * it cannot be loaded or an NCCL call fails (message in pb_last_error()).
+ *
+ * Partitions (rank g's block = pb_row_partition(rows, nranks, g, tri, align)):
+ *   gemm/2mm/3mm rows of ni, and 3mm's rows of F/C (nj): tri 0, align 128
+ *   syrk/syr2k rows of C (n): tri 1, align 256
+ *   atax/bicg/mvt/gesummv rows of A, and the reduce-scatter destinations
+ *   (atax y over n, bicg s over m, mvt x2 over n): tri 0, align 4
+ * "_blk" arguments point at the first row (element) of this rank's block and
+ * hold exactly its rows; other arrays are full and replicated on every rank.
+ * A rank whose block is empty still takes part in the collectives (its _blk
+ * pointers may then be NULL). Dims and scalars are GLOBAL and identical on
+ * every rank; calls must be issued in the same order on every rank, one
+ * stream sequence per comm at a time (NCCL rule). Workspace: kernel name
+ * "<k>_dist" with the kernel's dims followed by {nranks, rank}.
+ */
+typedef struct pb_comm pb_comm;
+/* 128 opaque bytes (an ncclUniqueId) created on one rank; the caller sends
+ * them to the other ranks out of band (e.g. torch.distributed). */
+pb_status pb_comm_unique_id(unsigned char id[128]);
+/* Collective over the nranks processes; binds the comm to the current device
+ * and creates its side stream. *out owned by the caller until
+ * pb_comm_destroy. */
+pb_status pb_comm_init(int nranks, int rank, const unsigned char id[128], pb_comm** out);
+pb_status pb_comm_destroy(pb_comm* comm);
+pb_status pb_comm_size(const pb_comm* comm, int* nranks, int* rank);
+
+/* C_blk = beta*C_blk + alpha*A_blk*B.  A_blk rows x nk, B nk x nj, C_blk rows x nj. */
+pb_status pb_gemm_dist(pb_comm* comm, int ni, int nj, int nk, float alpha, float beta, float* C_blk,
+                       const float* A_blk, const float* B, void* ws, size_t ws_bytes, pb_stream s);
+/* tmp_blk = alpha*A_blk*B (optional out);  D_blk = tmp_blk*C + beta*D_blk. */
+pb_status pb_2mm_dist(pb_comm* comm, int ni, int nj, int nk, int nl, float alpha, float beta,
+                      float* tmp_blk, const float* A_blk, const float* B, const float* C, float* D_blk,
+                      void* ws, size_t ws_bytes, pb_stream s);
+/* F[rows' of nj] = C_blk*D, all-gathered into the FULL F (nj x nl) on every
+ * rank; E_blk = A_blk*B;  G_blk = E_blk*F.  C_blk holds this rank's rows of C
+ * (partition of nj). */
+pb_status pb_3mm_dist(pb_comm* comm, int ni, int nj, int nk, int nl, int nm, float* E_blk,
+                      const float* A_blk, const float* B, float* F, const float* C_blk,
+                      const float* D, float* G_blk, void* ws, size_t ws_bytes, pb_stream s);
+/* Lower-triangle rows of this rank (tri partition); A (and B) FULL n x m. */
+pb_status pb_syrk_dist(pb_comm* comm, int n, int m, float alpha, float beta, float* C_blk,
+                       const float* A, void* ws, size_t ws_bytes, pb_stream s);
+pb_status pb_syr2k_dist(pb_comm* comm, int n, int m, float alpha, float beta, float* C_blk,
+                        const float* A, const float* B, void* ws, size_t ws_bytes, pb_stream s);
+/* tmp_blk = A_blk*x (optional out); y = sum over ranks of A_blk^T tmp_blk,
+ * reduce-scattered: y_blk = this rank's block of y (partition of n). */
+pb_status pb_atax_dist(pb_comm* comm, int m, int n, const float* A_blk, const float* x, float* y_blk,
+                       float* tmp_blk, void* ws, size_t ws_bytes, pb_stream s);
+/* A n x m by rows: q_blk = A_blk*p;  s = A^T r reduce-scattered into s_blk
+ * (partition of m); r_blk = this rank's rows of r. */
+pb_status pb_bicg_dist(pb_comm* comm, int m, int n, const float* A_blk, float* s_blk, float* q_blk,
+                       const float* p, const float* r_blk, void* ws, size_t ws_bytes, pb_stream s);
+/* x1_blk += A_blk*y_1;  x2 += A^T y_2 with x2_blk / y_2_blk this rank's blocks
+ * (same partition as A's rows). */
+pb_status pb_mvt_dist(pb_comm* comm, int n, float* x1_blk, float* x2_blk, const float* y_1,
+                      const float* y_2_blk, const float* A_blk, void* ws, size_t ws_bytes,
+                      pb_stream s);
+/* y_blk = alpha*A_blk*x + beta*B_blk*x; tmp_blk = A_blk*x (optional). */
+pb_status pb_gesummv_dist(pb_comm* comm, int n, float alpha, float beta, const float* A_blk,
+                          const float* B_blk, float* tmp_blk, const float* x, float* y_blk, void* ws,
+                          size_t ws_bytes, pb_stream s);
 
 /* ------------------------------------------------------------------------
  * Paper ablation: the GEMM of PAPER.md Listing 8

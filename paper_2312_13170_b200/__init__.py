@@ -19,7 +19,9 @@ __all__ = [
     "PBError", "lib", "workspace_size", "workspace", "pb_gemm", "pb_2mm", "pb_3mm", "pb_syrk",
     "pb_syr2k", "pb_covariance", "pb_correlation", "pb_atax", "pb_bicg", "pb_mvt", "pb_gesummv",
     "pb_row_partition", "pb_syrk_rows", "pb_gesummv_rows", "pb_syr2k_rows", "pb_matvec_partial", "pb_gemm_variant",
-    "pb_version", "last_launch_count", "ABI_FUNCTIONS",
+    "pb_version", "last_launch_count", "ABI_FUNCTIONS", "Comm", "pb_comm_unique_id", "pb_comm_init",
+    "pb_comm_destroy", "pb_gemm_dist", "pb_2mm_dist", "pb_3mm_dist", "pb_syrk_dist", "pb_syr2k_dist",
+    "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -55,6 +57,20 @@ ABI_FUNCTIONS = {
     "pb_matvec_partial": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gemm_variant": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gesummv_rows": ([_I, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    # multi-GPU (NCCL inside libpb)
+    "pb_comm_unique_id": ([_P], _I),
+    "pb_comm_init": ([_I, _I, _P, ctypes.POINTER(_P)], _I),
+    "pb_comm_destroy": ([_P], _I),
+    "pb_comm_size": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "pb_gemm_dist": ([_P, _I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_2mm_dist": ([_P, _I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_3mm_dist": ([_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_syrk_dist": ([_P, _I, _I, _F, _F, _P, _P, _P, _Z, _P], _I),
+    "pb_syr2k_dist": ([_P, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_atax_dist": ([_P, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_bicg_dist": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_mvt_dist": ([_P, _I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_gesummv_dist": ([_P, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
 }
 
 _lib = None
@@ -242,3 +258,97 @@ def pb_row_partition(rows, nranks, rank, triangular=False, align=1):
     _check("pb_row_partition", lib().pb_row_partition(rows, nranks, rank, int(triangular), align,
                                                       ctypes.byref(b), ctypes.byref(e)))
     return b.value, e.value
+
+
+# --------------------------------------------------------------------- multi-GPU (include/pb.h)
+class Comm:
+    """A libpb communicator (an NCCL communicator + side stream inside libpb)."""
+
+    def __init__(self, handle, nranks, rank):
+        self.handle, self.nranks, self.rank = handle, nranks, rank
+
+    def close(self):
+        if self.handle:
+            _check("pb_comm_destroy", lib().pb_comm_destroy(self.handle))
+            self.handle = None
+
+
+def pb_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check("pb_comm_unique_id", lib().pb_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def pb_comm_init(nranks, rank, uid: bytes) -> Comm:
+    if len(uid) != 128:
+        raise ValueError("unique id must be 128 bytes")
+    buf = ctypes.create_string_buffer(uid, 128)
+    h = ctypes.c_void_p()
+    _check("pb_comm_init", lib().pb_comm_init(nranks, rank, ctypes.cast(buf, ctypes.c_void_p), ctypes.byref(h)))
+    return Comm(h.value, nranks, rank)
+
+
+def pb_comm_destroy(comm: Comm):
+    comm.close()
+
+
+def _first(*ts):
+    return next(t for t in ts if t is not None and hasattr(t, "device"))
+
+
+def _dws(ws, name, dims, comm, *ts):
+    return _ws(ws, name + "_dist", tuple(dims) + (comm.nranks, comm.rank), _first(*ts))
+
+
+def pb_gemm_dist(comm, ni, nj, nk, alpha, beta, C_blk, A_blk, B, ws=None, stream=None):
+    p, n, keep = _dws(ws, "gemm", (ni, nj, nk), comm, B)
+    _check("pb_gemm_dist", lib().pb_gemm_dist(comm.handle, ni, nj, nk, alpha, beta, _ptr(C_blk), _ptr(A_blk),
+                                              _ptr(B), p, n, _stream(stream, B)))
+
+
+def pb_2mm_dist(comm, ni, nj, nk, nl, alpha, beta, tmp_blk, A_blk, B, C, D_blk, ws=None, stream=None):
+    p, n, keep = _dws(ws, "2mm", (ni, nj, nk, nl), comm, B)
+    _check("pb_2mm_dist", lib().pb_2mm_dist(comm.handle, ni, nj, nk, nl, alpha, beta, _ptr(tmp_blk), _ptr(A_blk),
+                                            _ptr(B), _ptr(C), _ptr(D_blk), p, n, _stream(stream, B)))
+
+
+def pb_3mm_dist(comm, ni, nj, nk, nl, nm, E_blk, A_blk, B, F, C_blk, D, G_blk, ws=None, stream=None):
+    p, n, keep = _dws(ws, "3mm", (ni, nj, nk, nl, nm), comm, F)
+    _check("pb_3mm_dist", lib().pb_3mm_dist(comm.handle, ni, nj, nk, nl, nm, _ptr(E_blk), _ptr(A_blk), _ptr(B),
+                                            _ptr(F), _ptr(C_blk), _ptr(D), _ptr(G_blk), p, n, _stream(stream, F)))
+
+
+def pb_syrk_dist(comm, n_, m, alpha, beta, C_blk, A, ws=None, stream=None):
+    p, n, keep = _dws(ws, "syrk", (n_, m), comm, A)
+    _check("pb_syrk_dist", lib().pb_syrk_dist(comm.handle, n_, m, alpha, beta, _ptr(C_blk), _ptr(A), p, n,
+                                              _stream(stream, A)))
+
+
+def pb_syr2k_dist(comm, n_, m, alpha, beta, C_blk, A, B, ws=None, stream=None):
+    p, n, keep = _dws(ws, "syr2k", (n_, m), comm, A)
+    _check("pb_syr2k_dist", lib().pb_syr2k_dist(comm.handle, n_, m, alpha, beta, _ptr(C_blk), _ptr(A), _ptr(B),
+                                                p, n, _stream(stream, A)))
+
+
+def pb_atax_dist(comm, m, n_, A_blk, x, y_blk, tmp_blk=None, ws=None, stream=None):
+    p, n, keep = _dws(ws, "atax", (m, n_), comm, x)
+    _check("pb_atax_dist", lib().pb_atax_dist(comm.handle, m, n_, _ptr(A_blk), _ptr(x), _ptr(y_blk), _ptr(tmp_blk),
+                                              p, n, _stream(stream, x)))
+
+
+def pb_bicg_dist(comm, m, n_, A_blk, s_blk, q_blk, p_, r_blk, ws=None, stream=None):
+    p, n, keep = _dws(ws, "bicg", (m, n_), comm, p_)
+    _check("pb_bicg_dist", lib().pb_bicg_dist(comm.handle, m, n_, _ptr(A_blk), _ptr(s_blk), _ptr(q_blk), _ptr(p_),
+                                              _ptr(r_blk), p, n, _stream(stream, p_)))
+
+
+def pb_mvt_dist(comm, n_, x1_blk, x2_blk, y_1, y_2_blk, A_blk, ws=None, stream=None):
+    p, n, keep = _dws(ws, "mvt", (n_,), comm, y_1)
+    _check("pb_mvt_dist", lib().pb_mvt_dist(comm.handle, n_, _ptr(x1_blk), _ptr(x2_blk), _ptr(y_1), _ptr(y_2_blk),
+                                            _ptr(A_blk), p, n, _stream(stream, y_1)))
+
+
+def pb_gesummv_dist(comm, n_, alpha, beta, A_blk, B_blk, tmp_blk, x, y_blk, ws=None, stream=None):
+    p, n, keep = _dws(ws, "gesummv", (n_,), comm, x)
+    _check("pb_gesummv_dist", lib().pb_gesummv_dist(comm.handle, n_, alpha, beta, _ptr(A_blk), _ptr(B_blk),
+                                                    _ptr(tmp_blk), _ptr(x), _ptr(y_blk), p, n, _stream(stream, x)))

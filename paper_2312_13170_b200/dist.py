@@ -18,6 +18,12 @@ Every arithmetic step runs in libpb through the C ABI (`K` below defaults to
 the binding; the CPU gloo tests inject an oracle-backed namespace to check
 the partition and collective logic without a GPU). Outputs stay row-sharded
 (reading R15).
+
+With an NCCL process group, `init_comm()` creates a libpb communicator and
+every call below goes to the C ABI's `pb_<k>_dist` entry points, which run the
+collectives with NCCL inside libpb (3mm's all-gather on the comm's side
+stream, overlapped with E = A B). Without one (gloo: the multi-rank tests on
+one GPU or on CPU), the same steps run here with torch.distributed.
 """
 from __future__ import annotations
 
@@ -27,6 +33,32 @@ import torch
 import torch.distributed as dist
 
 import paper_2312_13170_b200 as _pb
+
+
+_COMM = None  # libpb communicator (pb_comm_init), set by init_comm()
+
+
+def init_comm():
+    """Create the libpb communicator over the current torch.distributed group:
+    rank 0's NCCL unique id is broadcast through torch.distributed."""
+    global _COMM
+    world, rank = _world()
+    uid = [_pb.pb_comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    _COMM = _pb.pb_comm_init(world, rank, uid[0])
+    return _COMM
+
+
+def close_comm():
+    global _COMM
+    if _COMM is not None:
+        _COMM.close()
+        _COMM = None
+
+
+def comm():
+    return _COMM
 
 
 def _world():
@@ -101,6 +133,9 @@ def _reduce_scatter_vec(out_local, partial, world, bounds):
 # --------------------------------------------------------------------- contractions
 def mm2_rows(ctx, n, alpha, beta, tmp, A, B, C, D, ws, K=_pb):
     """2mm on this rank's rows (A, tmp, D are the local row blocks)."""
+    if _COMM is not None and K is _pb:
+        K.pb_2mm_dist(_COMM, n, n, n, n, alpha, beta, tmp, A, B, C, D, ws=ws)
+        return K.last_launch_count()
     rows = A.shape[0]
     if rows == 0:
         return 0
@@ -117,6 +152,9 @@ def mm3_rows(ctx, n, E, A, B, Fl, F, C, D, G, ws, K=_pb):
         return K.last_launch_count()
     bounds = [partition(n, world, g, False, 128, K) for g in range(world)]
     f0, f1 = bounds[rank]
+    if _COMM is not None and K is _pb:  # F rows -> all-gather (libpb side stream) || E -> G
+        K.pb_3mm_dist(_COMM, n, n, n, n, n, E, A, B, F, C[f0:f1], D, G, ws=ws)
+        return K.last_launch_count()
     if f1 > f0:
         K.pb_gemm(f1 - f0, n, n, 1.0, 0.0, Fl, C[f0:f1], D, ws=ws)  # F[R'] = C[R'] D
         L += K.last_launch_count()
@@ -135,6 +173,12 @@ def mm3_rows(ctx, n, E, A, B, Fl, F, C, D, G, ws, K=_pb):
 
 def syrk_rows(ctx, n, m, alpha, beta, C_blk, A, ws, B=None, K=_pb):
     world, rank = _world()
+    if _COMM is not None and K is _pb:
+        if B is None:
+            K.pb_syrk_dist(_COMM, n, m, alpha, beta, C_blk, A, ws=ws)
+        else:
+            K.pb_syr2k_dist(_COMM, n, m, alpha, beta, C_blk, A, B, ws=ws)
+        return K.last_launch_count()
     r0, r1 = partition(n, world, rank, True, 256, K)
     if r1 <= r0:
         return 0
@@ -165,12 +209,21 @@ def matvec(ctx, kernel, n, v, ws, alpha, beta, K=_pb):
         return K.last_launch_count()
     bounds = [partition(n, world, g, False, 4, K) for g in range(world)]
     r0, r1 = bounds[rank]
+    if _COMM is not None and K is _pb:  # local pass + NCCL reduce-scatter inside libpb
+        c = _COMM
+        if kernel == "atax":
+            K.pb_atax_dist(c, n, n, A, v["x"], v["y"][r0:r1], v["tmp"][:rows], ws=ws)
+        elif kernel == "bicg":
+            K.pb_bicg_dist(c, n, n, A, v["s"][r0:r1], v["q"][r0:r1], v["x"], v["r"][r0:r1], ws=ws)
+        elif kernel == "mvt":
+            K.pb_mvt_dist(c, n, v["x1"][r0:r1], v["x2"][r0:r1], v["x"], v["y2"][r0:r1], A, ws=ws)
+        else:
+            K.pb_gesummv_dist(c, n, alpha, beta, A, v["B"], v["tmp"][:rows], v["x"], v["yo"][r0:r1], ws=ws)
+        return K.last_launch_count()
     L = 0
     if kernel == "atax":  # tmp[R] = A[R] x ; y = sum_g A[R_g]^T tmp[R_g]
         part = v["yo"]
-        K.pb_matvec_partial(rows, n, A, v["x"], None, v["tmp"][:rows], None, None, None, ws=ws)
-        L += K.last_launch_count()
-        K.pb_matvec_partial(rows, n, A, None, None, None, v["tmp"][:rows], None, part, ws=ws)
+        K.pb_atax(rows, n, A, v["x"], part, v["tmp"][:rows], ws=ws)  # one pass over A[R]
         L += K.last_launch_count()
         _reduce_scatter_vec(v["y"][r0:r1], part, world, bounds)
     elif kernel == "bicg":  # q[R] = A[R] p ; s = sum_g A[R_g]^T r[R_g]

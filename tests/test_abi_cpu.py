@@ -95,3 +95,27 @@ def test_product_path_never_uses_oracle():
     assert "pbo_" not in out
     ldd = subprocess.check_output(["ldd", pb.LIB_PATH]).decode()
     assert "oracle" not in ldd and "pbgen" not in ldd
+
+
+def test_dist_workspace_sizes_cpu():
+    """pb_workspace_size for the multi-GPU entry points ("<k>_dist": dims + {nranks, rank}):
+    host-only, so it runs without a GPU or NCCL."""
+    import paper_2312_13170_b200 as pb
+    n = 32768
+    # atax: partial vector (n floats, 256-B aligned) + the local single-pass workspace
+    for G in (1, 2, 8):
+        for g in range(G):
+            r0, r1 = pb.pb_row_partition(n, G, g, False, 4)
+            need = pb.workspace_size("atax_dist", (n, n, G, g))
+            assert need >= n * 4 + pb.workspace_size("atax", (r1 - r0, n))
+            assert pb.workspace_size("gesummv_dist", (n, G, g)) == 0
+            assert pb.workspace_size("mvt_dist", (n, G, g)) >= 2 * n * 4
+    # the GEMM family needs at least its local shard's workspace
+    assert pb.workspace_size("gemm_dist", (4096, 4096, 4096, 2, 1)) >= pb.workspace_size("gemm", (2048, 4096, 4096))
+    assert pb.workspace_size("3mm_dist", (4096,) * 5 + (4, 3)) >= pb.workspace_size("gemm", (1024, 4096, 4096))
+    r0, r1 = pb.pb_row_partition(8192, 4, 3, True, 256)
+    assert pb.workspace_size("syr2k_dist", (8192, 8192, 4, 3)) == pb.workspace_size("syr2k_rows", (8192, 8192, r0, r1))
+    for bad in [("atax_dist", (n, n, 2, 2)), ("atax_dist", (n, n, 0, 0)), ("atax_dist", (n, n)),
+                ("nope_dist", (1, 1, 1)), ("gemm_dist", (0, 4, 4, 1, 0))]:
+        with pytest.raises(pb.PBError):
+            pb.workspace_size(*bad)

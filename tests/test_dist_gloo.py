@@ -71,6 +71,14 @@ def fake_kernels():
         if tmp is not None:
             tmp.copy_(torch.from_numpy((a @ xx).astype(np.float32)))
 
+    def atax(m, n, A, x, y, tmp, ws=None):  # tmp = A x; y = A^T tmp (A: this rank's rows)
+        a, xx = _np(A).astype(np.float64), _np(x).astype(np.float64)
+        t = a @ xx
+        y.copy_(torch.from_numpy((a.T @ t).astype(np.float32)))
+        if tmp is not None:
+            tmp.copy_(torch.from_numpy(t.astype(np.float32)))
+
+    K.pb_atax = atax
     K.pb_gemm = gemm
     K.pb_2mm = mm2
     K.pb_matvec_partial = matvec_partial

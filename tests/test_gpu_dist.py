@@ -37,6 +37,7 @@ def _worker(rank, world, port, q, backend="gloo"):
     if backend == "nccl":  # world size 1 kept on the sharded path: NCCL collectives on device tensors
         os.environ["PB_FORCE_DIST"] = "1"
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+        D.init_comm()  # the pb_<k>_dist entry points: NCCL inside libpb
     else:
         dist.init_process_group("gloo", rank=rank, world_size=world)
     dev = torch.device("cuda", 0)
@@ -50,12 +51,19 @@ def _worker(rank, world, port, q, backend="gloo"):
         E, G, F = (torch.empty(r1 - r0, n, device=dev), torch.empty(r1 - r0, n, device=dev),
                    torch.empty(n, n, device=dev))
         Fl = torch.empty(r1 - r0, n, device=dev)
-        ws = pb.workspace("3mm", (n, n, n, n, n), dev)
+        def wsz(*named):  # local and (with a libpb comm) "<k>_dist" workspaces
+            need = max(pb.workspace_size(k, d) for k, d in named)
+            if D.comm() is not None:
+                for k, d in named:
+                    if k in ("gemm", "2mm", "3mm", "syrk", "syr2k", "atax", "bicg", "mvt", "gesummv"):
+                        need = max(need, pb.workspace_size(k + "_dist", tuple(d) + (world, rank)))
+            return torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        ws = wsz(("3mm", (n, n, n, n, n)))
         D.mm3_rows(None, n, E, A[r0:r1].contiguous(), B, Fl, F, C, Dm, G, ws)
         # 2mm: row-local
         tmp = torch.empty(r1 - r0, n, device=dev)
         D2 = Dm[r0:r1].clone()
-        D.mm2_rows(None, n, 1.5, 1.2, tmp, A[r0:r1].contiguous(), B, C, D2, pb.workspace("2mm", (n,) * 4, dev))
+        D.mm2_rows(None, n, 1.5, 1.2, tmp, A[r0:r1].contiguous(), B, C, D2, wsz(("2mm", (n,) * 4)))
         torch.cuda.synchronize()
         res["3mm"] = (r0, r1, G.cpu().numpy(), F.cpu().numpy())
         res["2mm"] = (r0, r1, D2.cpu().numpy())
@@ -65,7 +73,7 @@ def _worker(rank, world, port, q, backend="gloo"):
         A2, B2 = H(n2, m2, 1), H(n2, m2, 2)
         Cf = H(n2, n2, 3, mode=pbgen.SYM)
         Cb, Cb2 = Cf[s0:s1].clone(), Cf[s0:s1].clone()
-        wsy = pb.workspace("syr2k_rows", (n2, m2, 0, n2), dev)
+        wsy = wsz(("syr2k_rows", (n2, m2, 0, n2)), ("syr2k", (n2, m2)))
         D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb, A2, wsy)
         D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb2, A2, wsy, B=B2)
         torch.cuda.synchronize()
@@ -76,7 +84,7 @@ def _worker(rank, world, port, q, backend="gloo"):
         v0, v1 = D.partition(nv, world, rank, False, 4)
         Av, Bv = H(nv, nv, 1), H(nv, nv, 2)
         vec = {k: H(1, nv, s).view(-1) for k, s in (("x", 6), ("r", 7), ("y2", 7), ("x1", 8), ("x2", 9))}
-        wsm = pb.workspace("atax", (nv, nv), dev)
+        wsm = wsz(("atax", (nv, nv)), ("bicg", (nv, nv)), ("mvt", (nv,)), ("matvec_partial", (nv, nv)))
         for kern in ("atax", "bicg", "mvt", "gesummv"):
             v = dict(A=Av[v0:v1].contiguous(), B=Bv[v0:v1].contiguous(), x=vec["x"].clone(), r=vec["r"].clone(),
                      y2=vec["y2"].clone(), x1=vec["x1"].clone(), x2=vec["x2"].clone(),
@@ -91,14 +99,17 @@ def _worker(rank, world, port, q, backend="gloo"):
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, {"error": repr(e)}))
     finally:
+        torch.cuda.synchronize()
+        D.close_comm()
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1)])
 def test_dist_ranks_one_gpu_real_kernels(backend, world):
-    """gloo: two ranks share cuda:0 (host-staged collectives). nccl: one rank with
-    PB_FORCE_DIST, i.e. the N>1 code path (partition, partial kernels,
-    all_gather_into_tensor / reduce_scatter_tensor on device tensors) end to end."""
+    """gloo: two ranks share cuda:0 (host-staged torch collectives). nccl: one rank
+    with PB_FORCE_DIST and a libpb communicator, i.e. the N>1 code path through
+    the C ABI's pb_<k>_dist entry points (NCCL all-gather / reduce-scatter inside
+    libpb, 3mm's side stream) end to end."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
