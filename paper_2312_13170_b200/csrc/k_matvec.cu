@@ -455,7 +455,14 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
                         cudaStream_t s, int* launches) {
   float* t = reinterpret_cast<float*>(static_cast<char*>(ws) + (atax_ws_bytes(m, n) - align_up((size_t)m * 4, 256)));
   if (!tmp) tmp = t;
-  if (n >= 1024 && n <= 2 * AX_SLICE && m >= 2 * 74) {
+  // Single pass only for long rows of a matrix larger than L2. With two stages of
+  // half-rows in flight per CTA, short rows leave too few bytes outstanding (the
+  // cluster kernel is then latency-bound), and a matrix that fits in L2 is read
+  // from HBM once by the two-pass form anyway. Measured crossover (B200, cold L2):
+  // n = 8192: 160 vs 96 us two-pass; n = 16384: 317 vs 346; n = 24576: 497 vs 713.
+  static const long long onepass_min = (getenv("PB_ATAX_ONEPASS_MIN_MB") ? atoll(getenv("PB_ATAX_ONEPASS_MIN_MB"))
+                                                                          : 96ll) << 20;
+  if (n >= 16384 && n <= 2 * AX_SLICE && m >= 2 * 74 && (long long)m * n * 4 >= onepass_min) {
     static int ncl = 0;
     const size_t smem = (size_t)AX_STAGES * AX_SLICE * 4 + sizeof(AxCtl);
     if (!ncl) {

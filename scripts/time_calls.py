@@ -49,6 +49,11 @@ def main():
         ws = pb.workspace("syrk", (n, n), dev)
         f = lambda: pb.pb_syrk(n, n, 1.5, 1.2, C, A, ws=ws)  # noqa: E731
         flops = n * (n + 1) * n
+    elif k == "atax":
+        A, x, y = g(n, n, 1), g(1, n, 6).view(-1), torch.empty(n, device=dev)
+        ws = pb.workspace("atax", (n, n), dev)
+        f = lambda: pb.pb_atax(n, n, A, x, y, None, ws=ws)  # noqa: E731
+        flops = 4 * n * n  # prints "TFLOP/s" = 1e3 GB/s of A (4 bytes per element)
     else:
         raise SystemExit(f"unknown kernel {k}")
     for _ in range(3):

@@ -203,8 +203,9 @@ def test_cov_corr_band_edges(m, n):
 
 
 # ------------------------------------------------------------------ matrix-vector
+# single-pass cluster kernel: n >= 16384 and A >= 96 MB (e.g. (2000, 32764), (1537, 16388)); else two passes
 @pytest.mark.parametrize("m,n", [(1, 4), (7, 8), (257, 516), (1000, 2052), (4096, 4096), (3001, 5000),
-                                 (150, 32768), (5000, 1024), (148, 1028), (2000, 32764)])
+                                 (150, 32768), (5000, 1024), (148, 1028), (2000, 32764), (1537, 16388)])
 def test_atax(m, n):
     _ok(P.check_atax(m, n))
 
@@ -225,7 +226,7 @@ def test_gesummv(n):
 
 
 def test_atax_onepass_deterministic_and_tmp_optional():
-    m, n = 3000, 8192
+    m, n = 1600, 16384  # single-pass path (n >= 16384, A >= 96 MB)
     A, x = P.dev(P.H(m, n, 1)), P.dev(P.H(1, n, 6)[0])
     ys = []
     for tmp in (None, torch.empty(m, device="cuda")):
