@@ -19,6 +19,7 @@ on this host's cores on bounded samples of the same workload.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -70,38 +71,54 @@ BOUND = {k: ("hbm" if k in ("atax", "bicg", "mvt", "gesummv") else "tensor") for
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """nvidia-smi sampler (every 20 ms). Started before the warm-up so it is running
+    when the timed region begins; stop() keeps only the samples whose timestamps fall
+    inside the timed region [mark_start(), stop()]."""
 
     def __init__(self, index):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.t0 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
     def stop(self):
+        t1 = time.time()
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.p.terminate()
         self.p.wait()
         self.f.flush()
-        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        rows = [[c.strip() for c in l.split(",")] for l in open(self.f.name).read().strip().splitlines() if l.strip()]
         os.unlink(self.f.name)
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+
+        def when(r):
+            try:
+                return datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except Exception:
+                return None
+        rows = [r for r in rows if len(r) >= 10]
+        inside = [r for r in rows if self.t0 is not None and when(r) is not None and self.t0 <= when(r) <= t1]
+        use = inside or rows[-3:]  # a very short timed region: the samples nearest its end
+        sm = [float(r[2]) for r in use if r[2].replace(".", "").isdigit()]
+        mx = [float(r[3]) for r in use if r[3].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in rows:
-            if len(r) >= 9:
-                for n, v in zip(names, r[5:9]):
-                    if "Active" in v and "Not" not in v:
-                        reasons.add(n)
+        for r in use:
+            for n, v in zip(names, r[6:10]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "in_timed_region": bool(inside)}
 
 
 # ====================================================================== our arm
@@ -293,13 +310,14 @@ def run_ours(args):
                 record[k][1].record(stream)
         return n
 
+    clocks = Clocks(local)
     for _ in range(args.warmup):
         step()
     barrier()
     ev = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in kernels}
           for _ in range(args.steps)]
-    clocks = Clocks(local)
     barrier()
+    clocks.mark_start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -601,7 +619,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernels", default="all", help="comma list (default: the whole suite)")
