@@ -109,6 +109,16 @@ pb_status pb_syrk(int n, int m, float alpha, float beta, float* C, const float* 
 pb_status pb_syr2k(int n, int m, float alpha, float beta, float* C, const float* A,
                    const float* B, void* ws, size_t ws_bytes, pb_stream s);
 
+/* Full-matrix forms (SYCL-Bench / PolyBench-GPU, reading R3 and SURVEY.md §8(f)
+ * NEXT-2): the same sums for EVERY (i, j), C need not be symmetric:
+ *   syrk_full:  C[i][j] = beta*C[i][j] + alpha * sum_k A[i][k]*A[j][k]
+ *   syr2k_full: C[i][j] = beta*C[i][j] + alpha * sum_k (A[j][k]*B[i][k] + B[j][k]*A[i][k])
+ * Workspace names "syrk_full" / "syr2k_full" with dims {n, m}. */
+pb_status pb_syrk_full(int n, int m, float alpha, float beta, float* C, const float* A, void* ws,
+                       size_t ws_bytes, pb_stream s);
+pb_status pb_syr2k_full(int n, int m, float alpha, float beta, float* C, const float* A,
+                        const float* B, void* ws, size_t ws_bytes, pb_stream s);
+
 /* covariance — PolyBench kernel_covariance (reading R4; data NOT mutated, R9):
  *   mean[j] = sum_i data[i][j] / float_n;  X = data - mean
  *   cov[i][j] = cov[j][i] = sum_k X[k][i]*X[k][j] / (float_n - 1)

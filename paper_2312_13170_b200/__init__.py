@@ -17,7 +17,7 @@ import os
 
 __all__ = [
     "PBError", "lib", "workspace_size", "workspace", "pb_gemm", "pb_2mm", "pb_3mm", "pb_syrk",
-    "pb_syr2k", "pb_covariance", "pb_correlation", "pb_atax", "pb_bicg", "pb_mvt", "pb_gesummv",
+    "pb_syr2k", "pb_syrk_full", "pb_syr2k_full", "pb_covariance", "pb_correlation", "pb_atax", "pb_bicg", "pb_mvt", "pb_gesummv",
     "pb_row_partition", "pb_syrk_rows", "pb_gesummv_rows", "pb_syr2k_rows", "pb_matvec_partial", "pb_gemm_variant",
     "pb_version", "last_launch_count", "ABI_FUNCTIONS", "Comm", "pb_comm_unique_id", "pb_comm_init",
     "pb_comm_destroy", "pb_gemm_dist", "pb_2mm_dist", "pb_3mm_dist", "pb_syrk_dist", "pb_syr2k_dist",
@@ -45,6 +45,8 @@ ABI_FUNCTIONS = {
     "pb_3mm": ([_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_syrk": ([_I, _I, _F, _F, _P, _P, _P, _Z, _P], _I),
     "pb_syr2k": ([_I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_syrk_full": ([_I, _I, _F, _F, _P, _P, _P, _Z, _P], _I),
+    "pb_syr2k_full": ([_I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
     "pb_covariance": ([_I, _I, _F, _P, _P, _P, _P, _Z, _P], _I),
     "pb_correlation": ([_I, _I, _F, _F, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_atax": ([_I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
@@ -192,6 +194,17 @@ def pb_syrk(n_, m, alpha, beta, C, A, ws=None, stream=None):
 def pb_syr2k(n_, m, alpha, beta, C, A, B, ws=None, stream=None):
     p, n, keep = _ws(ws, "syr2k", (n_, m), C)
     _check("pb_syr2k", lib().pb_syr2k(n_, m, alpha, beta, _ptr(C), _ptr(A), _ptr(B), p, n, _stream(stream, C)))
+
+
+def pb_syrk_full(n_, m, alpha, beta, C, A, ws=None, stream=None):
+    p, n, keep = _ws(ws, "syrk_full", (n_, m), C)
+    _check("pb_syrk_full", lib().pb_syrk_full(n_, m, alpha, beta, _ptr(C), _ptr(A), p, n, _stream(stream, C)))
+
+
+def pb_syr2k_full(n_, m, alpha, beta, C, A, B, ws=None, stream=None):
+    p, n, keep = _ws(ws, "syr2k_full", (n_, m), C)
+    _check("pb_syr2k_full", lib().pb_syr2k_full(n_, m, alpha, beta, _ptr(C), _ptr(A), _ptr(B), p, n,
+                                                _stream(stream, C)))
 
 
 def pb_syrk_rows(n_, m, r0, r1, alpha, beta, C_blk, A, ws=None, stream=None):

@@ -129,11 +129,11 @@ WsStat ws_stat(Carve& c, int m, int n) {
   return w;
 }
 struct WsSyrk { SplitBuf a, b; SplitK sk; };
-WsSyrk ws_syrk(Carve& c, int n, int m, int r0, int r1, bool two) {
+WsSyrk ws_syrk(Carve& c, int n, int m, int r0, int r1, bool two, bool full = false) {
   WsSyrk w;
   w.a = take_split(c, r1, m);
   if (two) w.b = take_split(c, r1, m);
-  w.sk = take_splitk(c, {shape(r1, r1, m, two ? 2 : 1, EPI_TRI, r0 / 128, (r1 + 127) / 128)});
+  w.sk = take_splitk(c, {shape(r1, r1, m, two ? 2 : 1, full ? 0u : (uint32_t)EPI_TRI, r0 / 128, (r1 + 127) / 128)});
   return w;
 }
 
@@ -215,6 +215,8 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   else if (k == "3mm" && need(5)) ws_3mm(c, d[0], d[1], d[2], d[3], d[4]);
   else if (k == "syrk" && need(2)) ws_syrk(c, d[0], d[1], 0, d[0], false);
   else if (k == "syr2k" && need(2)) ws_syrk(c, d[0], d[1], 0, d[0], true);
+  else if (k == "syrk_full" && need(2)) ws_syrk(c, d[0], d[1], 0, d[0], false, true);
+  else if (k == "syr2k_full" && need(2)) ws_syrk(c, d[0], d[1], 0, d[0], true, true);
   else if ((k == "covariance" || k == "correlation") && need(2)) ws_stat(c, d[0], d[1]);
   else if (k == "atax" && need(2)) c.take<char>(atax_ws_bytes(d[0], d[1]));
   else if (k == "bicg" && need(2)) c.take<char>(mvmt_ws_bytes(d[1], d[0]));
@@ -345,8 +347,10 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   return PB_OK;
 }
 
+// full == true: the SYCL-Bench / PolyBench-GPU form:
+// every C[i][j] is updated, not only j <= i (the product is symmetric, C need not be).
 static pb_status syrk_core(int n, int m, int r0, int r1, float alpha, float beta, float* C_blk, const float* A,
-                           const float* B, void* ws, size_t ws_bytes, pb_stream s) {
+                           const float* B, void* ws, size_t ws_bytes, pb_stream s, bool full = false) {
   Check ck;
   ck.dims({n, m});
   if (ck.st == PB_OK && (r0 < 0 || r1 > n || r0 >= r1 || r0 % 128 != 0))
@@ -356,10 +360,10 @@ static pb_status syrk_core(int n, int m, int r0, int r1, float alpha, float beta
   if (B) ck.arr(B, r1, m, false, "B");
   PB_TRY(ck.finish());
   Carve need(nullptr, 0);
-  ws_syrk(need, n, m, r0, r1, B != nullptr);
+  ws_syrk(need, n, m, r0, r1, B != nullptr, full);
   PB_TRY(check_ws(need, ws, ws_bytes));
   Carve c(ws, ws_bytes);
-  WsSyrk w = ws_syrk(c, n, m, r0, r1, B != nullptr);
+  WsSyrk w = ws_syrk(c, n, m, r0, r1, B != nullptr, full);
   SplitBuf sa = w.a, sb = w.b;
   cudaStream_t st = S(s);
   int L = 0;
@@ -375,7 +379,7 @@ static pb_status syrk_core(int n, int m, int r0, int r1, float alpha, float beta
   } else {
     d.a[0] = sa.op(); d.b[0] = sa.op();
   }
-  d.flags = EPI_TRI | EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
+  d.flags = (full ? 0u : (uint32_t)EPI_TRI) | EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
   d.alpha = alpha; d.beta = beta;
   d.cin = C_blk; d.ldc = n; d.out = C_blk; d.ldo = n; d.out_row0 = r0;
   d.tm0 = r0 / 128; d.tm1 = (r1 + 127) / 128;
@@ -393,6 +397,15 @@ pb_status pb_syr2k(int n, int m, float alpha, float beta, float* C, const float*
                    size_t ws_bytes, pb_stream s) {
   if (!B) return fail(PB_ERR_INVALID_ARG, "B is NULL");
   return syrk_core(n, m, 0, n, alpha, beta, C, A, B, ws, ws_bytes, s);
+}
+pb_status pb_syrk_full(int n, int m, float alpha, float beta, float* C, const float* A, void* ws, size_t ws_bytes,
+                       pb_stream s) {
+  return syrk_core(n, m, 0, n, alpha, beta, C, A, nullptr, ws, ws_bytes, s, true);
+}
+pb_status pb_syr2k_full(int n, int m, float alpha, float beta, float* C, const float* A, const float* B, void* ws,
+                        size_t ws_bytes, pb_stream s) {
+  if (!B) return fail(PB_ERR_INVALID_ARG, "B is NULL");
+  return syrk_core(n, m, 0, n, alpha, beta, C, A, B, ws, ws_bytes, s, true);
 }
 pb_status pb_syrk_rows(int n, int m, int r0, int r1, float alpha, float beta, float* C_blk, const float* A, void* ws,
                        size_t ws_bytes, pb_stream s) {

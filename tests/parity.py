@@ -118,6 +118,34 @@ def check_syr2k(n, m, alpha=1.5, beta=1.2, mode=pbgen.U01):
     return out
 
 
+def check_syrk_full(n, m, two=False, alpha=1.5, beta=1.2, mode=pbgen.U01):
+    """Full-matrix syrk / syr2k (SYCL-Bench form, reading R3): every C[i][j], with a
+    NON-symmetric C. Reference: the gemm oracle (the plain definition) with B = A^T
+    (syr2k: the sum of the B A^T and A B^T products), plus the symmetry of the
+    product part."""
+    A, B = H(n, m, S["A"], mode), H(n, m, S["B"], mode)
+    C = H(n, n, S["C"], mode)
+    dC, dA, dB = dev(C), dev(A), dev(B)
+    if two:
+        pb.pb_syr2k_full(n, m, alpha, beta, dC, dA, dB)
+        z = np.zeros((n, n), np.float32)
+        r = oracle.gemm(alpha, beta, C, B, A.T) + oracle.gemm(alpha, 0.0, z, A, B.T)
+        s = oracle.gemm(alpha, beta, C, B, A.T, absmode=True) + oracle.gemm(alpha, 0.0, z, A, B.T, absmode=True)
+    else:
+        pb.pb_syrk_full(n, m, alpha, beta, dC, dA)
+        r = oracle.gemm(alpha, beta, C, A, A.T)
+        s = oracle.gemm(alpha, beta, C, A, A.T, absmode=True)
+    g = host(dC)
+    out = _res(C=cerr(g, r, s))
+    # property: the product part (g - beta C) is symmetric (each entry computed independently
+    # by a different tile; plans differ from the lower-only kernel, so no bitwise pin)
+    P_ = g.astype(np.float64) - beta * C.astype(np.float64)
+    Ps = s - abs(beta) * np.abs(C.astype(np.float64))
+    out["symmetry"] = float(np.max(np.abs(P_ - P_.T) / np.maximum(Ps, 1e-30)))
+    out["ok"] = out["ok"] and out["symmetry"] <= 2 * TOL
+    return out
+
+
 def structured_data(n, m, seed=pbgen.SEED):
     """data n x m ~ U[0,1) with the parity columns of DESIGN.md's input recipe:
     col 0 constant 0.5; col 2 = col 1 (duplicate); col 3 = 1 - col 1 (negated);

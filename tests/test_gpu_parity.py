@@ -202,6 +202,13 @@ def test_cov_corr_band_edges(m, n):
     _ok(P.check_correlation(m, n))
 
 
+# full-matrix syrk / syr2k (SYCL-Bench form): non-symmetric C, ragged sizes, split-K and tile configs
+@pytest.mark.parametrize("n,m", [(4, 4), (132, 36), (300, 260), (1000, 516), (2048, 1028)])
+@pytest.mark.parametrize("two", [False, True])
+def test_syrk_full(n, m, two):
+    _ok(P.check_syrk_full(n, m, two))
+
+
 # ------------------------------------------------------------------ matrix-vector
 # single-pass cluster kernel: n >= 16384 and A >= 96 MB (e.g. (2000, 32764), (1537, 16388)); else two passes
 @pytest.mark.parametrize("m,n", [(1, 4), (7, 8), (257, 516), (1000, 2052), (4096, 4096), (3001, 5000),
