@@ -13,6 +13,9 @@
 namespace pb {
 namespace {
 
+__device__ int g_tl_on;                  // PB_TIMELINE (tuning only)
+__device__ unsigned long long g_tl[2];   // band_prep: [entry, exit]
+
 // ------------------------------------------------------------------ fused prep
 // Used for long columns (n > 2048; shorter ones take the banded prep below).
 // One CTA owns PC = 16 columns of data (n x m) and all n rows:
@@ -141,13 +144,27 @@ __global__ void __launch_bounds__(BT, 2)
   __shared__ BandScratch sc;
   pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
+  const int tl = g_tl_on;
+  tl_enter(tl, g_tl, 0);
   band_prep_block<CORR, CtaSync>(data, n, m, hiT, loT, ldo, band_mean, band_m2, blockIdx.x, blockIdx.y, threadIdx.x,
                                  sc);
+  tl_exit(tl, g_tl, 0);
 }
 
 }  // namespace
 
 int band_count(int n) { return (n + BAND - 1) / BAND; }
+
+void timeline_stats(bool reset, unsigned long long* out2) {
+  if (reset) {
+    const int on = 1;
+    const unsigned long long init[2] = {~0ull, 0ull};
+    cudaMemcpyToSymbol(g_tl_on, &on, sizeof on);
+    cudaMemcpyToSymbol(g_tl, init, sizeof init);
+  } else {
+    cudaMemcpyFromSymbol(out2, g_tl, 2 * sizeof(unsigned long long));
+  }
+}
 
 cudaError_t launch_band_prep(const float* data, int n, int m, bool corr, float* hiT, float* loT, int ldo,
                              double* band_mean, double* band_m2, cudaStream_t s) {

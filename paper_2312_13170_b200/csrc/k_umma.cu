@@ -46,6 +46,9 @@
 namespace pb {
 namespace {
 
+__device__ int g_tl_on;                  // PB_TIMELINE (tuning only)
+__device__ unsigned long long g_tl[4];   // [umma entry, exit, combine entry, exit]
+
 constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;
 constexpr int GROUP_M = 8;  // tile-rows per raster group (L2 reuse)
@@ -276,6 +279,8 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   tc_fence_after();
   pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();  // the setup above overlapped the producer kernel's tail (PDL)
+  const int tl = g_tl_on;
+  tl_enter(tl, g_tl, 0);
   const uint32_t tmem_base = ctl->tmem_base;
   const int nkb_total = p.nkb * p.npairs;
   const long long num_units = p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles);
@@ -538,6 +543,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
 
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
+  tl_exit(tl, g_tl, 0);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_cg<CG>(tmem_base, TMEM_COLS);
@@ -705,6 +711,8 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
   __shared__ __align__(16) float inv_s[NCOL];        // 1/(sqrt(float_n) sd) for rows, columns (1 for covariance)
   pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
+  const int tl = g_tl_on;
+  tl_enter(tl, g_tl, 1);
   const int blk = blockIdx.x;
   const long long t = blk / (CG * 4);
   const int rank = (blk / 4) % CG, rb = blk % 4;
@@ -834,6 +842,7 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
         *reinterpret_cast<float4*>(o + 4 * q4) = *reinterpret_cast<const float4*>(&tile_raw[r * BN + 4 * (q4 ^ (r & 7))]);
       }
     }
+    tl_exit(tl, g_tl, 1);
     return;
   }
   // General path (diagonal and ragged blocks): padded tile, per-element bounds.
@@ -863,9 +872,21 @@ __global__ void __launch_bounds__(256) gram_combine_kernel(const Params p, int d
       if (j < i) p.out[(long long)j * p.ldo + i] = tile_raw[lane * (BN + 1) + c];
     }
   }
+  tl_exit(tl, g_tl, 1);
 }
 
 }  // namespace
+
+void timeline_umma(bool reset, unsigned long long* out4) {
+  if (reset) {
+    const int on = 1;
+    const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+    cudaMemcpyToSymbol(g_tl_on, &on, sizeof on);
+    cudaMemcpyToSymbol(g_tl, init, sizeof init);
+  } else {
+    cudaMemcpyFromSymbol(out4, g_tl, 4 * sizeof(unsigned long long));
+  }
+}
 
 cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, const GramStats& st,
                                 cudaStream_t s, int* launches) {

@@ -438,6 +438,16 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
   cudaStream_t st = S(s);
   int L = 0;
   const bool banded = banded_stats(n);
+  // PB_TIMELINE (tuning only, eager calls): entry/exit of prep, Gram and combine
+  static const bool tl_env = getenv("PB_TIMELINE") != nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (tl_env) cudaStreamIsCapturing(st, &cap);
+  const bool tl = tl_env && cap == cudaStreamCaptureStatusNone;
+  if (tl) {
+    cudaStreamSynchronize(st);
+    timeline_stats(true, nullptr);
+    timeline_umma(true, nullptr);
+  }
   GramStats gs;
   if (banded) {  // one pass: band-centred split + per-band column statistics
     PB_CUDA(launch_band_prep(data, n, m, corr, w.xt.hi, w.xt.lo, w.xt.ld, w.band_mean, corr ? w.band_m2 : nullptr, st));
@@ -469,6 +479,16 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
   PB_CUDA(launch_umma_gemm(d, st, &L));
   if (d.flags & EPI_PARTIAL) PB_CUDA(launch_gram_combine(d, pl, corr, gs, st, &L));
   g_launches = L;
+  if (tl) {
+    cudaStreamSynchronize(st);
+    unsigned long long a[2] = {0, 0}, b[4] = {0, 0, 0, 0};
+    timeline_stats(false, a);
+    timeline_umma(false, b);
+    const double t0 = (double)a[0];
+    auto us = [&](unsigned long long v) { return v == ~0ull || v == 0 ? -1.0 : ((double)v - t0) / 1e3; };
+    fprintf(stderr, "[pb timeline] prep %.1f-%.1f | gram %.1f-%.1f | combine %.1f-%.1f us\n", us(a[0]), us(a[1]),
+            us(b[0]), us(b[1]), us(b[2]), us(b[3]));
+  }
   return PB_OK;
 }
 

@@ -50,6 +50,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---------------------------------------------------------------- PB_TIMELINE (tuning only)
+// First CTA entry / last CTA exit of a kernel, in %globaltimer ns, into a per-TU
+// device array (a[2k] = min entry, a[2k+1] = max exit). `on` is a device flag the
+// host sets only when PB_TIMELINE is in the environment.
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_enter(int on, unsigned long long* a, int k) {
+  if (on && threadIdx.x == 0) atomicMin(&a[2 * k], gtimer_ns());
+}
+__device__ __forceinline__ void tl_exit(int on, unsigned long long* a, int k) {
+  if (on && threadIdx.x == 0) atomicMax(&a[2 * k + 1], gtimer_ns());
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

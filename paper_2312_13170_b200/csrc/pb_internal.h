@@ -117,6 +117,9 @@ cudaError_t launch_gemm_listing8(int ni, int nj, int nk, float alpha, float beta
                                  const float* B, cudaStream_t s);
 cudaError_t launch_gemm_listing9(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                  const float* B, cudaStream_t s);
+// PB_TIMELINE (tuning only): reset the per-kernel entry/exit stamps, or read them back.
+void timeline_stats(bool reset, unsigned long long* out2);
+void timeline_umma(bool reset, unsigned long long* out4);
 cudaError_t launch_gemm_small(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                               const float* B, cudaStream_t s);
 cudaError_t launch_gemm_listing9_reg(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
