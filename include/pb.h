@@ -231,6 +231,42 @@ pb_status pb_comm_init(int nranks, int rank, const unsigned char id[128], pb_com
 pb_status pb_comm_destroy(pb_comm* comm);
 pb_status pb_comm_size(const pb_comm* comm, int* nranks, int* rank);
 
+/* Peer-memory collectives (the fused path). A pb_peer is one
+ * symmetric device buffer per rank (a 4 KiB header + data_bytes), mapped into
+ * every other rank's address space with CUDA IPC: NVLink/NVSwitch P2P between
+ * GPUs, or one GPU shared by several processes. A collective is two libpb
+ * kernels: push (each rank stores its data straight into the destinations'
+ * buffers, then release-stores a per-source flag at system scope) and consume
+ * (acquire every flag, then sum the slots in rank order — deterministic — or
+ * copy the gathered region out, then ack each source so that the next
+ * collective may overwrite its slot). Every wait is bounded: on timeout the
+ * status word (pb_peer_status) becomes non-zero instead of hanging.
+ *   pb_peer_create: allocates the buffer (cudaMalloc, owned by the pb_peer) and
+ *     writes this rank's 64-byte IPC handle; at most 8 ranks.
+ *   pb_peer_open: handles = nranks x 64 bytes (every rank's handle, in rank
+ *     order, gathered out of band); maps the other ranks' buffers.
+ *   pb_peer_reduce_scatter: out_blk = this rank's block (partition tri 0,
+ *     align 4) of the element-wise sum over ranks of partial[0, total).
+ *     Needs data_bytes >= nranks * max block * 4.
+ *   pb_peer_all_gather: every rank's row block send_blk (rows partition tri 0,
+ *     align 128, cols floats per row) -> the full rows x cols array recv on
+ *     every rank (send_blk may point into recv). Needs data_bytes >= rows*cols*4.
+ *   pb_comm_attach_peer: the comm's dist entry points then use the peer
+ *     collectives instead of NCCL (3mm's all-gather on the comm's side stream).
+ *   pb_comm_init_local: a comm without NCCL (collectives only via an attached
+ *     peer group), e.g. several processes sharing one GPU.
+ * Destroy a peer group only after every rank finished using it (barrier). */
+typedef struct pb_peer pb_peer;
+pb_status pb_peer_create(int nranks, int rank, size_t data_bytes, pb_peer** out, unsigned char handle[64]);
+pb_status pb_peer_open(pb_peer* peer, const unsigned char* handles);
+pb_status pb_peer_destroy(pb_peer* peer);
+pb_status pb_peer_status(const pb_peer* peer, unsigned* status);
+pb_status pb_peer_reduce_scatter(pb_peer* peer, const float* partial, float* out_blk, int total, pb_stream s);
+pb_status pb_peer_all_gather(pb_peer* peer, const float* send_blk, float* recv, int rows, int cols,
+                             pb_stream s);
+pb_status pb_comm_attach_peer(pb_comm* comm, pb_peer* peer);
+pb_status pb_comm_init_local(int nranks, int rank, pb_comm** out);
+
 /* C_blk = beta*C_blk + alpha*A_blk*B.  A_blk rows x nk, B nk x nj, C_blk rows x nj. */
 pb_status pb_gemm_dist(pb_comm* comm, int ni, int nj, int nk, float alpha, float beta, float* C_blk,
                        const float* A_blk, const float* B, void* ws, size_t ws_bytes, pb_stream s);

@@ -21,7 +21,8 @@ __all__ = [
     "pb_row_partition", "pb_syrk_rows", "pb_gesummv_rows", "pb_syr2k_rows", "pb_matvec_partial", "pb_gemm_variant",
     "pb_version", "last_launch_count", "ABI_FUNCTIONS", "Comm", "pb_comm_unique_id", "pb_comm_init",
     "pb_comm_destroy", "pb_gemm_dist", "pb_2mm_dist", "pb_3mm_dist", "pb_syrk_dist", "pb_syr2k_dist",
-    "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist",
+    "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist", "Peer", "pb_peer_create",
+    "pb_comm_init_local", "pb_comm_attach_peer",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -73,6 +74,15 @@ ABI_FUNCTIONS = {
     "pb_bicg_dist": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_mvt_dist": ([_P, _I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gesummv_dist": ([_P, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    # peer-memory collectives (CUDA IPC symmetric buffers)
+    "pb_peer_create": ([_I, _I, _Z, ctypes.POINTER(_P), _P], _I),
+    "pb_peer_open": ([_P, _P], _I),
+    "pb_peer_destroy": ([_P], _I),
+    "pb_peer_status": ([_P, ctypes.POINTER(ctypes.c_uint)], _I),
+    "pb_peer_reduce_scatter": ([_P, _P, _P, _I, _P], _I),
+    "pb_peer_all_gather": ([_P, _P, _P, _I, _I, _P], _I),
+    "pb_comm_attach_peer": ([_P, _P], _I),
+    "pb_comm_init_local": ([_I, _I, ctypes.POINTER(_P)], _I),
 }
 
 _lib = None
@@ -365,3 +375,51 @@ def pb_gesummv_dist(comm, n_, alpha, beta, A_blk, B_blk, tmp_blk, x, y_blk, ws=N
     p, n, keep = _dws(ws, "gesummv", (n_,), comm, x)
     _check("pb_gesummv_dist", lib().pb_gesummv_dist(comm.handle, n_, alpha, beta, _ptr(A_blk), _ptr(B_blk),
                                                     _ptr(tmp_blk), _ptr(x), _ptr(y_blk), p, n, _stream(stream, x)))
+
+
+class Peer:
+    """A libpb peer group: one symmetric device buffer per rank, mapped into every
+    rank with CUDA IPC (include/pb.h, pb_peer_*)."""
+
+    def __init__(self, handle, nranks, rank, ipc_handle):
+        self.handle, self.nranks, self.rank, self.ipc_handle = handle, nranks, rank, ipc_handle
+
+    def open(self, handles: bytes):
+        buf = ctypes.create_string_buffer(handles, len(handles))
+        _check("pb_peer_open", lib().pb_peer_open(self.handle, ctypes.cast(buf, ctypes.c_void_p)))
+
+    def status(self) -> int:
+        v = ctypes.c_uint(0)
+        _check("pb_peer_status", lib().pb_peer_status(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def reduce_scatter(self, partial, out_blk, total, stream=None):
+        _check("pb_peer_reduce_scatter", lib().pb_peer_reduce_scatter(self.handle, _ptr(partial), _ptr(out_blk),
+                                                                      total, _stream(stream, partial)))
+
+    def all_gather(self, send_blk, recv, rows, cols, stream=None):
+        _check("pb_peer_all_gather", lib().pb_peer_all_gather(self.handle, _ptr(send_blk), _ptr(recv), rows, cols,
+                                                              _stream(stream, recv)))
+
+    def close(self):
+        if self.handle:
+            _check("pb_peer_destroy", lib().pb_peer_destroy(self.handle))
+            self.handle = None
+
+
+def pb_peer_create(nranks, rank, data_bytes) -> Peer:
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(64)
+    _check("pb_peer_create", lib().pb_peer_create(nranks, rank, data_bytes, ctypes.byref(h),
+                                                  ctypes.cast(buf, ctypes.c_void_p)))
+    return Peer(h.value, nranks, rank, buf.raw)
+
+
+def pb_comm_init_local(nranks, rank) -> Comm:
+    h = ctypes.c_void_p()
+    _check("pb_comm_init_local", lib().pb_comm_init_local(nranks, rank, ctypes.byref(h)))
+    return Comm(h.value, nranks, rank)
+
+
+def pb_comm_attach_peer(comm: Comm, peer: Peer):
+    _check("pb_comm_attach_peer", lib().pb_comm_attach_peer(comm.handle, peer.handle if peer else None))

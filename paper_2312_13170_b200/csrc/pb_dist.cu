@@ -22,8 +22,20 @@
 
 using namespace pb;
 
+// Symmetric peer buffer (k_peer.cu): header (flags, acks, counters, status) + data region.
+struct pb_peer {
+  int nranks = 0, rank = 0, dev = -1;
+  char* base = nullptr;  // own allocation: PEER_HDR + data_bytes
+  size_t data_bytes = 0;
+  char* mapped[PEER_MAXR] = {};  // every rank's base in this process (own = base)
+  bool opened = false;
+  unsigned long long epoch = 0;  // collectives issued so far (identical on every rank)
+  PeerView view;
+};
+
 struct pb_comm {
-  ncclComm_t nc = nullptr;
+  ncclComm_t nc = nullptr;  // null for a local comm (pb_comm_init_local): collectives via the peer group
+  pb_peer* peer = nullptr;  // attached peer group: fused peer-memory collectives instead of NCCL
   int nranks = 0, rank = 0, dev = -1;
   cudaStream_t side = nullptr;  // collectives overlapped with compute (3mm's all-gather)
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
@@ -104,7 +116,7 @@ Blk block(int rows, int nranks, int g, bool tri, int align) {
 }
 
 pb_status comm_ok(const pb_comm* c) {
-  if (!c || !c->nc) return fail(PB_ERR_INVALID_ARG, "comm is NULL or destroyed");
+  if (!c || (!c->nc && !c->peer)) return fail(PB_ERR_INVALID_ARG, "comm is NULL, destroyed, or has no transport");
   int dev = -1;
   cudaGetDevice(&dev);
   if (dev != c->dev) return fail(PB_ERR_INVALID_ARG, "current device %d is not the comm's device %d", dev, c->dev);
@@ -172,9 +184,72 @@ size_t local_need(const std::string& k, const long long* d, int G, int g) {
   return 0;  // gesummv: none
 }
 
+// ---- peer-memory versions (k_peer.cu): one push + one consume kernel each
+pb_status peer_ready(const pb_peer* p) {
+  if (!p || !p->opened) return fail(PB_ERR_INVALID_ARG, "peer group is NULL or not opened");
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != p->dev) return fail(PB_ERR_INVALID_ARG, "current device %d is not the peer group's device %d", dev, p->dev);
+  return PB_OK;
+}
+
+pb_status peer_rs(pb_peer* P, const float* partial, float* dst, int total, int align, cudaStream_t s) {
+  PB_TRY(peer_ready(P));
+  long long slot = 0;
+  PeerPush push;
+  Blk me;
+  for (int g = 0; g < P->nranks; ++g) {
+    const Blk k = block(total, P->nranks, g, false, align);
+    if (g == P->rank) me = k;
+    slot = std::max<long long>(slot, k.n());
+  }
+  slot = (slot + 3) / 4 * 4;
+  if ((size_t)slot * P->nranks * sizeof(float) > P->data_bytes)
+    return fail(PB_ERR_WORKSPACE, "peer data region (%zu bytes) < %lld slots of %lld floats", P->data_bytes,
+                (long long)P->nranks, slot);
+  for (int g = 0; g < P->nranks; ++g) {
+    const Blk k = block(total, P->nranks, g, false, align);
+    push.src[g] = partial + k.b;
+    push.dst_off[g] = (long long)P->rank * slot;
+    push.count[g] = k.n();
+  }
+  PeerConsume con;
+  con.out = dst;
+  con.count = me.n();
+  con.slot = slot;
+  con.reduce = 1;
+  const unsigned long long e = ++P->epoch;
+  PB_CU(launch_peer_push(P->view, push, e, s));
+  PB_CU(launch_peer_consume(P->view, con, e, s));
+  return PB_OK;
+}
+
+pb_status peer_ag(pb_peer* P, const float* send_blk, float* recv, int rows, int cols, int align, cudaStream_t s) {
+  PB_TRY(peer_ready(P));
+  if ((size_t)rows * cols * sizeof(float) > P->data_bytes)
+    return fail(PB_ERR_WORKSPACE, "peer data region (%zu bytes) < %d x %d floats", P->data_bytes, rows, cols);
+  const Blk me = block(rows, P->nranks, P->rank, false, align);
+  PeerPush push;
+  for (int g = 0; g < P->nranks; ++g) {
+    push.src[g] = send_blk;
+    push.dst_off[g] = (long long)me.b * cols;
+    push.count[g] = (long long)me.n() * cols;
+  }
+  PeerConsume con;
+  con.out = recv;
+  con.count = (long long)rows * cols;
+  con.slot = 0;
+  con.reduce = 0;
+  const unsigned long long e = ++P->epoch;
+  PB_CU(launch_peer_push(P->view, push, e, s));
+  PB_CU(launch_peer_consume(P->view, con, e, s));
+  return PB_OK;
+}
+
 // dst (this rank's block of a length-`total` vector, partition tri 0 / align 4)
 //   <- sum over ranks of partial[0, total)
 pb_status reduce_scatter(pb_comm* c, const float* partial, float* dst, int total, cudaStream_t s) {
+  if (c->peer) return peer_rs(c->peer, partial, dst, total, ALIGN_MV, s);
   const Nccl& N = nccl();
   bool equal = true;
   const Blk me = block(total, c->nranks, c->rank, false, ALIGN_MV);
@@ -201,6 +276,10 @@ pb_status reduce_scatter(pb_comm* c, const float* partial, float* dst, int total
 
 // Every rank's rows of F (rows x cols, partition tri 0 / align 128) -> the full F, in place.
 pb_status all_gather_rows(pb_comm* c, float* F, int rows, int cols, cudaStream_t s) {
+  if (c->peer) {
+    const Blk me = block(rows, c->nranks, c->rank, false, ALIGN_MM);
+    return peer_ag(c->peer, F + (size_t)me.b * cols, F, rows, cols, ALIGN_MM, s);
+  }
   const Nccl& N = nccl();
   bool equal = true;
   const Blk me = block(rows, c->nranks, c->rank, false, ALIGN_MM);
@@ -309,6 +388,111 @@ pb_status pb_comm_size(const pb_comm* c, int* nranks, int* rank) {
   return PB_OK;
 }
 
+pb_status pb_comm_init_local(int nranks, int rank, pb_comm** out) {
+  if (!out || nranks <= 0 || rank < 0 || rank >= nranks)
+    return fail(PB_ERR_INVALID_ARG, "bad comm arguments (nranks %d, rank %d)", nranks, rank);
+  pb_comm* c = new pb_comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  cudaGetDevice(&c->dev);
+  pb_status st = cu_check(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+  if (st == PB_OK) st = cu_check(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming), "event");
+  if (st == PB_OK) st = cu_check(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming), "event");
+  if (st != PB_OK) {
+    pb_comm_destroy(c);
+    return st;
+  }
+  *out = c;
+  return PB_OK;
+}
+
+pb_status pb_comm_attach_peer(pb_comm* c, pb_peer* p) {
+  if (!c) return fail(PB_ERR_INVALID_ARG, "comm is NULL");
+  if (p && (p->nranks != c->nranks || p->rank != c->rank || !p->opened))
+    return fail(PB_ERR_INVALID_ARG, "peer group does not match the comm (or is not opened)");
+  c->peer = p;
+  return PB_OK;
+}
+
+pb_status pb_peer_create(int nranks, int rank, size_t data_bytes, pb_peer** out, unsigned char handle[64]) {
+  if (!out || !handle || nranks <= 0 || nranks > PEER_MAXR || rank < 0 || rank >= nranks)
+    return fail(PB_ERR_INVALID_ARG, "bad peer arguments (nranks %d (max %d), rank %d)", nranks, PEER_MAXR, rank);
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  pb_peer* p = new pb_peer;
+  p->nranks = nranks;
+  p->rank = rank;
+  p->data_bytes = (data_bytes + 255) / 256 * 256;
+  cudaGetDevice(&p->dev);
+  pb_status st = cu_check(cudaMalloc(&p->base, PEER_HDR + p->data_bytes), "cudaMalloc (peer buffer)");
+  if (st == PB_OK) st = cu_check(cudaMemset(p->base, 0, PEER_HDR), "cudaMemset (peer header)");
+  cudaIpcMemHandle_t h;
+  if (st == PB_OK) st = cu_check(cudaIpcGetMemHandle(&h, p->base), "cudaIpcGetMemHandle");
+  if (st != PB_OK) {
+    pb_peer_destroy(p);
+    return st;
+  }
+  memcpy(handle, &h, 64);
+  *out = p;
+  return PB_OK;
+}
+
+pb_status pb_peer_open(pb_peer* p, const unsigned char* handles) {
+  if (!p || !handles) return fail(PB_ERR_INVALID_ARG, "NULL argument");
+  if (p->opened) return fail(PB_ERR_INVALID_ARG, "peer group already opened");
+  for (int g = 0; g < p->nranks; ++g) {
+    if (g == p->rank) {
+      p->mapped[g] = p->base;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * (size_t)g, 64);
+    void* ptr = nullptr;
+    PB_CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    p->mapped[g] = static_cast<char*>(ptr);
+  }
+  PeerView& v = p->view;
+  v.nranks = p->nranks;
+  v.rank = p->rank;
+  for (int g = 0; g < p->nranks; ++g) {  // header: flags @0, acks @512, counters @1024, status @1536
+    v.data[g] = reinterpret_cast<float*>(p->mapped[g] + PEER_HDR);
+    v.flags[g] = reinterpret_cast<unsigned long long*>(p->mapped[g]);
+    v.acks[g] = reinterpret_cast<unsigned long long*>(p->mapped[g] + 512);
+  }
+  v.flags_mine = v.flags[p->rank];
+  v.acks_mine = v.acks[p->rank];
+  v.counter = reinterpret_cast<unsigned*>(p->base + 1024);
+  v.status = reinterpret_cast<unsigned*>(p->base + 1536);
+  p->opened = true;
+  return PB_OK;
+}
+
+pb_status pb_peer_destroy(pb_peer* p) {
+  if (!p) return PB_OK;
+  for (int g = 0; g < p->nranks; ++g)
+    if (g != p->rank && p->mapped[g]) cudaIpcCloseMemHandle(p->mapped[g]);
+  if (p->base) cudaFree(p->base);
+  delete p;
+  return PB_OK;
+}
+
+pb_status pb_peer_status(const pb_peer* p, unsigned* status) {
+  if (!p || !status) return fail(PB_ERR_INVALID_ARG, "NULL argument");
+  PB_CU(cudaMemcpy(status, p->base + 1536, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  return PB_OK;
+}
+
+pb_status pb_peer_reduce_scatter(pb_peer* p, const float* partial, float* out_blk, int total, pb_stream s) {
+  if (total <= 0 || total % 4) return fail(PB_ERR_UNSUPPORTED, "total %d must be a positive multiple of 4", total);
+  set_launches(2);
+  return peer_rs(p, partial, out_blk, total, ALIGN_MV, S(s));
+}
+
+pb_status pb_peer_all_gather(pb_peer* p, const float* send_blk, float* recv, int rows, int cols, pb_stream s) {
+  if (rows <= 0 || cols <= 0 || cols % 4) return fail(PB_ERR_UNSUPPORTED, "rows %d, cols %d (multiple of 4)", rows, cols);
+  set_launches(2);
+  return peer_ag(p, send_blk, recv, rows, cols, ALIGN_MM, S(s));
+}
+
 // ---- no exchange: the local entry point on this rank's rows
 pb_status pb_gemm_dist(pb_comm* c, int ni, int nj, int nk, float alpha, float beta, float* C_blk, const float* A_blk,
                        const float* B, void* ws, size_t ws_bytes, pb_stream s) {
@@ -382,6 +566,7 @@ pb_status pb_3mm_dist(pb_comm* c, int ni, int nj, int nk, int nl, int nm, float*
   PB_CU(cudaEventRecord(c->ev_ready, st));
   PB_CU(cudaStreamWaitEvent(c->side, c->ev_ready, 0));
   PB_TRY(all_gather_rows(c, F, nj, nl, c->side));
+  if (c->peer) L += 2;
   PB_CU(cudaEventRecord(c->ev_done, c->side));
   if (r.n()) {  // E = A B overlaps the all-gather
     PB_TRY(pb_gemm(r.n(), nj, nk, 1.f, 0.f, E_blk, A_blk, B, w.local, w.local_bytes, s));
@@ -419,7 +604,7 @@ pb_status pb_atax_dist(pb_comm* c, int m, int n, const float* A_blk, const float
     PB_CU(cudaMemsetAsync(w.partial, 0, sizeof(float) * n, S(s)));
   }
   PB_TRY(reduce_scatter(c, w.partial, y_blk, n, S(s)));
-  set_launches(L);
+  set_launches(L + (c->peer ? 2 : 0));
   return PB_OK;
 }
 
@@ -446,7 +631,7 @@ pb_status pb_bicg_dist(pb_comm* c, int m, int n, const float* A_blk, float* s_bl
     PB_CU(cudaMemsetAsync(w.partial, 0, sizeof(float) * m, S(s)));
   }
   PB_TRY(reduce_scatter(c, w.partial, s_blk, m, S(s)));
-  set_launches(L);
+  set_launches(L + (c->peer ? 2 : 0));
   return PB_OK;
 }
 
@@ -478,7 +663,7 @@ pb_status pb_mvt_dist(pb_comm* c, int n, float* x1_blk, float* x2_blk, const flo
     PB_CU(cudaMemsetAsync(w.partial, 0, sizeof(float) * n, st));
   }
   PB_TRY(reduce_scatter(c, w.partial, x2_blk, n, st));
-  set_launches(L);
+  set_launches(L + (c->peer ? 2 : 0));
   return PB_OK;
 }
 

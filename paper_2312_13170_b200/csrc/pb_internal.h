@@ -112,6 +112,33 @@ size_t atax_ws_bytes(int m, int n);
 cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, float* tmp, void* ws,
                         cudaStream_t s, int* launches);
 
+// ---- peer-memory collectives (k_peer.cu; host side in pb_dist.cu) ------------
+constexpr int PEER_MAXR = 8;            // ranks per peer group
+constexpr size_t PEER_HDR = 4096;       // header bytes before the data region
+// Device-side view of a peer group (pointers valid in this process).
+struct PeerView {
+  float* data[PEER_MAXR];                // data region of rank g
+  unsigned long long* flags[PEER_MAXR];  // flags array of rank g (indexed by source rank)
+  unsigned long long* acks[PEER_MAXR];   // acks array of rank g (indexed by consumer rank)
+  unsigned long long* flags_mine;        // == flags[rank]
+  unsigned long long* acks_mine;         // == acks[rank]
+  unsigned* counter;                     // this rank's grid counters [push, consume]
+  unsigned* status;                      // != 0: a bounded wait timed out
+  int nranks = 0, rank = 0;
+};
+struct PeerPush {  // for every destination g: count floats from src[g] to data[g] + dst_off[g]
+  const float* src[PEER_MAXR];
+  long long dst_off[PEER_MAXR];
+  long long count[PEER_MAXR];
+};
+struct PeerConsume {  // reduce: out[i] = sum_g data_mine[g * slot + i]; else out[i] = data_mine[i]
+  float* out;
+  long long count, slot;
+  int reduce;
+};
+cudaError_t launch_peer_push(const PeerView& v, const PeerPush& p, unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_peer_consume(const PeerView& v, const PeerConsume& c, unsigned long long epoch, cudaStream_t s);
+
 // ---- SIMT ablation kernels (k_simt.cu): PAPER.md Listing 8 / Listing 9 -------
 cudaError_t launch_gemm_listing8(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                  const float* B, cudaStream_t s);

@@ -35,26 +35,57 @@ import torch.distributed as dist
 import paper_2312_13170_b200 as _pb
 
 
-_COMM = None  # libpb communicator (pb_comm_init), set by init_comm()
+_COMM = None  # libpb communicator (pb_comm_init / pb_comm_init_local), set by init_comm()
+_PEER = None  # libpb peer group attached to it (fused peer-memory collectives)
 
 
-def init_comm():
-    """Create the libpb communicator over the current torch.distributed group:
-    rank 0's NCCL unique id is broadcast through torch.distributed."""
-    global _COMM
+def init_comm(transport=None, peer_bytes=64 << 20):
+    """Create the libpb communicator over the current torch.distributed group.
+
+    transport (default: env PB_TRANSPORT, else "nccl"):
+      "nccl"   NCCL inside libpb (rank 0's unique id broadcast through torch.distributed)
+      "peer"   NCCL comm + an attached peer group: the exchange steps run as libpb's
+               push/consume kernels over CUDA IPC mappings (NVLink/NVSwitch P2P)
+      "local"  no NCCL, peer group only (e.g. several processes sharing one GPU)
+    peer_bytes: data region of the peer group (3mm's all-gather needs n*n*4)."""
+    global _COMM, _PEER
+    transport = transport or os.environ.get("PB_TRANSPORT", "nccl")
     world, rank = _world()
-    uid = [_pb.pb_comm_unique_id() if rank == 0 else None]
-    if world > 1:
-        dist.broadcast_object_list(uid, src=0)
-    _COMM = _pb.pb_comm_init(world, rank, uid[0])
+    if transport == "local":
+        _COMM = _pb.pb_comm_init_local(world, rank)
+    else:
+        uid = [_pb.pb_comm_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        _COMM = _pb.pb_comm_init(world, rank, uid[0])
+    if transport in ("peer", "local"):
+        _PEER = _pb.pb_peer_create(world, rank, peer_bytes)
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, _PEER.ipc_handle)
+        else:
+            handles = [_PEER.ipc_handle]
+        _PEER.open(b"".join(handles))
+        _pb.pb_comm_attach_peer(_COMM, _PEER)
     return _COMM
 
 
 def close_comm():
-    global _COMM
+    """Destroy the communicator (and peer group). Call after every rank is done
+    (the caller synchronises and barriers first)."""
+    global _COMM, _PEER
     if _COMM is not None:
         _COMM.close()
         _COMM = None
+    if _PEER is not None:
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            dist.barrier()  # no rank may still write into this buffer
+        _PEER.close()
+        _PEER = None
+
+
+def peer():
+    return _PEER
 
 
 def comm():

@@ -34,12 +34,15 @@ def _worker(rank, world, port, q, backend="gloo"):
     from paper_2312_13170_b200 import dist as D
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
-    if backend == "nccl":  # world size 1 kept on the sharded path: NCCL collectives on device tensors
+    if backend.startswith("nccl"):  # world size 1 kept on the sharded path
         os.environ["PB_FORCE_DIST"] = "1"
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
-        D.init_comm()  # the pb_<k>_dist entry points: NCCL inside libpb
+        # the pb_<k>_dist entry points: NCCL inside libpb, or NCCL + peer-memory collectives
+        D.init_comm(transport="peer" if backend == "nccl-peer" else "nccl", peer_bytes=4 << 20)
     else:
         dist.init_process_group("gloo", rank=rank, world_size=world)
+        if backend == "gloo-peer":  # local libpb comm: collectives = peer-memory kernels over CUDA IPC
+            D.init_comm(transport="local", peer_bytes=4 << 20)
     dev = torch.device("cuda", 0)
     H = lambda r, c, s, **kw: torch.from_numpy(pbgen.gen_host(r, c, s, **kw)).to(dev)  # noqa: E731
     res = {}
@@ -104,12 +107,14 @@ def _worker(rank, world, port, q, backend="gloo"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1)])
+@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1), ("gloo-peer", 2), ("nccl-peer", 1)])
 def test_dist_ranks_one_gpu_real_kernels(backend, world):
     """gloo: two ranks share cuda:0 (host-staged torch collectives). nccl: one rank
     with PB_FORCE_DIST and a libpb communicator, i.e. the N>1 code path through
     the C ABI's pb_<k>_dist entry points (NCCL all-gather / reduce-scatter inside
-    libpb, 3mm's side stream) end to end."""
+    libpb, 3mm's side stream) end to end. gloo-peer: two processes on cuda:0 with
+    a local libpb comm whose collectives are the peer-memory push/consume kernels
+    over CUDA IPC (the fused path). nccl-peer: the same kernels at world size 1."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
@@ -180,3 +185,75 @@ def test_bench_forced_sharded_nccl():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["value"] > 0 and line["e2e"]["value"] > 0
     assert all(v["ms"] > 0 for v in line["kernels"].values())
+
+
+def _peer_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_2312_13170_b200 as pb
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        P = pb.pb_peer_create(world, rank, 1 << 20)
+        hs = [None] * world
+        dist.all_gather_object(hs, P.ipc_handle)
+        P.open(b"".join(hs))
+        dev = torch.device("cuda", 0)
+        out = []
+        for it, total in enumerate([1004, 4096, 12, 1004, 65536]):  # several epochs, uneven blocks
+            part = torch.from_numpy(pbgen.gen_host(1, total, 20 + it + 7 * rank)[0]).to(dev)
+            b, e = pb.pb_row_partition(total, world, rank, False, 4)
+            blk = torch.full((max(e - b, 1),), float("nan"), device=dev)
+            P.reduce_scatter(part, blk, total)
+            rows, cols = 300 + it, 8
+            fb, fe = pb.pb_row_partition(rows, world, rank, False, 128)
+            full = torch.full((rows, cols), float("nan"), device=dev)
+            mine = torch.from_numpy(pbgen.gen_host(rows, cols, 40 + it)[fb:fe].copy()).to(dev)
+            full[fb:fe].copy_(mine)
+            P.all_gather(full[fb:fe], full, rows, cols)  # in place
+            torch.cuda.synchronize()
+            out.append((total, b, e, blk.cpu().numpy()[: e - b], rows, full.cpu().numpy()))
+        res["out"] = out
+        res["status"] = P.status()
+        dist.barrier()
+        P.close()
+        q.put((rank, res))
+    except Exception as ex:  # report instead of hanging the parent
+        q.put((rank, {"error": repr(ex)}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_collectives_two_processes_one_gpu():
+    """pb_peer reduce-scatter / all-gather between two processes sharing cuda:0
+    (CUDA IPC): bitwise equal to the fp32 sum in rank order / the gathered rows,
+    over several epochs (the ack handshake lets a slot be reused)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world, port = 2, _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert "error" not in res[r], res[r]
+        assert res[r]["status"] == 0
+    for it in range(5):
+        total = res[0]["out"][it][0]
+        parts = [pbgen.gen_host(1, total, 20 + it + 7 * r)[0] for r in range(world)]
+        ref = parts[0].copy()
+        for r in range(1, world):
+            ref = (ref + parts[r]).astype(np.float32)  # fp32, rank order
+        rows = res[0]["out"][it][4]
+        full_ref = pbgen.gen_host(rows, 8, 40 + it)
+        for r in range(world):
+            _, b, e, blk, _, full = res[r]["out"][it]
+            assert np.array_equal(blk.view(np.uint32), ref[b:e].view(np.uint32)), (it, r)
+            assert np.array_equal(full.view(np.uint32), full_ref.view(np.uint32)), (it, r)
