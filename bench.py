@@ -256,10 +256,18 @@ def run_ours(args):
         os.environ.setdefault("WORLD_SIZE", "1")
         if os.environ.get("PB_SHARE_GPU"):
             dist.init_process_group("gloo")
+            if os.environ.get("PB_TRANSPORT") == "local":  # peer-memory kernels between processes on one GPU
+                import paper_2312_13170_b200.dist as D
+                D.init_comm(transport="local", peer_bytes=max(MM_N * MM_N * 4, MV_N * 4 * 2) + (1 << 20))
         else:
             dist.init_process_group("nccl", device_id=dev)
             import paper_2312_13170_b200.dist as D
-            D.init_comm()  # libpb's own NCCL communicator: the pb_<k>_dist entry points
+            # libpb's communicator for the pb_<k>_dist entry points. Default transport
+            # "peer": the exchange steps run as libpb's push/consume kernels over CUDA
+            # IPC peer memory (NVLink/NVSwitch), NCCL for bootstrap / fallback;
+            # PB_TRANSPORT=nccl uses NCCL collectives inside libpb instead.
+            D.init_comm(transport=os.environ.get("PB_TRANSPORT", "peer"),
+                        peer_bytes=max(MM_N * MM_N * 4, MV_N * 4 * 2) + (1 << 20))
     kernels = KERNELS if args.kernels == "all" else args.kernels.split(",")
     suite = Suite(rank, world, dev, kernels)
     W = work()
@@ -395,6 +403,7 @@ def run_ours(args):
                                  "syrk/syr2k": SY_N, "atax/bicg/mvt/gesummv": MV_N},
                        "alpha": ALPHA, "beta": BETA, "eps": EPS,
                        "parallelism": f"row-block x{world}" if world > 1 else "single-gpu",
+                       "transport": _transport(),
                        "l2": "inputs larger than L2 (each step streams > 8 GiB of matrices)",
                        "launch": "per-kernel CUDA graph replay" if graphs else "eager C-ABI calls"},
             "kernels": kern,
@@ -412,6 +421,16 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         D.close_comm()
         dist.destroy_process_group()
+
+
+def _transport():
+    try:
+        import paper_2312_13170_b200.dist as D
+    except Exception:
+        return None
+    if D.comm() is None:
+        return None
+    return "peer-memory kernels (CUDA IPC)" if D.peer() is not None else "nccl (inside libpb)"
 
 
 def load_traffic(kernel):

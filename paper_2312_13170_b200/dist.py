@@ -59,14 +59,33 @@ def init_comm(transport=None, peer_bytes=64 << 20):
             dist.broadcast_object_list(uid, src=0)
         _COMM = _pb.pb_comm_init(world, rank, uid[0])
     if transport in ("peer", "local"):
-        _PEER = _pb.pb_peer_create(world, rank, peer_bytes)
-        handles = [None] * world
+        err = None
+        try:
+            _PEER = _pb.pb_peer_create(world, rank, peer_bytes)
+            handles = [None] * world
+            if world > 1:
+                dist.all_gather_object(handles, _PEER.ipc_handle)
+            else:
+                handles = [_PEER.ipc_handle]
+            _PEER.open(b"".join(handles))
+        except _pb.PBError as e:  # e.g. no P2P between these GPUs
+            err = repr(e)
+        errs = [None] * world
         if world > 1:
-            dist.all_gather_object(handles, _PEER.ipc_handle)
+            dist.all_gather_object(errs, err)
         else:
-            handles = [_PEER.ipc_handle]
-        _PEER.open(b"".join(handles))
-        _pb.pb_comm_attach_peer(_COMM, _PEER)
+            errs = [err]
+        if any(errs):  # every rank must agree on the transport
+            if _PEER is not None:
+                _PEER.close()
+                _PEER = None
+            if transport == "local":
+                raise RuntimeError(f"peer group unavailable: {errs}")
+            import sys
+            print(f"pb: peer-memory collectives unavailable ({[e for e in errs if e][0]}); using NCCL",
+                  file=sys.stderr)
+        else:
+            _pb.pb_comm_attach_peer(_COMM, _PEER)
     return _COMM
 
 

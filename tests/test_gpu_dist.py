@@ -169,22 +169,26 @@ def test_dist_ranks_one_gpu_real_kernels(backend, world):
         assert np.max(np.abs(got - ref) / np.abs(ref)) <= P.TOL, k
 
 
-def test_bench_forced_sharded_nccl():
-    """bench.py on the sharded path over a world-size-1 NCCL group: one JSON line,
-    every kernel timed, e2e included."""
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_bench_forced_sharded_nccl(transport):
+    """bench.py on the sharded path over a world-size-1 NCCL group (collectives:
+    libpb's peer-memory kernels, or NCCL inside libpb): one JSON line, every
+    kernel timed, e2e included."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import json
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PB_FORCE_DIST="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    env = dict(os.environ, PB_FORCE_DIST="1", PB_TRANSPORT=transport, MASTER_ADDR="127.0.0.1",
+               MASTER_PORT=str(_free_port()))
     r = subprocess.run([sys.executable, "bench.py", "--steps", "1", "--warmup", "3", "--no-cpu"], cwd=root, env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["value"] > 0 and line["e2e"]["value"] > 0
     assert all(v["ms"] > 0 for v in line["kernels"].values())
+    assert ("peer" in line["config"]["transport"]) == (transport == "peer")
 
 
 def _peer_worker(rank, world, port, q):
@@ -257,3 +261,28 @@ def test_peer_collectives_two_processes_one_gpu():
             _, b, e, blk, _, full = res[r]["out"][it]
             assert np.array_equal(blk.view(np.uint32), ref[b:e].view(np.uint32)), (it, r)
             assert np.array_equal(full.view(np.uint32), full_ref.view(np.uint32)), (it, r)
+
+
+@pytest.mark.parametrize("transport", ["gloo", "local"])
+def test_bench_two_ranks_share_gpu(transport):
+    """bench.py under torchrun with 2 ranks on cuda:0 (PB_SHARE_GPU): host-staged
+    gloo collectives, or libpb's peer-memory kernels between the two processes
+    (PB_TRANSPORT=local). Checks the N=2 launch path end to end (timings are not
+    meaningful: the ranks share one GPU)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PB_SHARE_GPU="1")
+    if transport == "local":
+        env["PB_TRANSPORT"] = "local"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "3",
+           "--no-cpu", "--no-e2e", "--kernels", "3mm,atax,bicg,mvt,gesummv"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert (line["config"]["transport"] or "").startswith("peer") == (transport == "local")
