@@ -158,7 +158,7 @@ class Suite:
             t["mm"]["F"] = e(n, n)
         if "syrk" in kernels or "syr2k" in kernels:
             n = SY_N
-            r0, r1 = pb.pb_row_partition(n, world, rank, True, 256)
+            r0, r1 = pb.pb_row_partition(n, world, rank, 2, 256)
             self.sy_rows = (r0, r1)
             t["sy"] = dict(A=gen(n, n, S["A"]), B=gen(n, n, S["B"]),
                            C=gen(max(r1 - r0, 1), n, S["C"], mode=pbgen.U01 | pbgen.SYM, row0=r0, ld=n))

@@ -158,9 +158,11 @@ pb_status pb_gesummv(int n, float alpha, float beta, const float* A, const float
 
 /* ------------------------------------------------------------------------
  * Row-block sharding helpers (multi-GPU, one process per GPU).
- * Rank g owns output rows [begin, end). triangular != 0 balances the area of a
- * lower triangle (boundaries ~ rows*sqrt(g/G)); boundaries are multiples of
- * `align` (except the last, == rows).
+ * Rank g owns output rows [begin, end). triangular = 0: uniform; 1: balances
+ * the area of a lower triangle (boundaries ~ rows*sqrt(g/G)); 2: balances
+ * area + 267 * end (syrk/syr2k: a rank also splits rows [0, end) of its
+ * operands; the constant is the measured split-row / triangle-element cost
+ * ratio). Boundaries are multiples of `align` (except the last, == rows).
  */
 pb_status pb_row_partition(int rows, int nranks, int rank, int triangular, int align, int* begin,
                            int* end);
@@ -209,7 +211,7 @@ pb_status pb_gesummv_rows(int rows, int n, float alpha, float beta, const float*
  *
  * Partitions (rank g's block = pb_row_partition(rows, nranks, g, tri, align)):
  *   gemm/2mm/3mm rows of ni, and 3mm's rows of F/C (nj): tri 0, align 128
- *   syrk/syr2k rows of C (n): tri 1, align 256
+ *   syrk/syr2k rows of C (n): tri 2, align 256
  *   atax/bicg/mvt/gesummv rows of A, and the reduce-scatter destinations
  *   (atax y over n, bicg s over m, mvt x2 over n): tri 0, align 4
  * "_blk" arguments point at the first row (element) of this rank's block and

@@ -109,9 +109,9 @@ struct Blk {
   int b = 0, e = 0;
   int n() const { return e - b; }
 };
-Blk block(int rows, int nranks, int g, bool tri, int align) {
+Blk block(int rows, int nranks, int g, int mode, int align) {  // mode: pb_row_partition's `triangular`
   Blk k;
-  pb_row_partition(rows, nranks, g, tri ? 1 : 0, align, &k.b, &k.e);
+  pb_row_partition(rows, nranks, g, mode, align, &k.b, &k.e);
   return k;
 }
 
@@ -151,34 +151,34 @@ DistWs dist_ws(void* ws, size_t ws_bytes, long long partial_len, long long base_
 
 size_t local_need(const std::string& k, const long long* d, int G, int g) {
   if (k == "gemm") {
-    const Blk r = block(d[0], G, g, false, ALIGN_MM);
+    const Blk r = block(d[0], G, g, 0, ALIGN_MM);
     return r.n() ? ws_of("gemm", {r.n(), d[1], d[2]}) : 0;
   }
   if (k == "2mm") {
-    const Blk r = block(d[0], G, g, false, ALIGN_MM);
+    const Blk r = block(d[0], G, g, 0, ALIGN_MM);
     return r.n() ? ws_of("2mm", {r.n(), d[1], d[2], d[3]}) : 0;
   }
   if (k == "3mm") {  // ni nj nk nl nm
-    const Blk r = block(d[0], G, g, false, ALIGN_MM), f = block(d[1], G, g, false, ALIGN_MM);
+    const Blk r = block(d[0], G, g, 0, ALIGN_MM), f = block(d[1], G, g, 0, ALIGN_MM);
     size_t b = 0;
     if (f.n()) b = std::max(b, ws_of("gemm", {f.n(), d[3], d[4]}));
     if (r.n()) b = std::max({b, ws_of("gemm", {r.n(), d[1], d[2]}), ws_of("gemm", {r.n(), d[3], d[1]})});
     return b;
   }
   if (k == "syrk" || k == "syr2k") {
-    const Blk r = block(d[0], G, g, true, ALIGN_SY);
+    const Blk r = block(d[0], G, g, 2, ALIGN_SY);
     return r.n() ? ws_of(k == "syrk" ? "syrk_rows" : "syr2k_rows", {d[0], d[1], r.b, r.e}) : 0;
   }
   if (k == "atax") {  // m n: rows of m
-    const Blk r = block(d[0], G, g, false, ALIGN_MV);
+    const Blk r = block(d[0], G, g, 0, ALIGN_MV);
     return r.n() ? ws_of("atax", {r.n(), d[1]}) : 0;
   }
   if (k == "bicg") {  // m n: A n x m, rows of n
-    const Blk r = block(d[1], G, g, false, ALIGN_MV);
+    const Blk r = block(d[1], G, g, 0, ALIGN_MV);
     return r.n() ? ws_of("bicg", {d[0], r.n()}) : 0;
   }
   if (k == "mvt") {
-    const Blk r = block(d[0], G, g, false, ALIGN_MV);
+    const Blk r = block(d[0], G, g, 0, ALIGN_MV);
     return r.n() ? ws_of("matvec_partial", {r.n(), d[0]}) : 0;
   }
   return 0;  // gesummv: none
@@ -199,7 +199,7 @@ pb_status peer_rs(pb_peer* P, const float* partial, float* dst, int total, int a
   PeerPush push;
   Blk me;
   for (int g = 0; g < P->nranks; ++g) {
-    const Blk k = block(total, P->nranks, g, false, align);
+    const Blk k = block(total, P->nranks, g, 0, align);
     if (g == P->rank) me = k;
     slot = std::max<long long>(slot, k.n());
   }
@@ -208,7 +208,7 @@ pb_status peer_rs(pb_peer* P, const float* partial, float* dst, int total, int a
     return fail(PB_ERR_WORKSPACE, "peer data region (%zu bytes) < %lld slots of %lld floats", P->data_bytes,
                 (long long)P->nranks, slot);
   for (int g = 0; g < P->nranks; ++g) {
-    const Blk k = block(total, P->nranks, g, false, align);
+    const Blk k = block(total, P->nranks, g, 0, align);
     push.src[g] = partial + k.b;
     push.dst_off[g] = (long long)P->rank * slot;
     push.count[g] = k.n();
@@ -228,7 +228,7 @@ pb_status peer_ag(pb_peer* P, const float* send_blk, float* recv, int rows, int 
   PB_TRY(peer_ready(P));
   if ((size_t)rows * cols * sizeof(float) > P->data_bytes)
     return fail(PB_ERR_WORKSPACE, "peer data region (%zu bytes) < %d x %d floats", P->data_bytes, rows, cols);
-  const Blk me = block(rows, P->nranks, P->rank, false, align);
+  const Blk me = block(rows, P->nranks, P->rank, 0, align);
   PeerPush push;
   for (int g = 0; g < P->nranks; ++g) {
     push.src[g] = send_blk;
@@ -252,16 +252,16 @@ pb_status reduce_scatter(pb_comm* c, const float* partial, float* dst, int total
   if (c->peer) return peer_rs(c->peer, partial, dst, total, ALIGN_MV, s);
   const Nccl& N = nccl();
   bool equal = true;
-  const Blk me = block(total, c->nranks, c->rank, false, ALIGN_MV);
+  const Blk me = block(total, c->nranks, c->rank, 0, ALIGN_MV);
   for (int g = 0; g < c->nranks; ++g)
-    if (block(total, c->nranks, g, false, ALIGN_MV).n() != me.n()) equal = false;
+    if (block(total, c->nranks, g, 0, ALIGN_MV).n() != me.n()) equal = false;
   if (equal && (long long)me.n() * c->nranks == total) {
     PB_NC(N.ReduceScatter(partial, dst, (size_t)me.n(), ncclFloat32, ncclSum, c->nc, s));
     return PB_OK;
   }
   PB_NC(N.GroupStart());  // uneven blocks: one reduce per root
   for (int g = 0; g < c->nranks; ++g) {
-    const Blk k = block(total, c->nranks, g, false, ALIGN_MV);
+    const Blk k = block(total, c->nranks, g, 0, ALIGN_MV);
     if (!k.n()) continue;
     float* recv = g == c->rank ? dst : const_cast<float*>(partial + k.b);  // only the root's is written
     const ncclResult_t r = N.Reduce(partial + k.b, recv, (size_t)k.n(), ncclFloat32, ncclSum, g, c->nc, s);
@@ -277,14 +277,14 @@ pb_status reduce_scatter(pb_comm* c, const float* partial, float* dst, int total
 // Every rank's rows of F (rows x cols, partition tri 0 / align 128) -> the full F, in place.
 pb_status all_gather_rows(pb_comm* c, float* F, int rows, int cols, cudaStream_t s) {
   if (c->peer) {
-    const Blk me = block(rows, c->nranks, c->rank, false, ALIGN_MM);
+    const Blk me = block(rows, c->nranks, c->rank, 0, ALIGN_MM);
     return peer_ag(c->peer, F + (size_t)me.b * cols, F, rows, cols, ALIGN_MM, s);
   }
   const Nccl& N = nccl();
   bool equal = true;
-  const Blk me = block(rows, c->nranks, c->rank, false, ALIGN_MM);
+  const Blk me = block(rows, c->nranks, c->rank, 0, ALIGN_MM);
   for (int g = 0; g < c->nranks; ++g)
-    if (block(rows, c->nranks, g, false, ALIGN_MM).n() != me.n()) equal = false;
+    if (block(rows, c->nranks, g, 0, ALIGN_MM).n() != me.n()) equal = false;
   if (equal && (long long)me.n() * c->nranks == rows) {  // in place: send = recv + rank * count
     const size_t cnt = (size_t)me.n() * cols;
     PB_NC(N.AllGather(F + (size_t)me.b * cols, F, cnt, ncclFloat32, c->nc, s));
@@ -292,7 +292,7 @@ pb_status all_gather_rows(pb_comm* c, float* F, int rows, int cols, cudaStream_t
   }
   PB_NC(N.GroupStart());  // uneven blocks: one broadcast per owner
   for (int g = 0; g < c->nranks; ++g) {
-    const Blk k = block(rows, c->nranks, g, false, ALIGN_MM);
+    const Blk k = block(rows, c->nranks, g, 0, ALIGN_MM);
     if (!k.n()) continue;
     float* p = F + (size_t)k.b * cols;
     const ncclResult_t r = N.Broadcast(p, p, (size_t)k.n() * cols, ncclFloat32, g, c->nc, s);
@@ -498,7 +498,7 @@ pb_status pb_gemm_dist(pb_comm* c, int ni, int nj, int nk, float alpha, float be
                        const float* B, void* ws, size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
   if (ni <= 0) return fail(PB_ERR_INVALID_ARG, "ni %d", ni);
-  const Blk r = block(ni, c->nranks, c->rank, false, ALIGN_MM);
+  const Blk r = block(ni, c->nranks, c->rank, 0, ALIGN_MM);
   set_launches(0);
   return r.n() ? pb_gemm(r.n(), nj, nk, alpha, beta, C_blk, A_blk, B, ws, ws_bytes, s) : PB_OK;
 }
@@ -508,7 +508,7 @@ pb_status pb_2mm_dist(pb_comm* c, int ni, int nj, int nk, int nl, float alpha, f
                       pb_stream s) {
   PB_TRY(comm_ok(c));
   if (ni <= 0) return fail(PB_ERR_INVALID_ARG, "ni %d", ni);
-  const Blk r = block(ni, c->nranks, c->rank, false, ALIGN_MM);
+  const Blk r = block(ni, c->nranks, c->rank, 0, ALIGN_MM);
   set_launches(0);
   return r.n() ? pb_2mm(r.n(), nj, nk, nl, alpha, beta, tmp_blk, A_blk, B, C, D_blk, ws, ws_bytes, s) : PB_OK;
 }
@@ -517,7 +517,7 @@ pb_status pb_syrk_dist(pb_comm* c, int n, int m, float alpha, float beta, float*
                        size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
   if (n <= 0) return fail(PB_ERR_INVALID_ARG, "n %d", n);
-  const Blk r = block(n, c->nranks, c->rank, true, ALIGN_SY);
+  const Blk r = block(n, c->nranks, c->rank, 2, ALIGN_SY);
   set_launches(0);
   return r.n() ? pb_syrk_rows(n, m, r.b, r.e, alpha, beta, C_blk, A, ws, ws_bytes, s) : PB_OK;
 }
@@ -526,7 +526,7 @@ pb_status pb_syr2k_dist(pb_comm* c, int n, int m, float alpha, float beta, float
                         const float* B, void* ws, size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
   if (n <= 0) return fail(PB_ERR_INVALID_ARG, "n %d", n);
-  const Blk r = block(n, c->nranks, c->rank, true, ALIGN_SY);
+  const Blk r = block(n, c->nranks, c->rank, 2, ALIGN_SY);
   set_launches(0);
   return r.n() ? pb_syr2k_rows(n, m, r.b, r.e, alpha, beta, C_blk, A, B, ws, ws_bytes, s) : PB_OK;
 }
@@ -535,7 +535,7 @@ pb_status pb_gesummv_dist(pb_comm* c, int n, float alpha, float beta, const floa
                           float* tmp_blk, const float* x, float* y_blk, void* ws, size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
   if (n <= 0) return fail(PB_ERR_INVALID_ARG, "n %d", n);
-  const Blk r = block(n, c->nranks, c->rank, false, ALIGN_MV);
+  const Blk r = block(n, c->nranks, c->rank, 0, ALIGN_MV);
   set_launches(0);
   return r.n() ? pb_gesummv_rows(r.n(), n, alpha, beta, A_blk, B_blk, tmp_blk, x, y_blk, ws, ws_bytes, s) : PB_OK;
 }
@@ -545,8 +545,8 @@ pb_status pb_3mm_dist(pb_comm* c, int ni, int nj, int nk, int nl, int nm, float*
                       const float* B, float* F, const float* C_blk, const float* D, float* G_blk, void* ws,
                       size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
-  const Blk r = block(ni > 0 ? ni : 1, c->nranks, c->rank, false, ALIGN_MM);
-  const Blk f = block(nj > 0 ? nj : 1, c->nranks, c->rank, false, ALIGN_MM);
+  const Blk r = block(ni > 0 ? ni : 1, c->nranks, c->rank, 0, ALIGN_MM);
+  const Blk f = block(nj > 0 ? nj : 1, c->nranks, c->rank, 0, ALIGN_MM);
   Check ck;  // everything validated before anything is enqueued
   ck.dims({ni, nj, nk, nl, nm});
   ck.cols4(nj, "B/E"); ck.cols4(nk, "A"); ck.cols4(nl, "D/F/G"); ck.cols4(nm, "C");
@@ -585,8 +585,8 @@ pb_status pb_3mm_dist(pb_comm* c, int ni, int nj, int nk, int nl, int nm, float*
 pb_status pb_atax_dist(pb_comm* c, int m, int n, const float* A_blk, const float* x, float* y_blk, float* tmp_blk,
                        void* ws, size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
-  const Blk r = block(m > 0 ? m : 1, c->nranks, c->rank, false, ALIGN_MV);
-  const Blk o = block(n > 0 ? n : 1, c->nranks, c->rank, false, ALIGN_MV);
+  const Blk r = block(m > 0 ? m : 1, c->nranks, c->rank, 0, ALIGN_MV);
+  const Blk o = block(n > 0 ? n : 1, c->nranks, c->rank, 0, ALIGN_MV);
   Check ck;
   ck.dims({m, n});
   ck.cols4(n, "A");
@@ -611,8 +611,8 @@ pb_status pb_atax_dist(pb_comm* c, int m, int n, const float* A_blk, const float
 pb_status pb_bicg_dist(pb_comm* c, int m, int n, const float* A_blk, float* s_blk, float* q_blk, const float* p,
                        const float* r_blk, void* ws, size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
-  const Blk r = block(n > 0 ? n : 1, c->nranks, c->rank, false, ALIGN_MV);
-  const Blk o = block(m > 0 ? m : 1, c->nranks, c->rank, false, ALIGN_MV);
+  const Blk r = block(n > 0 ? n : 1, c->nranks, c->rank, 0, ALIGN_MV);
+  const Blk o = block(m > 0 ? m : 1, c->nranks, c->rank, 0, ALIGN_MV);
   Check ck;
   ck.dims({m, n});
   ck.cols4(m, "A");
@@ -638,7 +638,7 @@ pb_status pb_bicg_dist(pb_comm* c, int m, int n, const float* A_blk, float* s_bl
 pb_status pb_mvt_dist(pb_comm* c, int n, float* x1_blk, float* x2_blk, const float* y_1, const float* y_2_blk,
                       const float* A_blk, void* ws, size_t ws_bytes, pb_stream s) {
   PB_TRY(comm_ok(c));
-  const Blk r = block(n > 0 ? n : 1, c->nranks, c->rank, false, ALIGN_MV);
+  const Blk r = block(n > 0 ? n : 1, c->nranks, c->rank, 0, ALIGN_MV);
   Check ck;
   ck.dims({n});
   ck.cols4(n, "A");

@@ -229,7 +229,7 @@ def syrk_rows(ctx, n, m, alpha, beta, C_blk, A, ws, B=None, K=_pb):
         else:
             K.pb_syr2k_dist(_COMM, n, m, alpha, beta, C_blk, A, B, ws=ws)
         return K.last_launch_count()
-    r0, r1 = partition(n, world, rank, True, 256, K)
+    r0, r1 = partition(n, world, rank, 2, 256, K)
     if r1 <= r0:
         return 0
     if B is None:

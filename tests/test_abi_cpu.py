@@ -113,9 +113,31 @@ def test_dist_workspace_sizes_cpu():
     # the GEMM family needs at least its local shard's workspace
     assert pb.workspace_size("gemm_dist", (4096, 4096, 4096, 2, 1)) >= pb.workspace_size("gemm", (2048, 4096, 4096))
     assert pb.workspace_size("3mm_dist", (4096,) * 5 + (4, 3)) >= pb.workspace_size("gemm", (1024, 4096, 4096))
-    r0, r1 = pb.pb_row_partition(8192, 4, 3, True, 256)
+    r0, r1 = pb.pb_row_partition(8192, 4, 3, 2, 256)
     assert pb.workspace_size("syr2k_dist", (8192, 8192, 4, 3)) == pb.workspace_size("syr2k_rows", (8192, 8192, r0, r1))
     for bad in [("atax_dist", (n, n, 2, 2)), ("atax_dist", (n, n, 0, 0)), ("atax_dist", (n, n)),
                 ("nope_dist", (1, 1, 1)), ("gemm_dist", (0, 4, 4, 1, 0))]:
         with pytest.raises(pb.PBError):
             pb.workspace_size(*bad)
+
+
+def test_row_partition_syrk_cost_balance():
+    """triangular = 2 (syrk/syr2k): blocks tile [0, n) in order, aligned, and the
+    max per-rank cost (triangle area + 267 * end, the split of A[0:end]) is lower
+    than with the pure area balance (triangular = 1)."""
+    import paper_2312_13170_b200 as pb
+
+    def cost(b, e):
+        return (e * e - b * b) / 2 + 267.0 * e
+    for n in (8192, 4096):
+        for G in (2, 4, 8):
+            worst = {}
+            for mode in (1, 2):
+                bounds = [pb.pb_row_partition(n, G, g, mode, 256) for g in range(G)]
+                assert bounds[0][0] == 0 and bounds[-1][1] == n
+                assert all(bounds[g][1] == bounds[g + 1][0] for g in range(G - 1))
+                assert all(b % 256 == 0 for b, _ in bounds)
+                worst[mode] = max(cost(b, e) for b, e in bounds)
+            assert worst[2] <= 1.02 * worst[1]  # block snapping to 256 rows limits small G
+    b = [pb.pb_row_partition(8192, 8, g, 2, 256) for g in range(8)]
+    assert max(cost(*x) for x in b) < 0.93 * max(cost(*pb.pb_row_partition(8192, 8, g, 1, 256)) for g in range(8))

@@ -115,7 +115,7 @@ def _worker(rank, world, port, q):
         res["2mm_D"] = (r0, r1, _np(D2))
         # ---- syrk / syr2k triangular bands
         n2, m2 = 384, 40
-        s0, s1 = D.partition(n2, world, rank, True, 256, K)
+        s0, s1 = D.partition(n2, world, rank, 2, 256, K)
         A2, B2 = H(n2, m2, 1), H(n2, m2, 2)
         Cfull = H(n2, n2, 3, mode=pbgen.SYM)
         Cb = Cfull[s0:s1].clone()

@@ -72,7 +72,7 @@ def _worker(rank, world, port, q, backend="gloo"):
         res["2mm"] = (r0, r1, D2.cpu().numpy())
         # syrk / syr2k triangular bands
         n2, m2 = 768, 260
-        s0, s1 = D.partition(n2, world, rank, True, 256)
+        s0, s1 = D.partition(n2, world, rank, 2, 256)
         A2, B2 = H(n2, m2, 1), H(n2, m2, 2)
         Cf = H(n2, n2, 3, mode=pbgen.SYM)
         Cb, Cb2 = Cf[s0:s1].clone(), Cf[s0:s1].clone()
