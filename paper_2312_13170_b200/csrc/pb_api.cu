@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -159,6 +160,34 @@ pb_status cuda_check(cudaError_t e, const char* what) {
 
 inline cudaStream_t S(pb_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Side stream (per thread and device) for the memory-bound splits of operands that
+// the NEXT GEMM of a chain needs: they run concurrently with the current,
+// tensor-bound GEMM (a split CTA fits beside a GEMM CTA: 40 + 168 registers per
+// thread, 16.6 + 193 KB smem). fork/join are events, so graph capture follows.
+// PB_SIDE_SPLITS=0 keeps everything on the caller's stream.
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+Side* side_stream() {
+  static const bool off = getenv("PB_SIDE_SPLITS") && atoi(getenv("PB_SIDE_SPLITS")) == 0;
+  if (off) return nullptr;
+  thread_local std::map<int, Side> sides;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  Side& x = sides[dev];
+  if (!x.s) {
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x = Side();
+      return nullptr;
+    }
+  }
+  return &x;
+}
+
 // Below this many multiply-adds pb_gemm runs the single-launch SIMT kernel.
 constexpr long long SMALL_GEMM_MACS = 1ll << 21;
 
@@ -274,9 +303,17 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
   Ws2mm w = ws_2mm(c, ni, nj, nk, nl);
   cudaStream_t st = S(s);
   int L = 0;
+  Side* sd = side_stream();
   PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
   PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
-  PB_CUDA(launch_split_T(C, nj, nl, nl, w.ct.hi, w.ct.lo, w.ct.ld, nullptr, nullptr, st));
+  if (sd) {  // C^T's split (GEMM 2's B operand) starts with GEMM 1 and runs beside it
+    PB_CUDA(cudaEventRecord(sd->fork, st));
+    PB_CUDA(cudaStreamWaitEvent(sd->s, sd->fork, 0));
+    PB_CUDA(launch_split_T(C, nj, nl, nl, w.ct.hi, w.ct.lo, w.ct.ld, nullptr, nullptr, sd->s));
+    PB_CUDA(cudaEventRecord(sd->join, sd->s));
+  } else {
+    PB_CUDA(launch_split_T(C, nj, nl, nl, w.ct.hi, w.ct.lo, w.ct.ld, nullptr, nullptr, st));
+  }
   L += 3;
   GemmDesc g1;  // tmp = alpha * A * B  (epilogue emits tmp's split = GEMM 2's A operand)
   g1.M = ni; g1.N = nj; g1.K = nk;
@@ -287,6 +324,7 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
   g1.split_hi = w.tmp.hi; g1.split_lo = w.tmp.lo; g1.ld_split = w.tmp.ld;
   w.sk.attach(g1);
   PB_CUDA(launch_umma_gemm(g1, st, &L));
+  if (sd) PB_CUDA(cudaStreamWaitEvent(st, sd->join, 0));
   GemmDesc g2;  // D = tmp * C + beta * D
   g2.M = ni; g2.N = nl; g2.K = nj;
   g2.a[0] = w.tmp.op(); g2.b[0] = w.ct.op();
@@ -315,10 +353,18 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   Ws3mm w = ws_3mm(c, ni, nj, nk, nl, nm);
   cudaStream_t st = S(s);
   int L = 0;
+  Side* sd = side_stream();
+  cudaStream_t sab = st;
   PB_CUDA(launch_split(C, nj, nm, nm, w.c.hi, w.c.lo, w.c.ld, st));
   PB_CUDA(launch_split_T(D, nm, nl, nl, w.dt.hi, w.dt.lo, w.dt.ld, nullptr, nullptr, st));
-  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
-  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
+  if (sd) {  // E's operands (A, B^T) are split beside GEMM F (fork: F's operands are ready)
+    PB_CUDA(cudaEventRecord(sd->fork, st));
+    PB_CUDA(cudaStreamWaitEvent(sd->s, sd->fork, 0));
+    sab = sd->s;
+  }
+  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, sab));
+  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, sab));
+  if (sd) PB_CUDA(cudaEventRecord(sd->join, sd->s));
   L += 4;
   GemmDesc gf;  // F = C * D; epilogue also emits F^T split (G's K-major B operand)
   gf.M = nj; gf.N = nl; gf.K = nm;
@@ -328,6 +374,7 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   gf.split_hi = w.ft.hi; gf.split_lo = w.ft.lo; gf.ld_split = w.ft.ld;
   w.sk.attach(gf);
   PB_CUDA(launch_umma_gemm(gf, st, &L));
+  if (sd) PB_CUDA(cudaStreamWaitEvent(st, sd->join, 0));
   GemmDesc ge;  // E = A * B; epilogue also emits E split (G's A operand)
   ge.M = ni; ge.N = nj; ge.K = nk;
   ge.a[0] = w.a.op(); ge.b[0] = w.bt.op();

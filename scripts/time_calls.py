@@ -19,7 +19,9 @@ import pbgen  # noqa: E402
 
 def main():
     k = sys.argv[1]
-    n = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+    shape = sys.argv[2] if len(sys.argv) > 2 else "2048"
+    dims = [int(v) for v in shape.split("x")]  # gemm/2mm also take MxNxK (2mm: rows x n)
+    n = dims[0] if len(dims) == 1 else dims[-1]
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
     dev = torch.device("cuda", 0)
 
@@ -35,15 +37,17 @@ def main():
             (lambda: pb.pb_correlation(n, n, float(n), 0.1, data, out, None, None, ws=ws))
         flops = n * n * (n + 1)
     elif k == "gemm":
-        A, B, C = g(n, n, 1), g(n, n, 2), g(n, n, 3)
-        ws = pb.workspace("gemm", (n, n, n), dev)
-        f = lambda: pb.pb_gemm(n, n, n, 1.5, 1.2, C, A, B, ws=ws)  # noqa: E731
-        flops = 2 * n ** 3
+        M, N, K = dims if len(dims) == 3 else (n, n, n)
+        A, B, C = g(M, K, 1), g(K, N, 2), g(M, N, 3)
+        ws = pb.workspace("gemm", (M, N, K), dev)
+        f = lambda: pb.pb_gemm(M, N, K, 1.5, 1.2, C, A, B, ws=ws)  # noqa: E731
+        flops = 2 * M * N * K
     elif k == "2mm":
-        A, B, C, Dm, tmp = g(n, n, 1), g(n, n, 2), g(n, n, 3), g(n, n, 4), torch.empty(n, n, device=dev)
-        ws = pb.workspace("2mm", (n,) * 4, dev)
-        f = lambda: pb.pb_2mm(n, n, n, n, 1.5, 1.2, tmp, A, B, C, Dm, ws=ws)  # noqa: E731
-        flops = 4 * n ** 3
+        r = dims[0] if len(dims) == 2 else n  # 2mm on a row block: rows x n
+        A, B, C, Dm, tmp = g(r, n, 1), g(n, n, 2), g(n, n, 3), g(r, n, 4), torch.empty(r, n, device=dev)
+        ws = pb.workspace("2mm", (r, n, n, n), dev)
+        f = lambda: pb.pb_2mm(r, n, n, n, 1.5, 1.2, tmp, A, B, C, Dm, ws=ws)  # noqa: E731
+        flops = 4 * r * n * n
     elif k == "syrk":
         A, C = g(n, n, 1), g(n, n, 3)
         ws = pb.workspace("syrk", (n, n), dev)
