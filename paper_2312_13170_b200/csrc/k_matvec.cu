@@ -463,11 +463,16 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
   static const long long onepass_min = (getenv("PB_ATAX_ONEPASS_MIN_MB") ? atoll(getenv("PB_ATAX_ONEPASS_MIN_MB"))
                                                                           : 96ll) << 20;
   if (n >= 16384 && n <= 2 * AX_SLICE && m >= 2 * 74 && (long long)m * n * 4 >= onepass_min) {
-    static int ncl = 0;
+    static std::atomic<int> ncl_dev[64];  // clusters that fit, per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int ncl = ncl_dev[dev & 63].load(std::memory_order_relaxed);
     const size_t smem = (size_t)AX_STAGES * AX_SLICE * 4 + sizeof(AxCtl);
-    if (!ncl) {
-      cudaError_t e = cudaFuncSetAttribute(atax_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+      const cudaError_t e = ensure_smem<atax_onepass_kernel>(smem);
       if (e != cudaSuccess) return e;
+    }
+    if (!ncl) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(148);
       cfg.blockDim = dim3(AX_THREADS);
@@ -483,17 +488,16 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
         nc = 74;
       }
       ncl = nc < 74 ? nc : 74;
+      ncl_dev[dev & 63].store(ncl, std::memory_order_relaxed);
     }
     const int w0 = ((n / 4 + 1) / 2) * 4;
     float* ypart = static_cast<float*>(ws);
     static const int variant = getenv("PB_ATAX_VARIANT") ? atoi(getenv("PB_ATAX_VARIANT")) : 2;
     if (variant == 2) {
       const size_t smem2 = (size_t)(1 + AR_STAGES) * AX_SLICE * 4 + sizeof(ArCtl);
-      static bool set2 = false;
-      if (!set2) {
-        cudaError_t e = cudaFuncSetAttribute(atax_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+      {
+        const cudaError_t e = ensure_smem<atax_reg_kernel>(smem2);
         if (e != cudaSuccess) return e;
-        set2 = true;
       }
       atax_reg_kernel<<<2 * ncl, AX_THREADS, smem2, s>>>(A, x, m, n, w0, tmp, ypart);
     } else {

@@ -581,13 +581,15 @@ bool make_map(CUtensorMap* m, const float* base, int rows, int K, int ld, int bo
   return r == CUDA_SUCCESS;
 }
 
-int num_sms() {
-  static int n = 0;
+int num_sms() {  // per device (cached)
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int n = cache[dev & 63].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev & 63].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -632,11 +634,9 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
       return cudaErrorInvalidValue;
   }
   const size_t smem = C::STAGES * C::STAGE_BYTES + 1024 + sizeof(Ctl) + 64;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(umma3x_kernel<CG, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    const cudaError_t e = ensure_smem<umma3x_kernel<CG, BN>>(smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const long long max_units = num_sms() / CG;
   const long long work = p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles);

@@ -6,6 +6,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace pb {
 
 // ---- 3xTF32 tcgen05 GEMM (k_umma.cu) ---------------------------------------
@@ -151,6 +153,21 @@ cudaError_t launch_gemm_small(int ni, int nj, int nk, float alpha, float beta, f
                               const float* B, cudaStream_t s);
 cudaError_t launch_gemm_listing9_reg(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,
                                      const float* B, cudaStream_t s);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device (the
+// attribute is per device; a process may drive several GPUs from several threads).
+template <auto Kernel>
+cudaError_t ensure_smem(size_t bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled
 // while its predecessor drains; every kernel launched this way calls pdl_wait()
