@@ -300,3 +300,45 @@ def test_row_sharded_pieces_match_full():
     s, q = torch.empty(cols, device="cuda"), torch.empty(rows, device="cuda")
     pb.pb_bicg(cols, rows, A, s, q, v, w)
     assert np.array_equal(P.host(rd), P.host(q)) and np.array_equal(P.host(cp), P.host(s))
+
+
+# ------------------------------------------------------------------ degenerate cases
+def test_covariance_minimum_observations():
+    """n = 2 observations (the minimum for float_n - 1), m = 4 variables."""
+    _ok(P.check_covariance(4, 2, structured=False))
+    _ok(P.check_correlation(4, 2, structured=False))
+
+
+def test_correlation_single_observation_and_covariance_rejects_it():
+    """n = 1: every stddev is 0 <= eps -> 1, so corr is the identity; covariance
+    needs n >= 2 and must fail without touching its outputs."""
+    data = P.dev(P.H(1, 8, 5))
+    corr = torch.full((8, 8), 7.0, device="cuda")
+    pb.pb_correlation(8, 1, 1.0, 0.1, data, corr, None, None)
+    assert np.array_equal(P.host(corr), np.eye(8, dtype=np.float32))
+    cov = torch.full((8, 8), 7.0, device="cuda")
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_covariance(8, 1, 1.0, data, cov, None)
+    assert e.value.status == 1 and bool((cov == 7.0).all())
+
+
+@pytest.mark.parametrize("n", [3, 300, 2048, 2100])
+def test_constant_data(n):
+    """Every column constant (dyadic): covariance exactly 0, correlation exactly I
+    (eps rule), means exact — on the banded (n <= 2048) and exact-mean paths."""
+    m = 132
+    h = np.tile((np.arange(m, dtype=np.float32) % 7) * 0.25, (n, 1))
+    data = P.dev(h)
+    cov, corr = torch.empty(m, m, device="cuda"), torch.empty(m, m, device="cuda")
+    mean = torch.empty(m, device="cuda")
+    pb.pb_covariance(m, n, float(n), data, cov, mean)
+    pb.pb_correlation(m, n, float(n), 0.1, data, corr, None, None)
+    assert np.array_equal(P.host(cov), np.zeros((m, m), np.float32))
+    assert np.array_equal(P.host(corr), np.eye(m, dtype=np.float32))
+    assert np.array_equal(P.host(mean), h[0])
+
+
+def test_gemm_single_row_long_k_tensor_path():
+    """M = 1 (one ragged row in a 128-row tile), N = 8, K = 262144: the tensor-core
+    path (above the small-problem threshold) with split-K over a very long K."""
+    _ok(P.check_gemm(1, 8, 262144))
