@@ -947,15 +947,12 @@ cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
 //   cfg 2: 2-CTA 256x128;  cfg 1: 1-CTA 128x128 (under 256 rows / odd band start)
 // ksplit in 1..4 maximises wave efficiency x (1 - 3% per extra split), keeping
 // >= 8 k-blocks per split.
-UmmaPlan umma_plan(const GemmDesc& d) {
-  static const int force = getenv("PB_UMMA_TILE") ? atoi(getenv("PB_UMMA_TILE")) : 0;
-  static const int force_ks = getenv("PB_UMMA_KSPLIT") ? atoi(getenv("PB_UMMA_KSPLIT")) : 0;
+namespace {
+// Plan for a fixed tile configuration (1: 1-CTA 128x128, 2: 2-CTA 256x128, 3: 2-CTA 256x256).
+UmmaPlan plan_cfg(const GemmDesc& d, int cfg, int force_ks) {
   UmmaPlan pl;
-  const int rows = d.tm1 < 0 ? d.M : (d.tm1 - d.tm0) * 128;
-  const bool pair_ok = rows >= 256 && (d.tm0 % 2) == 0;
-  pl.cfg = pair_ok ? 3 : 1;
-  if (force >= 1 && force <= 3 && (force == 1 || pair_ok)) pl.cfg = force;
-  const int pm = pl.cfg == 1 ? 128 : 256, bn = pl.cfg == 3 ? 256 : 128, cg = pl.cfg == 1 ? 1 : 2;
+  pl.cfg = cfg;
+  const int pm = cfg == 1 ? 128 : 256, bn = cfg == 3 ? 256 : 128, cg = cfg == 1 ? 1 : 2;
   const int tm0 = d.tm0 * 128 / pm;
   const int tiles_m = (d.M + pm - 1) / pm;
   const int tm1 = d.tm1 < 0 ? tiles_m : std::min(tiles_m, (d.tm1 * 128 + pm - 1) / pm);
@@ -978,6 +975,28 @@ UmmaPlan umma_plan(const GemmDesc& d) {
   pl.split_tiles = R;
   pl.part_bytes = R > 0 ? (size_t)R * S * cg * 128 * bn * sizeof(float) : 0;
   pl.counter_bytes = (S > 1 && !(d.flags & EPI_PARTIAL)) ? (size_t)R * cg * sizeof(unsigned) : 0;
+  return pl;
+}
+}  // namespace
+
+UmmaPlan umma_plan(const GemmDesc& d) {
+  static const int force = getenv("PB_UMMA_TILE") ? atoi(getenv("PB_UMMA_TILE")) : 0;
+  static const int force_ks = getenv("PB_UMMA_KSPLIT") ? atoi(getenv("PB_UMMA_KSPLIT")) : 0;
+  const int rows = d.tm1 < 0 ? d.M : (d.tm1 - d.tm0) * 128;
+  const bool pair_ok = rows >= 256 && (d.tm0 % 2) == 0;
+  int cfg = pair_ok ? 3 : 1;
+  if (force >= 1 && force <= 3 && (force == 1 || pair_ok)) return plan_cfg(d, force, force_ks);
+  UmmaPlan pl = plan_cfg(d, cfg, force_ks);
+  // Single-wave shapes (fewer 256x256 tiles than SM pairs) that would need split-K:
+  // 256x128 tiles without (or with less) split-K win when they still fit in one wave —
+  // the split-K exchange and the 256-column epilogue cost more than the lower MMA
+  // efficiency of N = 128 (measured: M x 4096 x 4096 at M = 256: 111 vs 123 us,
+  // M = 512: 140 vs 147 us; gemm 1024^3: 46 vs 64 us). Triangular and Gram (partial)
+  // GEMMs keep 256x256 tiles.
+  if (cfg == 3 && !force_ks && pl.ksplit > 1 && pl.tiles < 74 && !(d.flags & (EPI_TRI | EPI_PARTIAL))) {
+    const UmmaPlan p2 = plan_cfg(d, 2, 0);
+    if (p2.tiles <= 74) pl = p2;
+  }
   return pl;
 }
 
