@@ -342,3 +342,52 @@ def test_gemm_single_row_long_k_tensor_path():
     """M = 1 (one ragged row in a 128-row tile), N = 8, K = 262144: the tensor-core
     path (above the small-problem threshold) with split-K over a very long K."""
     _ok(P.check_gemm(1, 8, 262144))
+
+
+# ------------------------------------------------------------------ P1 on the chains and the matvec family
+def test_2mm_3mm_integer_bitwise_P1():
+    """Values in {0..7}, dyadic alpha/beta, sizes keeping every partial sum < 2^24:
+    the 3xTF32 chain is exact (the intermediate's hi/lo split is exact too), so
+    tmp/D and E/F/G equal the oracle bit for bit."""
+    I8 = pbgen.INT8
+    ni, nj, nk, nl = 300, 32, 64, 260
+    A, B, C, D = P.H(ni, nk, 1, I8), P.H(nk, nj, 2, I8), P.H(nj, nl, 3, I8), P.H(ni, nl, 4, I8)
+    dtmp, dD = torch.empty(ni, nj, device="cuda"), P.dev(D)
+    pb.pb_2mm(ni, nj, nk, nl, 1.5, 0.5, dtmp, P.dev(A), P.dev(B), P.dev(C), dD)
+    t_r, D_r = oracle.mm2(1.5, 0.5, A, B, C, D)
+    assert np.array_equal(P.host(dtmp).astype(np.float64), t_r)
+    assert np.array_equal(P.host(dD).astype(np.float64), D_r)
+    ni, nj, nk, nl, nm = 260, 16, 8, 132, 8
+    A, B, C, D = P.H(ni, nk, 1, I8), P.H(nk, nj, 2, I8), P.H(nj, nm, 3, I8), P.H(nm, nl, 4, I8)
+    dE, dF, dG = (torch.empty(*sh, device="cuda") for sh in ((ni, nj), (nj, nl), (ni, nl)))
+    pb.pb_3mm(ni, nj, nk, nl, nm, dE, P.dev(A), P.dev(B), dF, P.dev(C), P.dev(D), dG)
+    for g, r in zip((dE, dF, dG), oracle.mm3(A, B, C, D)):
+        assert np.array_equal(P.host(g).astype(np.float64), r)
+
+
+def test_matvec_integer_bitwise_P1():
+    """bicg / mvt / gesummv with values in {0..7} at n = 2048 (sums < 2^24, dyadic
+    alpha/beta): exact, so bit-for-bit equal to the oracle despite different
+    reduction orders; mvt with a symmetric A and y_1 = y_2 then also gives
+    x1' - x1 == x2' - x2 exactly (P28 on the GPU)."""
+    I8 = pbgen.INT8
+    n = 2048
+    A = P.H(n, n, 1, I8)
+    p, r = P.H(1, n, 6, I8)[0], P.H(1, n, 7, I8)[0]
+    s, q = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+    pb.pb_bicg(n, n, P.dev(A), s, q, P.dev(p), P.dev(r))
+    s_r, q_r = oracle.bicg(A, p, r)
+    assert np.array_equal(P.host(s).astype(np.float64), s_r) and np.array_equal(P.host(q).astype(np.float64), q_r)
+    B = P.H(n, n, 2, I8)
+    y, t = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+    pb.pb_gesummv(n, 1.5, 0.5, P.dev(A), P.dev(B), t, P.dev(p), y)
+    t_r, y_r = oracle.gesummv(1.5, 0.5, A, B, p)
+    assert np.array_equal(P.host(t).astype(np.float64), t_r) and np.array_equal(P.host(y).astype(np.float64), y_r)
+    As = P.H(n, n, 1, I8 | pbgen.SYM)
+    x1, x2 = P.H(1, n, 8, I8)[0], P.H(1, n, 9, I8)[0]
+    d1, d2 = P.dev(x1), P.dev(x2)
+    pb.pb_mvt(n, d1, d2, P.dev(p), P.dev(p), P.dev(As))
+    o1, o2 = oracle.mvt(x1, x2, p, p, As)
+    g1, g2 = P.host(d1).astype(np.float64), P.host(d2).astype(np.float64)
+    assert np.array_equal(g1, o1) and np.array_equal(g2, o2)
+    assert np.array_equal(g1 - x1, g2 - x2)
