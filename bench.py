@@ -188,11 +188,12 @@ class Suite:
     def ws_dims(self):
         out = [("gemm", (GEMM_N,) * 3), ("covariance", (STAT_N, STAT_N)), ("2mm", (MM_N,) * 4),
                ("3mm", (MM_N,) * 5), ("gemm", (MM_N,) * 3), ("syr2k_rows", (SY_N, SY_N, 0, SY_N)),
-               ("matvec_partial", (MV_N, MV_N)), ("atax", (MV_N, MV_N))]
+               ("matvec_partial", (MV_N, MV_N)), ("atax", (MV_N, MV_N)), ("gesummv", (MV_N,))]
         if self.D.comm() is not None:  # pb_<k>_dist entry points: dims + (nranks, rank)
             G = (self.world, self.rank)
             out += [("2mm_dist", (MM_N,) * 4 + G), ("3mm_dist", (MM_N,) * 5 + G), ("syr2k_dist", (SY_N, SY_N) + G),
-                    ("atax_dist", (MV_N, MV_N) + G), ("bicg_dist", (MV_N, MV_N) + G), ("mvt_dist", (MV_N,) + G)]
+                    ("atax_dist", (MV_N, MV_N) + G), ("bicg_dist", (MV_N, MV_N) + G), ("mvt_dist", (MV_N,) + G),
+                    ("gesummv_dist", (MV_N,) + G)]
         return out
 
     def run(self, k, stream=None):

@@ -166,6 +166,74 @@ __global__ void __launch_bounds__(256, 2) mvmt_kernel(const float* __restrict__ 
   }
 }
 
+// gesummv in the 2-D tile pattern of mvmt_kernel (row dots only), A and B streamed
+// together: CTA (ct, rt) writes pa[ct][r] = A[r][tile] . x[tile] and pb likewise for
+// B; gesummv_reduce_kernel then forms y = alpha*sum_ct pa + beta*sum_ct pb in fixed
+// order. Each matrix is read once; 2 rows of each in flight per warp (<= 128 regs).
+constexpr int RU2 = 2;
+__global__ void __launch_bounds__(256, 2) gesummv_tile_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                              int rows, int cols, const float* __restrict__ x,
+                                                              float* __restrict__ pa, float* __restrict__ pb) {
+  const int ct = blockIdx.x, rt = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = ct * TC;
+  bool cok[G];
+  float4 xv[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int c = c0 + g * 128 + lane * 4;
+    cok[g] = c < cols;
+    xv[g] = cok[g] ? *reinterpret_cast<const float4*>(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int r_begin = rt * TR, r_end = min(r_begin + TR, rows);
+  for (int rb = r_begin + warp * RU2; rb < r_end; rb += 8 * RU2) {
+    float4 a[RU2][G], b[RU2][G];
+#pragma unroll
+    for (int u = 0; u < RU2; ++u) {
+      const int r = rb + u;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int c = c0 + g * 128 + lane * 4;
+        const bool ok = r < r_end && cok[g];
+        a[u][g] = ok ? ldg_stream(reinterpret_cast<const float4*>(A + (long long)r * cols + c))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        b[u][g] = ok ? ldg_stream(reinterpret_cast<const float4*>(B + (long long)r * cols + c))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU2; ++u) {
+      const int r = rb + u;
+      float sa = 0.f, sb = 0.f;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        sa += a[u][g].x * xv[g].x + a[u][g].y * xv[g].y + a[u][g].z * xv[g].z + a[u][g].w * xv[g].w;
+        sb += b[u][g].x * xv[g].x + b[u][g].y * xv[g].y + b[u][g].z * xv[g].z + b[u][g].w * xv[g].w;
+      }
+      sa = warp_sum(sa);
+      sb = warp_sum(sb);
+      if (lane == 0 && r < r_end) {
+        pa[(long long)ct * rows + r] = sa;
+        pb[(long long)ct * rows + r] = sb;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) gesummv_reduce_kernel(const float* __restrict__ pa, const float* __restrict__ pb,
+                                                             int nparts, int rows, float alpha, float beta,
+                                                             float* __restrict__ y, float* __restrict__ tmp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  float sa = 0.f, sb = 0.f;
+  for (int t = 0; t < nparts; ++t) {
+    sa += pa[(long long)t * rows + i];
+    sb += pb[(long long)t * rows + i];
+  }
+  y[i] = alpha * sa + beta * sb;
+  if (tmp) tmp[i] = sa;
+}
+
 // out[i] = (base ? base[i] : 0) + sum_{t < nparts} part[t][i]
 __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restrict__ part, int nparts, int len,
                                                            const float* __restrict__ base, float* __restrict__ out) {
@@ -523,6 +591,22 @@ cudaError_t launch_rowdot(const float* A, const float* B, const float* x, int ro
     constexpr int R = 8;
     rowdot_kernel<R, false><<<(rows + R - 1) / R, 256, 0, s>>>(A, nullptr, x, rows, cols, alpha, beta, y, tmp);
   }
+  return cudaGetLastError();
+}
+
+size_t gesummv_ws_bytes(int rows, int cols) {
+  const size_t nct = (cols + TC - 1) / TC;
+  return 2 * align_up(nct * rows * 4, 256);
+}
+
+cudaError_t launch_gesummv(const float* A, const float* B, const float* x, int rows, int cols, float alpha, float beta,
+                           float* y, float* tmp, void* ws, cudaStream_t s, int* launches) {
+  const int nct = (cols + TC - 1) / TC, nrt = (rows + TR - 1) / TR;
+  float* pa = static_cast<float*>(ws);
+  float* pb = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up((size_t)nct * rows * 4, 256));
+  gesummv_tile_kernel<<<dim3(nct, nrt), 256, 0, s>>>(A, B, rows, cols, x, pa, pb);
+  gesummv_reduce_kernel<<<(rows + 255) / 256, 256, 0, s>>>(pa, pb, nct, rows, alpha, beta, y, tmp);
+  *launches += 2;
   return cudaGetLastError();
 }
 

@@ -250,8 +250,8 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   else if (k == "atax" && need(2)) c.take<char>(atax_ws_bytes(d[0], d[1]));
   else if (k == "bicg" && need(2)) c.take<char>(mvmt_ws_bytes(d[1], d[0]));
   else if (k == "mvt" && need(1)) c.take<char>(mvmt_ws_bytes(d[0], d[0]));
-  else if (k == "gesummv" && need(1)) {}
-  else if (k == "gesummv_rows" && need(2)) {}
+  else if (k == "gesummv" && need(1)) c.take<char>(gesummv_ws_bytes(d[0], d[0]));
+  else if (k == "gesummv_rows" && need(2)) c.take<char>(gesummv_ws_bytes(d[0], d[1]));
   else if (k == "syrk_rows" && need(4)) ws_syrk(c, d[0], d[1], d[2], d[3], false);
   else if (k == "syr2k_rows" && need(4)) ws_syrk(c, d[0], d[1], d[2], d[3], true);
   else if (k == "matvec_partial" && need(2)) c.take<char>(mvmt_ws_bytes(d[0], d[1]));
@@ -601,15 +601,18 @@ pb_status pb_mvt(int n, float* x1, float* x2, const float* y_1, const float* y_2
 
 pb_status pb_gesummv_rows(int rows, int n, float alpha, float beta, const float* A, const float* B, float* tmp,
                           const float* x, float* y, void* ws, size_t ws_bytes, pb_stream s) {
-  (void)ws; (void)ws_bytes;
   Check ck;
   ck.dims({rows, n});
   ck.cols4(n, "A/B");
   ck.arr(A, rows, n, false, "A"); ck.arr(B, rows, n, false, "B"); ck.arr(tmp, 1, rows, true, "tmp", false);
   ck.arr(x, 1, n, false, "x"); ck.arr(y, 1, rows, true, "y");
   PB_TRY(ck.finish());
-  PB_CUDA(launch_rowdot(A, B, x, rows, n, alpha, beta, y, tmp, S(s)));
-  g_launches = 1;
+  Carve need(nullptr, 0);
+  need.take<char>(gesummv_ws_bytes(rows, n));
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  int L = 0;
+  PB_CUDA(launch_gesummv(A, B, x, rows, n, alpha, beta, y, tmp, ws, S(s), &L));
+  g_launches = L;
   return PB_OK;
 }
 

@@ -181,7 +181,11 @@ size_t local_need(const std::string& k, const long long* d, int G, int g) {
     const Blk r = block(d[0], G, g, 0, ALIGN_MV);
     return r.n() ? ws_of("matvec_partial", {r.n(), d[0]}) : 0;
   }
-  return 0;  // gesummv: none
+  if (k == "gesummv") {
+    const Blk r = block(d[0], G, g, 0, ALIGN_MV);
+    return r.n() ? ws_of("gesummv_rows", {r.n(), d[0]}) : 0;
+  }
+  return 0;
 }
 
 // ---- peer-memory versions (k_peer.cu): one push + one consume kernel each

@@ -104,6 +104,11 @@ cudaError_t launch_rowdot(const float* A, const float* B, const float* x, int ro
 //   colpart[rt][j] = sum_{i in row tile rt} A[i][j]*w[i]        (if w)
 // then out_row[i] = base_row[i] + sum_ct rowpart, out_col[j] = base_col[j] + sum_rt colpart.
 size_t mvmt_ws_bytes(int rows, int cols);
+// gesummv: y = alpha*A x + beta*B x (tmp = A x, optional), A and B streamed once in
+// 512 x 256 tiles (per-tile row partials in ws, then a fixed-order reduce).
+size_t gesummv_ws_bytes(int rows, int cols);
+cudaError_t launch_gesummv(const float* A, const float* B, const float* x, int rows, int cols, float alpha, float beta,
+                           float* y, float* tmp, void* ws, cudaStream_t s, int* launches);
 cudaError_t launch_mvmt(const float* A, int rows, int cols, const float* v, const float* w,
                         const float* base_row, float* out_row, const float* base_col, float* out_col,
                         void* ws, cudaStream_t s, int* launches);

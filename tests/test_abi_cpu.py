@@ -108,7 +108,7 @@ def test_dist_workspace_sizes_cpu():
             r0, r1 = pb.pb_row_partition(n, G, g, False, 4)
             need = pb.workspace_size("atax_dist", (n, n, G, g))
             assert need >= n * 4 + pb.workspace_size("atax", (r1 - r0, n))
-            assert pb.workspace_size("gesummv_dist", (n, G, g)) == 0
+            assert pb.workspace_size("gesummv_dist", (n, G, g)) == pb.workspace_size("gesummv_rows", (r1 - r0, n))
             assert pb.workspace_size("mvt_dist", (n, G, g)) >= 2 * n * 4
     # the GEMM family needs at least its local shard's workspace
     assert pb.workspace_size("gemm_dist", (4096, 4096, 4096, 2, 1)) >= pb.workspace_size("gemm", (2048, 4096, 4096))
