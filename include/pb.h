@@ -242,7 +242,9 @@ pb_status pb_comm_size(const pb_comm* comm, int* nranks, int* rank);
  * (acquire every flag, then sum the slots in rank order — deterministic — or
  * copy the gathered region out, then ack each source so that the next
  * collective may overwrite its slot). Every wait is bounded: on timeout the
- * status word (pb_peer_status) becomes non-zero instead of hanging.
+ * status word (pb_peer_status) becomes non-zero instead of hanging. The epoch
+ * that orders the collectives lives in device memory, so the calls can be
+ * captured into a CUDA graph and replayed.
  *   pb_peer_create: allocates the buffer (cudaMalloc, owned by the pb_peer) and
  *     writes this rank's 64-byte IPC handle; at most 8 ranks.
  *   pb_peer_open: handles = nranks x 64 bytes (every rank's handle, in rank

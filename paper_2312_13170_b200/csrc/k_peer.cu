@@ -5,7 +5,8 @@
 // several processes) instead of NCCL's multi-step protocols.
 //
 // Every rank owns one symmetric buffer: a header (flags[src], acks[src], two
-// grid counters, a status word) and a data region. A collective with epoch e:
+// grid counters, a status word, the epoch) and a data region. A collective with
+// epoch e (= the header's epoch + 1, read on the device: graph-replay safe):
 //   push    (peer_push_kernel)    every CTA first waits until each destination
 //                                 acked epoch e-1 (its data region is free), then
 //                                 copies its part of the send data into the
@@ -70,7 +71,15 @@ __device__ bool last_cta(unsigned* counter) {
   return last;
 }
 
-__global__ void __launch_bounds__(256) peer_push_kernel(PeerView v, PeerPush p, unsigned long long epoch) {
+// The epoch lives in this rank's header (device memory), so captured CUDA graphs
+// replay correctly: push and consume both read it at entry; consume's last CTA
+// advances it once every source has been acked.
+__device__ __forceinline__ unsigned long long next_epoch(const PeerView& v) {
+  return *reinterpret_cast<volatile unsigned long long*>(v.epoch) + 1;
+}
+
+__global__ void __launch_bounds__(256) peer_push_kernel(PeerView v, PeerPush p) {
+  const unsigned long long epoch = next_epoch(v);
   wait_all(v.acks_mine, v.nranks, epoch - 1, v.status, 1u);  // destinations consumed epoch - 1
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
   for (int g = 0; g < v.nranks; ++g) {
@@ -83,7 +92,8 @@ __global__ void __launch_bounds__(256) peer_push_kernel(PeerView v, PeerPush p, 
     st_release_sys(v.flags[threadIdx.x] + v.rank, epoch);  // flags[me] in destination g
 }
 
-__global__ void __launch_bounds__(256) peer_consume_kernel(PeerView v, PeerConsume c, unsigned long long epoch) {
+__global__ void __launch_bounds__(256) peer_consume_kernel(PeerView v, PeerConsume c) {
+  const unsigned long long epoch = next_epoch(v);
   wait_all(v.flags_mine, v.nranks, epoch, v.status, 2u);
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
   const float4* base = reinterpret_cast<const float4*>(v.data[v.rank]);
@@ -102,23 +112,26 @@ __global__ void __launch_bounds__(256) peer_consume_kernel(PeerView v, PeerConsu
   } else {  // copy the gathered region out
     for (long long i = tid; i < n4; i += nth) out[i] = __ldcv(base + i);
   }
-  if (last_cta(v.counter + 1) && threadIdx.x < v.nranks)
-    st_release_sys(v.acks[threadIdx.x] + v.rank, epoch);  // acks[me] in source g
+  if (last_cta(v.counter + 1)) {
+    if (threadIdx.x < v.nranks) st_release_sys(v.acks[threadIdx.x] + v.rank, epoch);  // acks[me] in source g
+    __syncthreads();
+    if (threadIdx.x == 0) *v.epoch = epoch;  // the next collective uses epoch + 1
+  }
 }
 
 }  // namespace
 
-cudaError_t launch_peer_push(const PeerView& v, const PeerPush& p, unsigned long long epoch, cudaStream_t s) {
+cudaError_t launch_peer_push(const PeerView& v, const PeerPush& p, cudaStream_t s) {
   long long mx = 0;
   for (int g = 0; g < v.nranks; ++g) mx = p.count[g] > mx ? p.count[g] : mx;
   const int grid = (int)std::min<long long>(64, std::max<long long>(1, (mx / 4 + 255) / 256));
-  peer_push_kernel<<<grid, 256, 0, s>>>(v, p, epoch);
+  peer_push_kernel<<<grid, 256, 0, s>>>(v, p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_peer_consume(const PeerView& v, const PeerConsume& c, unsigned long long epoch, cudaStream_t s) {
+cudaError_t launch_peer_consume(const PeerView& v, const PeerConsume& c, cudaStream_t s) {
   const int grid = (int)std::min<long long>(64, std::max<long long>(1, (c.count / 4 + 255) / 256));
-  peer_consume_kernel<<<grid, 256, 0, s>>>(v, c, epoch);
+  peer_consume_kernel<<<grid, 256, 0, s>>>(v, c);
   return cudaGetLastError();
 }
 

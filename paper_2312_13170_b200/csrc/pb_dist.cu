@@ -29,7 +29,6 @@ struct pb_peer {
   size_t data_bytes = 0;
   char* mapped[PEER_MAXR] = {};  // every rank's base in this process (own = base)
   bool opened = false;
-  unsigned long long epoch = 0;  // collectives issued so far (identical on every rank)
   PeerView view;
 };
 
@@ -222,9 +221,8 @@ pb_status peer_rs(pb_peer* P, const float* partial, float* dst, int total, int a
   con.count = me.n();
   con.slot = slot;
   con.reduce = 1;
-  const unsigned long long e = ++P->epoch;
-  PB_CU(launch_peer_push(P->view, push, e, s));
-  PB_CU(launch_peer_consume(P->view, con, e, s));
+  PB_CU(launch_peer_push(P->view, push, s));
+  PB_CU(launch_peer_consume(P->view, con, s));
   return PB_OK;
 }
 
@@ -244,9 +242,8 @@ pb_status peer_ag(pb_peer* P, const float* send_blk, float* recv, int rows, int 
   con.count = (long long)rows * cols;
   con.slot = 0;
   con.reduce = 0;
-  const unsigned long long e = ++P->epoch;
-  PB_CU(launch_peer_push(P->view, push, e, s));
-  PB_CU(launch_peer_consume(P->view, con, e, s));
+  PB_CU(launch_peer_push(P->view, push, s));
+  PB_CU(launch_peer_consume(P->view, con, s));
   return PB_OK;
 }
 
@@ -457,7 +454,7 @@ pb_status pb_peer_open(pb_peer* p, const unsigned char* handles) {
   PeerView& v = p->view;
   v.nranks = p->nranks;
   v.rank = p->rank;
-  for (int g = 0; g < p->nranks; ++g) {  // header: flags @0, acks @512, counters @1024, status @1536
+  for (int g = 0; g < p->nranks; ++g) {  // header: flags @0, acks @512, counters @1024, status @1536, epoch @1600
     v.data[g] = reinterpret_cast<float*>(p->mapped[g] + PEER_HDR);
     v.flags[g] = reinterpret_cast<unsigned long long*>(p->mapped[g]);
     v.acks[g] = reinterpret_cast<unsigned long long*>(p->mapped[g] + 512);
@@ -466,6 +463,7 @@ pb_status pb_peer_open(pb_peer* p, const unsigned char* handles) {
   v.acks_mine = v.acks[p->rank];
   v.counter = reinterpret_cast<unsigned*>(p->base + 1024);
   v.status = reinterpret_cast<unsigned*>(p->base + 1536);
+  v.epoch = reinterpret_cast<unsigned long long*>(p->base + 1600);
   p->opened = true;
   return PB_OK;
 }

@@ -131,6 +131,7 @@ struct PeerView {
   unsigned long long* acks_mine;         // == acks[rank]
   unsigned* counter;                     // this rank's grid counters [push, consume]
   unsigned* status;                      // != 0: a bounded wait timed out
+  unsigned long long* epoch;             // collectives completed (this rank's header)
   int nranks = 0, rank = 0;
 };
 struct PeerPush {  // for every destination g: count floats from src[g] to data[g] + dst_off[g]
@@ -143,8 +144,8 @@ struct PeerConsume {  // reduce: out[i] = sum_g data_mine[g * slot + i]; else ou
   long long count, slot;
   int reduce;
 };
-cudaError_t launch_peer_push(const PeerView& v, const PeerPush& p, unsigned long long epoch, cudaStream_t s);
-cudaError_t launch_peer_consume(const PeerView& v, const PeerConsume& c, unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_peer_push(const PeerView& v, const PeerPush& p, cudaStream_t s);
+cudaError_t launch_peer_consume(const PeerView& v, const PeerConsume& c, cudaStream_t s);
 
 // ---- SIMT ablation kernels (k_simt.cu): PAPER.md Listing 8 / Listing 9 -------
 cudaError_t launch_gemm_listing8(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A,

@@ -286,3 +286,51 @@ def test_bench_two_ranks_share_gpu(transport):
     line = json.loads([ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
     assert (line["config"]["transport"] or "").startswith("peer") == (transport == "local")
+
+
+def test_peer_collectives_graph_replay():
+    """pb_atax_dist / pb_mvt_dist over a (world-size-1, local) peer group captured
+    into one CUDA graph and replayed with new inputs: the collective epoch lives in
+    device memory, so every replay waits for (and sums) the right data."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_13170_b200 as pb
+    dev = torch.device("cuda", 0)
+    comm = pb.pb_comm_init_local(1, 0)
+    peer = pb.pb_peer_create(1, 0, 1 << 20)
+    peer.open(peer.ipc_handle)
+    pb.pb_comm_attach_peer(comm, peer)
+    try:
+        m, n = 1000, 2048
+        A = torch.from_numpy(pbgen.gen_host(m, n, 1)).to(dev)
+        x = torch.empty(n, device=dev)
+        y, tmp = torch.empty(n, device=dev), torch.empty(m, device=dev)
+        ws = pb.workspace("atax_dist", (m, n, 1, 0), dev)
+        An = torch.from_numpy(pbgen.gen_host(n, n, 2)).to(dev)
+        x1, x2 = torch.empty(n, device=dev), torch.empty(n, device=dev)
+        y1 = torch.from_numpy(pbgen.gen_host(1, n, 8)[0]).to(dev)
+        wsm = pb.workspace("mvt_dist", (n, 1, 0), dev)
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        x.copy_(torch.from_numpy(pbgen.gen_host(1, n, 6)[0]))
+        with torch.cuda.graph(g, stream=s):
+            pb.pb_atax_dist(comm, m, n, A, x, y, tmp, ws=ws, stream=s)
+            pb.pb_mvt_dist(comm, n, x1, x2, y1, x, An, ws=wsm, stream=s)
+        for it in range(4):
+            xh = pbgen.gen_host(1, n, 30 + it)[0]
+            x1h, x2h = pbgen.gen_host(1, n, 40 + it)[0], pbgen.gen_host(1, n, 50 + it)[0]
+            x.copy_(torch.from_numpy(xh))
+            x1.copy_(torch.from_numpy(x1h))
+            x2.copy_(torch.from_numpy(x2h))
+            g.replay()
+            torch.cuda.synchronize()
+            y_r = oracle.atax(pbgen.gen_host(m, n, 1), xh)[0]
+            assert np.max(np.abs(y.cpu().numpy() - y_r) / np.abs(y_r)) <= P.TOL, it
+            o1, o2 = oracle.mvt(x1h, x2h, pbgen.gen_host(1, n, 8)[0], xh, pbgen.gen_host(n, n, 2))
+            assert np.max(np.abs(x1.cpu().numpy() - o1) / np.abs(o1)) <= P.TOL, it
+            assert np.max(np.abs(x2.cpu().numpy() - o2) / np.abs(o2)) <= P.TOL, it
+        assert peer.status() == 0
+    finally:
+        torch.cuda.synchronize()
+        comm.close()
+        peer.close()
