@@ -334,3 +334,34 @@ def test_peer_collectives_graph_replay():
         torch.cuda.synchronize()
         comm.close()
         peer.close()
+
+
+def test_comm_and_peer_argument_errors():
+    """Multi-GPU ABI validation: a peer group that does not match the comm, an
+    unopened peer group, and collectives on a comm without any transport are
+    rejected with PB_ERR_INVALID_ARG before anything is enqueued."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_13170_b200 as pb
+    comm = pb.pb_comm_init_local(2, 0)
+    p1 = pb.pb_peer_create(1, 0, 1 << 16)
+    p1.open(p1.ipc_handle)
+    p2 = pb.pb_peer_create(2, 0, 1 << 16)  # not opened
+    try:
+        with pytest.raises(pb.PBError) as e:
+            pb.pb_comm_attach_peer(comm, p1)  # nranks mismatch
+        assert e.value.status == 1
+        with pytest.raises(pb.PBError) as e:
+            pb.pb_comm_attach_peer(comm, p2)  # not opened
+        assert e.value.status == 1
+        y = torch.full((1024,), 5.0, device="cuda")
+        with pytest.raises(pb.PBError) as e:  # local comm, no peer attached: no transport
+            pb.pb_atax_dist(comm, 2048, 2048, torch.ones(1024, 2048, device="cuda"), torch.ones(2048, device="cuda"),
+                            y, None)
+        assert e.value.status == 1 and bool((y == 5.0).all())
+        with pytest.raises(pb.PBError):
+            pb.pb_peer_create(9, 0, 1 << 16)  # more than 8 ranks
+    finally:
+        comm.close()
+        p1.close()
+        p2.close()
