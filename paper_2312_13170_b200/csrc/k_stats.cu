@@ -5,6 +5,10 @@
 // split of the Gram operand. Variance: (sum x^2 - (sum x) mu) / float_n in fp64
 // (reading R17 in DESIGN.md). Deterministic: every sum has a fixed order.
 #include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
 
 #include "pb_band_prep.cuh"
 #include "pb_device.cuh"
@@ -15,6 +19,7 @@ namespace {
 
 __device__ int g_tl_on;                  // PB_TIMELINE (tuning only)
 __device__ unsigned long long g_tl[2];   // band_prep: [entry, exit]
+__device__ unsigned long long g_phase[1024][4];  // band_prep per CTA: entry, loads, stats, stores
 
 // ------------------------------------------------------------------ fused prep
 // Used for long columns (n > 2048; shorter ones take the banded prep below).
@@ -142,12 +147,16 @@ __global__ void __launch_bounds__(BT, 2)
     band_prep_kernel(const float* __restrict__ data, int n, int m, float* __restrict__ hiT, float* __restrict__ loT,
                      int ldo, double* __restrict__ band_mean, double* __restrict__ band_m2) {
   __shared__ BandScratch sc;
+  extern __shared__ __align__(16) float band_tile[];  // BAND_TILE_BYTES (dynamic)
   pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
   const int tl = g_tl_on;
   tl_enter(tl, g_tl, 0);
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  unsigned long long* ph = (tl && cta < 1024) ? g_phase[cta] : nullptr;
+  if (ph && threadIdx.x == 0) ph[0] = gtimer_ns();
   band_prep_block<CORR, CtaSync>(data, n, m, hiT, loT, ldo, band_mean, band_m2, blockIdx.x, blockIdx.y, threadIdx.x,
-                                 sc);
+                                 sc, band_tile, ph);
   tl_exit(tl, g_tl, 0);
 }
 
@@ -163,15 +172,37 @@ void timeline_stats(bool reset, unsigned long long* out2) {
     cudaMemcpyToSymbol(g_tl, init, sizeof init);
   } else {
     cudaMemcpyFromSymbol(out2, g_tl, 2 * sizeof(unsigned long long));
+    // per-CTA phase medians (tuning only)
+    static unsigned long long ph[1024][4];
+    cudaMemcpyFromSymbol(ph, g_phase, sizeof ph);
+    std::vector<double> ld, st, sto, start;
+    for (int i = 0; i < 1024; ++i) {
+      if (!ph[i][0] || !ph[i][3]) continue;
+      start.push_back((ph[i][0] - out2[0]) / 1e3);
+      ld.push_back((ph[i][1] - ph[i][0]) / 1e3);
+      st.push_back((ph[i][2] - ph[i][1]) / 1e3);
+      sto.push_back((ph[i][3] - ph[i][2]) / 1e3);
+    }
+    auto med = [](std::vector<double> v) { if (v.empty()) return 0.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+    auto mx = [](std::vector<double> v) { return v.empty() ? 0.0 : *std::max_element(v.begin(), v.end()); };
+    fprintf(stderr, "[pb prep phases] n=%zu start med %.1f max %.1f | loads %.1f (max %.1f) | stats %.1f | stores %.1f (max %.1f) us\n",
+            ld.size(), med(start), mx(start), med(ld), mx(ld), med(st), med(sto), mx(sto));
+    cudaMemset(nullptr, 0, 0);
   }
 }
 
 cudaError_t launch_band_prep(const float* data, int n, int m, bool corr, float* hiT, float* loT, int ldo,
                              double* band_mean, double* band_m2, cudaStream_t s) {
   dim3 grid((m + BCOLS - 1) / BCOLS, band_count(n));
-  if (corr)
-    return launch_pdl(band_prep_kernel<true>, grid, dim3(BT), 0, s, data, n, m, hiT, loT, ldo, band_mean, band_m2);
-  return launch_pdl(band_prep_kernel<false>, grid, dim3(BT), 0, s, data, n, m, hiT, loT, ldo, band_mean, band_m2);
+  cudaError_t e;
+  if (corr) {
+    if ((e = ensure_smem<band_prep_kernel<true>>(BAND_TILE_BYTES)) != cudaSuccess) return e;
+    return launch_pdl(band_prep_kernel<true>, grid, dim3(BT), BAND_TILE_BYTES, s, data, n, m, hiT, loT, ldo,
+                      band_mean, band_m2);
+  }
+  if ((e = ensure_smem<band_prep_kernel<false>>(BAND_TILE_BYTES)) != cudaSuccess) return e;
+  return launch_pdl(band_prep_kernel<false>, grid, dim3(BT), BAND_TILE_BYTES, s, data, n, m, hiT, loT, ldo, band_mean,
+                    band_m2);
 }
 
 cudaError_t launch_stats_split(const float* data, int n, int m, double float_n, double eps, bool corr, float* hiT,

@@ -26,25 +26,46 @@ struct NamedSync256 {  // barrier 2 over threads 0..255 (the rest of the CTA doe
   __device__ static void run() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
 };
 
+// Padded row stride (floats) of the band tile staged in shared memory: the
+// column-wise reads below then hit distinct banks (2-way at worst).
+constexpr int TS = BCOLS + 1;
+constexpr size_t BAND_TILE_BYTES = (size_t)BAND * TS * sizeof(float);
+
 template <bool CORR, class Sync>
 __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, int n, int m, float* __restrict__ hiT,
                                                 float* __restrict__ loT, int ldo, double* __restrict__ band_mean,
-                                                double* __restrict__ band_m2, int cb, int b, int t, BandScratch& sc) {
+                                                double* __restrict__ band_m2, int cb, int b, int t, BandScratch& sc,
+                                                float* __restrict__ tile, unsigned long long* phase = nullptr) {
   const int c0 = cb * BCOLS;
   const int r_begin = b * BAND, r_end = min(r_begin + BAND, n);
   const double nb = (double)(r_end - r_begin);
+  {  // coalesced loads: a warp reads 2 rows x 256 B per instruction, staged into the padded tile
+    const int cql = t & 15, rs = t >> 4;
+    const int cc = c0 + 4 * cql;
+    float4 v[BAND / 16];
+#pragma unroll
+    for (int i = 0; i < BAND / 16; ++i) {
+      const int r = r_begin + rs + 16 * i;
+      v[i] = (cc < m && r < r_end) ? *reinterpret_cast<const float4*>(data + (long long)r * m + cc)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < BAND / 16; ++i) {
+      float* tp = tile + (rs + 16 * i) * TS + 4 * cql;
+      tp[0] = v[i].x; tp[1] = v[i].y; tp[2] = v[i].z; tp[3] = v[i].w;
+    }
+  }
+  Sync::run();
   const int rq0 = t & 15, cq = t >> 4;  // lanes on row quads: coalesced transposed stores
   const int c = c0 + 4 * cq;
   float x[BB][4][4];
 #pragma unroll
   for (int k = 0; k < BB; ++k) {
-    const int r = r_begin + 4 * (rq0 + 16 * k);
+    const int rr = 4 * (rq0 + 16 * k);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (c < m && r + u < r_end) v = *reinterpret_cast<const float4*>(data + (long long)(r + u) * m + c);
-      x[k][u][0] = v.x; x[k][u][1] = v.y; x[k][u][2] = v.z; x[k][u][3] = v.w;
-    }
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) x[k][u][v] = tile[(rr + u) * TS + 4 * cq + v];
   }
   {
     double sv[4] = {0, 0, 0, 0};
@@ -57,6 +78,7 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
 #pragma unroll
     for (int v = 0; v < 4; ++v) sc.red[rq0][4 * cq + v] = sv[v];
   }
+  if (phase && t == 0) phase[1] = gtimer_ns();  // thread 0's loads arrived
   Sync::run();
   if (t < BCOLS) {
     double S = 0.0;
@@ -93,6 +115,7 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
       band_m2[(long long)b * m + c0 + t] = Q;
     }
   }
+  if (phase && t == 0) phase[2] = gtimer_ns();  // band statistics done
   if (c < m) {
 #pragma unroll
     for (int k = 0; k < BB; ++k) {
@@ -113,6 +136,7 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
     }
   }
   Sync::run();  // scratch reusable by the next block
+  if (phase && t == 0) phase[3] = gtimer_ns();  // stores issued by every thread
 }
 
 }  // namespace pb
