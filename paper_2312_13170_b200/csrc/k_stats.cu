@@ -187,7 +187,6 @@ void timeline_stats(bool reset, unsigned long long* out2) {
     auto mx = [](std::vector<double> v) { return v.empty() ? 0.0 : *std::max_element(v.begin(), v.end()); };
     fprintf(stderr, "[pb prep phases] n=%zu start med %.1f max %.1f | loads %.1f (max %.1f) | stats %.1f | stores %.1f (max %.1f) us\n",
             ld.size(), med(start), mx(start), med(ld), mx(ld), med(st), med(sto), mx(sto));
-    cudaMemset(nullptr, 0, 0);
   }
 }
 
