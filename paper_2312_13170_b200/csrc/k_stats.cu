@@ -168,8 +168,10 @@ void timeline_stats(bool reset, unsigned long long* out2) {
   if (reset) {
     const int on = 1;
     const unsigned long long init[2] = {~0ull, 0ull};
+    static const unsigned long long zeros[1024][4] = {};
     cudaMemcpyToSymbol(g_tl_on, &on, sizeof on);
     cudaMemcpyToSymbol(g_tl, init, sizeof init);
+    cudaMemcpyToSymbol(g_phase, zeros, sizeof zeros);  // CTAs of this call only
   } else {
     cudaMemcpyFromSymbol(out2, g_tl, 2 * sizeof(unsigned long long));
     // per-CTA phase medians (tuning only)
