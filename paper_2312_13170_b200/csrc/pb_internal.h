@@ -113,8 +113,9 @@ cudaError_t launch_mvmt(const float* A, int rows, int cols, const float* v, cons
                         const float* base_row, float* out_row, const float* base_col, float* out_col,
                         void* ws, cudaStream_t s, int* launches);
 
-// atax: single pass (2-CTA cluster, row slice in smem, DSMEM partial-dot exchange)
-// when 1024 <= n <= 32768, else two passes. ws: atax_ws_bytes(m, n).
+// atax: single pass (2-CTA cluster, row halves staged by 1-D bulk copies, DSMEM
+// partial-dot exchange) when 16384 <= n <= 32768 and A >= 96 MB (larger than L2),
+// else two passes (the second from L2). ws: atax_ws_bytes(m, n).
 size_t atax_ws_bytes(int m, int n);
 cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, float* tmp, void* ws,
                         cudaStream_t s, int* launches);
