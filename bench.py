@@ -7,7 +7,8 @@ at its BASELINE.json config size, on synthetic pbgen inputs resident in HBM:
     gemm 128^3 | covariance + correlation 2048x2048 | 2mm + 3mm 4096 |
     syrk + syr2k 8192 | atax / bicg / mvt / gesummv 32768.
 value = algorithmic GFLOP of the step / step time (whole job, all ranks).
-Per-kernel GFLOP/s, GB/s and roofline fractions are in "kernels".
+Per-kernel GFLOP/s, GB/s and roofline fractions are in "kernels" (from the mean over the timed
+steps, as the paper averages; ms_median and ms_min are reported beside it).
 
 N>1 (torchrun): every sharded kernel is split by output row blocks
 (paper_2312_13170_b200.dist); gemm128 and cov/corr (1-GPU configs) run on
@@ -337,13 +338,21 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     total_ms = t0.elapsed_time(t1)
-    per_k = {k: statistics.mean(e[k][0].elapsed_time(e[k][1]) for e in ev) for k in kernels}
+    samples = {k: [e[k][0].elapsed_time(e[k][1]) for e in ev] for k in kernels}
+    per_k = {k: statistics.mean(v) for k, v in samples.items()}  # mean: paper-comparable
+    med_k = {k: statistics.median(v) for k, v in samples.items()}
+    min_k = {k: min(v) for k, v in samples.items()}
     if sharded:
         cdev = dev if dist.get_backend() == "nccl" else "cpu"
         tt = torch.tensor([total_ms] + [per_k[k] for k in kernels], device=cdev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt[0])
         per_k = {k: float(tt[i + 1]) for i, k in enumerate(kernels)}
+        tm = torch.tensor([med_k[k] for k in kernels] + [min_k[k] for k in kernels], device=cdev,
+                          dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        med_k = {k: float(tm[i]) for i, k in enumerate(kernels)}
+        min_k = {k: float(tm[len(kernels) + i]) for i, k in enumerate(kernels)}
         lt = torch.tensor([launches], device=cdev, dtype=torch.int64)
         dist.all_reduce(lt)
         launches = int(lt[0])
@@ -366,7 +375,8 @@ def run_ours(args):
         for k in kernels:
             f, b = W[k]
             t = per_k[k] * 1e-3
-            kern[k] = {"ms": round(per_k[k], 4), "gflops": round(f / t / 1e9, 1), "gbs": round(b / t / 1e9, 1),
+            kern[k] = {"ms": round(per_k[k], 4), "ms_median": round(med_k[k], 4), "ms_min": round(min_k[k], 4),
+                       "gflops": round(f / t / 1e9, 1), "gbs": round(b / t / 1e9, 1),
                        "bound": BOUND[k],
                        "frac": round((b / t / 1e9) / hbm if BOUND[k] == "hbm" else (f / t / 1e12) / useful, 4)}
             if BOUND[k] == "tensor":
