@@ -990,10 +990,11 @@ UmmaPlan umma_plan(const GemmDesc& d) {
   // Single-wave shapes (fewer 256x256 tiles than SM pairs) that would need split-K:
   // 256x128 tiles without (or with less) split-K win when they still fit in one wave —
   // the split-K exchange and the 256-column epilogue cost more than the lower MMA
-  // efficiency of N = 128 (measured: M x 4096 x 4096 at M = 256: 111 vs 123 us,
-  // M = 512: 140 vs 147 us; gemm 1024^3: 46 vs 64 us). Triangular and Gram (partial)
-  // GEMMs keep 256x256 tiles.
-  if (cfg == 3 && !force_ks && pl.ksplit > 1 && pl.tiles < 74 && !(d.flags & (EPI_TRI | EPI_PARTIAL))) {
+  // efficiency of N = 128. Measured: M x 4096 x 4096 at M = 256: 111 vs 123 us,
+  // M = 512: 140 vs 147 us; gemm 1024^3: 46 vs 64 us; syrk 1024: 41 vs 67 us,
+  // 2048: 68 vs 91 us; syr2k 1024: 50 vs 77 us, 2048: 119 vs 132 us. The Gram
+  // (partials + combine) keeps 256x256 tiles (its 256x128 form measured slower).
+  if (cfg == 3 && !force_ks && pl.ksplit > 1 && pl.tiles < 74 && !(d.flags & EPI_PARTIAL)) {
     const UmmaPlan p2 = plan_cfg(d, 2, 0);
     if (p2.tiles <= 74) pl = p2;
   }

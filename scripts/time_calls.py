@@ -53,6 +53,11 @@ def main():
         ws = pb.workspace("syrk", (n, n), dev)
         f = lambda: pb.pb_syrk(n, n, 1.5, 1.2, C, A, ws=ws)  # noqa: E731
         flops = n * (n + 1) * n
+    elif k == "syr2k":
+        A, B, C = g(n, n, 1), g(n, n, 2), g(n, n, 3)
+        ws = pb.workspace("syr2k", (n, n), dev)
+        f = lambda: pb.pb_syr2k(n, n, 1.5, 1.2, C, A, B, ws=ws)  # noqa: E731
+        flops = 2 * n * (n + 1) * n
     elif k == "atax":
         A, x, y = g(n, n, 1), g(1, n, 6).view(-1), torch.empty(n, device=dev)
         ws = pb.workspace("atax", (n, n), dev)
