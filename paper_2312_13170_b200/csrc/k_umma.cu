@@ -998,6 +998,15 @@ UmmaPlan umma_plan(const GemmDesc& d) {
     const UmmaPlan p2 = plan_cfg(d, 2, 0);
     if (p2.tiles <= 74) pl = p2;
   }
+  // Gram (partials + combine) in a single wave: compare wave fill x relative MMA
+  // efficiency (1-CTA 128x128 tiles ~0.72 of 2-CTA 256x256 per SM). Measured: cov
+  // 1024^2: 128x128 with split-K 4 29 us vs 37 us; at 2048^2 256x256 stays (66 us).
+  if (cfg == 3 && !force_ks && (d.flags & EPI_PARTIAL)) {
+    const long long u3 = pl.split_tiles * pl.ksplit + (pl.tiles - pl.split_tiles);
+    const UmmaPlan p1 = plan_cfg(d, 1, 0);
+    const long long u1 = p1.split_tiles * p1.ksplit + (p1.tiles - p1.split_tiles);
+    if (u3 <= 74 && u1 <= 148 && 0.72 * (double)u1 / 148.0 > (double)u3 / 74.0) pl = p1;
+  }
   return pl;
 }
 
