@@ -12,23 +12,35 @@
 namespace pb {
 namespace {
 
+// Threads along the columns (float4 c4 = blockIdx.x * 256 + tid), CTAs step over rows
+// SPLIT_U at a time: SPLIT_U independent float4 loads in flight per thread, no index
+// division, coalesced 4 KiB row segments per CTA.
+constexpr int SPLIT_U = 4;
 __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X, int rows, int cols4, int ldx,
                                                     float* __restrict__ hi, float* __restrict__ lo, int ldo) {
   pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
-  const long long total = (long long)rows * cols4;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long r = e / cols4;
-    const int c = (int)(e - r * cols4) * 4;
-    float4 v = *reinterpret_cast<const float4*>(X + r * ldx + c);
-    float4 h, l;
-    split3x(v.x, h.x, l.x);
-    split3x(v.y, h.y, l.y);
-    split3x(v.z, h.z, l.z);
-    split3x(v.w, h.w, l.w);
-    *reinterpret_cast<float4*>(hi + r * ldo + c) = h;
-    *reinterpret_cast<float4*>(lo + r * ldo + c) = l;
+  const int c4 = blockIdx.x * 256 + threadIdx.x;
+  if (c4 >= cols4) return;
+  const int c = 4 * c4;
+  for (int r0 = blockIdx.y * SPLIT_U; r0 < rows; r0 += gridDim.y * SPLIT_U) {
+    float4 v[SPLIT_U];
+#pragma unroll
+    for (int u = 0; u < SPLIT_U; ++u)
+      v[u] = r0 + u < rows ? *reinterpret_cast<const float4*>(X + (long long)(r0 + u) * ldx + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < SPLIT_U; ++u) {
+      if (r0 + u >= rows) break;
+      float4 h, l;
+      split3x(v[u].x, h.x, l.x);
+      split3x(v[u].y, h.y, l.y);
+      split3x(v[u].z, h.z, l.z);
+      split3x(v[u].w, h.w, l.w);
+      const long long o = (long long)(r0 + u) * ldo + c;
+      *reinterpret_cast<float4*>(hi + o) = h;
+      *reinterpret_cast<float4*>(lo + o) = l;
+    }
   }
 }
 
@@ -93,11 +105,13 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
 cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi, float* lo, int ldo,
                          cudaStream_t s) {
   const int cols4 = cols / 4;  // cols % 4 == 0 validated by the ABI
-  long long total = (long long)rows * cols4;
-  long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-  return launch_pdl(split_kernel, dim3((unsigned)blocks), dim3(256), 0, s, X, rows, cols4, ldx, hi, lo, ldo);
+  const int gx = (cols4 + 255) / 256;
+  const int row_steps = (rows + SPLIT_U - 1) / SPLIT_U;
+  int gy = (148 * 8 + gx - 1) / gx;  // ~8 CTAs per SM in total
+  if (gy > row_steps) gy = row_steps;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  return launch_pdl(split_kernel, dim3((unsigned)gx, (unsigned)gy), dim3(256), 0, s, X, rows, cols4, ldx, hi, lo, ldo);
 }
 
 cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* hiT, float* loT, int ldo,
