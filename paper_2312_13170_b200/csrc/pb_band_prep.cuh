@@ -58,15 +58,9 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
   Sync::run();
   const int rq0 = t & 15, cq = t >> 4;  // lanes on row quads: coalesced transposed stores
   const int c = c0 + 4 * cq;
-  float x[BB][4][4];
-#pragma unroll
-  for (int k = 0; k < BB; ++k) {
-    const int rr = 4 * (rq0 + 16 * k);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) x[k][u][v] = tile[(rr + u) * TS + 4 * cq + v];
-  }
+  // this thread's 4x4 blocks are read from the tile in each pass (no register copy:
+  // keeps the kernel free of spills, correlation's second pass included)
+  auto x = [&](int k, int u, int v) -> float { return tile[(4 * (rq0 + 16 * k) + u) * TS + 4 * cq + v]; };
   {
     double sv[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -74,7 +68,7 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) sv[v] += (double)x[k][u][v];
+        for (int v = 0; v < 4; ++v) sv[v] += (double)x(k, u, v);
 #pragma unroll
     for (int v = 0; v < 4; ++v) sc.red[rq0][4 * cq + v] = sv[v];
   }
@@ -91,7 +85,7 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
   double mu[4];
 #pragma unroll
   for (int v = 0; v < 4; ++v) mu[v] = sc.mu[4 * cq + v];
-  if (CORR) {  // M2_b = sum (x - mu_b)^2, second pass over the registers
+  if (CORR) {  // M2_b = sum (x - mu_b)^2, second pass over the tile
     double qv[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int k = 0; k < BB; ++k) {
@@ -101,7 +95,7 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
 #pragma unroll
         for (int v = 0; v < 4; ++v)
           if (r + u < r_end) {
-            const double d = (double)x[k][u][v] - mu[v];
+            const double d = (double)x(k, u, v) - mu[v];
             qv[v] += d * d;
           }
     }
@@ -126,7 +120,7 @@ __device__ __forceinline__ void band_prep_block(const float* __restrict__ data, 
         float h[4], l[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float val = (r + u < r_end) ? (float)((double)x[k][u][v] - mu[v]) : 0.f;
+          const float val = (r + u < r_end) ? (float)((double)x(k, u, v) - mu[v]) : 0.f;
           split3x(val, h[u], l[u]);
         }
         const long long o = (long long)(c + v) * ldo + r;
