@@ -46,6 +46,10 @@ _SIGS = {
     "pbo_syrk_at": [_I, _I, _D, _D, _F, _F, _F, _I, _F, _F, _F, _I],
     "pbo_rows_mm": [_I, _I, _I, _I, _F, _F, _F, _I],
     "pbo_dmm": [_I, _I, _I, _F, _F, _F, _I],
+    "pbo_conv2d": [_I, _I, _F, _F, _F, _I, _I, _F, _I],
+    "pbo_conv3d": [_I, _I, _I, _F, _F, _F, _I, _I, _F, _I],
+    "pbo_fdtd2d": [_I, _I, _I, _F, _F, _F, _F, _F, _F, _F],
+    "pbo_fdtd2d_f32": [_I, _I, _I, _F, _F, _F, _F, _F, _F, _F],
 }
 
 
@@ -259,3 +263,45 @@ def mm3_rows(A, B, C, D, rows, absmode=False):
     # so do the double x double product here in plain numpy (library primitive, R14).
     G = E @ Fd
     return E, F, G
+
+
+# ---------------------------------------------------------------- stencils
+def _w(w, n):
+    w = np.ascontiguousarray(np.asarray(w, dtype=np.float64).reshape(-1))
+    assert w.size == n
+    return w
+
+
+def conv2d(w, A, B_in, rows=None, absmode=False):
+    """2DConvolution (reading R19): rows [i0, i1) of B (default: all), float64."""
+    A, B_in = _f32(A), _f32(B_in)
+    ni, nj = A.shape
+    i0, i1 = (0, ni) if rows is None else rows
+    w = _w(w, 9)
+    out = np.empty((i1 - i0, nj))
+    lib().pbo_conv2d(ni, nj, _p(w), _p(A), _p(B_in), i0, i1, _p(out), int(absmode))
+    return out
+
+
+def conv3d(w, A, B_in, planes=None, absmode=False):
+    """3DConvolution (reading R20): planes [i0, i1) of B (default: all), float64."""
+    A, B_in = _f32(A), _f32(B_in)
+    ni, nj, nk = A.shape
+    i0, i1 = (0, ni) if planes is None else planes
+    w = _w(w, 27)
+    out = np.empty((i1 - i0, nj, nk))
+    lib().pbo_conv3d(ni, nj, nk, _p(w), _p(A), _p(B_in), i0, i1, _p(out), int(absmode))
+    return out
+
+
+def fdtd2d(tmax, ex, ey, hz, fict, f32=False):
+    """FDTD-2D (reading R21): returns (ex, ey, hz) after tmax steps; float64 state,
+    or (f32=True) the PolyBench statements evaluated in fp32."""
+    ex, ey, hz, fict = _f32(ex), _f32(ey), _f32(hz), _f32(fict)
+    nx, ny = ex.shape
+    assert fict.size >= tmax
+    dt = np.float32 if f32 else np.float64
+    o = [np.empty((nx, ny), dtype=dt) for _ in range(3)]
+    fn = lib().pbo_fdtd2d_f32 if f32 else lib().pbo_fdtd2d
+    fn(tmax, nx, ny, _p(ex), _p(ey), _p(hz), _p(fict), _p(o[0]), _p(o[1]), _p(o[2]))
+    return tuple(o)

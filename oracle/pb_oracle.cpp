@@ -392,4 +392,125 @@ void pbo_dmm(int rows, int inner, int cols, const double* X, const float* Y, dou
   }
 }
 
+// ---- SYCL-Bench polybench stencils (§VIII lists "2D Convolution",
+// "3D Convolution", "FDTD2D"). The paper gives no body for
+// them; readings R19-R21 in DESIGN.md fix the definitions used here.
+
+// conv2d (reading R19): the SYCL-Bench / PolyBench-GPU 2DConvolution is a 3x3
+// weighted stencil (a cross-correlation) over the interior:
+//   B[i][j] = sum_{di=-1..1} sum_{dj=-1..1} w[(di+1)*3 + (dj+1)] * A[i+di][j+dj]
+//   for 1 <= i <= ni-2, 1 <= j <= nj-2;  border entries of B keep B_in.
+// A, B ni x nj. Rows [i0, i1) of the result are written to out ((i1-i0) x nj).
+void pbo_conv2d(int ni, int nj, const double* w, const float* A, const float* B_in, int i0, int i1,
+                double* out, int absmode) {
+#pragma omp parallel for schedule(static)
+  for (int i = i0; i < i1; ++i) {
+    for (int j = 0; j < nj; ++j) {
+      size_t e = (size_t)i * nj + j;
+      double r;
+      if (i == 0 || i == ni - 1 || j == 0 || j == nj - 1) {
+        r = V(B_in[e], absmode);
+      } else {
+        r = 0.0;
+        for (int di = -1; di <= 1; ++di)
+          for (int dj = -1; dj <= 1; ++dj)
+            r += S(w[(di + 1) * 3 + (dj + 1)], absmode) * V(A[(size_t)(i + di) * nj + (j + dj)], absmode);
+      }
+      out[(size_t)(i - i0) * nj + j] = r;
+    }
+  }
+}
+
+// conv3d (reading R20): 3x3x3 weighted stencil over the interior of an
+// ni x nj x nk array (row-major, k fastest):
+//   B[i][j][k] = sum_{di,dj,dk in -1..1} w[(di+1)*9 + (dj+1)*3 + (dk+1)] * A[i+di][j+dj][k+dk]
+//   for 1 <= i <= ni-2, 1 <= j <= nj-2, 1 <= k <= nk-2; border entries keep B_in.
+// Planes [i0, i1) of the result are written to out ((i1-i0) x nj x nk).
+void pbo_conv3d(int ni, int nj, int nk, const double* w, const float* A, const float* B_in, int i0, int i1,
+                double* out, int absmode) {
+  const size_t plane = (size_t)nj * nk;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int i = i0; i < i1; ++i) {
+    for (int j = 0; j < nj; ++j) {
+      for (int k = 0; k < nk; ++k) {
+        size_t e = (size_t)i * plane + (size_t)j * nk + k;
+        double r;
+        if (i == 0 || i == ni - 1 || j == 0 || j == nj - 1 || k == 0 || k == nk - 1) {
+          r = V(B_in[e], absmode);
+        } else {
+          r = 0.0;
+          for (int di = -1; di <= 1; ++di)
+            for (int dj = -1; dj <= 1; ++dj)
+              for (int dk = -1; dk <= 1; ++dk)
+                r += S(w[(di + 1) * 9 + (dj + 1) * 3 + (dk + 1)], absmode) *
+                     V(A[(size_t)(i + di) * plane + (size_t)(j + dj) * nk + (k + dk)], absmode);
+        }
+        out[(size_t)(i - i0) * plane + (size_t)j * nk + k] = r;
+      }
+    }
+  }
+}
+
+// fdtd-2d (reading R21; PolyBench/C 4.2 kernel_fdtd_2d, the SYCL-Bench FDTD2D):
+//   for t in 0..tmax-1:
+//     ey[0][j] = fict[t]                                             (all j)
+//     ey[i][j] = ey[i][j] - 0.5*(hz[i][j] - hz[i-1][j])              (1 <= i < nx, all j)
+//     ex[i][j] = ex[i][j] - 0.5*(hz[i][j] - hz[i][j-1])              (all i, 1 <= j < ny)
+//     hz[i][j] = hz[i][j] - 0.7*(ex[i][j+1] - ex[i][j] + ey[i+1][j] - ey[i][j])
+//                                                                    (i < nx-1, j < ny-1)
+// ex, ey, hz nx x ny; fict tmax. The three sweeps run in this order, each over
+// the state the previous sweep left (Jacobi within a sweep: no statement reads a
+// value its own sweep writes). State kept in double; inputs are the fp32 arrays.
+void pbo_fdtd2d(int tmax, int nx, int ny, const float* ex, const float* ey, const float* hz,
+                const float* fict, double* ex_o, double* ey_o, double* hz_o) {
+  const size_t N = (size_t)nx * ny;
+  for (size_t e = 0; e < N; ++e) { ex_o[e] = ex[e]; ey_o[e] = ey[e]; hz_o[e] = hz[e]; }
+  for (int t = 0; t < tmax; ++t) {
+    for (int j = 0; j < ny; ++j) ey_o[j] = (double)fict[t];
+#pragma omp parallel for schedule(static)
+    for (int i = 1; i < nx; ++i)
+      for (int j = 0; j < ny; ++j)
+        ey_o[(size_t)i * ny + j] = ey_o[(size_t)i * ny + j] - 0.5 * (hz_o[(size_t)i * ny + j] - hz_o[(size_t)(i - 1) * ny + j]);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nx; ++i)
+      for (int j = 1; j < ny; ++j)
+        ex_o[(size_t)i * ny + j] = ex_o[(size_t)i * ny + j] - 0.5 * (hz_o[(size_t)i * ny + j] - hz_o[(size_t)i * ny + j - 1]);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nx - 1; ++i)
+      for (int j = 0; j < ny - 1; ++j) {
+        size_t e = (size_t)i * ny + j;
+        hz_o[e] = hz_o[e] - 0.7 * (ex_o[e + 1] - ex_o[e] + ey_o[e + ny] - ey_o[e]);
+      }
+  }
+}
+
+// The same statements evaluated in fp32 (PolyBench's DATA_TYPE float, constants
+// 0.5f / 0.7f, C left-to-right evaluation, no contraction: built with
+// -ffp-contract=off, SSE arithmetic, so every operation is one IEEE fp32 RN op).
+// A GPU that issues the same fp32 operations in the same order reproduces it bitwise.
+void pbo_fdtd2d_f32(int tmax, int nx, int ny, const float* ex, const float* ey, const float* hz,
+                    const float* fict, float* ex_o, float* ey_o, float* hz_o) {
+  const size_t N = (size_t)nx * ny;
+  std::memcpy(ex_o, ex, N * sizeof(float));
+  std::memcpy(ey_o, ey, N * sizeof(float));
+  std::memcpy(hz_o, hz, N * sizeof(float));
+  for (int t = 0; t < tmax; ++t) {
+    for (int j = 0; j < ny; ++j) ey_o[j] = fict[t];
+#pragma omp parallel for schedule(static)
+    for (int i = 1; i < nx; ++i)
+      for (int j = 0; j < ny; ++j)
+        ey_o[(size_t)i * ny + j] = ey_o[(size_t)i * ny + j] - 0.5f * (hz_o[(size_t)i * ny + j] - hz_o[(size_t)(i - 1) * ny + j]);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nx; ++i)
+      for (int j = 1; j < ny; ++j)
+        ex_o[(size_t)i * ny + j] = ex_o[(size_t)i * ny + j] - 0.5f * (hz_o[(size_t)i * ny + j] - hz_o[(size_t)i * ny + j - 1]);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nx - 1; ++i)
+      for (int j = 0; j < ny - 1; ++j) {
+        size_t e = (size_t)i * ny + j;
+        hz_o[e] = hz_o[e] - 0.7f * (ex_o[e + 1] - ex_o[e] + ey_o[e + ny] - ey_o[e]);
+      }
+  }
+}
+
 }  // extern "C"

@@ -10,7 +10,7 @@ cap syr2k umma3x 3 syr2k
 cap 2mm umma3x 6 2mm
 cap atax atax 3 atax
 cap bicg mvmt 3 bicg
-cap gesummv rowdot 3 gesummv
+cap gesummv gesummv_tile 3 gesummv
 cap cov_gram umma3x 3 covariance
 cap cov_prep band_prep 3 covariance
 cap cov_combine gram_combine 3 covariance
