@@ -67,10 +67,12 @@ const char* pb_last_error(void);
 const char* pb_version(void);
 
 /* Workspace bytes needed by `kernel` ("gemm", "2mm", "3mm", "syrk", "syr2k",
- * "covariance", "correlation", "atax", "bicg", "mvt", "gesummv") for the dims
+ * "covariance", "correlation", "atax", "bicg", "mvt", "gesummv", "conv2d",
+ * "conv3d", "fdtd_2d") for the dims
  * given in that kernel's argument order (e.g. gemm: {ni, nj, nk}; 2mm:
  * {ni, nj, nk, nl}; 3mm: {ni, nj, nk, nl, nm}; syrk/syr2k: {n, m};
- * covariance/correlation: {m, n}; atax/bicg: {m, n}; mvt/gesummv: {n}).
+ * covariance/correlation: {m, n}; atax/bicg: {m, n}; mvt/gesummv: {n};
+ * conv2d: {ni, nj}; conv3d: {ni, nj, nk}; fdtd_2d: {nx, ny}).
  * Writes *bytes; PB_ERR_INVALID_ARG on unknown kernel or bad dims. */
 pb_status pb_workspace_size(const char* kernel, const long long* dims, int ndims, size_t* bytes);
 
@@ -318,6 +320,47 @@ pb_status pb_gesummv_dist(pb_comm* comm, int n, float alpha, float beta, const f
  */
 pb_status pb_gemm_variant(int variant, int ni, int nj, int nk, float alpha, float beta, float* C,
                           const float* A, const float* B, void* ws, size_t ws_bytes, pb_stream s);
+
+/* ------------------------------------------------------------------------
+ * SYCL-Bench polybench stencils. PAPER.md:524 (§VIII
+ * "Evaluation") lists "2D Convolution", "3D Convolution" and "FDTD2D" among the
+ * polybench benchmarks it measures, at problem size 1024 (3D Convolution,
+ * FDTD2D) and 4096 (2D Convolution); it gives no bodies, so the definitions are
+ * readings R19-R21 in DESIGN.md. All arrays row-major fp32 device memory,
+ * 16-byte aligned, innermost extent a multiple of 4.
+ *
+ * conv2d (R19) — 3x3 weighted stencil (cross-correlation) over the interior:
+ *   B[i][j] = sum_{di,dj in -1..1} w[(di+1)*3 + (dj+1)] * A[i+di][j+dj]
+ *   for 1 <= i <= ni-2, 1 <= j <= nj-2. Border entries of B are not written.
+ * A, B ni x nj (B out; must not overlap A). w: HOST pointer to 9 floats, read
+ * during the call (copied into the kernel parameters; the caller may reuse it on
+ * return). The SYCL-Bench / PolyBench-GPU kernel is w = {0.2, 0.5, -0.8,
+ * -0.3, 0.6, -0.9, 0.4, 0.7, 0.1}. No workspace. ni or nj < 3: nothing to do. */
+pb_status pb_conv2d(int ni, int nj, const float* w, const float* A, float* B, pb_stream s);
+
+/* conv3d (R20) — 3x3x3 weighted stencil over the interior of ni x nj x nk
+ * (k fastest):
+ *   B[i][j][k] = sum_{di,dj,dk in -1..1} w[(di+1)*9 + (dj+1)*3 + (dk+1)] * A[i+di][j+dj][k+dk]
+ *   for 1 <= i <= ni-2, 1 <= j <= nj-2, 1 <= k <= nk-2; border entries not written.
+ * w: HOST pointer to 27 floats (the PolyBench-GPU 3DConvolution is 11 nonzero
+ * taps: its 15 source terms with equal offsets added, R20). Requires
+ * nk % 4 == 0, ni*nj <= 2^31. No workspace. */
+pb_status pb_conv3d(int ni, int nj, int nk, const float* w, const float* A, float* B, pb_stream s);
+
+/* fdtd_2d (R21) — PolyBench/C 4.2 kernel_fdtd_2d, argument order as there:
+ *   for t < tmax:  ey[0][j] = fict[t];
+ *                  ey[i][j] -= 0.5f*(hz[i][j] - hz[i-1][j])         (i >= 1)
+ *                  ex[i][j] -= 0.5f*(hz[i][j] - hz[i][j-1])         (j >= 1)
+ *                  hz[i][j] -= 0.7f*(ex[i][j+1] - ex[i][j] + ey[i+1][j] - ey[i][j])
+ *                                                                   (i < nx-1, j < ny-1)
+ * ex, ey, hz nx x ny (in/out, distinct), fict tmax floats (device; may be NULL
+ * when tmax == 0). Every update is evaluated with the statement's fp32
+ * operations in C order (no contraction), so the result is bitwise that of the
+ * sequential PolyBench sweeps in fp32. ws: pb_workspace_size("fdtd_2d",
+ * {nx, ny}) bytes (one ping-pong copy of the three fields). One kernel launch
+ * per time step (+3 device copies when tmax is odd). */
+pb_status pb_fdtd_2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
+                     size_t ws_bytes, pb_stream s);
 
 /* Number of kernels launched by the last successful pb_* call on this thread. */
 int pb_last_launch_count(void);

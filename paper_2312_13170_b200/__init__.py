@@ -22,7 +22,7 @@ __all__ = [
     "pb_version", "last_launch_count", "ABI_FUNCTIONS", "Comm", "pb_comm_unique_id", "pb_comm_init",
     "pb_comm_destroy", "pb_gemm_dist", "pb_2mm_dist", "pb_3mm_dist", "pb_syrk_dist", "pb_syr2k_dist",
     "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist", "Peer", "pb_peer_create",
-    "pb_comm_init_local", "pb_comm_attach_peer",
+    "pb_comm_init_local", "pb_comm_attach_peer", "pb_conv2d", "pb_conv3d", "pb_fdtd_2d",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -60,6 +60,9 @@ ABI_FUNCTIONS = {
     "pb_matvec_partial": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gemm_variant": ([_I, _I, _I, _I, _F, _F, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gesummv_rows": ([_I, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_conv2d": ([_I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
+    "pb_conv3d": ([_I, _I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
+    "pb_fdtd_2d": ([_I, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
     # multi-GPU (NCCL inside libpb)
     "pb_comm_unique_id": ([_P], _I),
     "pb_comm_init": ([_I, _I, _P, ctypes.POINTER(_P)], _I),
@@ -273,6 +276,29 @@ def pb_matvec_partial(rows, cols, A_blk, v, base_row, rowdot, w, base_col, colpa
     _check("pb_matvec_partial", lib().pb_matvec_partial(rows, cols, _ptr(A_blk), _ptr(v), _ptr(base_row),
                                                         _ptr(rowdot), _ptr(w), _ptr(base_col), _ptr(colpart),
                                                         p, n, _stream(stream, A_blk)))
+
+
+def _host_w(w, n):
+    vals = [float(v) for v in (w.reshape(-1).tolist() if hasattr(w, "reshape") else w)]
+    if len(vals) != n:
+        raise ValueError(f"expected {n} weights, got {len(vals)}")
+    return (_F * n)(*vals)
+
+
+def pb_conv2d(ni, nj, w, A, B, stream=None):
+    """w: 9 weights (host), w[(di+1)*3 + (dj+1)]."""
+    _check("pb_conv2d", lib().pb_conv2d(ni, nj, _host_w(w, 9), _ptr(A), _ptr(B), _stream(stream, B)))
+
+
+def pb_conv3d(ni, nj, nk, w, A, B, stream=None):
+    """w: 27 weights (host), w[(di+1)*9 + (dj+1)*3 + (dk+1)]."""
+    _check("pb_conv3d", lib().pb_conv3d(ni, nj, nk, _host_w(w, 27), _ptr(A), _ptr(B), _stream(stream, B)))
+
+
+def pb_fdtd_2d(tmax, nx, ny, ex, ey, hz, fict, ws=None, stream=None):
+    p, n, keep = _ws(ws, "fdtd_2d", (nx, ny), ex)
+    _check("pb_fdtd_2d", lib().pb_fdtd_2d(tmax, nx, ny, _ptr(ex), _ptr(ey), _ptr(hz), _ptr(fict), p, n,
+                                          _stream(stream, ex)))
 
 
 def pb_row_partition(rows, nranks, rank, triangular=False, align=1):

@@ -256,6 +256,9 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   else if (k == "syr2k_rows" && need(4)) ws_syrk(c, d[0], d[1], d[2], d[3], true);
   else if (k == "matvec_partial" && need(2)) c.take<char>(mvmt_ws_bytes(d[0], d[1]));
   else if (k == "gemm_variant" && need(3)) ws_gemm(c, d[0], d[1], d[2]);
+  else if (k == "conv2d" && need(2)) (void)0;
+  else if (k == "conv3d" && need(3)) (void)0;
+  else if (k == "fdtd_2d" && need(2)) c.take<char>(fdtd_ws_bytes(d[0], d[1]));
   else return fail(PB_ERR_INVALID_ARG, "unknown kernel '%s' or wrong number of dims (%d)", kernel, nd);
   *bytes = align_up(c.off, 256);
   return PB_OK;
@@ -722,6 +725,52 @@ pb_status pb_gemm_variant(int variant, int ni, int nj, int nk, float alpha, floa
   if (variant == 1) PB_CUDA(launch_gemm_listing9(ni, nj, nk, alpha, beta, C, A, B, st));
   if (variant == 2) PB_CUDA(launch_gemm_listing9_reg(ni, nj, nk, alpha, beta, C, A, B, st));
   g_launches = 1;
+  return PB_OK;
+}
+
+// ---- SYCL-Bench stencils (§VIII; readings R19-R21) -------------
+pb_status pb_conv2d(int ni, int nj, const float* w, const float* A, float* B, pb_stream s) {
+  Check ck;
+  ck.dims({ni, nj});
+  ck.cols4(nj, "A/B");
+  if (ck.st == PB_OK && w == nullptr) ck.st = fail(PB_ERR_INVALID_ARG, "w is NULL");
+  ck.arr(A, ni, nj, false, "A"); ck.arr(B, ni, nj, true, "B");
+  PB_TRY(ck.finish());
+  int L = 0;
+  PB_CUDA(launch_conv2d(A, B, ni, nj, w, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_conv3d(int ni, int nj, int nk, const float* w, const float* A, float* B, pb_stream s) {
+  Check ck;
+  ck.dims({ni, nj, nk});
+  ck.cols4(nk, "A/B");
+  if (ck.st == PB_OK && (long long)ni * nj > (1ll << 31)) ck.st = fail(PB_ERR_INVALID_ARG, "ni*nj too large");
+  if (ck.st == PB_OK && w == nullptr) ck.st = fail(PB_ERR_INVALID_ARG, "w is NULL");
+  ck.arr(A, (long long)ni * nj, nk, false, "A"); ck.arr(B, (long long)ni * nj, nk, true, "B");
+  PB_TRY(ck.finish());
+  int L = 0;
+  PB_CUDA(launch_conv3d(A, B, ni, nj, nk, w, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_fdtd_2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
+                     size_t ws_bytes, pb_stream s) {
+  Check ck;
+  if (tmax < 0) ck.st = fail(PB_ERR_INVALID_ARG, "tmax %d < 0", tmax);
+  ck.dims({nx, ny});
+  ck.cols4(ny, "ex/ey/hz");
+  ck.arr(ex, nx, ny, true, "ex"); ck.arr(ey, nx, ny, true, "ey"); ck.arr(hz, nx, ny, true, "hz");
+  ck.arr(fict, 1, tmax > 0 ? tmax : 1, false, "fict", tmax > 0);
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  need.take<char>(fdtd_ws_bytes(nx, ny));
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  int L = 0;
+  PB_CUDA(launch_fdtd2d(tmax, nx, ny, ex, ey, hz, fict, ws, S(s), &L));
+  g_launches = L;
   return PB_OK;
 }
 

@@ -120,6 +120,15 @@ size_t atax_ws_bytes(int m, int n);
 cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, float* tmp, void* ws,
                         cudaStream_t s, int* launches);
 
+// ---- stencils (k_stencil.cu): SYCL-Bench 2D/3D convolution, FDTD-2D -------
+// w9 / w27 are host arrays (copied into the kernel parameters).
+cudaError_t launch_conv2d(const float* A, float* B, int ni, int nj, const float* w9, cudaStream_t s, int* launches);
+cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, const float* w27, cudaStream_t s,
+                          int* launches);
+size_t fdtd_ws_bytes(int nx, int ny);
+cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
+                          cudaStream_t s, int* launches);
+
 // ---- peer-memory collectives (k_peer.cu; host side in pb_dist.cu) ------------
 constexpr int PEER_MAXR = 8;            // ranks per peer group
 constexpr size_t PEER_HDR = 4096;       // header bytes before the data region

@@ -19,7 +19,24 @@ SEED = 13170
 U01, INT8, BIN = 0, 1, 2
 SYM = 1 << 8
 STREAM = dict(A=1, B=2, C=3, D=4, data=5, x=6, p=6, y_1=6, r=7, y_2=7, x1=8, x2=9, y=10,
-              E=11, F=12, G=13, tmp=14)
+              E=11, F=12, G=13, tmp=14, ex=8, ey=9, hz=10, fict=6)
+
+# Workload constants of the SYCL-Bench / PolyBench-GPU stencils (inputs, not
+# method arithmetic; R19/R20). 2DConvolution's c11..c33 laid out as
+# w[(di+1)*3 + (dj+1)] (row = row offset di, column = column offset dj).
+CONV2D_W = [0.2, 0.5, -0.8, -0.3, 0.6, -0.9, 0.4, 0.7, 0.1]
+# 3DConvolution's 15 source terms [weight, di, dj, dk] (tests/golden/conv3d_3x3x3.json).
+CONV3D_TERMS = [[2, -1, -1, -1], [4, 1, -1, -1], [5, -1, -1, -1], [7, 1, -1, -1], [-8, -1, -1, -1],
+                [10, 1, -1, -1], [-3, 0, -1, 0], [6, 0, 0, 0], [-9, 0, 1, 0], [2, -1, -1, 1], [4, 1, -1, 1],
+                [5, -1, 0, 1], [7, 1, 0, 1], [-8, -1, 1, 1], [10, 1, 1, 1]]
+
+
+def conv3d_w27(terms=None):
+    """27-tap table w[(di+1)*9 + (dj+1)*3 + (dk+1)] with equal-offset terms added."""
+    w = [0.0] * 27
+    for c, di, dj, dk in (CONV3D_TERMS if terms is None else terms):
+        w[(di + 1) * 9 + (dj + 1) * 3 + (dk + 1)] += float(c)
+    return w
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _host = None

@@ -234,8 +234,66 @@ def check_gesummv(n, alpha=1.5, beta=1.2):
     return _res(tmp=cerr(host(dt), t_r, t_s), y=cerr(host(dy), y_r, y_s))
 
 
+# ---------------------------------------------------------------- stencils (NEXT-3)
+def _border_mask(shape):
+    m = np.ones(shape, bool)
+    m[(slice(1, -1),) * len(shape)] = False
+    return m
+
+
+def check_conv2d(ni, nj, w=None, seed=pbgen.SEED):
+    w = pbgen.CONV2D_W if w is None else list(w)
+    A = H(ni, nj, S["A"], seed=seed)
+    B0 = H(ni, nj, S["B"], seed=seed)
+    dB = dev(B0)
+    pb.pb_conv2d(ni, nj, w, dev(A), dB)
+    g = host(dB)
+    r, s = oracle.conv2d(w, A, B0), oracle.conv2d(w, A, B0, absmode=True)
+    border_ok = bool(np.array_equal(g[_border_mask(g.shape)].view(np.uint32), B0[_border_mask(g.shape)].view(np.uint32)))
+    out = _res(B=cerr(g, r, s) if border_ok else float("inf"))
+    out["border_bitwise"] = border_ok
+    return out
+
+
+def check_conv3d(ni, nj, nk, w=None, seed=pbgen.SEED):
+    w = pbgen.conv3d_w27() if w is None else list(w)
+    A = H(ni * nj, nk, S["A"], seed=seed).reshape(ni, nj, nk)
+    B0 = H(ni * nj, nk, S["B"], seed=seed).reshape(ni, nj, nk)
+    dB = dev(B0)
+    pb.pb_conv3d(ni, nj, nk, w, dev(A), dB)
+    g = host(dB)
+    r, s = oracle.conv3d(w, A, B0), oracle.conv3d(w, A, B0, absmode=True)
+    m = _border_mask(g.shape)
+    border_ok = bool(np.array_equal(g[m].view(np.uint32), B0[m].view(np.uint32)))
+    out = _res(B=cerr(g, r, s) if border_ok else float("inf"))
+    out["border_bitwise"] = border_ok
+    return out
+
+
+def fdtd_inputs(nx, ny, tmax, seed=pbgen.SEED):
+    return (H(nx, ny, S["ex"], seed=seed), H(nx, ny, S["ey"], seed=seed), H(nx, ny, S["hz"], seed=seed),
+            H(1, max(tmax, 1), S["fict"], seed=seed).reshape(-1))
+
+
+FDTD_TOL = 1e-4  # fp64 check: |g - r| <= FDTD_TOL * max|r| (reading R21); the fp32 check is bitwise
+
+
+def check_fdtd2d(nx, ny, tmax, seed=pbgen.SEED):
+    ex, ey, hz, f = fdtd_inputs(nx, ny, tmax, seed)
+    d = [dev(a) for a in (ex, ey, hz)]
+    pb.pb_fdtd_2d(tmax, nx, ny, d[0], d[1], d[2], dev(f))
+    g = [host(t) for t in d]
+    r32 = oracle.fdtd2d(tmax, ex, ey, hz, f, f32=True)
+    r64 = oracle.fdtd2d(tmax, ex, ey, hz, f)
+    bitwise = all(np.array_equal(a.view(np.uint32), b.view(np.uint32)) for a, b in zip(g, r32))
+    scale = max(float(np.abs(a).max()) for a in r64)
+    e64 = max(float(np.abs(a.astype(np.float64) - b).max()) for a, b in zip(g, r64)) / scale
+    return {"err": e64, "ok": bool(bitwise and e64 <= FDTD_TOL), "bitwise_f32": bitwise,
+            "parts": {"rel_to_max_f64": e64}}
+
+
 def check_all_small(n=132, seed=pbgen.SEED):
-    """One ragged-size pass over all eleven kernels (used by smoke())."""
+    """One ragged-size pass over the eleven kernels and the three stencils (used by smoke())."""
     m = n + 4
     return {
         "gemm": check_gemm(n + 3, n - 4, m),
@@ -249,4 +307,7 @@ def check_all_small(n=132, seed=pbgen.SEED):
         "bicg": check_bicg(n, m + 1),
         "mvt": check_mvt(n),
         "gesummv": check_gesummv(n),
+        "conv2d": check_conv2d(n + 5, n),
+        "conv3d": check_conv3d(n // 4 + 3, n // 4 + 5, n),
+        "fdtd_2d": check_fdtd2d(n - 3, n, 7),
     }

@@ -1,0 +1,156 @@
+"""GPU parity of the SYCL-Bench stencils (readings R19-R21):
+pb_conv2d / pb_conv3d / pb_fdtd_2d through the C ABI against the oracle on pbgen
+inputs. conv: componentwise 1e-4 (R8) and border entries untouched bitwise;
+fdtd: bitwise equal to the fp32 evaluation of the PolyBench statements and within
+1e-4 of max|state| of the fp64 oracle. Sizes span several tiles with ragged tails,
+the minimal interiors, and the paper's / bench sizes (sampled rows or planes)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import paper_2312_13170_b200 as pb  # noqa: E402
+import pbgen  # noqa: E402
+from tests import parity as P  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _ok(r):
+    assert r["ok"], r
+
+
+RW9 = list(np.random.default_rng(7).normal(size=9))
+RW27 = list(np.random.default_rng(8).normal(size=27))
+
+
+@pytest.mark.parametrize("ni,nj", [(3, 4), (3, 132), (4, 8), (5, 128), (37, 132), (130, 260), (300, 516), (1030, 1028)])
+@pytest.mark.parametrize("w", ["pbgpu", "random"])
+def test_conv2d(ni, nj, w):
+    _ok(P.check_conv2d(ni, nj, None if w == "pbgpu" else RW9))
+
+
+@pytest.mark.parametrize("ni,nj,nk", [(3, 3, 4), (3, 4, 132), (5, 9, 12), (12, 17, 132), (33, 11, 260), (70, 20, 128),
+                                      (9, 130, 136)])
+@pytest.mark.parametrize("w", ["pbgpu", "random"])
+def test_conv3d(ni, nj, nk, w):
+    _ok(P.check_conv3d(ni, nj, nk, None if w == "pbgpu" else RW27))
+
+
+@pytest.mark.parametrize("nx,ny,tmax", [(1, 4, 3), (2, 4, 1), (5, 8, 2), (33, 36, 7), (64, 132, 10), (130, 260, 9),
+                                        (257, 512, 20)])
+def test_fdtd2d(nx, ny, tmax):
+    _ok(P.check_fdtd2d(nx, ny, tmax))
+
+
+def test_fdtd2d_zero_steps_is_identity():
+    ex, ey, hz, f = P.fdtd_inputs(16, 20, 0)
+    d = [P.dev(a) for a in (ex, ey, hz)]
+    pb.pb_fdtd_2d(0, 16, 20, d[0], d[1], d[2], None)
+    for a, b in zip(d, (ex, ey, hz)):
+        assert np.array_equal(P.host(a), b)
+
+
+def test_small_interiors_are_noops():
+    A = P.dev(P.H(2, 8, 1))
+    B0 = P.H(2, 8, 2)
+    dB = P.dev(B0)
+    pb.pb_conv2d(2, 8, pbgen.CONV2D_W, A, dB)
+    assert np.array_equal(P.host(dB), B0)
+    A3 = P.dev(P.H(2 * 5, 8, 1))
+    B3 = P.H(2 * 5, 8, 2)
+    dB3 = P.dev(B3)
+    pb.pb_conv3d(2, 5, 8, pbgen.conv3d_w27(), A3, dB3)
+    assert np.array_equal(P.host(dB3), B3)
+
+
+def test_stencils_deterministic():
+    A = P.dev(P.H(64 * 33, 260, 1))
+    outs = []
+    for _ in range(2):
+        B = torch.zeros(64 * 33 * 260, device="cuda")
+        pb.pb_conv3d(64, 33, 260, pbgen.conv3d_w27(), A, B)
+        outs.append(P.host(B))
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+def test_stencil_abi_errors():
+    A = torch.zeros(16, 16, device="cuda")
+    B = torch.zeros(16, 16, device="cuda")
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_conv2d(16, 16, pbgen.CONV2D_W, A, A)  # output overlaps input
+    assert e.value.status == 3
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_conv2d(16, 15, pbgen.CONV2D_W, A, B)  # nj % 4 != 0
+    assert e.value.status == 2
+    st = pb.lib().pb_conv2d(16, 16, None, A.data_ptr(), B.data_ptr(), None)  # NULL weights
+    assert st == 1
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_fdtd_2d(3, 16, 16, A, B, A, torch.zeros(3, device="cuda"))  # ex aliases hz
+    assert e.value.status == 3
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_fdtd_2d(-1, 16, 16, A, B, torch.zeros(16, 16, device="cuda"), None)
+    assert e.value.status == 1
+
+
+# ------------------------------------------------------------------ bench / paper sizes
+def test_conv2d_paper_size_4096_full():
+    _ok(P.check_conv2d(4096, 4096))
+
+
+def test_conv2d_16384_sampled_rows():
+    n = 16384
+    A = torch.empty(n, n, device="cuda")
+    pbgen.gen_device(A, P.S["A"])
+    B = torch.empty(n, n, device="cuda")
+    pbgen.gen_device(B, P.S["B"])
+    pb.pb_conv2d(n, n, pbgen.CONV2D_W, A, B)
+    torch.cuda.synchronize()
+    for i in (1, 2, 221, 222, 223, 8191, n - 3, n - 2):  # strip edges included
+        Ah = P.host(A[i - 1:i + 2])
+        Bin = np.zeros_like(Ah)
+        Bin[1] = pbgen.gen_host(1, n, P.S["B"], row0=i)
+        r = oracle.conv2d(pbgen.CONV2D_W, Ah, Bin, rows=(1, 2))[0]
+        s = oracle.conv2d(pbgen.CONV2D_W, Ah, Bin, rows=(1, 2), absmode=True)[0]
+        g = P.host(B[i])
+        assert P.cerr(g, r, s) <= P.TOL, i
+        assert g[0] == Bin[1][0] and g[-1] == Bin[1][-1]
+    for i in (0, n - 1):  # border rows untouched
+        assert np.array_equal(P.host(B[i]), pbgen.gen_host(1, n, P.S["B"], row0=i)[0])
+
+
+def test_conv3d_bench_size_1024_sampled_planes():
+    n = 1024
+    A = torch.empty(n * n, n, device="cuda")
+    pbgen.gen_device(A, P.S["A"])
+    B = torch.empty(n * n, n, device="cuda")
+    pbgen.gen_device(B, P.S["B"])
+    w = pbgen.conv3d_w27()
+    pb.pb_conv3d(n, n, n, w, A, B)
+    torch.cuda.synchronize()
+    for p0 in (1, 500, n - 2):
+        Ah = P.host(A[(p0 - 1) * n:(p0 + 2) * n]).reshape(3, n, n)
+        Bin = np.zeros_like(Ah)
+        Bin[1] = pbgen.gen_host(n, n, P.S["B"], row0=p0 * n)
+        r = oracle.conv3d(w, Ah, Bin, planes=(1, 2))[0]
+        s = oracle.conv3d(w, Ah, Bin, planes=(1, 2), absmode=True)[0]
+        g = P.host(B[p0 * n:(p0 + 1) * n])
+        assert P.cerr(g, r, s) <= P.TOL
+        m = P._border_mask((n, n))
+        assert np.array_equal(g[m], Bin[1][m])
+    # border planes untouched
+    g0 = P.host(B[0:n])
+    assert np.array_equal(g0, pbgen.gen_host(n, n, P.S["B"], row0=0))
+
+
+def test_fdtd2d_paper_size_1024_500_steps():
+    r = P.check_fdtd2d(1024, 1024, 500)
+    _ok(r)
+    assert r["bitwise_f32"]
