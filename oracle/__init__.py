@@ -50,6 +50,7 @@ _SIGS = {
     "pbo_conv3d": [_I, _I, _I, _F, _F, _F, _I, _I, _F, _I],
     "pbo_fdtd2d": [_I, _I, _I, _F, _F, _F, _F, _F, _F, _F],
     "pbo_fdtd2d_f32": [_I, _I, _I, _F, _F, _F, _F, _F, _F, _F],
+    "pbo_gramschmidt": [_I, _I, _F, _F, _F, _F],
 }
 
 
@@ -305,3 +306,13 @@ def fdtd2d(tmax, ex, ey, hz, fict, f32=False):
     fn = lib().pbo_fdtd2d_f32 if f32 else lib().pbo_fdtd2d
     fn(tmax, nx, ny, _p(ex), _p(ey), _p(hz), _p(fict), _p(o[0]), _p(o[1]), _p(o[2]))
     return tuple(o)
+
+
+def gramschmidt(A):
+    """Modified Gram-Schmidt (reading R22): returns (A_out, R, Q) in float64 for the
+    fp32 input A (m x n); R's strict lower triangle is 0 (not written by the kernel)."""
+    A = _f32(A)
+    m, n = A.shape
+    Ao, R, Q = np.empty((m, n)), np.empty((n, n)), np.empty((m, n))
+    lib().pbo_gramschmidt(m, n, _p(A), _p(Ao), _p(R), _p(Q))
+    return Ao, R, Q

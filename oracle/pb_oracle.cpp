@@ -513,4 +513,31 @@ void pbo_fdtd2d_f32(int tmax, int nx, int ny, const float* ex, const float* ey, 
   }
 }
 
+// gramschmidt (reading R22; PolyBench/C 4.2 kernel_gramschmidt, the SYCL-Bench
+// "Gramschmidt" of PAPER.md:524 — the benchmark whose candidate loop sits in a
+// divergent region). Modified Gram-Schmidt, in this order:
+//   for k < n:  nrm = sum_{i<m} A[i][k]^2;  R[k][k] = sqrt(nrm);
+//               Q[i][k] = A[i][k] / R[k][k]                       (i < m)
+//               for j in k+1..n-1:  R[k][j] = sum_{i<m} Q[i][k]*A[i][j];
+//                                   A[i][j] = A[i][j] - Q[i][k]*R[k][j]   (i < m)
+// A m x n (in/out), R n x n (entries j < k not written: R_out keeps 0 there),
+// Q m x n. State and outputs in double; inputs are the fp32 A.
+void pbo_gramschmidt(int m, int n, const float* A, double* A_out, double* R, double* Q) {
+  for (size_t e = 0; e < (size_t)m * n; ++e) A_out[e] = (double)A[e];
+  for (size_t e = 0; e < (size_t)n * n; ++e) R[e] = 0.0;
+  for (int k = 0; k < n; ++k) {
+    double nrm = 0.0;
+    for (int i = 0; i < m; ++i) nrm += A_out[(size_t)i * n + k] * A_out[(size_t)i * n + k];
+    R[(size_t)k * n + k] = std::sqrt(nrm);
+    for (int i = 0; i < m; ++i) Q[(size_t)i * n + k] = A_out[(size_t)i * n + k] / R[(size_t)k * n + k];
+#pragma omp parallel for schedule(static)
+    for (int j = k + 1; j < n; ++j) {
+      double r = 0.0;
+      for (int i = 0; i < m; ++i) r += Q[(size_t)i * n + k] * A_out[(size_t)i * n + j];
+      R[(size_t)k * n + j] = r;
+      for (int i = 0; i < m; ++i) A_out[(size_t)i * n + j] = A_out[(size_t)i * n + j] - Q[(size_t)i * n + k] * r;
+    }
+  }
+}
+
 }  // extern "C"

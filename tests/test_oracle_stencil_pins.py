@@ -6,6 +6,9 @@ Each oracle function is pinned to something other than itself:
     delta / constant closed forms, border preservation, hand-worked golden values
     (tests/golden/conv2d_3x4.json, conv3d_3x3x3.json — the latter built from the
     PolyBench-GPU 15-term source list, so the 27-tap reading R20 is pinned too).
+  * gramschmidt (R22): LAPACK Householder QR via numpy (sign-normalised), Q^T Q = I,
+    Q R = A, the final A = Q diag(R), and exact closed forms (upper-triangular input
+    -> Q = I, R = A; orthogonal columns -> signed permutation / |D|).
   * fdtd2d: hand-worked single steps (tests/golden/fdtd2d_impulse.json), exact
     telescoping sums of each sweep, the light cone of an impulse (a wrong index
     moves the support), exact linearity under scaling by 2, and the fp32 twin
@@ -206,3 +209,49 @@ def test_fdtd2d_f32_twin_close_to_f64():
     scale = max(np.abs(a).max() for a in r64)
     for a, b in zip(r64, r32):
         assert np.abs(a - b).max() <= 1e-5 * scale
+
+
+# ------------------------------------------------------------------ gramschmidt (R22)
+def _qr_pos(A):
+    """numpy (LAPACK Householder) QR with the sign convention diag(R) > 0."""
+    Qn, Rn = np.linalg.qr(A.astype(np.float64))
+    d = np.sign(np.diag(Rn))
+    return Qn * d, Rn * d[:, None]
+
+
+@pytest.mark.parametrize("m,n", [(4, 4), (9, 5), (33, 33), (64, 40)])
+def test_gramschmidt_matches_lapack_qr(m, n):
+    A = _rand(m, n, lo=-1, hi=1)
+    Ao, R, Q = oracle.gramschmidt(A)
+    Qn, Rn = _qr_pos(A)
+    np.testing.assert_allclose(Q, Qn, atol=1e-9)
+    np.testing.assert_allclose(R, Rn, atol=1e-9 * np.abs(A).max() * m)
+    assert np.all(np.tril(R, -1) == 0)
+    np.testing.assert_allclose(Q.T @ Q, np.eye(n), atol=1e-10)
+    np.testing.assert_allclose(Q @ R, A.astype(np.float64), atol=1e-12)
+    # after the sweep, column j of A holds the vector Q[:, j] was normalised from
+    np.testing.assert_allclose(Ao, Q * np.diag(R)[None, :], atol=1e-12)
+
+
+def test_gramschmidt_upper_triangular_is_exact():
+    """QR of an upper-triangular matrix with positive diagonal is Q = I, R = A (uniqueness);
+    MGS reaches it exactly (each projection removes one entry exactly)."""
+    n = 12
+    A = np.triu(_rand(n, n, lo=0.5, hi=2.0))
+    Ao, R, Q = oracle.gramschmidt(A)
+    assert np.array_equal(Q, np.eye(n))
+    assert np.array_equal(R, A.astype(np.float64))
+
+
+def test_gramschmidt_orthogonal_columns_closed_form():
+    """Columns already orthogonal: a scaled signed permutation P D -> Q = P sign(D), R = |D|."""
+    n = 10
+    perm = RNG.permutation(n)
+    d = RNG.choice([-4.0, -0.5, 0.25, 2.0, 8.0], size=n)
+    A = np.zeros((n, n), np.float32)
+    A[perm, np.arange(n)] = d
+    Ao, R, Q = oracle.gramschmidt(A)
+    Qe = np.zeros((n, n))
+    Qe[perm, np.arange(n)] = np.sign(d)
+    assert np.array_equal(Q, Qe)
+    assert np.array_equal(R, np.diag(np.abs(d)))
