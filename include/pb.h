@@ -68,11 +68,11 @@ const char* pb_version(void);
 
 /* Workspace bytes needed by `kernel` ("gemm", "2mm", "3mm", "syrk", "syr2k",
  * "covariance", "correlation", "atax", "bicg", "mvt", "gesummv", "conv2d",
- * "conv3d", "fdtd_2d") for the dims
+ * "conv3d", "fdtd_2d", "gramschmidt") for the dims
  * given in that kernel's argument order (e.g. gemm: {ni, nj, nk}; 2mm:
  * {ni, nj, nk, nl}; 3mm: {ni, nj, nk, nl, nm}; syrk/syr2k: {n, m};
  * covariance/correlation: {m, n}; atax/bicg: {m, n}; mvt/gesummv: {n};
- * conv2d: {ni, nj}; conv3d: {ni, nj, nk}; fdtd_2d: {nx, ny}).
+ * conv2d: {ni, nj}; conv3d: {ni, nj, nk}; fdtd_2d: {nx, ny}; gramschmidt: {m, n}).
  * Writes *bytes; PB_ERR_INVALID_ARG on unknown kernel or bad dims. */
 pb_status pb_workspace_size(const char* kernel, const long long* dims, int ndims, size_t* bytes);
 
@@ -361,6 +361,21 @@ pb_status pb_conv3d(int ni, int nj, int nk, const float* w, const float* A, floa
  * per time step (+3 device copies when tmax is odd). */
 pb_status pb_fdtd_2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                      size_t ws_bytes, pb_stream s);
+
+/* gramschmidt (R22) — PolyBench/C 4.2 kernel_gramschmidt (the SYCL-Bench
+ * "Gramschmidt" of PAPER.md:524; PAPER.md:551 notes its candidate loop sits in a
+ * divergent region). Modified Gram-Schmidt, for k < n:
+ *   R[k][k] = sqrt(sum_i A[i][k]^2);  Q[i][k] = A[i][k] / R[k][k];
+ *   for j > k:  R[k][j] = sum_i Q[i][k]*A[i][j];  A[i][j] -= Q[i][k]*R[k][j]
+ * A m x n (in/out: on return column j holds R[j][j]*Q[:,j], as in PolyBench),
+ * R n x n (out; entries below the diagonal are not written), Q m x n (out). All
+ * distinct. Computed in fp64 (state and reductions), rounded to fp32 once.
+ * Linearly dependent columns give Inf/NaN (division by R[k][k] = 0), as in
+ * PolyBench. ws: pb_workspace_size("gramschmidt", {m, n}) bytes. One persistent
+ * cooperative kernel (one CTA per SM) plus three transposes; the co-residency
+ * of the persistent kernel needs m * ceil(n / #SMs) * 8 <= 200 KiB for the
+ * shared-memory path, else its columns stay in the (L2-resident) workspace. */
+pb_status pb_gramschmidt(int m, int n, float* A, float* R, float* Q, void* ws, size_t ws_bytes, pb_stream s);
 
 /* Number of kernels launched by the last successful pb_* call on this thread. */
 int pb_last_launch_count(void);

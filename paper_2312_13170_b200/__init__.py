@@ -23,6 +23,7 @@ __all__ = [
     "pb_comm_destroy", "pb_gemm_dist", "pb_2mm_dist", "pb_3mm_dist", "pb_syrk_dist", "pb_syr2k_dist",
     "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist", "Peer", "pb_peer_create",
     "pb_comm_init_local", "pb_comm_attach_peer", "pb_conv2d", "pb_conv3d", "pb_fdtd_2d",
+    "pb_gramschmidt",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -63,6 +64,7 @@ ABI_FUNCTIONS = {
     "pb_conv2d": ([_I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
     "pb_conv3d": ([_I, _I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
     "pb_fdtd_2d": ([_I, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_gramschmidt": ([_I, _I, _P, _P, _P, _P, _Z, _P], _I),
     # multi-GPU (NCCL inside libpb)
     "pb_comm_unique_id": ([_P], _I),
     "pb_comm_init": ([_I, _I, _P, ctypes.POINTER(_P)], _I),
@@ -299,6 +301,11 @@ def pb_fdtd_2d(tmax, nx, ny, ex, ey, hz, fict, ws=None, stream=None):
     p, n, keep = _ws(ws, "fdtd_2d", (nx, ny), ex)
     _check("pb_fdtd_2d", lib().pb_fdtd_2d(tmax, nx, ny, _ptr(ex), _ptr(ey), _ptr(hz), _ptr(fict), p, n,
                                           _stream(stream, ex)))
+
+
+def pb_gramschmidt(m, n_, A, R, Q, ws=None, stream=None):
+    p, n, keep = _ws(ws, "gramschmidt", (m, n_), A)
+    _check("pb_gramschmidt", lib().pb_gramschmidt(m, n_, _ptr(A), _ptr(R), _ptr(Q), p, n, _stream(stream, A)))
 
 
 def pb_row_partition(rows, nranks, rank, triangular=False, align=1):

@@ -259,6 +259,7 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   else if (k == "conv2d" && need(2)) (void)0;
   else if (k == "conv3d" && need(3)) (void)0;
   else if (k == "fdtd_2d" && need(2)) c.take<char>(fdtd_ws_bytes(d[0], d[1]));
+  else if (k == "gramschmidt" && need(2)) c.take<char>(gramschmidt_ws_bytes(d[0], d[1]));
   else return fail(PB_ERR_INVALID_ARG, "unknown kernel '%s' or wrong number of dims (%d)", kernel, nd);
   *bytes = align_up(c.off, 256);
   return PB_OK;
@@ -770,6 +771,21 @@ pb_status pb_fdtd_2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, 
   PB_TRY(check_ws(need, ws, ws_bytes));
   int L = 0;
   PB_CUDA(launch_fdtd2d(tmax, nx, ny, ex, ey, hz, fict, ws, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+// ---- gramschmidt (reading R22) ---------------------------
+pb_status pb_gramschmidt(int m, int n, float* A, float* R, float* Q, void* ws, size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({m, n});
+  ck.arr(A, m, n, true, "A"); ck.arr(R, n, n, true, "R"); ck.arr(Q, m, n, true, "Q");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  need.take<char>(gramschmidt_ws_bytes(m, n));
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  int L = 0;
+  PB_CUDA(launch_gramschmidt(m, n, A, R, Q, ws, S(s), &L));
   g_launches = L;
   return PB_OK;
 }

@@ -129,6 +129,10 @@ size_t fdtd_ws_bytes(int nx, int ny);
 cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                           cudaStream_t s, int* launches);
 
+// ---- gramschmidt (k_gramschmidt.cu): persistent modified Gram-Schmidt, fp64 state
+size_t gramschmidt_ws_bytes(int m, int n);
+cudaError_t launch_gramschmidt(int m, int n, float* A, float* R, float* Q, void* ws, cudaStream_t s, int* launches);
+
 // ---- peer-memory collectives (k_peer.cu; host side in pb_dist.cu) ------------
 constexpr int PEER_MAXR = 8;            // ranks per peer group
 constexpr size_t PEER_HDR = 4096;       // header bytes before the data region

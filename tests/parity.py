@@ -292,6 +292,30 @@ def check_fdtd2d(nx, ny, tmax, seed=pbgen.SEED):
             "parts": {"rel_to_max_f64": e64}}
 
 
+def check_gramschmidt(m, n, seed=pbgen.SEED):
+    """Reading R22: Q and the final A columnwise against max|column| of the oracle's,
+    R[k][j] against ||A_in[:, j]||_2 (a bound on |R[k][j]|); R's strict lower
+    triangle must keep its input bitwise."""
+    A = H(m, n, S["A"], seed=seed)
+    R0 = H(n, n, S["B"], seed=seed)
+    dA, dR, dQ = dev(A), dev(R0), torch.zeros(m, n, device="cuda")
+    pb.pb_gramschmidt(m, n, dA, dR, dQ)
+    gA, gR, gQ = host(dA), host(dR), host(dQ)
+    rA, rR, rQ = oracle.gramschmidt(A)
+    low = np.tril(np.ones((n, n), bool), -1)
+    lower_ok = bool(np.array_equal(gR[low].view(np.uint32), R0[low].view(np.uint32)))
+    colA = np.abs(rA).max(0)
+    colQ = np.abs(rQ).max(0)
+    cn = np.sqrt((A.astype(np.float64) ** 2).sum(0))
+    eA = float((np.abs(gA - rA) / colA[None, :]).max())
+    eQ = float((np.abs(gQ - rQ) / colQ[None, :]).max())
+    up = ~low
+    eR = float((np.abs(gR - rR) / cn[None, :])[up].max())
+    out = _res(A=eA, Q=eQ, R=eR if lower_ok else float("inf"))
+    out["lower_untouched"] = lower_ok
+    return out
+
+
 def check_all_small(n=132, seed=pbgen.SEED):
     """One ragged-size pass over the eleven kernels and the three stencils (used by smoke())."""
     m = n + 4
@@ -310,4 +334,5 @@ def check_all_small(n=132, seed=pbgen.SEED):
         "conv2d": check_conv2d(n + 5, n),
         "conv3d": check_conv3d(n // 4 + 3, n // 4 + 5, n),
         "fdtd_2d": check_fdtd2d(n - 3, n, 7),
+        "gramschmidt": check_gramschmidt(n + 7, n - 5),
     }

@@ -154,3 +154,26 @@ def test_fdtd2d_paper_size_1024_500_steps():
     r = P.check_fdtd2d(1024, 1024, 500)
     _ok(r)
     assert r["bitwise_f32"]
+
+
+# ------------------------------------------------------------------ gramschmidt (R22)
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 1), (4, 4), (37, 20), (132, 132), (300, 149), (149, 296), (517, 300),
+                                 (1024, 1024)])
+def test_gramschmidt(m, n):
+    _ok(P.check_gramschmidt(m, n))
+
+
+def test_gramschmidt_global_column_path():
+    """m * ceil(n / SMs) * 8 B > 200 KiB: the owned columns stay in the workspace (L2)."""
+    _ok(P.check_gramschmidt(8192, 600))
+
+
+def test_gramschmidt_deterministic():
+    m, n = 256, 200
+    A = P.H(m, n, 1)
+    outs = []
+    for _ in range(2):
+        dA, dR, dQ = P.dev(A), torch.zeros(n, n, device="cuda"), torch.zeros(m, n, device="cuda")
+        pb.pb_gramschmidt(m, n, dA, dR, dQ)
+        outs.append([P.host(t).view(np.uint32) for t in (dA, dR, dQ)])
+    assert all(np.array_equal(a, b) for a, b in zip(*outs))
