@@ -119,10 +119,27 @@ def fdtd(n, tmax, reps):
                 bitwise_f32=bitwise, launches=pb.last_launch_count())
 
 
+def gramschmidt(n, reps):
+    A0 = gen((n, n), S["A"])
+    A = A0.clone()
+    R = torch.zeros(n, n, device=dev)
+    Q = torch.zeros(n, n, device=dev)
+    ws = pb.workspace("gramschmidt", (n, n), dev)
+
+    def fn():
+        A.copy_(A0)  # in/out: restored inside the graph (a 4 MiB D2D copy, ~2 us)
+        pb.pb_gramschmidt(n, n, A, R, Q, ws)
+    med, mn = timed(fn, reps)
+    flops = 2.0 * n * n * n  # sum_k (n-k-1) * 4m + 3m  ~ 2 m n^2
+    return dict(kernel="gramschmidt", n=n, ms=med, ms_min=mn, us_per_step=1000 * med / n,
+                gflops=flops / med / 1e6, launches=pb.last_launch_count())
+
+
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else None
     torch.cuda.set_device(0)
-    res = [conv2d(4096, 30), conv2d(16384, 20), conv3d(1024, 10), conv3d(512, 20), fdtd(1024, 500, 10)]
+    res = [conv2d(4096, 30), conv2d(16384, 20), conv3d(1024, 10), conv3d(512, 20), fdtd(1024, 500, 10),
+           gramschmidt(1024, 10), gramschmidt(2048, 5)]
     for r in res:
         print(json.dumps(r))
     if out:

@@ -157,9 +157,11 @@ def test_fdtd2d_paper_size_1024_500_steps():
 
 
 # ------------------------------------------------------------------ gramschmidt (R22)
-@pytest.mark.parametrize("m,n", [(1, 1), (5, 1), (4, 4), (37, 20), (132, 132), (300, 149), (149, 296), (517, 300),
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 1), (4, 4), (37, 20), (132, 132), (300, 149), (149, 148), (517, 300),
                                  (1024, 1024)])
 def test_gramschmidt(m, n):
+    """m >= n: with n > m the columns k >= m are linearly dependent, R[k][k] is
+    rounding noise and Q[:, k] = noise / noise (Inf/NaN or arbitrary), on both sides."""
     _ok(P.check_gramschmidt(m, n))
 
 
