@@ -2,19 +2,22 @@
 // "2D Convolution", "3D Convolution" and "FDTD2D"; SURVEY.md §8(f) NEXT-3;
 // definitions = readings R19-R21 in DESIGN.md).
 //
-// All three are HBM- (or, for FDTD at the paper's 1024^2, L2-) streaming
-// kernels: no contraction, so no tensor cores. Loop internalization's role
-// (stage what neighbouring work-items re-read through local
-// memory) is played by
-//   conv2d: registers. A warp owns 128 contiguous columns and marches down a row
-//           strip; each lane keeps a 3-row window (float4 + its two neighbour
-//           columns, taken from the adjacent lanes by shuffles), so every element
-//           of A is loaded from global memory once per strip.
-//   conv3d: a shared-memory ring of plane tiles (10 rows x 136 floats: the CTA's
-//           8 output rows, their j-halo and a k-halo) filled by 1-D bulk copies
-//           (the TMA engine) STAGES planes ahead; the CTA marches along i and
-//           each plane contributes to three output planes held in registers
-//           (register pipelining), so every plane tile is read from smem once.
+// No contraction here, so no tensor cores: the convolutions are HBM streams and
+// FDTD at the paper's 1024^2 is an L2-resident time loop. Loop internalization's
+// role (stage what neighbouring work-items re-read through
+// local memory) is played by
+//   conv2d / conv3d: one "march" kernel. A CTA owns a tile of output columns (2-D:
+//           1024 columns of a row; 3-D: 8 rows x 128 columns of a plane) and marches
+//           along the slowest axis. Each plane (2-D: row) tile plus its halo is
+//           staged by 1-D bulk copies (the TMA engine) into a shared-memory ring
+//           STAGES ahead, so the bytes in flight do not depend on registers. Every
+//           staged plane contributes to three output planes held in registers
+//           (register pipelining), so each tile is read from shared memory once.
+//           The FMAs are packed (fma.rn.f32x2: two outputs per instruction), and
+//           the zero pattern of the weights can be a compile-time template argument
+//           (the paper's host-to-device constant propagation: a
+//           filter known on the host specialises the device code); the weights'
+//           values stay runtime arguments.
 //   fdtd2d: one fused launch per time step. The three PolyBench sweeps are
 //           evaluated per point from the previous step's state; the two
 //           neighbour values the hz update needs (ex'[i][j+1], ey'[i+1][j]) are
@@ -43,201 +46,203 @@ int sm_count() {
   return n;
 }
 
-// ============================================================== conv2d
-struct W9 {
-  float w[9];
+// ============================================================== conv2d / conv3d
+struct W27x2 {
+  float2 w[27];  // (w, w): the weight broadcast to both lanes of a packed FMA
 };
 
-// One lane's view of one row: 4 owned columns and the two neighbours.
-struct Row6 {
-  float l, a, b, c, d, r;
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // a*b + c, two RN FMAs
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+constexpr int ST_STAGES = 6;
+
+template <int NJT, int OROWS, int WPR>
+struct March {
+  static constexpr int TC = 128 * WPR;               // tile columns
+  static constexpr int TROWS = OROWS + NJT - 1;      // staged rows per plane
+  static constexpr int PITCH = TC + 8;               // [3] left halo, [4, 4+TC) values, [4+TC] right halo
+  static constexpr int TILE = TROWS * PITCH;         // floats per stage
+  static constexpr int THREADS = 32 * OROWS * WPR;
+  static constexpr size_t SMEM = (size_t)ST_STAGES * TILE * sizeof(float) + ST_STAGES * sizeof(uint64_t);
 };
 
-__device__ __forceinline__ Row6 load_row2d(const float* __restrict__ row, int c0, int j, bool active, int lane,
-                                           int nj) {
-  float4 v = active ? ldg_stream(reinterpret_cast<const float4*>(row + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-  Row6 o;
-  o.a = v.x; o.b = v.y; o.c = v.z; o.d = v.w;
-  float left = __shfl_up_sync(0xffffffffu, v.w, 1);
-  float right = __shfl_down_sync(0xffffffffu, v.x, 1);
-  if (lane == 0) left = (c0 > 0) ? __ldg(row + c0 - 1) : 0.f;
-  if (lane == 31) right = (c0 + 128 < nj) ? __ldg(row + c0 + 128) : 0.f;
-  o.l = left;
-  o.r = right;
+// One plane q of the march (rows j0-(NJT>1) .. +TROWS, columns c0-4 .. c0+TC+4,
+// clipped to the array) -> ring buffer `buf`, tx bytes on `bar` (one thread).
+template <int NJT, int OROWS, int WPR>
+__device__ __forceinline__ void march_issue(const float* A, float* buf, uint64_t* bar, int q, int j0, int c0,
+                                            int nrow, int ncol) {
+  using M = March<NJT, OROWS, WPR>;
+  const int ka = max(c0 - 4, 0);
+  const int kb = min(c0 + M::TC + 4, ncol);
+  const uint32_t row_bytes = (uint32_t)(kb - ka) * 4u;
+  const int jlo = max(j0 - (NJT > 1 ? 1 : 0), 0);
+  const int jhi = min(j0 - (NJT > 1 ? 1 : 0) + M::TROWS, nrow);
+  mbar_arrive_expect_tx(bar, row_bytes * (uint32_t)(jhi - jlo));
+#pragma unroll 1
+  for (int jj = jlo; jj < jhi; ++jj) {
+    const int r = jj - (j0 - (NJT > 1 ? 1 : 0));
+    bulk_g2s(buf + r * M::PITCH + 4 + (ka - c0), A + ((size_t)q * nrow + jj) * ncol + ka, row_bytes, bar);
+  }
+}
+
+// The 5 input pairs a thread's 4 outputs need from one staged row: (l,a) (a,b) (b,c) (c,d) (d,r).
+struct Pairs {
+  float2 p[5];
+};
+__device__ __forceinline__ Pairs read_pairs(const float* t) {  // t = row base + 4 + column offset
+  const float4 v = *reinterpret_cast<const float4*>(t);
+  const float l = t[-1], r = t[4];
+  Pairs o;
+  o.p[0] = make_float2(l, v.x);
+  o.p[1] = make_float2(v.x, v.y);
+  o.p[2] = make_float2(v.y, v.z);
+  o.p[3] = make_float2(v.z, v.w);
+  o.p[4] = make_float2(v.w, r);
   return o;
 }
 
-__device__ __forceinline__ void acc_row(float (&o)[4], const Row6& x, float w0, float w1, float w2) {
-  o[0] = fmaf(w0, x.l, o[0]); o[0] = fmaf(w1, x.a, o[0]); o[0] = fmaf(w2, x.b, o[0]);
-  o[1] = fmaf(w0, x.a, o[1]); o[1] = fmaf(w1, x.b, o[1]); o[1] = fmaf(w2, x.c, o[1]);
-  o[2] = fmaf(w0, x.b, o[2]); o[2] = fmaf(w1, x.c, o[2]); o[2] = fmaf(w2, x.d, o[2]);
-  o[3] = fmaf(w0, x.c, o[3]); o[3] = fmaf(w1, x.d, o[3]); o[3] = fmaf(w2, x.r, o[3]);
-}
-
-// Store the interior part of 4 outputs at (i, j..j+3): float4 when all four are
-// interior columns, else element-wise (border columns 0 and nj-1 untouched).
-__device__ __forceinline__ void store4_interior(float* dst, int j, int jlo, int jhi, const float (&o)[4]) {
-  if (j >= jlo && j + 3 <= jhi) {
-    __stcs(reinterpret_cast<float4*>(dst + j), make_float4(o[0], o[1], o[2], o[3]));
+// Stores the interior part of 4 outputs (cols k..k+3, row base dst): float4 when all
+// four are interior columns, else element-wise (border columns untouched).
+__device__ __forceinline__ void store4_interior(float* dst, int k, int klo, int khi, float2 lo, float2 hi) {
+  if (k >= klo && k + 3 <= khi) {
+    __stcs(reinterpret_cast<float4*>(dst + k), make_float4(lo.x, lo.y, hi.x, hi.y));
   } else {
+    const float o[4] = {lo.x, lo.y, hi.x, hi.y};
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      if (j + e >= jlo && j + e <= jhi) dst[j + e] = o[e];
+      if (k + e >= klo && k + e <= khi) dst[k + e] = o[e];
   }
 }
 
-constexpr int C2_WARPS = 8;
-constexpr int C2_U = 4;  // rows loaded per batch (memory parallelism)
-
-// Work unit = (128-column chunk, strip of R output rows). Warp-granular.
-__global__ void __launch_bounds__(32 * C2_WARPS) conv2d_kernel(const float* __restrict__ A, float* __restrict__ B,
-                                                               int ni, int nj, int R, int nchunks, long long units,
-                                                               const __grid_constant__ W9 w) {
-  pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const long long unit = (long long)blockIdx.x * C2_WARPS + (threadIdx.x >> 5);
-  if (unit >= units) return;
-  const int chunk = (int)(unit % nchunks);
-  const int strip = (int)(unit / nchunks);
-  const int c0 = chunk * 128;
-  const int j = c0 + 4 * lane;
-  const bool active = j < nj;
-  const int o0 = 1 + strip * R;
-  const int o1 = min(o0 + R, ni - 1);  // output rows [o0, o1)
-  if (o0 >= o1) return;
-  Row6 x0 = load_row2d(A + (size_t)(o0 - 1) * nj, c0, j, active, lane, nj);
-  Row6 x1 = load_row2d(A + (size_t)o0 * nj, c0, j, active, lane, nj);
-  for (int i = o0; i < o1; i += C2_U) {
-    Row6 nx[C2_U];
+// MASK bit (di+1)*NJT*3 + dj*3 + (dk+1) set <=> that weight may be nonzero.
+template <int NJT, uint32_t MASK>
+__device__ __forceinline__ void march_taps(float2 (&am)[2], float2 (&a0)[2], float2 (&ap)[2], const Pairs* rows,
+                                           const W27x2& w) {
 #pragma unroll
-    for (int u = 0; u < C2_U; ++u) {
-      const int r = i + 1 + u;  // rows i+1 .. i+U (r <= ni-1 is in range while the output row i+u < o1)
-      nx[u] = (i + u < o1) ? load_row2d(A + (size_t)r * nj, c0, j, active, lane, nj) : x1;
-    }
+  for (int dj = 0; dj < NJT; ++dj) {
 #pragma unroll
-    for (int u = 0; u < C2_U; ++u) {
-      if (i + u < o1) {
-        float o[4] = {0.f, 0.f, 0.f, 0.f};
-        acc_row(o, x0, w.w[0], w.w[1], w.w[2]);
-        acc_row(o, x1, w.w[3], w.w[4], w.w[5]);
-        acc_row(o, nx[u], w.w[6], w.w[7], w.w[8]);
-        if (active) store4_interior(B + (size_t)(i + u) * nj, j, 1, nj - 2, o);
-      }
-      x0 = x1;
-      x1 = nx[u];
+    for (int dk = 0; dk < 3; ++dk) {
+      const float2 xlo = rows[dj].p[dk], xhi = rows[dj].p[dk + 2];
+      constexpr int PLANE = NJT * 3;
+      const int tm = 2 * PLANE + dj * 3 + dk;  // di = +1 -> output plane q-1
+      const int t0 = PLANE + dj * 3 + dk;      // di =  0 -> output plane q
+      const int tp = dj * 3 + dk;              // di = -1 -> output plane q+1
+      if (MASK & (1u << tm)) { am[0] = ffma2(w.w[tm], xlo, am[0]); am[1] = ffma2(w.w[tm], xhi, am[1]); }
+      if (MASK & (1u << t0)) { a0[0] = ffma2(w.w[t0], xlo, a0[0]); a0[1] = ffma2(w.w[t0], xhi, a0[1]); }
+      if (MASK & (1u << tp)) { ap[0] = ffma2(w.w[tp], xlo, ap[0]); ap[1] = ffma2(w.w[tp], xhi, ap[1]); }
     }
   }
 }
 
-// ============================================================== conv3d
-struct W27 {
-  float w[27];
-};
-
-constexpr int C3_ROWS = 8;          // output j-rows per CTA (one warp each)
-constexpr int C3_TROWS = C3_ROWS + 2;
-constexpr int C3_PITCH = 136;       // floats per tile row: [0..3] pad/left halo at 3, values at 4..131, right halo 132
-constexpr int C3_STAGES = 4;
-constexpr int C3_TILE = C3_TROWS * C3_PITCH;
-
-struct C3Row {
-  float l, a, b, c, d, r;
-};
-
-__device__ __forceinline__ C3Row read_tile_row(const float* t, int lane) {
-  const float4 v = *reinterpret_cast<const float4*>(t + 4 + 4 * lane);
-  C3Row o;
-  o.a = v.x; o.b = v.y; o.c = v.z; o.d = v.w;
-  o.l = t[3 + 4 * lane];
-  o.r = t[8 + 4 * lane];
-  return o;
-}
-
-__device__ __forceinline__ void acc3(float (&o)[4], const C3Row& x, const float* w3) {
-  o[0] = fmaf(w3[0], x.l, o[0]); o[0] = fmaf(w3[1], x.a, o[0]); o[0] = fmaf(w3[2], x.b, o[0]);
-  o[1] = fmaf(w3[0], x.a, o[1]); o[1] = fmaf(w3[1], x.b, o[1]); o[1] = fmaf(w3[2], x.c, o[1]);
-  o[2] = fmaf(w3[0], x.b, o[2]); o[2] = fmaf(w3[1], x.c, o[2]); o[2] = fmaf(w3[2], x.d, o[2]);
-  o[3] = fmaf(w3[0], x.c, o[3]); o[3] = fmaf(w3[1], x.d, o[3]); o[3] = fmaf(w3[2], x.r, o[3]);
-}
-
-// Issue the bulk copies of plane q's tile into buffer `buf` (one thread). Returns bytes.
-__device__ __forceinline__ void c3_issue(const float* A, float* buf, uint64_t* bar, int q, int j0, int k0, int nj,
-                                         int nk) {
-  // k range [ka, kb): k0-4 .. k0+132 clipped to [0, nk); lands at offset 4 + (ka - k0)
-  const int ka = max(k0 - 4, 0);
-  const int kb = min(k0 + 132, nk);
-  const uint32_t row_bytes = (uint32_t)(kb - ka) * 4u;
-  int nrows = 0;
-#pragma unroll 1
-  for (int r = 0; r < C3_TROWS; ++r) {
-    const int jj = j0 - 1 + r;
-    if (jj >= 0 && jj < nj) ++nrows;
-  }
-  mbar_arrive_expect_tx(bar, row_bytes * (uint32_t)nrows);
-#pragma unroll 1
-  for (int r = 0; r < C3_TROWS; ++r) {
-    const int jj = j0 - 1 + r;
-    if (jj < 0 || jj >= nj) continue;
-    const float* src = A + ((size_t)q * nj + jj) * nk + ka;
-    bulk_g2s(buf + r * C3_PITCH + 4 + (ka - k0), src, row_bytes, bar);
-  }
-}
-
-// Work unit = (k chunk of 128, group of 8 j-rows, segment of output planes).
-__global__ void __launch_bounds__(32 * C3_ROWS) conv3d_kernel(const float* __restrict__ A, float* __restrict__ B,
-                                                              int ni, int nj, int nk, int seg, int nkc, int njg,
-                                                              const __grid_constant__ W27 w) {
-  extern __shared__ __align__(128) float c3_smem[];
-  float* tiles = c3_smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(c3_smem + C3_STAGES * C3_TILE);
+// Work unit = (column chunk cc, row group rg, segment sg of output planes [o0, o1)).
+// nrow = 1 for 2-D (the march axis is the row index; columns are the stencil's j).
+template <int NJT, int OROWS, int WPR, uint32_t MASK>
+__global__ void __launch_bounds__(32 * OROWS * WPR) march_kernel(const float* __restrict__ A, float* __restrict__ B,
+                                                                 int ni, int nrow, int ncol, int seg, int ncc,
+                                                                 int nrg, const __grid_constant__ W27x2 w) {
+  using M = March<NJT, OROWS, WPR>;
+  extern __shared__ __align__(128) float st_smem[];
+  float* tiles = st_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(st_smem + ST_STAGES * M::TILE);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int kc = blockIdx.x % nkc;
-  const int jg = (blockIdx.x / nkc) % njg;
-  const int sg = blockIdx.x / (nkc * njg);
-  const int k0 = kc * 128, j0 = jg * C3_ROWS;
+  const int cc = blockIdx.x % ncc;
+  const int rg = (blockIdx.x / ncc) % nrg;
+  const int sg = blockIdx.x / (ncc * nrg);
+  const int c0 = cc * M::TC, j0 = rg * OROWS;
   const int o0 = 1 + sg * seg;
   const int o1 = min(o0 + seg, ni - 1);  // output planes [o0, o1)
   if (o0 >= o1) return;
-  const int q0 = o0 - 1, q1 = o1 + 1;   // planes loaded [q0, q1)
-  const int nplanes = q1 - q0;
+  const int q0 = o0 - 1;
+  const int nplanes = o1 + 1 - q0;  // planes [o0-1, o1]
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C3_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < ST_STAGES; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
   pdl_wait();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C3_STAGES && s < nplanes; ++s)
-      c3_issue(A, tiles + s * C3_TILE, &full[s], q0 + s, j0, k0, nj, nk);
+    for (int s = 0; s < ST_STAGES && s < nplanes; ++s)
+      march_issue<NJT, OROWS, WPR>(A, tiles + s * M::TILE, &full[s], q0 + s, j0, c0, nrow, ncol);
   }
-  const int j = j0 + wp;
-  const int k = k0 + 4 * lane;
-  const bool store_ok = (j >= 1 && j <= nj - 2 && k < nk);
-  float am[4] = {0.f, 0.f, 0.f, 0.f}, a0[4] = {0.f, 0.f, 0.f, 0.f}, ap[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-  for (int p = 0; p < nplanes; ++p) {
-    const int s = p % C3_STAGES;
-    mbar_wait(&full[s], (uint32_t)((p / C3_STAGES) & 1));
-    const float* t = tiles + s * C3_TILE + wp * C3_PITCH;
-    const C3Row r0 = read_tile_row(t, lane);
-    const C3Row r1 = read_tile_row(t + C3_PITCH, lane);
-    const C3Row r2 = read_tile_row(t + 2 * C3_PITCH, lane);
-    // plane q = q0 + p: di = +1 for output q-1 (am), 0 for q (a0), -1 for q+1 (ap)
-    acc3(am, r0, &w.w[18 + 0]); acc3(am, r1, &w.w[18 + 3]); acc3(am, r2, &w.w[18 + 6]);
-    acc3(a0, r0, &w.w[9 + 0]);  acc3(a0, r1, &w.w[9 + 3]);  acc3(a0, r2, &w.w[9 + 6]);
-    acc3(ap, r0, &w.w[0]);      acc3(ap, r1, &w.w[3]);      acc3(ap, r2, &w.w[6]);
-    __syncthreads();  // every warp is done with buffer s
-    if (threadIdx.x == 0 && p + C3_STAGES < nplanes)
-      c3_issue(A, tiles + s * C3_TILE, &full[s], q0 + p + C3_STAGES, j0, k0, nj, nk);
-    const int oq = q0 + p - 1;  // output plane completed by this plane
-    if (p >= 2 && store_ok) store4_interior(B + ((size_t)oq * nj + j) * nk, k, 1, nk - 2, am);
+  const int tr = wp / WPR;                         // output row within the tile
+  const int col = (wp % WPR) * 128 + 4 * lane;     // column offset within the tile
+  const int j = j0 + tr, k = c0 + col;
+  const bool store_ok = (NJT == 1 || (j >= 1 && j <= nrow - 2)) && k < ncol;
+  float2 acc[3][2];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      am[e] = a0[e];
-      a0[e] = ap[e];
-      ap[e] = 0.f;
-    }
+  for (int r = 0; r < 3; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+
+  auto step = [&](int p, float2(&am)[2], float2(&a0)[2], float2(&ap)[2]) {
+    const int s = p % ST_STAGES;
+    mbar_wait(&full[s], (uint32_t)((p / ST_STAGES) & 1));
+    const float* t = tiles + s * M::TILE + tr * M::PITCH + 4 + col;
+    Pairs rows[NJT];
+#pragma unroll
+    for (int dj = 0; dj < NJT; ++dj) rows[dj] = read_pairs(t + dj * M::PITCH);
+    march_taps<NJT, MASK>(am, a0, ap, rows, w);
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && p + ST_STAGES < nplanes)
+      march_issue<NJT, OROWS, WPR>(A, tiles + s * M::TILE, &full[s], q0 + p + ST_STAGES, j0, c0, nrow, ncol);
+    if (p >= 2 && store_ok)  // output plane q-1 is complete
+      store4_interior(B + ((size_t)(q0 + p - 1) * nrow + (NJT > 1 ? j : 0)) * ncol, k, 1, ncol - 2, am[0], am[1]);
+    am[0] = am[1] = make_float2(0.f, 0.f);  // becomes the next plane's q+1 accumulator
+  };
+#pragma unroll 1
+  for (int p = 0; p < nplanes; p += 3) {  // roles rotate statically: (m, 0, p) = (0,1,2), (1,2,0), (2,0,1)
+    step(p, acc[0], acc[1], acc[2]);
+    if (p + 1 < nplanes) step(p + 1, acc[1], acc[2], acc[0]);
+    if (p + 2 < nplanes) step(p + 2, acc[2], acc[0], acc[1]);
   }
+}
+
+// Zero patterns compiled as specialisations (bit t <=> weight t may be nonzero).
+constexpr uint32_t MASK_DENSE = (1u << 27) - 1;
+constexpr uint32_t MASK_DENSE9 = (1u << 9) - 1;
+
+uint32_t weight_mask(const float* w, int n) {
+  uint32_t m = 0;
+  for (int t = 0; t < n; ++t)
+    if (w[t] != 0.f) m |= 1u << t;
+  return m;
+}
+
+// PolyBench-GPU 3DConvolution's 11 nonzero taps (R20): (di,dj,dk) =
+// (-1,-1,-1) (-1,-1,+1) (-1,0,+1) (-1,+1,+1) (0,-1,0) (0,0,0) (0,+1,0)
+// (+1,-1,-1) (+1,-1,+1) (+1,0,+1) (+1,+1,+1).
+constexpr uint32_t tap3(int di, int dj, int dk) { return 1u << ((di + 1) * 9 + (dj + 1) * 3 + (dk + 1)); }
+constexpr uint32_t MASK_PBGPU3D = tap3(-1, -1, -1) | tap3(-1, -1, 1) | tap3(-1, 0, 1) | tap3(-1, 1, 1) |
+                                  tap3(0, -1, 0) | tap3(0, 0, 0) | tap3(0, 1, 0) | tap3(1, -1, -1) |
+                                  tap3(1, -1, 1) | tap3(1, 0, 1) | tap3(1, 1, 1);
+
+template <int NJT, int OROWS, int WPR, uint32_t MASK>
+cudaError_t launch_march(const float* A, float* B, int ni, int nrow, int ncol, const W27x2& w, cudaStream_t s) {
+  using M = March<NJT, OROWS, WPR>;
+  auto kern = march_kernel<NJT, OROWS, WPR, MASK>;
+  cudaError_t e = ensure_smem<march_kernel<NJT, OROWS, WPR, MASK>>(M::SMEM);
+  if (e != cudaSuccess) return e;
+  static int per_sm = 0;  // resident CTAs per SM (same on every B200)
+  if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, M::THREADS, M::SMEM) != cudaSuccess ||
+                  per_sm <= 0))
+    per_sm = 4;
+  const int ncc = (ncol + M::TC - 1) / M::TC;
+  const int nrg = (nrow + OROWS - 1) / OROWS;
+  const long long tiles = (long long)ncc * nrg;
+  const int interior = ni - 2;
+  // segments of the march: ~2 waves of resident CTAs (each segment re-reads 2 halo planes)
+  const long long want = (long long)sm_count() * per_sm * 2;
+  long long nseg = (want + tiles - 1) / tiles;
+  if (nseg > interior) nseg = interior;
+  if (nseg < 1) nseg = 1;
+  const int seg = (int)((interior + nseg - 1) / nseg);
+  nseg = (interior + seg - 1) / seg;
+  return launch_pdl(kern, dim3((unsigned)(tiles * nseg)), dim3(M::THREADS), M::SMEM, s, A, B, ni, nrow, ncol, seg,
+                    ncc, nrg, w);
 }
 
 // ============================================================== fdtd-2d
@@ -313,54 +318,23 @@ __global__ void __launch_bounds__(256) fdtd_step_kernel(const float* __restrict_
 
 cudaError_t launch_conv2d(const float* A, float* B, int ni, int nj, const float* w9, cudaStream_t s, int* launches) {
   if (ni < 3 || nj < 3) return cudaSuccess;  // no interior
-  W9 w;
-  for (int e = 0; e < 9; ++e) w.w[e] = w9[e];
-  const int nchunks = (nj + 127) / 128;
-  const int interior = ni - 2;
-  // strips so that the warp units fill the resident warps about once
-  static int per_sm = 0;  // resident CTAs per SM (same on every B200)
-  if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv2d_kernel, 32 * C2_WARPS, 0) !=
-                      cudaSuccess || per_sm <= 0))
-    per_sm = 4;
-  const long long resident = (long long)sm_count() * per_sm * C2_WARPS;
-  long long strips = (resident + nchunks - 1) / nchunks;
-  if (strips > interior) strips = interior;
-  int R = (int)((interior + strips - 1) / strips);
-  R = (R + C2_U - 1) / C2_U * C2_U;
-  strips = (interior + R - 1) / R;
-  const long long units = strips * nchunks;
-  const unsigned grid = (unsigned)((units + C2_WARPS - 1) / C2_WARPS);
+  W27x2 w = {};
+  for (int e = 0; e < 9; ++e) w.w[e] = make_float2(w9[e], w9[e]);
   ++*launches;
-  return launch_pdl(conv2d_kernel, dim3(grid), dim3(32 * C2_WARPS), 0, s, A, B, ni, nj, R, nchunks, units, w);
+  // 2-D: the march axis is i, the stencil's column axis j is the tile's column axis
+  // (no tile rows), taps w[(di+1)*3 + (dj+1)]
+  return launch_march<1, 1, 8, MASK_DENSE9>(A, B, ni, 1, nj, w, s);
 }
 
 cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, const float* w27, cudaStream_t s,
                           int* launches) {
   if (ni < 3 || nj < 3 || nk < 3) return cudaSuccess;
-  W27 w;
-  for (int e = 0; e < 27; ++e) w.w[e] = w27[e];
-  const size_t smem = (size_t)C3_STAGES * C3_TILE * sizeof(float) + C3_STAGES * sizeof(uint64_t);
-  cudaError_t e = ensure_smem<conv3d_kernel>(smem);
-  if (e != cudaSuccess) return e;
-  const int nkc = (nk + 127) / 128;
-  const int njg = (nj + C3_ROWS - 1) / C3_ROWS;
-  const long long tiles = (long long)nkc * njg;
-  const int interior = ni - 2;
-  // segments of the i march: enough CTAs for ~4 waves
-  static int per_sm = 0;
-  if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv3d_kernel, 32 * C3_ROWS, smem) !=
-                      cudaSuccess || per_sm <= 0))
-    per_sm = 4;
-  const long long want = (long long)sm_count() * per_sm * 4;
-  long long nseg = (want + tiles - 1) / tiles;
-  if (nseg > interior) nseg = interior;
-  if (nseg < 1) nseg = 1;
-  const int seg = (int)((interior + nseg - 1) / nseg);
-  nseg = (interior + seg - 1) / seg;
-  const long long grid = tiles * nseg;
+  W27x2 w;
+  for (int e = 0; e < 27; ++e) w.w[e] = make_float2(w27[e], w27[e]);
   ++*launches;
-  return launch_pdl(conv3d_kernel, dim3((unsigned)grid), dim3(32 * C3_ROWS), smem, s, A, B, ni, nj, nk, seg, nkc,
-                    njg, w);
+  const uint32_t m = weight_mask(w27, 27);
+  if ((m & ~MASK_PBGPU3D) == 0) return launch_march<3, 8, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s);
+  return launch_march<3, 8, 1, MASK_DENSE>(A, B, ni, nj, nk, w, s);
 }
 
 size_t fdtd_ws_bytes(int nx, int ny) { return 3 * align_up((size_t)nx * ny * sizeof(float), 256); }
