@@ -27,6 +27,7 @@
 //           neighbours).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "pb_device.cuh"
 #include "pb_internal.h"
@@ -53,41 +54,66 @@ struct W27x2 {
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // a*b + c, two RN FMAs
   unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;"
       : "=l"(d)
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
   return *reinterpret_cast<float2*>(&d);
 }
 
-constexpr int ST_STAGES = 6;
+
+// 1-D bulk copy with an L2 eviction-priority hint (policy from createpolicy).
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t p = 0;
+  if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 template <int NJT, int OROWS, int WPR>
 struct March {
+  static constexpr int STAGES = NJT == 1 ? 6 : 12;  // planes in flight (Little's law: ~100+ KB per SM)
   static constexpr int TC = 128 * WPR;               // tile columns
   static constexpr int TROWS = OROWS + NJT - 1;      // staged rows per plane
   static constexpr int PITCH = TC + 8;               // [3] left halo, [4, 4+TC) values, [4+TC] right halo
   static constexpr int TILE = TROWS * PITCH;         // floats per stage
-  static constexpr int THREADS = 32 * OROWS * WPR;
-  static constexpr size_t SMEM = (size_t)ST_STAGES * TILE * sizeof(float) + ST_STAGES * sizeof(uint64_t);
+  static constexpr int THREADS = 32 * (OROWS * WPR + 1);  // + one producer warp
+  static constexpr size_t SMEM = (size_t)STAGES * TILE * sizeof(float) + 2 * STAGES * sizeof(uint64_t);
 };
 
 // One plane q of the march (rows j0-(NJT>1) .. +TROWS, columns c0-4 .. c0+TC+4,
-// clipped to the array) -> ring buffer `buf`, tx bytes on `bar` (one thread).
+// clipped to the array) -> ring buffer `buf`, tx bytes on `bar`. Called by the whole
+// producer warp: lane 0 posts the byte count, lane r copies tile row r.
 template <int NJT, int OROWS, int WPR>
 __device__ __forceinline__ void march_issue(const float* A, float* buf, uint64_t* bar, int q, int j0, int c0,
-                                            int nrow, int ncol) {
+                                            int nrow, int ncol, int hint, uint64_t pol, int lane) {
   using M = March<NJT, OROWS, WPR>;
   const int ka = max(c0 - 4, 0);
   const int kb = min(c0 + M::TC + 4, ncol);
+  const int jb = j0 - (NJT > 1 ? 1 : 0);  // global row of tile row 0
+  const int jlo = max(jb, 0);
+  const int jhi = min(jb + M::TROWS, nrow);
   const uint32_t row_bytes = (uint32_t)(kb - ka) * 4u;
-  const int jlo = max(j0 - (NJT > 1 ? 1 : 0), 0);
-  const int jhi = min(j0 - (NJT > 1 ? 1 : 0) + M::TROWS, nrow);
-  mbar_arrive_expect_tx(bar, row_bytes * (uint32_t)(jhi - jlo));
-#pragma unroll 1
-  for (int jj = jlo; jj < jhi; ++jj) {
-    const int r = jj - (j0 - (NJT > 1 ? 1 : 0));
-    bulk_g2s(buf + r * M::PITCH + 4 + (ka - c0), A + ((size_t)q * nrow + jj) * ncol + ka, row_bytes, bar);
+  if (lane == 0) mbar_arrive_expect_tx(bar, row_bytes * (uint32_t)(jhi - jlo));
+  __syncwarp();
+  const int jj = jb + lane;
+  if (lane < M::TROWS && jj >= jlo && jj < jhi) {
+    float* dst = buf + lane * M::PITCH + 4 + (ka - c0);
+    const float* src = A + ((size_t)q * nrow + jj) * ncol + ka;
+    if (hint)
+      bulk_g2s_hint(dst, src, row_bytes, bar, pol);
+    else
+      bulk_g2s(dst, src, row_bytes, bar);
   }
 }
 
@@ -142,17 +168,25 @@ __device__ __forceinline__ void march_taps(float2 (&am)[2], float2 (&a0)[2], flo
 
 // Work unit = (column chunk cc, row group rg, segment sg of output planes [o0, o1)).
 // nrow = 1 for 2-D (the march axis is the row index; columns are the stencil's j).
+// Warps 0..OROWS*WPR-1 compute; the last warp only issues the bulk copies. Stage s is
+// handed over by full[s] (tx bytes) and released by empty[s] (one arrive per compute
+// warp): no CTA-wide barrier inside the march.
 template <int NJT, int OROWS, int WPR, uint32_t MASK>
-__global__ void __launch_bounds__(32 * OROWS * WPR) march_kernel(const float* __restrict__ A, float* __restrict__ B,
-                                                                 int ni, int nrow, int ncol, int seg, int ncc,
-                                                                 int nrg, const __grid_constant__ W27x2 w) {
+__global__ void __launch_bounds__(32 * (OROWS * WPR + 1)) march_kernel(const float* __restrict__ A,
+                                                                       float* __restrict__ B, int ni, int nrow,
+                                                                       int ncol, int seg, int ncc, int nrg, int hint,
+                                                                       int order, const __grid_constant__ W27x2 w) {
   using M = March<NJT, OROWS, WPR>;
+  constexpr int CW = OROWS * WPR;  // compute warps
   extern __shared__ __align__(128) float st_smem[];
   float* tiles = st_smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(st_smem + ST_STAGES * M::TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(st_smem + M::STAGES * M::TILE);
+  uint64_t* empty = full + M::STAGES;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int cc = blockIdx.x % ncc;
-  const int rg = (blockIdx.x / ncc) % nrg;
+  // order 0: column chunks fastest; 1: row groups fastest (vertical neighbours, which
+  // share a halo row, are adjacent in launch order)
+  const int cc = order ? (blockIdx.x / nrg) % ncc : blockIdx.x % ncc;
+  const int rg = order ? blockIdx.x % nrg : (blockIdx.x / ncc) % nrg;
   const int sg = blockIdx.x / (ncc * nrg);
   const int c0 = cc * M::TC, j0 = rg * OROWS;
   const int o0 = 1 + sg * seg;
@@ -161,14 +195,23 @@ __global__ void __launch_bounds__(32 * OROWS * WPR) march_kernel(const float* __
   const int q0 = o0 - 1;
   const int nplanes = o1 + 1 - q0;  // planes [o0-1, o1]
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < M::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   pdl_wait();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST_STAGES && s < nplanes; ++s)
-      march_issue<NJT, OROWS, WPR>(A, tiles + s * M::TILE, &full[s], q0 + s, j0, c0, nrow, ncol);
+  if (wp == CW) {  // producer warp
+    const uint64_t pol = hint ? l2_policy(hint) : 0;
+#pragma unroll 1
+    for (int p = 0; p < nplanes; ++p) {
+      const int s = p % M::STAGES;
+      if (p >= M::STAGES) mbar_wait(&empty[s], (uint32_t)(((p / M::STAGES) - 1) & 1));
+      march_issue<NJT, OROWS, WPR>(A, tiles + s * M::TILE, &full[s], q0 + p, j0, c0, nrow, ncol, hint, pol, lane);
+    }
+    return;
   }
   const int tr = wp / WPR;                         // output row within the tile
   const int col = (wp % WPR) * 128 + 4 * lane;     // column offset within the tile
@@ -179,16 +222,15 @@ __global__ void __launch_bounds__(32 * OROWS * WPR) march_kernel(const float* __
   for (int r = 0; r < 3; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
 
   auto step = [&](int p, float2(&am)[2], float2(&a0)[2], float2(&ap)[2]) {
-    const int s = p % ST_STAGES;
-    mbar_wait(&full[s], (uint32_t)((p / ST_STAGES) & 1));
+    const int s = p % M::STAGES;
+    mbar_wait(&full[s], (uint32_t)((p / M::STAGES) & 1));
     const float* t = tiles + s * M::TILE + tr * M::PITCH + 4 + col;
     Pairs rows[NJT];
 #pragma unroll
     for (int dj = 0; dj < NJT; ++dj) rows[dj] = read_pairs(t + dj * M::PITCH);
     march_taps<NJT, MASK>(am, a0, ap, rows, w);
-    __syncthreads();  // every warp is done with stage s
-    if (threadIdx.x == 0 && p + ST_STAGES < nplanes)
-      march_issue<NJT, OROWS, WPR>(A, tiles + s * M::TILE, &full[s], q0 + p + ST_STAGES, j0, c0, nrow, ncol);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
     if (p >= 2 && store_ok)  // output plane q-1 is complete
       store4_interior(B + ((size_t)(q0 + p - 1) * nrow + (NJT > 1 ? j : 0)) * ncol, k, 1, ncol - 2, am[0], am[1]);
     am[0] = am[1] = make_float2(0.f, 0.f);  // becomes the next plane's q+1 accumulator
@@ -241,8 +283,10 @@ cudaError_t launch_march(const float* A, float* B, int ni, int nrow, int ncol, c
   if (nseg < 1) nseg = 1;
   const int seg = (int)((interior + nseg - 1) / nseg);
   nseg = (interior + seg - 1) / seg;
+  static const int hint = getenv("PB_ST_L2") ? atoi(getenv("PB_ST_L2")) : 0;        // tuning aid
+  static const int order = getenv("PB_ST_ORDER") ? atoi(getenv("PB_ST_ORDER")) : 0;  // tuning aid
   return launch_pdl(kern, dim3((unsigned)(tiles * nseg)), dim3(M::THREADS), M::SMEM, s, A, B, ni, nrow, ncol, seg,
-                    ncc, nrg, w);
+                    ncc, nrg, hint, order, w);
 }
 
 // ============================================================== fdtd-2d
@@ -333,7 +377,10 @@ cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, cons
   for (int e = 0; e < 27; ++e) w.w[e] = make_float2(w27[e], w27[e]);
   ++*launches;
   const uint32_t m = weight_mask(w27, 27);
-  if ((m & ~MASK_PBGPU3D) == 0) return launch_march<3, 8, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s);
+  static const int rows16 = getenv("PB_C3_ROWS") && atoi(getenv("PB_C3_ROWS")) == 16;  // tuning aid
+  if ((m & ~MASK_PBGPU3D) == 0)
+    return rows16 ? launch_march<3, 16, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s)
+                  : launch_march<3, 8, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s);
   return launch_march<3, 8, 1, MASK_DENSE>(A, B, ni, nj, nk, w, s);
 }
 
