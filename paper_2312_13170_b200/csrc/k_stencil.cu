@@ -29,6 +29,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "pb_device.cuh"
 #include "pb_internal.h"
 
@@ -358,6 +360,183 @@ __global__ void __launch_bounds__(256) fdtd_step_kernel(const float* __restrict_
   pdl_trigger();
 }
 
+
+// ---- persistent variant: the whole state lives in shared memory --------------
+// One CTA per FT_I x FT_J tile (cooperative launch: every tile co-resident). Each
+// step a tile publishes its OLD edge values (hz top/bottom rows and left/right
+// columns, ey top row, ex left column) to a parity-double-buffered halo area in
+// global memory (L2), releases its step flag, acquires its (up to 4) neighbours'
+// flags, reads their halos and updates its points in place (new values computed
+// into registers from the old state, CTA barrier, then stored). HBM sees the state
+// once in and once out; a step costs one neighbour flag round trip through L2
+// instead of a kernel launch.
+constexpr int FT_I = 64, FT_J = 128, FT_THREADS = 512;
+constexpr int FT_G = FT_I * FT_J / 4 / FT_THREADS;  // float4 groups per thread (4)
+constexpr int FT_HALO = 3 * FT_J + 3 * FT_I;          // floats per tile per parity
+struct FtHalo {  // offsets into a tile's halo slot
+  static constexpr int TOP_HZ = 0, TOP_EY = FT_J, BOT_HZ = 2 * FT_J, LEFT_HZ = 3 * FT_J, LEFT_EX = 3 * FT_J + FT_I,
+                       RIGHT_HZ = 3 * FT_J + 2 * FT_I;
+};
+
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(FT_THREADS, 1) fdtd_persist_kernel(float* __restrict__ ex, float* __restrict__ ey,
+                                                                     float* __restrict__ hz,
+                                                                     const float* __restrict__ fict, int tmax, int nx,
+                                                                     int ny, int tiles_j, float* __restrict__ halo,
+                                                                     unsigned* __restrict__ flags) {
+  extern __shared__ __align__(16) float ft_smem[];
+  float* sx = ft_smem;                 // ex [FT_I][FT_J]
+  float* sy = sx + FT_I * FT_J;        // ey
+  float* sh = sy + FT_I * FT_J;        // hz
+  float* h_up = sh + FT_I * FT_J;      // hz[i0-1][*]
+  float* h_dn = h_up + FT_J;           // hz[i1][*]
+  float* y_dn = h_dn + FT_J;           // ey[i1][*]
+  float* h_lf = y_dn + FT_J;           // hz[*][j0-1]
+  float* h_rt = h_lf + FT_I;           // hz[*][j1]
+  float* x_rt = h_rt + FT_I;           // ex[*][j1]
+  const int ti = blockIdx.x / tiles_j, tj = blockIdx.x % tiles_j;
+  const int tiles_i = gridDim.x / tiles_j;
+  const int i0 = ti * FT_I, j0 = tj * FT_J;
+  const int ri = min(FT_I, nx - i0), rj = min(FT_J, ny - j0);  // valid extent (rj % 4 == 0)
+  const int tid = threadIdx.x;
+  pdl_wait();
+  // load the tile
+  for (int g = tid; g < FT_I * FT_J / 4; g += FT_THREADS) {
+    const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
+    if (r < ri && c < rj) {
+      const size_t e = (size_t)(i0 + r) * ny + j0 + c;
+      *reinterpret_cast<float4*>(sx + r * FT_J + c) = *reinterpret_cast<const float4*>(ex + e);
+      *reinterpret_cast<float4*>(sy + r * FT_J + c) = *reinterpret_cast<const float4*>(ey + e);
+      *reinterpret_cast<float4*>(sh + r * FT_J + c) = *reinterpret_cast<const float4*>(hz + e);
+    }
+  }
+  __syncthreads();
+  const bool has_up = ti > 0, has_dn = ti + 1 < tiles_i, has_lf = tj > 0, has_rt = tj + 1 < tiles_j;
+  for (int t = 0; t < tmax; ++t) {
+    // 1. publish the old edges (parity t&1), release flag = t+1
+    float* mine = halo + ((size_t)(t & 1) * gridDim.x + blockIdx.x) * FT_HALO;
+    for (int c = tid; c < rj; c += FT_THREADS) {
+      mine[FtHalo::TOP_HZ + c] = sh[c];
+      mine[FtHalo::TOP_EY + c] = sy[c];
+      mine[FtHalo::BOT_HZ + c] = sh[(ri - 1) * FT_J + c];
+    }
+    for (int r = tid; r < ri; r += FT_THREADS) {
+      mine[FtHalo::LEFT_HZ + r] = sh[r * FT_J];
+      mine[FtHalo::LEFT_EX + r] = sx[r * FT_J];
+      mine[FtHalo::RIGHT_HZ + r] = sh[r * FT_J + rj - 1];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_rel(&flags[blockIdx.x], (unsigned)(t + 1));
+    }
+    // 2. acquire the neighbours' step-t edges (lanes 0..3 of warp 0 poll one neighbour each)
+    if (tid < 4) {
+      const bool need = (tid == 0 && has_up) || (tid == 1 && has_dn) || (tid == 2 && has_lf) || (tid == 3 && has_rt);
+      const int nb = tid == 0 ? blockIdx.x - tiles_j : tid == 1 ? blockIdx.x + tiles_j : tid == 2 ? blockIdx.x - 1
+                                                                                                   : blockIdx.x + 1;
+      if (need) {
+        unsigned long long spins = 0;
+        while (ld_acq(&flags[nb]) < (unsigned)(t + 1)) {
+          if (++spins > (1ull << 30)) asm volatile("trap;");
+        }
+      }
+    }
+    __syncthreads();
+    const float* hb = halo + (size_t)(t & 1) * gridDim.x * FT_HALO;
+    for (int c = tid; c < rj; c += FT_THREADS) {
+      h_up[c] = has_up ? __ldcg(hb + (size_t)(blockIdx.x - tiles_j) * FT_HALO + FtHalo::BOT_HZ + c) : 0.f;
+      h_dn[c] = has_dn ? __ldcg(hb + (size_t)(blockIdx.x + tiles_j) * FT_HALO + FtHalo::TOP_HZ + c) : 0.f;
+      y_dn[c] = has_dn ? __ldcg(hb + (size_t)(blockIdx.x + tiles_j) * FT_HALO + FtHalo::TOP_EY + c) : 0.f;
+    }
+    for (int r = tid; r < ri; r += FT_THREADS) {
+      h_lf[r] = has_lf ? __ldcg(hb + (size_t)(blockIdx.x - 1) * FT_HALO + FtHalo::RIGHT_HZ + r) : 0.f;
+      h_rt[r] = has_rt ? __ldcg(hb + (size_t)(blockIdx.x + 1) * FT_HALO + FtHalo::LEFT_HZ + r) : 0.f;
+      x_rt[r] = has_rt ? __ldcg(hb + (size_t)(blockIdx.x + 1) * FT_HALO + FtHalo::LEFT_EX + r) : 0.f;
+    }
+    __syncthreads();
+    // 3. new values of this thread's groups from the old state
+    float4 nxv[FT_G], nyv[FT_G], nhv[FT_G];
+    const float f = fict[t];
+#pragma unroll
+    for (int u = 0; u < FT_G; ++u) {
+      const int g = tid + u * FT_THREADS;
+      const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
+      if (r >= ri || c >= rj) continue;
+      const int i = i0 + r, j = j0 + c;
+      const float4 h = *reinterpret_cast<const float4*>(sh + r * FT_J + c);
+      const float4 x = *reinterpret_cast<const float4*>(sx + r * FT_J + c);
+      const float4 y = *reinterpret_cast<const float4*>(sy + r * FT_J + c);
+      const float hl = (c > 0) ? sh[r * FT_J + c - 1] : h_lf[r];
+      const bool last_col = (j + 4 >= ny);
+      const bool tile_rt = (c + 4 >= rj);
+      const float hr = last_col ? 0.f : (tile_rt ? h_rt[r] : sh[r * FT_J + c + 4]);
+      const float xr = last_col ? 0.f : (tile_rt ? x_rt[r] : sx[r * FT_J + c + 4]);
+      float4 yn;
+      if (i == 0) {
+        yn = make_float4(f, f, f, f);
+      } else {
+        const float4 hu = (r > 0) ? *reinterpret_cast<const float4*>(sh + (r - 1) * FT_J + c)
+                                  : *reinterpret_cast<const float4*>(h_up + c);
+        yn = make_float4(ey_upd(y.x, h.x, hu.x), ey_upd(y.y, h.y, hu.y), ey_upd(y.z, h.z, hu.z),
+                         ey_upd(y.w, h.w, hu.w));
+      }
+      float4 xn;
+      xn.x = (j == 0) ? x.x : ex_upd(x.x, h.x, hl);
+      xn.y = ex_upd(x.y, h.y, h.x);
+      xn.z = ex_upd(x.z, h.z, h.y);
+      xn.w = ex_upd(x.w, h.w, h.z);
+      float4 hn = h;
+      if (i < nx - 1) {
+        const bool tile_dn = (r + 1 >= ri);
+        const float4 yd = tile_dn ? *reinterpret_cast<const float4*>(y_dn + c)
+                                  : *reinterpret_cast<const float4*>(sy + (r + 1) * FT_J + c);
+        const float4 hd = tile_dn ? *reinterpret_cast<const float4*>(h_dn + c)
+                                  : *reinterpret_cast<const float4*>(sh + (r + 1) * FT_J + c);
+        const float4 ydn = make_float4(ey_upd(yd.x, hd.x, h.x), ey_upd(yd.y, hd.y, h.y), ey_upd(yd.z, hd.z, h.z),
+                                       ey_upd(yd.w, hd.w, h.w));
+        const float xrn = last_col ? 0.f : ex_upd(xr, hr, h.w);
+        hn.x = hz_upd(h.x, xn.y, xn.x, ydn.x, yn.x);
+        hn.y = hz_upd(h.y, xn.z, xn.y, ydn.y, yn.y);
+        hn.z = hz_upd(h.z, xn.w, xn.z, ydn.z, yn.z);
+        if (!last_col) hn.w = hz_upd(h.w, xrn, xn.w, ydn.w, yn.w);
+      }
+      nxv[u] = xn;
+      nyv[u] = yn;
+      nhv[u] = hn;
+    }
+    __syncthreads();  // every thread has read the old state
+#pragma unroll
+    for (int u = 0; u < FT_G; ++u) {
+      const int g = tid + u * FT_THREADS;
+      const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
+      if (r >= ri || c >= rj) continue;
+      *reinterpret_cast<float4*>(sx + r * FT_J + c) = nxv[u];
+      *reinterpret_cast<float4*>(sy + r * FT_J + c) = nyv[u];
+      *reinterpret_cast<float4*>(sh + r * FT_J + c) = nhv[u];
+    }
+    __syncthreads();
+  }
+  // write the tile back
+  for (int g = tid; g < FT_I * FT_J / 4; g += FT_THREADS) {
+    const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
+    if (r < ri && c < rj) {
+      const size_t e = (size_t)(i0 + r) * ny + j0 + c;
+      *reinterpret_cast<float4*>(ex + e) = *reinterpret_cast<const float4*>(sx + r * FT_J + c);
+      *reinterpret_cast<float4*>(ey + e) = *reinterpret_cast<const float4*>(sy + r * FT_J + c);
+      *reinterpret_cast<float4*>(hz + e) = *reinterpret_cast<const float4*>(sh + r * FT_J + c);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_conv2d(const float* A, float* B, int ni, int nj, const float* w9, cudaStream_t s, int* launches) {
@@ -384,10 +563,44 @@ cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, cons
   return launch_march<3, 8, 1, MASK_DENSE>(A, B, ni, nj, nk, w, s);
 }
 
-size_t fdtd_ws_bytes(int nx, int ny) { return 3 * align_up((size_t)nx * ny * sizeof(float), 256); }
+namespace {
+constexpr size_t FT_SMEM = (size_t)(3 * FT_I * FT_J + 3 * FT_J + 3 * FT_I) * sizeof(float);
+size_t fdtd_persist_ws(int nx, int ny) {
+  const size_t tiles = (size_t)((nx + FT_I - 1) / FT_I) * ((ny + FT_J - 1) / FT_J);
+  return align_up(2 * tiles * FT_HALO * sizeof(float), 256) + align_up(tiles * sizeof(unsigned), 256);
+}
+}  // namespace
+
+size_t fdtd_ws_bytes(int nx, int ny) {
+  return std::max(3 * align_up((size_t)nx * ny * sizeof(float), 256), fdtd_persist_ws(nx, ny));
+}
 
 cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                           cudaStream_t s, int* launches) {
+  // Persistent path when every tile fits on the GPU at once (one 98 KB CTA per SM).
+  static const int force_steps = getenv("PB_FDTD_STEPS") && atoi(getenv("PB_FDTD_STEPS")) == 1;  // tuning aid
+  const int tiles_i = (nx + FT_I - 1) / FT_I, tiles_j = (ny + FT_J - 1) / FT_J;
+  if (!force_steps && tmax > 0 && tiles_i * tiles_j <= sm_count()) {
+    cudaError_t e = ensure_smem<fdtd_persist_kernel>(FT_SMEM);
+    if (e != cudaSuccess) return e;
+    const int tiles = tiles_i * tiles_j;
+    float* halo = static_cast<float*>(ws);
+    unsigned* flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) +
+                                                  align_up(2 * (size_t)tiles * FT_HALO * sizeof(float), 256));
+    if ((e = cudaMemsetAsync(flags, 0, tiles * sizeof(unsigned), s)) != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tiles);
+    cfg.blockDim = dim3(FT_THREADS);
+    cfg.dynamicSmemBytes = FT_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // all tiles co-resident: the flag waits are safe
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ++*launches;
+    return cudaLaunchKernelEx(&cfg, fdtd_persist_kernel, ex, ey, hz, fict, tmax, nx, ny, tiles_j, halo, flags);
+  }
   const size_t plane = align_up((size_t)nx * ny * sizeof(float), 256);
   float* wex = static_cast<float*>(ws);
   float* wey = reinterpret_cast<float*>(static_cast<char*>(ws) + plane);

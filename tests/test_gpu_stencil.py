@@ -50,6 +50,13 @@ def test_fdtd2d(nx, ny, tmax):
     _ok(P.check_fdtd2d(nx, ny, tmax))
 
 
+def test_fdtd2d_per_step_path():
+    """More tiles than SMs: the one-launch-per-step kernel (ping-pong through the workspace)."""
+    r = P.check_fdtd2d(2048, 2052, 5)
+    _ok(r)
+    assert r["bitwise_f32"]
+
+
 def test_fdtd2d_zero_steps_is_identity():
     ex, ey, hz, f = P.fdtd_inputs(16, 20, 0)
     d = [P.dev(a) for a in (ex, ey, hz)]
