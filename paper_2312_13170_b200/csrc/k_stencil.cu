@@ -30,6 +30,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "pb_device.cuh"
 #include "pb_internal.h"
@@ -278,11 +279,23 @@ cudaError_t launch_march(const float* A, float* B, int ni, int nrow, int ncol, c
   const int nrg = (nrow + OROWS - 1) / OROWS;
   const long long tiles = (long long)ncc * nrg;
   const int interior = ni - 2;
-  // segments of the march: ~2 waves of resident CTAs (each segment re-reads 2 halo planes)
-  const long long want = (long long)sm_count() * per_sm * 2;
-  long long nseg = (want + tiles - 1) / tiles;
-  if (nseg > interior) nseg = interior;
-  if (nseg < 1) nseg = 1;
+  // Segments of the march: the CTA count tiles*nseg should fill whole waves of the
+  // resident slots (a last wave 30% full costs a third of the run), and each segment
+  // re-reads 2 halo planes. Score = wave efficiency x seg / (seg + 2).
+  // (2-D: measured best with ~2 waves of long segments; the HBM stream, not the wave
+  // tail, bounds it there.)
+  const long long slots = (long long)sm_count() * per_sm;
+  long long nseg = 1;
+  double best = -1.0;
+  for (long long c = 1; NJT > 1 && c <= 2048 && c <= interior; ++c) {
+    const int sgl = (int)((interior + c - 1) / c);
+    const long long cnt = tiles * ((interior + sgl - 1) / sgl);
+    const double waves = (double)cnt / (double)slots;
+    const double eff = waves / std::ceil(waves);
+    const double score = eff * sgl / (sgl + 2.0);
+    if (score > best + 1e-9) { best = score; nseg = c; }
+  }
+  if (NJT == 1) nseg = std::max(1ll, std::min<long long>(interior, (2 * slots + tiles - 1) / tiles));
   const int seg = (int)((interior + nseg - 1) / nseg);
   nseg = (interior + seg - 1) / seg;
   static const int hint = getenv("PB_ST_L2") ? atoi(getenv("PB_ST_L2")) : 0;        // tuning aid
