@@ -374,22 +374,22 @@ __global__ void __launch_bounds__(256) fdtd_step_kernel(const float* __restrict_
 }
 
 
-// ---- persistent variant: the whole state lives in shared memory --------------
-// One CTA per FT_I x FT_J tile (cooperative launch: every tile co-resident). Each
-// step a tile publishes its OLD edge values (hz top/bottom rows and left/right
-// columns, ey top row, ex left column) to a parity-double-buffered halo area in
-// global memory (L2), releases its step flag, acquires its (up to 4) neighbours'
-// flags, reads their halos and updates its points in place (new values computed
-// into registers from the old state, CTA barrier, then stored). HBM sees the state
-// once in and once out; a step costs one neighbour flag round trip through L2
-// instead of a kernel launch.
-constexpr int FT_I = 64, FT_J = 128, FT_THREADS = 512;
-constexpr int FT_G = FT_I * FT_J / 4 / FT_THREADS;  // float4 groups per thread (4)
-constexpr int FT_HALO = 3 * FT_J + 3 * FT_I;          // floats per tile per parity
-struct FtHalo {  // offsets into a tile's halo slot
-  static constexpr int TOP_HZ = 0, TOP_EY = FT_J, BOT_HZ = 2 * FT_J, LEFT_HZ = 3 * FT_J, LEFT_EX = 3 * FT_J + FT_I,
-                       RIGHT_HZ = 3 * FT_J + 2 * FT_I;
-};
+// ---- persistent, temporally blocked variant ------------------------------------
+// One CTA per FT_I x FT_J core tile (cooperative launch: every tile co-resident).
+// A tile keeps its core plus an FT_H-wide halo of all three fields in shared memory
+// and advances FT_H steps on that region without talking to anyone: values near
+// the region's edge go stale (each step reads old neighbours one row/column out),
+// but the staleness moves inward one point per step, so after FT_H steps the core
+// is still exact. Then the tiles exchange: each publishes its core into a
+// parity-double-buffered copy of the grid in global memory (L2-resident), releases
+// its epoch flag, acquires its 8 neighbours' flags and reloads its region. HBM sees
+// the state once in and once out; one neighbour round trip through L2 per FT_H steps
+// replaces FT_H kernel launches. Every update is the PolyBench statement's fp32
+// operations, so the result is bitwise the sequential sweeps'.
+constexpr int FT_I = 64, FT_J = 128, FT_H = 8, FT_THREADS = 512;
+constexpr int FT_RI = FT_I + 2 * FT_H, FT_RJ = FT_J + 2 * FT_H;  // region 80 x 144
+constexpr int FT_GROUPS = FT_RI * FT_RJ / 4;
+constexpr int FT_G = (FT_GROUPS + FT_THREADS - 1) / FT_THREADS;  // float4 groups per thread (6)
 
 __device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
   unsigned v;
@@ -400,152 +400,155 @@ __device__ __forceinline__ void st_rel(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(FT_THREADS, 1) fdtd_persist_kernel(float* __restrict__ ex, float* __restrict__ ey,
-                                                                     float* __restrict__ hz,
-                                                                     const float* __restrict__ fict, int tmax, int nx,
-                                                                     int ny, int tiles_j, float* __restrict__ halo,
-                                                                     unsigned* __restrict__ flags) {
-  extern __shared__ __align__(16) float ft_smem[];
-  float* sx = ft_smem;                 // ex [FT_I][FT_J]
-  float* sy = sx + FT_I * FT_J;        // ey
-  float* sh = sy + FT_I * FT_J;        // hz
-  float* h_up = sh + FT_I * FT_J;      // hz[i0-1][*]
-  float* h_dn = h_up + FT_J;           // hz[i1][*]
-  float* y_dn = h_dn + FT_J;           // ey[i1][*]
-  float* h_lf = y_dn + FT_J;           // hz[*][j0-1]
-  float* h_rt = h_lf + FT_I;           // hz[*][j1]
-  float* x_rt = h_rt + FT_I;           // ex[*][j1]
-  const int ti = blockIdx.x / tiles_j, tj = blockIdx.x % tiles_j;
-  const int tiles_i = gridDim.x / tiles_j;
-  const int i0 = ti * FT_I, j0 = tj * FT_J;
-  const int ri = min(FT_I, nx - i0), rj = min(FT_J, ny - j0);  // valid extent (rj % 4 == 0)
+// Waits until every existing neighbour (8-neighbourhood) has flag >= v.
+__device__ __forceinline__ void ft_wait_neighbours(const unsigned* flags, int ti, int tj, int tiles_i, int tiles_j,
+                                                   unsigned v) {
   const int tid = threadIdx.x;
-  pdl_wait();
-  // load the tile
-  for (int g = tid; g < FT_I * FT_J / 4; g += FT_THREADS) {
-    const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
-    if (r < ri && c < rj) {
-      const size_t e = (size_t)(i0 + r) * ny + j0 + c;
-      *reinterpret_cast<float4*>(sx + r * FT_J + c) = *reinterpret_cast<const float4*>(ex + e);
-      *reinterpret_cast<float4*>(sy + r * FT_J + c) = *reinterpret_cast<const float4*>(ey + e);
-      *reinterpret_cast<float4*>(sh + r * FT_J + c) = *reinterpret_cast<const float4*>(hz + e);
+  if (tid < 9 && tid != 4) {
+    const int ni = ti + tid / 3 - 1, nj = tj + tid % 3 - 1;
+    if (ni >= 0 && ni < tiles_i && nj >= 0 && nj < tiles_j) {
+      unsigned long long spins = 0;
+      while (ld_acq(&flags[ni * tiles_j + nj]) < v) {
+        if (++spins > (1ull << 30)) asm volatile("trap;");
+      }
     }
   }
   __syncthreads();
-  const bool has_up = ti > 0, has_dn = ti + 1 < tiles_i, has_lf = tj > 0, has_rt = tj + 1 < tiles_j;
-  for (int t = 0; t < tmax; ++t) {
-    // 1. publish the old edges (parity t&1), release flag = t+1
-    float* mine = halo + ((size_t)(t & 1) * gridDim.x + blockIdx.x) * FT_HALO;
-    for (int c = tid; c < rj; c += FT_THREADS) {
-      mine[FtHalo::TOP_HZ + c] = sh[c];
-      mine[FtHalo::TOP_EY + c] = sy[c];
-      mine[FtHalo::BOT_HZ + c] = sh[(ri - 1) * FT_J + c];
-    }
-    for (int r = tid; r < ri; r += FT_THREADS) {
-      mine[FtHalo::LEFT_HZ + r] = sh[r * FT_J];
-      mine[FtHalo::LEFT_EX + r] = sx[r * FT_J];
-      mine[FtHalo::RIGHT_HZ + r] = sh[r * FT_J + rj - 1];
+}
+
+__global__ void __launch_bounds__(FT_THREADS, 1) fdtd_persist_kernel(float* __restrict__ ex, float* __restrict__ ey,
+                                                                     float* __restrict__ hz,
+                                                                     const float* __restrict__ fict, int tmax, int nx,
+                                                                     int ny, int tiles_j, float* __restrict__ grid2,
+                                                                     unsigned* __restrict__ flags) {
+  extern __shared__ __align__(16) float ft_smem[];
+  float* sx = ft_smem;                  // ex [FT_RI][FT_RJ]
+  float* sy = sx + FT_RI * FT_RJ;       // ey
+  float* sh = sy + FT_RI * FT_RJ;       // hz
+  const int tiles_i = gridDim.x / tiles_j;
+  const int ti = blockIdx.x / tiles_j, tj = blockIdx.x % tiles_j;
+  const int i0 = ti * FT_I, j0 = tj * FT_J;  // core origin; region origin (i0 - H, j0 - H)
+  const int tid = threadIdx.x;
+  const size_t N = (size_t)nx * ny;
+  pdl_wait();
+  const int nep = (tmax + FT_H - 1) / FT_H;
+  for (int e = 0; e < nep; ++e) {
+    // 1. region <- the state after e*H steps (epoch 0: the caller's arrays)
+    const float* gx = e == 0 ? ex : grid2 + (size_t)(e & 1) * 3 * N;
+    const float* gy = e == 0 ? ey : gx + N;
+    const float* gh = e == 0 ? hz : gx + 2 * N;
+    if (e > 0) ft_wait_neighbours(flags, ti, tj, tiles_i, tiles_j, (unsigned)e);
+    for (int g = tid; g < FT_GROUPS; g += FT_THREADS) {
+      const int r = g / (FT_RJ / 4), c = (g % (FT_RJ / 4)) * 4;
+      const int i = i0 - FT_H + r, j = j0 - FT_H + c;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f), y = x, h = x;
+      if (i >= 0 && i < nx && j >= 0 && j < ny) {
+        const size_t o = (size_t)i * ny + j;
+        x = __ldcg(reinterpret_cast<const float4*>(gx + o));
+        y = __ldcg(reinterpret_cast<const float4*>(gy + o));
+        h = __ldcg(reinterpret_cast<const float4*>(gh + o));
+      }
+      *reinterpret_cast<float4*>(sx + r * FT_RJ + c) = x;
+      *reinterpret_cast<float4*>(sy + r * FT_RJ + c) = y;
+      *reinterpret_cast<float4*>(sh + r * FT_RJ + c) = h;
     }
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_rel(&flags[blockIdx.x], (unsigned)(t + 1));
-    }
-    // 2. acquire the neighbours' step-t edges (lanes 0..3 of warp 0 poll one neighbour each)
-    if (tid < 4) {
-      const bool need = (tid == 0 && has_up) || (tid == 1 && has_dn) || (tid == 2 && has_lf) || (tid == 3 && has_rt);
-      const int nb = tid == 0 ? blockIdx.x - tiles_j : tid == 1 ? blockIdx.x + tiles_j : tid == 2 ? blockIdx.x - 1
-                                                                                                   : blockIdx.x + 1;
-      if (need) {
-        unsigned long long spins = 0;
-        while (ld_acq(&flags[nb]) < (unsigned)(t + 1)) {
-          if (++spins > (1ull << 30)) asm volatile("trap;");
+    // 2. up to H steps on the region
+    const int t_end = min(tmax, (e + 1) * FT_H);
+    for (int t = e * FT_H; t < t_end; ++t) {
+      float4 nxv[FT_G], nyv[FT_G], nhv[FT_G];
+      const float f = __ldg(fict + t);
+#pragma unroll
+      for (int u = 0; u < FT_G; ++u) {
+        const int g = tid + u * FT_THREADS;
+        if (g >= FT_GROUPS) continue;
+        const int r = g / (FT_RJ / 4), c = (g % (FT_RJ / 4)) * 4;
+        const int i = i0 - FT_H + r, j = j0 - FT_H + c;
+        const float4 h = *reinterpret_cast<const float4*>(sh + r * FT_RJ + c);
+        const float4 x = *reinterpret_cast<const float4*>(sx + r * FT_RJ + c);
+        const float4 y = *reinterpret_cast<const float4*>(sy + r * FT_RJ + c);
+        nxv[u] = x;
+        nyv[u] = y;
+        nhv[u] = h;
+        if (i < 0 || i >= nx || j < 0 || j >= ny) continue;  // outside the grid: never read by grid points
+        // neighbours one out (clamped at the region edge: stale there, see above)
+        const int ru = max(r - 1, 0), rd = min(r + 1, FT_RI - 1);
+        const float hl = sh[r * FT_RJ + max(c - 1, 0)];
+        const bool last_col = (j + 4 >= ny);
+        const int cr = min(c + 4, FT_RJ - 1);
+        const float hr = sh[r * FT_RJ + cr];
+        const float xr = sx[r * FT_RJ + cr];
+        float4 yn;
+        if (i == 0) {
+          yn = make_float4(f, f, f, f);
+        } else {
+          const float4 hu = *reinterpret_cast<const float4*>(sh + ru * FT_RJ + c);
+          yn = make_float4(ey_upd(y.x, h.x, hu.x), ey_upd(y.y, h.y, hu.y), ey_upd(y.z, h.z, hu.z),
+                           ey_upd(y.w, h.w, hu.w));
         }
+        float4 xn;
+        xn.x = (j == 0) ? x.x : ex_upd(x.x, h.x, hl);
+        xn.y = ex_upd(x.y, h.y, h.x);
+        xn.z = ex_upd(x.z, h.z, h.y);
+        xn.w = ex_upd(x.w, h.w, h.z);
+        float4 hn = h;
+        if (i < nx - 1) {
+          const float4 yd = *reinterpret_cast<const float4*>(sy + rd * FT_RJ + c);
+          const float4 hd = *reinterpret_cast<const float4*>(sh + rd * FT_RJ + c);
+          const float4 ydn = make_float4(ey_upd(yd.x, hd.x, h.x), ey_upd(yd.y, hd.y, h.y), ey_upd(yd.z, hd.z, h.z),
+                                         ey_upd(yd.w, hd.w, h.w));
+          const float xrn = ex_upd(xr, hr, h.w);
+          hn.x = hz_upd(h.x, xn.y, xn.x, ydn.x, yn.x);
+          hn.y = hz_upd(h.y, xn.z, xn.y, ydn.y, yn.y);
+          hn.z = hz_upd(h.z, xn.w, xn.z, ydn.z, yn.z);
+          if (!last_col) hn.w = hz_upd(h.w, xrn, xn.w, ydn.w, yn.w);
+        }
+        nxv[u] = xn;
+        nyv[u] = yn;
+        nhv[u] = hn;
       }
-    }
-    __syncthreads();
-    const float* hb = halo + (size_t)(t & 1) * gridDim.x * FT_HALO;
-    for (int c = tid; c < rj; c += FT_THREADS) {
-      h_up[c] = has_up ? __ldcg(hb + (size_t)(blockIdx.x - tiles_j) * FT_HALO + FtHalo::BOT_HZ + c) : 0.f;
-      h_dn[c] = has_dn ? __ldcg(hb + (size_t)(blockIdx.x + tiles_j) * FT_HALO + FtHalo::TOP_HZ + c) : 0.f;
-      y_dn[c] = has_dn ? __ldcg(hb + (size_t)(blockIdx.x + tiles_j) * FT_HALO + FtHalo::TOP_EY + c) : 0.f;
-    }
-    for (int r = tid; r < ri; r += FT_THREADS) {
-      h_lf[r] = has_lf ? __ldcg(hb + (size_t)(blockIdx.x - 1) * FT_HALO + FtHalo::RIGHT_HZ + r) : 0.f;
-      h_rt[r] = has_rt ? __ldcg(hb + (size_t)(blockIdx.x + 1) * FT_HALO + FtHalo::LEFT_HZ + r) : 0.f;
-      x_rt[r] = has_rt ? __ldcg(hb + (size_t)(blockIdx.x + 1) * FT_HALO + FtHalo::LEFT_EX + r) : 0.f;
-    }
-    __syncthreads();
-    // 3. new values of this thread's groups from the old state
-    float4 nxv[FT_G], nyv[FT_G], nhv[FT_G];
-    const float f = fict[t];
+      __syncthreads();  // every thread has read the old state
 #pragma unroll
-    for (int u = 0; u < FT_G; ++u) {
-      const int g = tid + u * FT_THREADS;
+      for (int u = 0; u < FT_G; ++u) {
+        const int g = tid + u * FT_THREADS;
+        if (g >= FT_GROUPS) continue;
+        const int r = g / (FT_RJ / 4), c = (g % (FT_RJ / 4)) * 4;
+        *reinterpret_cast<float4*>(sx + r * FT_RJ + c) = nxv[u];
+        *reinterpret_cast<float4*>(sy + r * FT_RJ + c) = nyv[u];
+        *reinterpret_cast<float4*>(sh + r * FT_RJ + c) = nhv[u];
+      }
+      __syncthreads();
+    }
+    // 3. publish the core: into the exchange copy (parity e+1), or - after the last
+    //    epoch, once every neighbour is done reading - into the caller's arrays
+    const bool last = (e + 1 == nep);
+    if (last) {
+      if (tid == 0) {
+        __threadfence();
+        st_rel(&flags[blockIdx.x], (unsigned)(nep + 1));  // "done reading" marker
+      }
+      ft_wait_neighbours(flags, ti, tj, tiles_i, tiles_j, (unsigned)(nep + 1));
+    }
+    float* px = last ? ex : grid2 + (size_t)((e + 1) & 1) * 3 * N;
+    float* py = last ? ey : px + N;
+    float* ph = last ? hz : px + 2 * N;
+    for (int g = tid; g < FT_I * FT_J / 4; g += FT_THREADS) {
       const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
-      if (r >= ri || c >= rj) continue;
       const int i = i0 + r, j = j0 + c;
-      const float4 h = *reinterpret_cast<const float4*>(sh + r * FT_J + c);
-      const float4 x = *reinterpret_cast<const float4*>(sx + r * FT_J + c);
-      const float4 y = *reinterpret_cast<const float4*>(sy + r * FT_J + c);
-      const float hl = (c > 0) ? sh[r * FT_J + c - 1] : h_lf[r];
-      const bool last_col = (j + 4 >= ny);
-      const bool tile_rt = (c + 4 >= rj);
-      const float hr = last_col ? 0.f : (tile_rt ? h_rt[r] : sh[r * FT_J + c + 4]);
-      const float xr = last_col ? 0.f : (tile_rt ? x_rt[r] : sx[r * FT_J + c + 4]);
-      float4 yn;
-      if (i == 0) {
-        yn = make_float4(f, f, f, f);
-      } else {
-        const float4 hu = (r > 0) ? *reinterpret_cast<const float4*>(sh + (r - 1) * FT_J + c)
-                                  : *reinterpret_cast<const float4*>(h_up + c);
-        yn = make_float4(ey_upd(y.x, h.x, hu.x), ey_upd(y.y, h.y, hu.y), ey_upd(y.z, h.z, hu.z),
-                         ey_upd(y.w, h.w, hu.w));
+      if (i < nx && j < ny) {
+        const size_t o = (size_t)i * ny + j;
+        const int so = (r + FT_H) * FT_RJ + c + FT_H;
+        *reinterpret_cast<float4*>(px + o) = *reinterpret_cast<const float4*>(sx + so);
+        *reinterpret_cast<float4*>(py + o) = *reinterpret_cast<const float4*>(sy + so);
+        *reinterpret_cast<float4*>(ph + o) = *reinterpret_cast<const float4*>(sh + so);
       }
-      float4 xn;
-      xn.x = (j == 0) ? x.x : ex_upd(x.x, h.x, hl);
-      xn.y = ex_upd(x.y, h.y, h.x);
-      xn.z = ex_upd(x.z, h.z, h.y);
-      xn.w = ex_upd(x.w, h.w, h.z);
-      float4 hn = h;
-      if (i < nx - 1) {
-        const bool tile_dn = (r + 1 >= ri);
-        const float4 yd = tile_dn ? *reinterpret_cast<const float4*>(y_dn + c)
-                                  : *reinterpret_cast<const float4*>(sy + (r + 1) * FT_J + c);
-        const float4 hd = tile_dn ? *reinterpret_cast<const float4*>(h_dn + c)
-                                  : *reinterpret_cast<const float4*>(sh + (r + 1) * FT_J + c);
-        const float4 ydn = make_float4(ey_upd(yd.x, hd.x, h.x), ey_upd(yd.y, hd.y, h.y), ey_upd(yd.z, hd.z, h.z),
-                                       ey_upd(yd.w, hd.w, h.w));
-        const float xrn = last_col ? 0.f : ex_upd(xr, hr, h.w);
-        hn.x = hz_upd(h.x, xn.y, xn.x, ydn.x, yn.x);
-        hn.y = hz_upd(h.y, xn.z, xn.y, ydn.y, yn.y);
-        hn.z = hz_upd(h.z, xn.w, xn.z, ydn.z, yn.z);
-        if (!last_col) hn.w = hz_upd(h.w, xrn, xn.w, ydn.w, yn.w);
+    }
+    if (!last) {
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_rel(&flags[blockIdx.x], (unsigned)(e + 1));
       }
-      nxv[u] = xn;
-      nyv[u] = yn;
-      nhv[u] = hn;
-    }
-    __syncthreads();  // every thread has read the old state
-#pragma unroll
-    for (int u = 0; u < FT_G; ++u) {
-      const int g = tid + u * FT_THREADS;
-      const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
-      if (r >= ri || c >= rj) continue;
-      *reinterpret_cast<float4*>(sx + r * FT_J + c) = nxv[u];
-      *reinterpret_cast<float4*>(sy + r * FT_J + c) = nyv[u];
-      *reinterpret_cast<float4*>(sh + r * FT_J + c) = nhv[u];
-    }
-    __syncthreads();
-  }
-  // write the tile back
-  for (int g = tid; g < FT_I * FT_J / 4; g += FT_THREADS) {
-    const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
-    if (r < ri && c < rj) {
-      const size_t e = (size_t)(i0 + r) * ny + j0 + c;
-      *reinterpret_cast<float4*>(ex + e) = *reinterpret_cast<const float4*>(sx + r * FT_J + c);
-      *reinterpret_cast<float4*>(ey + e) = *reinterpret_cast<const float4*>(sy + r * FT_J + c);
-      *reinterpret_cast<float4*>(hz + e) = *reinterpret_cast<const float4*>(sh + r * FT_J + c);
     }
   }
 }
@@ -577,10 +580,10 @@ cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, cons
 }
 
 namespace {
-constexpr size_t FT_SMEM = (size_t)(3 * FT_I * FT_J + 3 * FT_J + 3 * FT_I) * sizeof(float);
+constexpr size_t FT_SMEM = (size_t)3 * FT_RI * FT_RJ * sizeof(float);
 size_t fdtd_persist_ws(int nx, int ny) {
   const size_t tiles = (size_t)((nx + FT_I - 1) / FT_I) * ((ny + FT_J - 1) / FT_J);
-  return align_up(2 * tiles * FT_HALO * sizeof(float), 256) + align_up(tiles * sizeof(unsigned), 256);
+  return 2 * align_up(3 * (size_t)nx * ny * sizeof(float), 256) + align_up(tiles * sizeof(unsigned), 256);
 }
 }  // namespace
 
@@ -590,16 +593,16 @@ size_t fdtd_ws_bytes(int nx, int ny) {
 
 cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                           cudaStream_t s, int* launches) {
-  // Persistent path when every tile fits on the GPU at once (one 98 KB CTA per SM).
+  // Persistent path when every tile fits on the GPU at once (one 135 KB CTA per SM).
   static const int force_steps = getenv("PB_FDTD_STEPS") && atoi(getenv("PB_FDTD_STEPS")) == 1;  // tuning aid
   const int tiles_i = (nx + FT_I - 1) / FT_I, tiles_j = (ny + FT_J - 1) / FT_J;
   if (!force_steps && tmax > 0 && tiles_i * tiles_j <= sm_count()) {
     cudaError_t e = ensure_smem<fdtd_persist_kernel>(FT_SMEM);
     if (e != cudaSuccess) return e;
     const int tiles = tiles_i * tiles_j;
-    float* halo = static_cast<float*>(ws);
+    float* grid2 = static_cast<float*>(ws);
     unsigned* flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) +
-                                                  align_up(2 * (size_t)tiles * FT_HALO * sizeof(float), 256));
+                                                  2 * align_up(3 * (size_t)nx * ny * sizeof(float), 256));
     if ((e = cudaMemsetAsync(flags, 0, tiles * sizeof(unsigned), s)) != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tiles);
@@ -612,7 +615,7 @@ cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float*
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ++*launches;
-    return cudaLaunchKernelEx(&cfg, fdtd_persist_kernel, ex, ey, hz, fict, tmax, nx, ny, tiles_j, halo, flags);
+    return cudaLaunchKernelEx(&cfg, fdtd_persist_kernel, ex, ey, hz, fict, tmax, nx, ny, tiles_j, grid2, flags);
   }
   const size_t plane = align_up((size_t)nx * ny * sizeof(float), 256);
   float* wex = static_cast<float*>(ws);
