@@ -31,7 +31,8 @@ namespace {
 
 constexpr int GS_THREADS = 512;
 constexpr int GS_WARPS = GS_THREADS / 32;
-constexpr int GS_MAXC = 32;  // owned columns handled per batch
+constexpr int GS_MAXC = 16;  // owned columns handled per batch
+constexpr int GS_QREG = 4;   // q elements kept in registers per thread (m <= 2048 fully)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -73,8 +74,7 @@ __device__ __forceinline__ void wait_ready(const unsigned* ready, unsigned need)
   if (threadIdx.x == 0) {
     unsigned long long spins = 0;
     while (ld_acquire_u32(ready) < need) {
-      __nanosleep(32);
-      if (++spins > (1ull << 28)) asm volatile("trap;");
+      if (++spins > (1ull << 31)) asm volatile("trap;");
     }
   }
   __syncthreads();
@@ -124,15 +124,31 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gs_kernel(GsArgs a) {
     const int t0 = (k + 1 - cta + G - 1) >= 0 ? (k + 1 - cta + G - 1) / G : 0;
     if (t0 >= nown) break;  // nothing left to update here (all later steps too)
     wait_ready(a.ready, (unsigned)(k + 1));
+    // q_k into registers once (one L2 round trip per step): element i = tid + u*GS_THREADS
     const double* q = a.Qc + (size_t)k * m;
+    double qr[GS_QREG];
+#pragma unroll
+    for (int u = 0; u < GS_QREG; ++u) {
+      const int i = threadIdx.x + u * GS_THREADS;
+      qr[u] = i < m ? ld_cg_f64(q + i) : 0.0;
+    }
+    // f(i, q_i) over this thread's rows: register part unrolled, the rest (m > 2048) from L2
+    auto rows = [&](auto&& f) {
+#pragma unroll
+      for (int u = 0; u < GS_QREG; ++u) {
+        const int i = threadIdx.x + u * GS_THREADS;
+        if (i < m) f(i, qr[u]);
+      }
+      for (int i = threadIdx.x + GS_QREG * GS_THREADS; i < m; i += GS_THREADS) f(i, ld_cg_f64(q + i));
+    };
     // critical column k+1 first (if owned)
     int tb = t0;
     if (cta + t0 * G == k + 1) {
       double* c = colp(t0);
       double s = 0.0;
-      for (int i = threadIdx.x; i < m; i += GS_THREADS) s += ld_cg_f64(q + i) * c[i];
+      rows([&](int i, double qi) { s += qi * c[i]; });
       const double r = block_sum1(s, red);
-      for (int i = threadIdx.x; i < m; i += GS_THREADS) c[i] = c[i] - ld_cg_f64(q + i) * r;
+      rows([&](int i, double qi) { c[i] = c[i] - qi * r; });
       if (threadIdx.x == 0) a.R[(size_t)k * n + (k + 1)] = (float)r;
       __syncthreads();
       make_q(a, c, k + 1, red);
@@ -144,12 +160,11 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gs_kernel(GsArgs a) {
       double part[GS_MAXC];
 #pragma unroll
       for (int c = 0; c < GS_MAXC; ++c) part[c] = 0.0;
-      for (int i = threadIdx.x; i < m; i += GS_THREADS) {
-        const double qi = ld_cg_f64(q + i);
+      rows([&](int i, double qi) {
 #pragma unroll
         for (int c = 0; c < GS_MAXC; ++c)
           if (c < nb) part[c] += qi * colp(b0 + c)[i];
-      }
+      });
 #pragma unroll
       for (int c = 0; c < GS_MAXC; ++c) {
         if (c < nb) {
@@ -165,15 +180,14 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gs_kernel(GsArgs a) {
         a.R[(size_t)k * n + (cta + (b0 + threadIdx.x) * G)] = (float)s;
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < m; i += GS_THREADS) {
-        const double qi = ld_cg_f64(q + i);
+      rows([&](int i, double qi) {
 #pragma unroll
         for (int c = 0; c < GS_MAXC; ++c)
           if (c < nb) {
             double* cp = colp(b0 + c);
             cp[i] = cp[i] - qi * rsum[c];
           }
-      }
+      });
       __syncthreads();
     }
   }
