@@ -132,3 +132,84 @@ def gen_device(t, stream, seed=SEED, mode=U01, scale=1.0, offset=0.0, row0=0, ld
     if rc != 0:
         raise RuntimeError(f"pbgen_fill_device failed: cuda error {rc}")
     return t
+
+
+# ---------------------------------------------------------------- PolyBench/C 4.2 init_array
+# the PolyBench/C 4.2 `init_array` formulas (recollection of the
+# suite's sources), evaluated with PolyBench's DATA_TYPE
+# float arithmetic: (float)(integer expression) / n is one fp32 division (RN), as
+# numpy float32 does it. Inputs only - no kernel arithmetic. Returns float32 arrays.
+def _q(num, den):
+    return (np.asarray(num).astype(np.float32) / np.float32(den)).astype(np.float32)
+
+
+def polybench_init(kernel, *dims):
+    i2 = lambda r, c: np.meshgrid(np.arange(r, dtype=np.int64), np.arange(c, dtype=np.int64), indexing="ij")  # noqa: E731
+    if kernel == "gemm":
+        ni, nj, nk = dims
+        i, j = i2(ni, nj); C = _q((i * j + 1) % ni, ni)
+        i, j = i2(ni, nk); A = _q(i * (j + 1) % nk, nk)
+        i, j = i2(nk, nj); B = _q(i * (j + 2) % nj, nj)
+        return dict(alpha=1.5, beta=1.2, C=C, A=A, B=B)
+    if kernel == "2mm":
+        ni, nj, nk, nl = dims
+        i, j = i2(ni, nk); A = _q((i * j + 1) % ni, ni)
+        i, j = i2(nk, nj); B = _q(i * (j + 1) % nj, nj)
+        i, j = i2(nj, nl); C = _q((i * (j + 3) + 1) % nl, nl)
+        i, j = i2(ni, nl); D = _q(i * (j + 2) % nk, nk)
+        return dict(alpha=1.5, beta=1.2, A=A, B=B, C=C, D=D)
+    if kernel == "3mm":
+        ni, nj, nk, nl, nm = dims
+        i, j = i2(ni, nk); A = _q((i * j + 1) % ni, 5 * ni)
+        i, j = i2(nk, nj); B = _q((i * (j + 1) + 2) % nj, 5 * nj)
+        i, j = i2(nj, nm); C = _q(i * (j + 3) % nl, 5 * nl)
+        i, j = i2(nm, nl); D = _q((i * (j + 2) + 2) % nk, 5 * nk)
+        return dict(A=A, B=B, C=C, D=D)
+    if kernel in ("syrk", "syr2k"):
+        n, m = dims
+        i, j = i2(n, m); A = _q((i * j + 1) % n, n); B = _q((i * j + 2) % m, m)
+        i, j = i2(n, n)
+        C = _q((i * j + 2) % m, m) if kernel == "syrk" else _q((i * j + 3) % n, m)
+        return dict(alpha=1.5, beta=1.2, A=A, B=B, C=C)
+    if kernel in ("covariance", "correlation"):
+        m, n = dims
+        i, j = i2(n, m)
+        data = (i.astype(np.float32) * j.astype(np.float32)).astype(np.float32) / np.float32(m)
+        if kernel == "correlation":
+            data = (data + i.astype(np.float32)).astype(np.float32)
+        return dict(float_n=float(n), data=data.astype(np.float32))
+    if kernel == "atax":
+        m, n = dims
+        fn = np.float32(n)
+        x = (np.float32(1) + np.arange(n, dtype=np.float32) / fn).astype(np.float32)
+        i, j = i2(m, n); A = _q((i + j) % n, 5 * m)
+        return dict(A=A, x=x)
+    if kernel == "bicg":
+        m, n = dims
+        p = _q(np.arange(m) % m, m); r = _q(np.arange(n) % n, n)
+        i, j = i2(n, m); A = _q(i * (j + 1) % n, n)
+        return dict(A=A, p=p, r=r)
+    if kernel == "mvt":
+        (n,) = dims
+        k = np.arange(n)
+        i, j = i2(n, n)
+        return dict(x1=_q(k % n, n), x2=_q((k + 1) % n, n), y_1=_q((k + 3) % n, n), y_2=_q((k + 4) % n, n),
+                    A=_q(i * j % n, n))
+    if kernel == "gesummv":
+        (n,) = dims
+        i, j = i2(n, n)
+        return dict(alpha=1.5, beta=1.2, x=_q(np.arange(n) % n, n), A=_q((i * j + 1) % n, n), B=_q((i * j + 2) % n, n))
+    if kernel == "fdtd_2d":
+        tmax, nx, ny = dims
+        i, j = i2(nx, ny)
+        fi = i.astype(np.float32)
+        return dict(fict=np.arange(tmax, dtype=np.float32),
+                    ex=((fi * (j + 1).astype(np.float32)) / np.float32(nx)).astype(np.float32),
+                    ey=((fi * (j + 2).astype(np.float32)) / np.float32(ny)).astype(np.float32),
+                    hz=((fi * (j + 3).astype(np.float32)) / np.float32(nx)).astype(np.float32))
+    if kernel == "gramschmidt":
+        m, n = dims
+        i, j = i2(m, n)
+        A = (_q((i * j) % m, m) * np.float32(100) + np.float32(10)).astype(np.float32)
+        return dict(A=A)
+    raise ValueError(kernel)

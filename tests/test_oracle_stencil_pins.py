@@ -255,3 +255,27 @@ def test_gramschmidt_orthogonal_columns_closed_form():
     Qe[perm, np.arange(n)] = np.sign(d)
     assert np.array_equal(Q, Qe)
     assert np.array_equal(R, np.diag(np.abs(d)))
+
+
+# ------------------------------------------------------------------ PolyBench init data (NEXT-2)
+def test_polybench_init_correlation_closed_form():
+    """PolyBench's correlation data i*j/M + i = i (1 + j/M): every column is a positive
+    multiple of i, so every correlation is 1 (up to the fp32 rounding of the data)."""
+    import pbgen
+    d = pbgen.polybench_init("correlation", 24, 40)
+    corr, mean, sd = oracle.correlation(d["float_n"], 0.1, d["data"])
+    assert np.abs(corr - 1.0).max() < 1e-6
+    # and the mean of column j is mean(i) (1 + j/M) = (n-1)/2 (1 + j/M)
+    np.testing.assert_allclose(mean, 19.5 * (1 + np.arange(24) / 24), rtol=1e-6)
+
+
+def test_polybench_init_covariance_closed_form():
+    """PolyBench's covariance data i*j/M: cov[a][b] = (a/M)(b/M) var(i), var(i) = n(n+1)/12
+    (ddof 1); column 0 is constant 0, so row and column 0 vanish exactly."""
+    import pbgen
+    m, n = 16, 64  # i*j/M exact in fp32 (M a power of two)
+    d = pbgen.polybench_init("covariance", m, n)
+    cov, mean = oracle.covariance(d["float_n"], d["data"])
+    a = np.arange(m) / m
+    np.testing.assert_allclose(cov, np.outer(a, a) * n * (n + 1) / 12.0, rtol=1e-12, atol=1e-12)
+    assert np.all(cov[0] == 0) and np.all(cov[:, 0] == 0)
