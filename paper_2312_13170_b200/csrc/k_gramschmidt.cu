@@ -60,6 +60,17 @@ __device__ __forceinline__ double block_sum1(double v, double* red) {
   return t;
 }
 
+// As block_sum1 with one barrier: the caller alternates buffers (red, red + GS_WARPS)
+// so a buffer is rewritten only after a later barrier.
+__device__ __forceinline__ double block_sum_buf(double v, double* red) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  v = warp_sum_d(v);
+  if (lane == 0) red[wp] = v;
+  __syncthreads();
+  double t = (lane < GS_WARPS) ? red[lane] : 0.0;
+  return warp_sum_d(t);
+}
+
 struct GsArgs {
   int m, n, cpc;  // rows, columns, columns per CTA (ceil(n / G))
   double* W;      // column-major fp64 working copy, n x m (column j at W + j*m)
@@ -144,14 +155,30 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gs_kernel(GsArgs a) {
     // critical column k+1 first (if owned)
     int tb = t0;
     if (cta + t0 * G == k + 1) {
+      // dot, then axpy fused with the new column's norm, then q_{k+1}: three CTA
+      // barriers (the reductions use separate buffers, so none needs a second one)
       double* c = colp(t0);
       double s = 0.0;
       rows([&](int i, double qi) { s += qi * c[i]; });
-      const double r = block_sum1(s, red);
-      rows([&](int i, double qi) { c[i] = c[i] - qi * r; });
-      if (threadIdx.x == 0) a.R[(size_t)k * n + (k + 1)] = (float)r;
+      const double r = block_sum_buf(s, red);
+      double s2 = 0.0;
+      rows([&](int i, double qi) {
+        const double v = c[i] - qi * r;
+        c[i] = v;
+        s2 += v * v;
+      });
+      const double rkk = sqrt(block_sum_buf(s2, red + GS_WARPS));
+      double* qn = a.Qc + (size_t)(k + 1) * m;
+      for (int i = threadIdx.x; i < m; i += GS_THREADS) qn[i] = c[i] / rkk;  // this thread's own c[i]
+      if (threadIdx.x == 0) {
+        a.R[(size_t)k * n + (k + 1)] = (float)r;
+        a.R[(size_t)(k + 1) * n + (k + 1)] = (float)rkk;
+      }
       __syncthreads();
-      make_q(a, c, k + 1, red);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u32(a.ready, (unsigned)(k + 2));
+      }
       tb = t0 + 1;
     }
     // the other owned columns j > k+1, in batches of GS_MAXC
