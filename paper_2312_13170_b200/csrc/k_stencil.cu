@@ -386,10 +386,7 @@ __global__ void __launch_bounds__(256) fdtd_step_kernel(const float* __restrict_
 // the state once in and once out; one neighbour round trip through L2 per FT_H steps
 // replaces FT_H kernel launches. Every update is the PolyBench statement's fp32
 // operations, so the result is bitwise the sequential sweeps'.
-constexpr int FT_I = 64, FT_J = 128, FT_H = 8, FT_THREADS = 512;
-constexpr int FT_RI = FT_I + 2 * FT_H, FT_RJ = FT_J + 2 * FT_H;  // region 80 x 144
-constexpr int FT_GROUPS = FT_RI * FT_RJ / 4;
-constexpr int FT_G = (FT_GROUPS + FT_THREADS - 1) / FT_THREADS;  // float4 groups per thread (6)
+constexpr int FT_I = 64, FT_J = 128, FT_THREADS = 512;  // core tile; halo width FT_H is a template argument
 
 __device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
   unsigned v;
@@ -416,11 +413,15 @@ __device__ __forceinline__ void ft_wait_neighbours(const unsigned* flags, int ti
   __syncthreads();
 }
 
+template <int FT_H>
 __global__ void __launch_bounds__(FT_THREADS, 1) fdtd_persist_kernel(float* __restrict__ ex, float* __restrict__ ey,
                                                                      float* __restrict__ hz,
                                                                      const float* __restrict__ fict, int tmax, int nx,
                                                                      int ny, int tiles_j, float* __restrict__ grid2,
                                                                      unsigned* __restrict__ flags) {
+  constexpr int FT_RI = FT_I + 2 * FT_H, FT_RJ = FT_J + 2 * FT_H;  // region (H = 8: 80 x 144)
+  constexpr int FT_GROUPS = FT_RI * FT_RJ / 4;
+  constexpr int FT_G = (FT_GROUPS + FT_THREADS - 1) / FT_THREADS;  // float4 groups per thread
   extern __shared__ __align__(16) float ft_smem[];
   float* sx = ft_smem;                  // ex [FT_RI][FT_RJ]
   float* sy = sx + FT_RI * FT_RJ;       // ey
@@ -580,7 +581,7 @@ cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, cons
 }
 
 namespace {
-constexpr size_t FT_SMEM = (size_t)3 * FT_RI * FT_RJ * sizeof(float);
+constexpr size_t ft_smem_bytes(int h) { return (size_t)3 * (FT_I + 2 * h) * (FT_J + 2 * h) * sizeof(float); }
 size_t fdtd_persist_ws(int nx, int ny) {
   const size_t tiles = (size_t)((nx + FT_I - 1) / FT_I) * ((ny + FT_J - 1) / FT_J);
   return 2 * align_up(3 * (size_t)nx * ny * sizeof(float), 256) + align_up(tiles * sizeof(unsigned), 256);
@@ -593,11 +594,14 @@ size_t fdtd_ws_bytes(int nx, int ny) {
 
 cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                           cudaStream_t s, int* launches) {
-  // Persistent path when every tile fits on the GPU at once (one 135 KB CTA per SM).
+  // Persistent path when every tile fits on the GPU at once (one CTA per SM: 135 KB at H = 8).
   static const int force_steps = getenv("PB_FDTD_STEPS") && atoi(getenv("PB_FDTD_STEPS")) == 1;  // tuning aid
   const int tiles_i = (nx + FT_I - 1) / FT_I, tiles_j = (ny + FT_J - 1) / FT_J;
   if (!force_steps && tmax > 0 && tiles_i * tiles_j <= sm_count()) {
-    cudaError_t e = ensure_smem<fdtd_persist_kernel>(FT_SMEM);
+    static const int h = getenv("PB_FDTD_H") ? atoi(getenv("PB_FDTD_H")) : 8;  // tuning aid: 4, 8, 16
+    const size_t smem = ft_smem_bytes(h);
+    cudaError_t e = h == 4 ? ensure_smem<fdtd_persist_kernel<4>>(smem)
+                   : h == 16 ? ensure_smem<fdtd_persist_kernel<16>>(smem) : ensure_smem<fdtd_persist_kernel<8>>(smem);
     if (e != cudaSuccess) return e;
     const int tiles = tiles_i * tiles_j;
     float* grid2 = static_cast<float*>(ws);
@@ -607,7 +611,7 @@ cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float*
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tiles);
     cfg.blockDim = dim3(FT_THREADS);
-    cfg.dynamicSmemBytes = FT_SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;  // all tiles co-resident: the flag waits are safe
@@ -615,7 +619,10 @@ cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float*
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ++*launches;
-    return cudaLaunchKernelEx(&cfg, fdtd_persist_kernel, ex, ey, hz, fict, tmax, nx, ny, tiles_j, grid2, flags);
+    if (h == 4) return cudaLaunchKernelEx(&cfg, fdtd_persist_kernel<4>, ex, ey, hz, fict, tmax, nx, ny, tiles_j, grid2, flags);
+    if (h == 16)
+      return cudaLaunchKernelEx(&cfg, fdtd_persist_kernel<16>, ex, ey, hz, fict, tmax, nx, ny, tiles_j, grid2, flags);
+    return cudaLaunchKernelEx(&cfg, fdtd_persist_kernel<8>, ex, ey, hz, fict, tmax, nx, ny, tiles_j, grid2, flags);
   }
   const size_t plane = align_up((size_t)nx * ny * sizeof(float), 256);
   float* wex = static_cast<float*>(ws);
