@@ -428,6 +428,10 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline(kernels, budget_s=args.cpu_budget)
         if world == 1 and not args.no_next:
             line["next_rows"] = measure_next_rows(dev)
+            if not args.no_cpu:
+                for k, v in next_rows_cpu().items():
+                    v.update(kind="oracle", cores=int(os.environ.get("OMP_NUM_THREADS", cpu_threads())))
+                    line["next_rows"][k]["cpu_oracle"] = v
         print(json.dumps(line), flush=True)
     if sharded:
         import paper_2312_13170_b200.dist as D
@@ -480,14 +484,16 @@ def measure_next_rows(dev, reps=10):
     A, B = gen((n, n), S["A"]), gen((n, n), S["B"])
     ms, L = timed(lambda: pb.pb_conv2d(n, n, pbgen.CONV2D_W, A, B))
     by = 4 * n * n + 4 * (n - 2) ** 2
-    out["conv2d"] = {"n": n, "ms": round(ms, 4), "gbs": round(by / ms / 1e6, 1), "bound": "hbm",
+    out["conv2d"] = {"n": n, "ms": round(ms, 4), "gpoints_per_s": round(n * n / ms / 1e6, 2),
+                     "gbs": round(by / ms / 1e6, 1), "bound": "hbm",
                      "frac": round(by / ms / 1e6 / hbm, 4), "bytes": by, "launches": L}
     del A, B
     n = 1024
     A, B = gen((n, n, n), S["A"]), gen((n, n, n), S["B"])
     ms, L = timed(lambda: pb.pb_conv3d(n, n, n, pbgen.conv3d_w27(), A, B))
     by = 4 * n ** 3 + 4 * (n - 2) ** 3
-    out["conv3d"] = {"n": n, "ms": round(ms, 4), "gbs": round(by / ms / 1e6, 1), "bound": "hbm",
+    out["conv3d"] = {"n": n, "ms": round(ms, 4), "gpoints_per_s": round(n ** 3 / ms / 1e6, 2),
+                     "gbs": round(by / ms / 1e6, 1), "bound": "hbm",
                      "frac": round(by / ms / 1e6 / hbm, 4), "bytes": by, "launches": L}
     del A, B
     T = 500
@@ -497,6 +503,7 @@ def measure_next_rows(dev, reps=10):
     ms, L = timed(lambda: pb.pb_fdtd_2d(T, n, n, ex, ey, hz, f, ws))
     by = 24 * n * n * T
     out["fdtd_2d"] = {"n": n, "tmax": T, "ms": round(ms, 4), "us_per_step": round(1000 * ms / T, 3),
+                      "gpoint_steps_per_s": round(n * n * T / ms / 1e6, 2),
                       "gbs": round(by / ms / 1e6, 1), "bound": "l2 (state resident) / launch latency",
                       "frac_of_hbm_copy": round(by / ms / 1e6 / hbm, 4), "launches": L}
     A0 = gen((n, n), S["A"])
@@ -669,6 +676,49 @@ def oracle_rates(kernels, budget_s=30.0):
                 break
         rates[k] = f * reps / el / 1e9
     return rates
+
+
+def next_rows_cpu(budget_s=8.0):
+    """The NEXT-3 rows' oracles as they stand, timed on a bounded sample on this
+    host (the cpu_baseline leg; not part of any value): conv2d 2048^2, conv3d 128^3,
+    fdtd 256^2 x 20 steps (fp32 statements), gramschmidt 256^2. Rates in the rows'
+    own units (points/s or column steps/s) so they sit beside the GPU numbers."""
+    import numpy as np
+
+    import oracle
+    import pbgen
+    S = pbgen.STREAM
+    H = lambda r, c, s: pbgen.gen_host(r, c, s)  # noqa: E731
+
+    def rate(fn, units):
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            fn()
+            reps += 1
+            el = time.perf_counter() - t0
+            if el > budget_s / 4 or reps >= 20:
+                break
+        return units * reps / el
+
+    out = {}
+    n = 2048
+    A, B = H(n, n, S["A"]), H(n, n, S["B"])
+    out["conv2d"] = {"value": round(rate(lambda: oracle.conv2d(pbgen.CONV2D_W, A, B), n * n) / 1e9, 4),
+                     "unit": "Gpoint/s", "sample": "2048^2"}
+    n = 128
+    A3, B3 = H(n * n, n, S["A"]).reshape(n, n, n), H(n * n, n, S["B"]).reshape(n, n, n)
+    out["conv3d"] = {"value": round(rate(lambda: oracle.conv3d(pbgen.conv3d_w27(), A3, B3), n ** 3) / 1e9, 4),
+                     "unit": "Gpoint/s", "sample": "128^3"}
+    n, T = 256, 20
+    ex, ey, hz, f = H(n, n, S["ex"]), H(n, n, S["ey"]), H(n, n, S["hz"]), H(1, T, S["fict"])[0]
+    out["fdtd_2d"] = {"value": round(rate(lambda: oracle.fdtd2d(T, ex, ey, hz, f, f32=True), n * n * T) / 1e9, 4),
+                      "unit": "Gpoint-steps/s", "sample": "256^2 x 20 steps (fp32 statements)"}
+    n = 256
+    G = H(n, n, S["A"])
+    out["gramschmidt"] = {"value": round(rate(lambda: oracle.gramschmidt(G), 2.0 * n ** 3) / 1e9, 4),
+                          "unit": "GFLOP/s (fp64)", "sample": "256^2"}
+    return out
 
 
 def cpu_threads():
