@@ -279,3 +279,87 @@ def test_polybench_init_covariance_closed_form():
     a = np.arange(m) / m
     np.testing.assert_allclose(cov, np.outer(a, a) * n * (n + 1) / 12.0, rtol=1e-12, atol=1e-12)
     assert np.all(cov[0] == 0) and np.all(cov[:, 0] == 0)
+
+
+# ------------------------------------------------------------------ the pins bite
+def _fdtd_np(T, ex, ey, hz, f, mut=None):
+    """A numpy FDTD with optional plausible mistakes, to show the pins above reject them."""
+    ex, ey, hz = (a.astype(np.float64).copy() for a in (ex, ey, hz))
+    ce, ch = (0.7, 0.5) if mut == "swap_coef" else (0.5, 0.7)
+    for t in range(T):
+        if mut != "no_source":
+            ey[0, :] = f[t]
+        if mut == "hz_first":
+            hz[:-1, :-1] -= ch * (ex[:-1, 1:] - ex[:-1, :-1] + ey[1:, :-1] - ey[:-1, :-1])
+        ey[1:, :] -= ce * (hz[1:, :] - hz[:-1, :]) if mut != "ey_sign" else -ce * (hz[1:, :] - hz[:-1, :])
+        if mut == "ex_rows":
+            ex[1:, :] -= ce * (hz[1:, :] - hz[:-1, :])
+        else:
+            ex[:, 1:] -= ce * (hz[:, 1:] - hz[:, :-1])
+        if mut != "hz_first":
+            hz[:-1, :-1] -= ch * (ex[:-1, 1:] - ex[:-1, :-1] + ey[1:, :-1] - ey[:-1, :-1])
+    return ex, ey, hz
+
+
+def test_fdtd_pins_reject_mutants():
+    g = json.load(open(os.path.join(HERE, "golden", "fdtd2d_impulse.json")))
+    c = g["impulse"]
+    z = np.zeros((c["nx"], c["ny"]), np.float32)
+    hz = z.copy()
+    hz[tuple(c["hz_at"])] = 1.0
+    f = np.array(c["fict"], np.float32)
+
+    def golden_ok(res):
+        for arr, key in zip(res, ("ex_nonzero", "ey_nonzero", "hz_nonzero")):
+            ref = np.zeros_like(arr)
+            for i, j, v in c[key]:
+                ref[i, j] = v
+            if np.abs(arr - ref).max() > 1e-12:
+                return False
+        return True
+
+    src = g["source_case"]
+    zs = np.zeros((src["nx"], src["ny"]), np.float32)
+
+    def source_ok(res):
+        return np.allclose(res[1][0], src["ey_row0"]) and np.allclose(res[2][0], src["hz_row0"])
+
+    assert golden_ok(_fdtd_np(1, z, z, hz, f)) and source_ok(_fdtd_np(1, zs, zs, zs, np.array(src["fict"], np.float32)))
+    for mut in ("swap_coef", "hz_first", "ey_sign", "ex_rows", "no_source"):
+        res = _fdtd_np(1, z, z, hz, f, mut)
+        res_s = _fdtd_np(1, zs, zs, zs, np.array(src["fict"], np.float32), mut)
+        assert not (golden_ok(res) and source_ok(res_s)), mut
+
+
+def test_conv_pins_reject_mutants():
+    """scipy's correlate rejects a convolution (flipped kernel), transposed weights,
+    a dropped tap and a shifted window."""
+    A = _rand(9, 11, lo=-1, hi=1).astype(np.float64)
+    w = RNG.normal(size=(3, 3))
+    ref = signal.correlate2d(A, w, mode="valid")
+    mutants = [signal.convolve2d(A, w, mode="valid"), signal.correlate2d(A, w.T, mode="valid"),
+               signal.correlate2d(A, np.where(np.arange(9).reshape(3, 3) == 4, 0, w), mode="valid"),
+               signal.correlate2d(A, w, mode="full")[2:-2, 1:-3]]
+    for mtt in mutants:
+        assert np.abs(mtt - ref).max() > 1e-6
+
+
+def test_gramschmidt_pins_reject_mutants():
+    """The LAPACK-QR pin rejects an unnormalised Q, a missing projection and a wrong sign."""
+    A = _rand(20, 12, lo=-1, hi=1).astype(np.float64)
+    Qn, Rn = _qr_pos(A.astype(np.float32))
+    Ao, R, Q = oracle.gramschmidt(A.astype(np.float32))
+    assert np.abs(Q - Qn).max() < 1e-9
+    bad_unnorm = Q * np.diag(R)[None, :]
+    bad_sign = Q.copy()
+    bad_sign[:, 3] *= -1
+    # classical GS with one projection dropped (q_0 never removed from column 2)
+    Qd = np.zeros_like(A)
+    for k in range(A.shape[1]):
+        v = A[:, k].copy()
+        for i in range(k):
+            if not (k == 2 and i == 0):
+                v -= (Qd[:, i] @ A[:, k]) * Qd[:, i]
+        Qd[:, k] = v / np.linalg.norm(v)
+    for mtt in (bad_unnorm, bad_sign, Qd):
+        assert np.abs(mtt - Qn).max() > 1e-6
