@@ -159,19 +159,20 @@ def structured_data(n, m, seed=pbgen.SEED):
     return d
 
 
-def check_covariance(m, n, structured=True):
+def check_covariance(m, n, structured=True, float_n=None):
     data = structured_data(n, m) if structured else H(n, m, S["data"])
+    fn = float(n) if float_n is None else float(float_n)
     dcov = torch.empty(m, m, device="cuda")
     dmean = torch.empty(m, device="cuda")
     ddata = dev(data)
-    pb.pb_covariance(m, n, float(n), ddata, dcov, dmean)
-    cov_r, mean_r = oracle.covariance(float(n), data)
-    cov_s, mean_s = oracle.covariance(float(n), data, absmode=True)
+    pb.pb_covariance(m, n, fn, ddata, dcov, dmean)
+    cov_r, mean_r = oracle.covariance(fn, data)
+    cov_s, mean_s = oracle.covariance(fn, data, absmode=True)
     g = host(dcov)
     out = _res(cov=cerr(g, cov_r, cov_s), mean=cerr(host(dmean), mean_r, mean_s))
     out["symmetric"] = bool(np.array_equal(g, g.T))
     out["data_untouched"] = bool(np.array_equal(host(ddata), data))
-    if structured and m >= 5:
+    if structured and m >= 5 and float_n is None:  # with float_n != n the "mean" is not the mean
         out["const_col_zero"] = bool(np.all(g[0, :] == 0) and np.all(g[:, 0] == 0))
     else:
         out["const_col_zero"] = True
@@ -179,14 +180,15 @@ def check_covariance(m, n, structured=True):
     return out
 
 
-def check_correlation(m, n, eps=0.1, structured=True):
+def check_correlation(m, n, eps=0.1, structured=True, float_n=None):
     data = structured_data(n, m) if structured else H(n, m, S["data"])
+    fn = float(n) if float_n is None else float(float_n)
     dcorr = torch.empty(m, m, device="cuda")
     dmean = torch.empty(m, device="cuda")
     dsd = torch.empty(m, device="cuda")
-    pb.pb_correlation(m, n, float(n), eps, dev(data), dcorr, dmean, dsd)
-    c_r, m_r, sd_r = oracle.correlation(float(n), eps, data)
-    c_s, m_s, sd_s = oracle.correlation(float(n), eps, data, absmode=True)
+    pb.pb_correlation(m, n, fn, eps, dev(data), dcorr, dmean, dsd)
+    c_r, m_r, sd_r = oracle.correlation(fn, eps, data)
+    c_s, m_s, sd_s = oracle.correlation(fn, eps, data, absmode=True)
     g = host(dcorr)
     out = _res(corr=cerr(g, c_r, c_s), mean=cerr(host(dmean), m_r, m_s), stddev=cerr(host(dsd), sd_r, sd_r))
     out["diag_one"] = bool(np.all(np.diag(g) == 1.0))

@@ -122,3 +122,15 @@ def test_gramschmidt_polybench_matrix():
     assert (np.abs(gQ - rQ) / np.abs(rQ).max(0)).max() <= TOL
     assert (np.abs(gA - rA) / np.abs(rA).max(0)).max() <= TOL
     assert (np.abs(gR - rR) / cn[None, :])[up].max() <= TOL
+
+
+# PolyBench-GPU / SYCL-Bench constants (readings R4/R5): a fixed
+# FLOAT_N = 3214212.01 that is not the observation count (so the "mean" is not the
+# mean and nothing cancels) and eps = 0.005.
+@pytest.mark.parametrize("m,n", [(132, 260), (2048, 2048), (128, 3000)])
+@pytest.mark.parametrize("float_n", [3214212.01, None])
+def test_polybench_gpu_constants(m, n, float_n):
+    r = P.check_covariance(m, n, float_n=float_n)
+    assert r["ok"], r
+    r = P.check_correlation(m, n, eps=0.005, float_n=float_n)
+    assert r["ok"], r
