@@ -2,7 +2,7 @@
 // deviations for covariance / correlation ("array reduction" opportunities,
 // PAPER.md:542; detect-reduction PAPER.md:344-374: each column sum is a
 // register accumulator) fused with the centring / normalisation and the TF32
-// split of the Gram operand. Variance: (sum x^2 - (sum x) mu) / float_n in fp64
+// split of the Gram operand. Variance: (sum x^2 - 2 mu sum x + n mu^2) / float_n in fp64
 // (reading R17 in DESIGN.md). Deterministic: every sum has a fixed order.
 #include <math.h>
 #include <stdio.h>
@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(PT, 1) stats_split_kernel(const float* __restr
     if (c0 + t < m) {
       if (mean_out) mean_out[c0 + t] = (float)mu;
       if (CORR) {
-        double var = (Q - S * mu) / float_n;
+        // sum_i (x_i - mu)^2 = Q - 2 mu S + n mu^2 (mu = S / float_n; float_n need not be n)
+        double var = (Q - 2.0 * mu * S + (double)n * mu * mu) / float_n;
         if (var < 0.0) var = 0.0;
         double sd = sqrt(var);
         if (sd <= eps) sd = 1.0;
