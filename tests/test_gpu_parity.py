@@ -391,3 +391,34 @@ def test_matvec_integer_bitwise_P1():
     g1, g2 = P.host(d1).astype(np.float64), P.host(d2).astype(np.float64)
     assert np.array_equal(g1, o1) and np.array_equal(g2, o2)
     assert np.array_equal(g1 - x1, g2 - x2)
+
+
+@pytest.mark.parametrize("two", [False, True])
+def test_syrk_syr2k_beta0_nan_not_read(two):
+    """beta == 0: C's lower triangle is write-only (include/pb.h BLAS convention), so NaN
+    there must not propagate; the strict upper triangle is untouched (NaN stays NaN)."""
+    n, m = 260, 132
+    A, B = P.H(n, m, 1), P.H(n, m, 2)
+    C = np.full((n, n), np.nan, dtype=np.float32)
+    dC = P.dev(C)
+    if two:
+        pb.pb_syr2k(n, m, 1.5, 0.0, dC, P.dev(A), P.dev(B))
+        r = oracle.syr2k(1.5, 0.0, np.zeros_like(C), A, B)
+        s = oracle.syr2k(1.5, 0.0, np.zeros_like(C), A, B, absmode=True)
+    else:
+        pb.pb_syrk(n, m, 1.5, 0.0, dC, P.dev(A))
+        r = oracle.syrk(1.5, 0.0, np.zeros_like(C), A)
+        s = oracle.syrk(1.5, 0.0, np.zeros_like(C), A, absmode=True)
+    g = P.host(dC)
+    low = np.tril(np.ones((n, n), bool))
+    assert P.cerr(g[low], r[low], s[low]) <= P.TOL
+    assert np.all(np.isnan(g[~low]))
+
+
+def test_2mm_beta0_nan_not_read():
+    ni, nj, nk, nl = 132, 136, 260, 128
+    A, B, C = P.H(ni, nk, 1), P.H(nk, nj, 2), P.H(nj, nl, 3)
+    dD = P.dev(np.full((ni, nl), np.nan, dtype=np.float32))
+    pb.pb_2mm(ni, nj, nk, nl, 1.5, 0.0, None, P.dev(A), P.dev(B), P.dev(C), dD)
+    (_, Dr), (_, Ds) = (oracle.mm2(1.5, 0.0, A, B, C, np.zeros((ni, nl), np.float32), absmode=a) for a in (False, True))
+    assert P.cerr(P.host(dD), Dr, Ds) <= P.TOL

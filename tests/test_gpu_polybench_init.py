@@ -134,3 +134,12 @@ def test_polybench_gpu_constants(m, n, float_n):
     assert r["ok"], r
     r = P.check_correlation(m, n, eps=0.005, float_n=float_n)
     assert r["ok"], r
+
+
+@pytest.mark.parametrize("m,n", [(132, 260), (256, 2048), (128, 3000)])
+@pytest.mark.parametrize("eps", [0.0, 10.0])
+def test_correlation_eps_extremes(m, n, eps):
+    """eps = 0: only the constant column (sd = 0 <= eps) is replaced; eps = 10: every
+    column's sd is replaced by 1 (reading R5), on the banded and the long-column paths."""
+    r = P.check_correlation(m, n, eps=eps)
+    assert r["ok"], r

@@ -186,3 +186,35 @@ def test_gramschmidt_deterministic():
         pb.pb_gramschmidt(m, n, dA, dR, dQ)
         outs.append([P.host(t).view(np.uint32) for t in (dA, dR, dQ)])
     assert all(np.array_equal(a, b) for a, b in zip(*outs))
+
+
+def test_next_rows_on_a_side_stream():
+    """Every NEXT-3 entry point enqueues on the caller's stream (not the default one)."""
+    st = torch.cuda.Stream()
+    A = P.dev(P.H(260, 516, 1))
+    B = torch.zeros(260, 516, device="cuda")
+    ex, ey, hz, f = P.fdtd_inputs(130, 132, 9)
+    d = [P.dev(a) for a in (ex, ey, hz)]
+    G = P.dev(P.H(200, 132, 1))
+    R, Q = torch.zeros(132, 132, device="cuda"), torch.zeros(200, 132, device="cuda")
+    torch.cuda.synchronize()
+    with torch.cuda.stream(st):
+        pb.pb_conv2d(260, 516, pbgen.CONV2D_W, A, B)
+        pb.pb_fdtd_2d(9, 130, 132, d[0], d[1], d[2], P.dev(f))
+        pb.pb_gramschmidt(200, 132, G, R, Q)
+    st.synchronize()
+    r = oracle.conv2d(pbgen.CONV2D_W, P.H(260, 516, 1), np.zeros((260, 516), np.float32))
+    s = oracle.conv2d(pbgen.CONV2D_W, P.H(260, 516, 1), np.zeros((260, 516), np.float32), absmode=True)
+    assert P.cerr(P.host(B), r, s) <= P.TOL
+    r32 = oracle.fdtd2d(9, ex, ey, hz, f, f32=True)
+    assert all(np.array_equal(P.host(a).view(np.uint32), b.view(np.uint32)) for a, b in zip(d, r32))
+    rA, rR, rQ = oracle.gramschmidt(P.H(200, 132, 1))
+    assert (np.abs(P.host(Q) - rQ) / np.abs(rQ).max(0)).max() <= P.TOL
+
+
+def test_conv_zero_weights():
+    A = P.dev(P.H(37 * 9, 132, 1))
+    B = P.dev(P.H(37 * 9, 132, 2))
+    pb.pb_conv3d(37, 9, 132, [0.0] * 27, A, B)
+    g = P.host(B).reshape(37, 9, 132)
+    assert np.all(g[1:-1, 1:-1, 1:-1] == 0)
