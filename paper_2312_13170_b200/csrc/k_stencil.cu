@@ -83,24 +83,26 @@ __device__ __forceinline__ uint64_t l2_policy(int kind) {
   return p;
 }
 
-template <int NJT, int OROWS, int WPR>
+template <int NJT, int OROWS, int WPR, int RPW = 1>
 struct March {
-  static constexpr int STAGES = NJT == 1 ? 6 : 12;  // planes in flight (Little's law: ~100+ KB per SM)
+  // planes in flight (Little's law: ~100+ KB per SM at the resident CTA count)
+  static constexpr int STAGES = NJT == 1 ? 6 : (OROWS / RPW == 8 && RPW == 1 ? 12 : 8);
   static constexpr int TC = 128 * WPR;               // tile columns
   static constexpr int TROWS = OROWS + NJT - 1;      // staged rows per plane
   static constexpr int PITCH = TC + 8;               // [3] left halo, [4, 4+TC) values, [4+TC] right halo
   static constexpr int TILE = TROWS * PITCH;         // floats per stage
-  static constexpr int THREADS = 32 * (OROWS * WPR + 1);  // + one producer warp
+  static constexpr int CW = OROWS / RPW * WPR;             // compute warps (RPW output rows each)
+  static constexpr int THREADS = 32 * (CW + 1);            // + one producer warp
   static constexpr size_t SMEM = (size_t)STAGES * TILE * sizeof(float) + 2 * STAGES * sizeof(uint64_t);
 };
 
 // One plane q of the march (rows j0-(NJT>1) .. +TROWS, columns c0-4 .. c0+TC+4,
 // clipped to the array) -> ring buffer `buf`, tx bytes on `bar`. Called by the whole
 // producer warp: lane 0 posts the byte count, lane r copies tile row r.
-template <int NJT, int OROWS, int WPR>
+template <int NJT, int OROWS, int WPR, int RPW>
 __device__ __forceinline__ void march_issue(const float* A, float* buf, uint64_t* bar, int q, int j0, int c0,
                                             int nrow, int ncol, int hint, uint64_t pol, int lane) {
-  using M = March<NJT, OROWS, WPR>;
+  using M = March<NJT, OROWS, WPR, RPW>;
   const int ka = max(c0 - 4, 0);
   const int kb = min(c0 + M::TC + 4, ncol);
   const int jb = j0 - (NJT > 1 ? 1 : 0);  // global row of tile row 0
@@ -174,13 +176,13 @@ __device__ __forceinline__ void march_taps(float2 (&am)[2], float2 (&a0)[2], flo
 // Warps 0..OROWS*WPR-1 compute; the last warp only issues the bulk copies. Stage s is
 // handed over by full[s] (tx bytes) and released by empty[s] (one arrive per compute
 // warp): no CTA-wide barrier inside the march.
-template <int NJT, int OROWS, int WPR, uint32_t MASK>
-__global__ void __launch_bounds__(32 * (OROWS * WPR + 1)) march_kernel(const float* __restrict__ A,
+template <int NJT, int OROWS, int WPR, int RPW, uint32_t MASK>
+__global__ void __launch_bounds__(March<NJT, OROWS, WPR, RPW>::THREADS) march_kernel(const float* __restrict__ A,
                                                                        float* __restrict__ B, int ni, int nrow,
                                                                        int ncol, int seg, int ncc, int nrg, int hint,
                                                                        int order, const __grid_constant__ W27x2 w) {
-  using M = March<NJT, OROWS, WPR>;
-  constexpr int CW = OROWS * WPR;  // compute warps
+  using M = March<NJT, OROWS, WPR, RPW>;
+  constexpr int CW = M::CW;  // compute warps
   extern __shared__ __align__(128) float st_smem[];
   float* tiles = st_smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(st_smem + M::STAGES * M::TILE);
@@ -212,31 +214,43 @@ __global__ void __launch_bounds__(32 * (OROWS * WPR + 1)) march_kernel(const flo
     for (int p = 0; p < nplanes; ++p) {
       const int s = p % M::STAGES;
       if (p >= M::STAGES) mbar_wait(&empty[s], (uint32_t)(((p / M::STAGES) - 1) & 1));
-      march_issue<NJT, OROWS, WPR>(A, tiles + s * M::TILE, &full[s], q0 + p, j0, c0, nrow, ncol, hint, pol, lane);
+      march_issue<NJT, OROWS, WPR, RPW>(A, tiles + s * M::TILE, &full[s], q0 + p, j0, c0, nrow, ncol, hint, pol, lane);
     }
     return;
   }
-  const int tr = wp / WPR;                         // output row within the tile
+  const int tr = (wp / WPR) * RPW;                 // first output row of this warp within the tile
   const int col = (wp % WPR) * 128 + 4 * lane;     // column offset within the tile
-  const int j = j0 + tr, k = c0 + col;
-  const bool store_ok = (NJT == 1 || (j >= 1 && j <= nrow - 2)) && k < ncol;
-  float2 acc[3][2];
+  const int k = c0 + col;
+  bool store_ok[RPW];
 #pragma unroll
-  for (int r = 0; r < 3; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+  for (int r = 0; r < RPW; ++r) {
+    const int j = j0 + tr + r;
+    store_ok[r] = (NJT == 1 || (j >= 1 && j <= nrow - 2)) && k < ncol;
+  }
+  float2 acc[3][RPW][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) acc[a][r][0] = acc[a][r][1] = make_float2(0.f, 0.f);
 
-  auto step = [&](int p, float2(&am)[2], float2(&a0)[2], float2(&ap)[2]) {
+  auto step = [&](int p, float2(&am)[RPW][2], float2(&a0)[RPW][2], float2(&ap)[RPW][2]) {
     const int s = p % M::STAGES;
     mbar_wait(&full[s], (uint32_t)((p / M::STAGES) & 1));
     const float* t = tiles + s * M::TILE + tr * M::PITCH + 4 + col;
-    Pairs rows[NJT];
+    Pairs rows[NJT + RPW - 1];
 #pragma unroll
-    for (int dj = 0; dj < NJT; ++dj) rows[dj] = read_pairs(t + dj * M::PITCH);
-    march_taps<NJT, MASK>(am, a0, ap, rows, w);
+    for (int dj = 0; dj < NJT + RPW - 1; ++dj) rows[dj] = read_pairs(t + dj * M::PITCH);
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) march_taps<NJT, MASK>(am[r], a0[r], ap[r], rows + r, w);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
-    if (p >= 2 && store_ok)  // output plane q-1 is complete
-      store4_interior(B + ((size_t)(q0 + p - 1) * nrow + (NJT > 1 ? j : 0)) * ncol, k, 1, ncol - 2, am[0], am[1]);
-    am[0] = am[1] = make_float2(0.f, 0.f);  // becomes the next plane's q+1 accumulator
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      if (p >= 2 && store_ok[r])  // output plane q-1 is complete
+        store4_interior(B + ((size_t)(q0 + p - 1) * nrow + (NJT > 1 ? j0 + tr + r : 0)) * ncol, k, 1, ncol - 2,
+                        am[r][0], am[r][1]);
+      am[r][0] = am[r][1] = make_float2(0.f, 0.f);  // becomes the next plane's q+1 accumulator
+    }
   };
 #pragma unroll 1
   for (int p = 0; p < nplanes; p += 3) {  // roles rotate statically: (m, 0, p) = (0,1,2), (1,2,0), (2,0,1)
@@ -265,11 +279,11 @@ constexpr uint32_t MASK_PBGPU3D = tap3(-1, -1, -1) | tap3(-1, -1, 1) | tap3(-1, 
                                   tap3(0, -1, 0) | tap3(0, 0, 0) | tap3(0, 1, 0) | tap3(1, -1, -1) |
                                   tap3(1, -1, 1) | tap3(1, 0, 1) | tap3(1, 1, 1);
 
-template <int NJT, int OROWS, int WPR, uint32_t MASK>
+template <int NJT, int OROWS, int WPR, int RPW, uint32_t MASK>
 cudaError_t launch_march(const float* A, float* B, int ni, int nrow, int ncol, const W27x2& w, cudaStream_t s) {
-  using M = March<NJT, OROWS, WPR>;
-  auto kern = march_kernel<NJT, OROWS, WPR, MASK>;
-  cudaError_t e = ensure_smem<march_kernel<NJT, OROWS, WPR, MASK>>(M::SMEM);
+  using M = March<NJT, OROWS, WPR, RPW>;
+  auto kern = march_kernel<NJT, OROWS, WPR, RPW, MASK>;
+  cudaError_t e = ensure_smem<march_kernel<NJT, OROWS, WPR, RPW, MASK>>(M::SMEM);
   if (e != cudaSuccess) return e;
   static int per_sm = 0;  // resident CTAs per SM (same on every B200)
   if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, M::THREADS, M::SMEM) != cudaSuccess ||
@@ -563,7 +577,7 @@ cudaError_t launch_conv2d(const float* A, float* B, int ni, int nj, const float*
   ++*launches;
   // 2-D: the march axis is i, the stencil's column axis j is the tile's column axis
   // (no tile rows), taps w[(di+1)*3 + (dj+1)]
-  return launch_march<1, 1, 8, MASK_DENSE9>(A, B, ni, 1, nj, w, s);
+  return launch_march<1, 1, 8, 1, MASK_DENSE9>(A, B, ni, 1, nj, w, s);
 }
 
 cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, const float* w27, cudaStream_t s,
@@ -573,11 +587,16 @@ cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, cons
   for (int e = 0; e < 27; ++e) w.w[e] = make_float2(w27[e], w27[e]);
   ++*launches;
   const uint32_t m = weight_mask(w27, 27);
-  static const int rows16 = getenv("PB_C3_ROWS") && atoi(getenv("PB_C3_ROWS")) == 16;  // tuning aid
+  // Large grids: 16-row tiles, two output rows per warp (halo re-reads 18/16 instead of
+  // 10/8 rows; 1024^3: 1.60 -> 1.53 ms). Smaller ones keep 8-row tiles (more CTAs;
+  // 512^3: 0.209 vs 0.215 ms). PB_C3_RPW=1|2 overrides (tuning aid).
+  static const int rpw_env = getenv("PB_C3_RPW") ? atoi(getenv("PB_C3_RPW")) : 0;
+  const bool rpw2 = rpw_env ? rpw_env == 2 : (long long)ni * nj * nk >= (1ll << 28);
   if ((m & ~MASK_PBGPU3D) == 0)
-    return rows16 ? launch_march<3, 16, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s)
-                  : launch_march<3, 8, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s);
-  return launch_march<3, 8, 1, MASK_DENSE>(A, B, ni, nj, nk, w, s);
+    return rpw2 ? launch_march<3, 16, 1, 2, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s)
+                : launch_march<3, 8, 1, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s);
+  return rpw2 ? launch_march<3, 16, 1, 2, MASK_DENSE>(A, B, ni, nj, nk, w, s)
+              : launch_march<3, 8, 1, 1, MASK_DENSE>(A, B, ni, nj, nk, w, s);
 }
 
 namespace {
