@@ -106,6 +106,61 @@ __device__ void make_q(const GsArgs& a, const double* col, int k, double* red) {
   }
 }
 
+// q_k (this thread's rows in qr, the rest from L2) applied to NB owned columns at
+// base + c*cs (c < NB), global column index j0 + c*G: dot -> CTA reduce -> R -> axpy.
+template <int NB>
+__device__ __forceinline__ void gs_batch(const GsArgs& a, const double (&qr)[GS_QREG], const double* q, double* base,
+                                         size_t cs, int j0, int G, int k, double* red, double* rsum) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int m = a.m;
+  double part[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) part[c] = 0.0;
+#pragma unroll
+  for (int u = 0; u < GS_QREG; ++u) {
+    const int i = threadIdx.x + u * GS_THREADS;
+    if (i < m) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) part[c] += qr[u] * base[c * cs + i];
+    }
+  }
+  for (int i = threadIdx.x + GS_QREG * GS_THREADS; i < m; i += GS_THREADS) {
+    const double qi = ld_cg_f64(q + i);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) part[c] += qi * base[c * cs + i];
+  }
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    const double v = warp_sum_d(part[c]);
+    if (lane == 0) red[wp * GS_MAXC + c] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NB) {
+    double s = 0.0;
+    for (int w = 0; w < GS_WARPS; ++w) s += red[w * GS_MAXC + threadIdx.x];
+    rsum[threadIdx.x] = s;
+    a.R[(size_t)k * a.n + (j0 + threadIdx.x * G)] = (float)s;
+  }
+  __syncthreads();
+  double r[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) r[c] = rsum[c];
+#pragma unroll
+  for (int u = 0; u < GS_QREG; ++u) {
+    const int i = threadIdx.x + u * GS_THREADS;
+    if (i < m) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) base[c * cs + i] -= qr[u] * r[c];
+    }
+  }
+  for (int i = threadIdx.x + GS_QREG * GS_THREADS; i < m; i += GS_THREADS) {
+    const double qi = ld_cg_f64(q + i);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) base[c * cs + i] -= qi * r[c];
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(GS_THREADS, 1) gs_kernel(GsArgs a) {
   extern __shared__ __align__(16) double gs_smem[];
   __shared__ double red[GS_WARPS * GS_MAXC];
@@ -181,41 +236,21 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gs_kernel(GsArgs a) {
       }
       tb = t0 + 1;
     }
-    // the other owned columns j > k+1, in batches of GS_MAXC
+    // the other owned columns j > k+1, in batches of up to GS_MAXC with a compile-time
+    // width (no predicated work for absent columns): dot -> CTA reduce -> axpy
     for (int b0 = tb; b0 < nown; b0 += GS_MAXC) {
       const int nb = min(GS_MAXC, nown - b0);
-      double part[GS_MAXC];
-#pragma unroll
-      for (int c = 0; c < GS_MAXC; ++c) part[c] = 0.0;
-      rows([&](int i, double qi) {
-#pragma unroll
-        for (int c = 0; c < GS_MAXC; ++c)
-          if (c < nb) part[c] += qi * colp(b0 + c)[i];
-      });
-#pragma unroll
-      for (int c = 0; c < GS_MAXC; ++c) {
-        if (c < nb) {
-          const double v = warp_sum_d(part[c]);
-          if (lane == 0) red[wp * GS_MAXC + c] = v;
-        }
+      double* base = colp(b0);
+      const size_t cs = a.in_smem ? (size_t)m : (size_t)G * m;  // column stride
+      const int j0 = cta + b0 * G;
+      switch (nb) {
+#define PB_GS_CASE(N) \
+  case N: gs_batch<N>(a, qr, q, base, cs, j0, G, k, red, rsum); break;
+        PB_GS_CASE(1) PB_GS_CASE(2) PB_GS_CASE(3) PB_GS_CASE(4) PB_GS_CASE(5) PB_GS_CASE(6) PB_GS_CASE(7)
+        PB_GS_CASE(8) PB_GS_CASE(9) PB_GS_CASE(10) PB_GS_CASE(11) PB_GS_CASE(12) PB_GS_CASE(13) PB_GS_CASE(14)
+        PB_GS_CASE(15) PB_GS_CASE(16)
+#undef PB_GS_CASE
       }
-      __syncthreads();
-      if (threadIdx.x < nb) {
-        double s = 0.0;
-        for (int w = 0; w < GS_WARPS; ++w) s += red[w * GS_MAXC + threadIdx.x];
-        rsum[threadIdx.x] = s;
-        a.R[(size_t)k * n + (cta + (b0 + threadIdx.x) * G)] = (float)s;
-      }
-      __syncthreads();
-      rows([&](int i, double qi) {
-#pragma unroll
-        for (int c = 0; c < GS_MAXC; ++c)
-          if (c < nb) {
-            double* cp = colp(b0 + c);
-            cp[i] = cp[i] - qi * rsum[c];
-          }
-      });
-      __syncthreads();
     }
   }
   if (a.in_smem) {
