@@ -218,3 +218,32 @@ def test_conv_zero_weights():
     pb.pb_conv3d(37, 9, 132, [0.0] * 27, A, B)
     g = P.host(B).reshape(37, 9, 132)
     assert np.all(g[1:-1, 1:-1, 1:-1] == 0)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_conv_row_blocks_equal_whole(G):
+    """Row-block sharding of the convolutions needs no new entry point and no data-path
+    exchange: rank g calls pb_conv2d / pb_conv3d on its rows (planes) plus one halo row
+    (plane) on each side; the local call leaves its first and last rows unwritten, which
+    are exactly the halo. The union equals the single call bitwise (per-point FMA order
+    is independent of the decomposition)."""
+    ni, nj = 1000, 1028
+    A = P.dev(P.H(ni, nj, 1))
+    whole = P.dev(P.H(ni, nj, 2))
+    pb.pb_conv2d(ni, nj, pbgen.CONV2D_W, A, whole)
+    sharded = P.dev(P.H(ni, nj, 2))
+    for g in range(G):
+        r0, r1 = pb.pb_row_partition(ni, G, g)
+        lo, hi = max(r0 - 1, 0), min(r1 + 1, ni)
+        pb.pb_conv2d(hi - lo, nj, pbgen.CONV2D_W, A[lo:hi], sharded[lo:hi])
+    assert np.array_equal(P.host(whole).view(np.uint32), P.host(sharded).view(np.uint32))
+    n3, nj3, nk3 = 67, 33, 260
+    A3 = P.dev(P.H(n3 * nj3, nk3, 1)).view(n3, nj3, nk3)
+    w3 = torch.zeros(n3, nj3, nk3, device="cuda")
+    s3 = torch.zeros(n3, nj3, nk3, device="cuda")
+    pb.pb_conv3d(n3, nj3, nk3, pbgen.conv3d_w27(), A3, w3)
+    for g in range(G):
+        p0, p1 = pb.pb_row_partition(n3, G, g)
+        lo, hi = max(p0 - 1, 0), min(p1 + 1, n3)
+        pb.pb_conv3d(hi - lo, nj3, nk3, pbgen.conv3d_w27(), A3[lo:hi], s3[lo:hi])
+    assert np.array_equal(P.host(w3).view(np.uint32), P.host(s3).view(np.uint32))
