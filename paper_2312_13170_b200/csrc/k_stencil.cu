@@ -396,7 +396,8 @@ __global__ void __launch_bounds__(256) fdtd_step_kernel(const float* __restrict_
 // but the staleness moves inward one point per step, so after FT_H steps the core
 // is still exact. Then the tiles exchange: each publishes its core into a
 // parity-double-buffered copy of the grid in global memory (L2-resident), releases
-// its epoch flag, acquires its 8 neighbours' flags and reloads its region. HBM sees
+// its epoch flag, acquires its 8 neighbours' flags and reloads its halo ring (only
+// the core's FT_H-wide outer band is published, only the ring is read back). HBM sees
 // the state once in and once out; one neighbour round trip through L2 per FT_H steps
 // replaces FT_H kernel launches. Every update is the PolyBench statement's fp32
 // operations, so the result is bitwise the sequential sweeps'.
@@ -453,8 +454,11 @@ __global__ void __launch_bounds__(FT_THREADS, 1) fdtd_persist_kernel(float* __re
     const float* gy = e == 0 ? ey : gx + N;
     const float* gh = e == 0 ? hz : gx + 2 * N;
     if (e > 0) ft_wait_neighbours(flags, ti, tj, tiles_i, tiles_j, (unsigned)e);
+    // epoch 0 loads the whole region; later epochs only the halo ring (the core in
+    // shared memory is exact: it is this tile's own state)
     for (int g = tid; g < FT_GROUPS; g += FT_THREADS) {
       const int r = g / (FT_RJ / 4), c = (g % (FT_RJ / 4)) * 4;
+      if (e > 0 && r >= FT_H && r < FT_H + FT_I && c >= FT_H && c < FT_H + FT_J) continue;
       const int i = i0 - FT_H + r, j = j0 - FT_H + c;
       float4 x = make_float4(0.f, 0.f, 0.f, 0.f), y = x, h = x;
       if (i >= 0 && i < nx && j >= 0 && j < ny) {
@@ -549,6 +553,8 @@ __global__ void __launch_bounds__(FT_THREADS, 1) fdtd_persist_kernel(float* __re
     float* ph = last ? hz : px + 2 * N;
     for (int g = tid; g < FT_I * FT_J / 4; g += FT_THREADS) {
       const int r = g / (FT_J / 4), c = (g % (FT_J / 4)) * 4;
+      // exchange copies need only the core's outer FT_H-wide band (what neighbours' halos read)
+      if (!last && r >= FT_H && r < FT_I - FT_H && c >= FT_H && c < FT_J - FT_H) continue;
       const int i = i0 + r, j = j0 + c;
       if (i < nx && j < ny) {
         const size_t o = (size_t)i * ny + j;
