@@ -144,9 +144,14 @@ class Suite:
         if "gemm" in kernels and rank == 0:
             n = GEMM_N
             t["gemm"] = dict(A=gen(n, n, S["A"]), B=gen(n, n, S["B"]), C=gen(n, n, S["C"]))
-        if rank == 0 and ("covariance" in kernels or "correlation" in kernels):
+        if "covariance" in kernels or "correlation" in kernels:
+            # one GPU: the whole matrix (banded single-pass path); N > 1: the data
+            # replicated, each rank computes its output row band (no exchange)
             n = STAT_N
-            t["stat"] = dict(data=gen(n, n, S["data"]), cov=e(n, n), corr=e(n, n), mean=e(n), sd=e(n))
+            r0, r1 = pb.pb_row_partition(n, world, rank, False, 128) if world > 1 else (0, n)
+            self.stat_rows = (r0, r1)
+            t["stat"] = dict(data=gen(n, n, S["data"]), cov=e(max(r1 - r0, 1), n), corr=e(max(r1 - r0, 1), n),
+                             mean=e(n), sd=e(n))
         if "2mm" in kernels or "3mm" in kernels:
             n = MM_N
             r0, r1 = pb.pb_row_partition(n, world, rank, False, 128)
@@ -187,7 +192,9 @@ class Suite:
         return t
 
     def ws_dims(self):
-        out = [("gemm", (GEMM_N,) * 3), ("covariance", (STAT_N, STAT_N)), ("2mm", (MM_N,) * 4),
+        out = [("gemm", (GEMM_N,) * 3), ("covariance", (STAT_N, STAT_N)),
+               ("covariance_rows", (STAT_N, STAT_N) + tuple(getattr(self, "stat_rows", (0, STAT_N)))),
+               ("2mm", (MM_N,) * 4),
                ("3mm", (MM_N,) * 5), ("gemm", (MM_N,) * 3), ("syr2k_rows", (SY_N, SY_N, 0, SY_N)),
                ("matvec_partial", (MV_N, MV_N)), ("atax", (MV_N, MV_N)), ("gesummv", (MV_N,))]
         if self.D.comm() is not None:  # pb_<k>_dist entry points: dims + (nranks, rank)
@@ -205,16 +212,22 @@ class Suite:
                 return 0
             g = t["gemm"]
             pb.pb_gemm(GEMM_N, GEMM_N, GEMM_N, ALPHA, BETA, g["C"], g["A"], g["B"], ws=ws)
-        elif k == "covariance":
-            if self.rank != 0:
-                return 0
+        elif k in ("covariance", "correlation"):
             s = t["stat"]
-            pb.pb_covariance(STAT_N, STAT_N, float(STAT_N), s["data"], s["cov"], s["mean"], ws=ws)
-        elif k == "correlation":
-            if self.rank != 0:
+            r0, r1 = self.stat_rows
+            if self.world == 1:
+                if k == "covariance":
+                    pb.pb_covariance(STAT_N, STAT_N, float(STAT_N), s["data"], s["cov"], s["mean"], ws=ws)
+                else:
+                    pb.pb_correlation(STAT_N, STAT_N, float(STAT_N), EPS, s["data"], s["corr"], s["mean"], s["sd"],
+                                      ws=ws)
+            elif r1 <= r0:
                 return 0
-            s = t["stat"]
-            pb.pb_correlation(STAT_N, STAT_N, float(STAT_N), EPS, s["data"], s["corr"], s["mean"], s["sd"], ws=ws)
+            elif k == "covariance":
+                pb.pb_covariance_rows(STAT_N, STAT_N, float(STAT_N), r0, r1, s["data"], s["cov"], s["mean"], ws=ws)
+            else:
+                pb.pb_correlation_rows(STAT_N, STAT_N, float(STAT_N), EPS, r0, r1, s["data"], s["corr"], s["mean"],
+                                       s["sd"], ws=ws)
         elif k == "2mm":
             m = t["mm"]
             return D.mm2_rows(self, MM_N, ALPHA, BETA, m["tmp"], m["A"], m["B"], m["C"], m["D"], ws)

@@ -137,6 +137,20 @@ pb_status pb_covariance(int m, int n, float float_n, const float* data, float* c
 pb_status pb_correlation(int m, int n, float float_n, float eps, const float* data, float* corr,
                          float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s);
 
+/* Row bands of covariance / correlation (multi-GPU: the data replicated on every
+ * rank, output rows [r0, r1) per rank, no exchange; SURVEY.md §8(e) "alternative").
+ * cov_blk / corr_blk: (r1 - r0) x m, rows r0.. of the full result (both triangles;
+ * corr's diagonal entries in the band are exactly 1). r0 a multiple of 128,
+ * 0 <= r0 < r1 <= m. Centring by the exact mean first (the long-column path of
+ * reading R18), so the band is symmetric with the other ranks' bands only up to
+ * rounding (the single call mirrors; bands cannot). mean / stddev (optional) get
+ * all m values. ws: pb_workspace_size("covariance_rows" | "correlation_rows",
+ * {m, n, r0, r1}). */
+pb_status pb_covariance_rows(int m, int n, float float_n, int r0, int r1, const float* data, float* cov_blk,
+                             float* mean, void* ws, size_t ws_bytes, pb_stream s);
+pb_status pb_correlation_rows(int m, int n, float float_n, float eps, int r0, int r1, const float* data,
+                              float* corr_blk, float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s);
+
 /* atax — PolyBench kernel_atax:  tmp = A*x;  y = A^T * tmp
  * A m x n, x n, y n (out), tmp m (optional out). */
 pb_status pb_atax(int m, int n, const float* A, const float* x, float* y, float* tmp, void* ws,

@@ -23,7 +23,7 @@ __all__ = [
     "pb_comm_destroy", "pb_gemm_dist", "pb_2mm_dist", "pb_3mm_dist", "pb_syrk_dist", "pb_syr2k_dist",
     "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist", "Peer", "pb_peer_create",
     "pb_comm_init_local", "pb_comm_attach_peer", "pb_conv2d", "pb_conv3d", "pb_fdtd_2d",
-    "pb_gramschmidt",
+    "pb_gramschmidt", "pb_covariance_rows", "pb_correlation_rows",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -65,6 +65,8 @@ ABI_FUNCTIONS = {
     "pb_conv3d": ([_I, _I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
     "pb_fdtd_2d": ([_I, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gramschmidt": ([_I, _I, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_covariance_rows": ([_I, _I, _F, _I, _I, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_correlation_rows": ([_I, _I, _F, _F, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
     # multi-GPU (NCCL inside libpb)
     "pb_comm_unique_id": ([_P], _I),
     "pb_comm_init": ([_I, _I, _P, ctypes.POINTER(_P)], _I),
@@ -244,6 +246,18 @@ def pb_correlation(m, n_, float_n, eps, data, corr, mean=None, stddev=None, ws=N
     p, n, keep = _ws(ws, "correlation", (m, n_), corr)
     _check("pb_correlation", lib().pb_correlation(m, n_, float_n, eps, _ptr(data), _ptr(corr), _ptr(mean),
                                                   _ptr(stddev), p, n, _stream(stream, corr)))
+
+
+def pb_covariance_rows(m, n_, float_n, r0, r1, data, cov_blk, mean=None, ws=None, stream=None):
+    p, n, keep = _ws(ws, "covariance_rows", (m, n_, r0, r1), cov_blk)
+    _check("pb_covariance_rows", lib().pb_covariance_rows(m, n_, float_n, r0, r1, _ptr(data), _ptr(cov_blk),
+                                                          _ptr(mean), p, n, _stream(stream, cov_blk)))
+
+
+def pb_correlation_rows(m, n_, float_n, eps, r0, r1, data, corr_blk, mean=None, stddev=None, ws=None, stream=None):
+    p, n, keep = _ws(ws, "correlation_rows", (m, n_, r0, r1), corr_blk)
+    _check("pb_correlation_rows", lib().pb_correlation_rows(m, n_, float_n, eps, r0, r1, _ptr(data), _ptr(corr_blk),
+                                                            _ptr(mean), _ptr(stddev), p, n, _stream(stream, corr_blk)))
 
 
 def pb_atax(m, n_, A, x, y, tmp=None, ws=None, stream=None):

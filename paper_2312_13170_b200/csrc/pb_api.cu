@@ -129,6 +129,15 @@ WsStat ws_stat(Carve& c, int m, int n) {
   }
   return w;
 }
+// covariance/correlation row band [r0, r1) (multi-GPU: replicated data, output row
+// blocks, no exchange): exact-mean prep of all m variables + a full-width GEMM.
+struct WsStatRows { SplitBuf xt; SplitK sk; };
+WsStatRows ws_stat_rows(Carve& c, int m, int n, int r0, int r1) {
+  WsStatRows w;
+  w.xt = take_split(c, m, n);
+  w.sk = take_splitk(c, {shape(r1, m, n, 1, EPI_OUT, r0 / 128, (r1 + 127) / 128)});
+  return w;
+}
 struct WsSyrk { SplitBuf a, b; SplitK sk; };
 WsSyrk ws_syrk(Carve& c, int n, int m, int r0, int r1, bool two, bool full = false) {
   WsSyrk w;
@@ -260,6 +269,7 @@ pb_status pb_workspace_size(const char* kernel, const long long* d, int nd, size
   else if (k == "conv3d" && need(3)) (void)0;
   else if (k == "fdtd_2d" && need(2)) c.take<char>(fdtd_ws_bytes(d[0], d[1]));
   else if (k == "gramschmidt" && need(2)) c.take<char>(gramschmidt_ws_bytes(d[0], d[1]));
+  else if ((k == "covariance_rows" || k == "correlation_rows") && need(4)) ws_stat_rows(c, d[0], d[1], d[2], d[3]);
   else return fail(PB_ERR_INVALID_ARG, "unknown kernel '%s' or wrong number of dims (%d)", kernel, nd);
   *bytes = align_up(c.off, 256);
   return PB_OK;
@@ -541,6 +551,54 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
             us(b[0]), us(b[1]), us(b[2]), us(b[3]));
   }
   return PB_OK;
+}
+
+static pb_status stat_rows_core(bool corr, int m, int n, float float_n, float eps, int r0, int r1, const float* data,
+                                float* out_blk, float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s) {
+  Check ck;
+  ck.dims({m, n});
+  if (ck.st == PB_OK && (r0 < 0 || r1 > m || r0 >= r1 || r0 % 128 != 0))
+    ck.st = fail(PB_ERR_INVALID_ARG, "row range [%d,%d) invalid (r0 multiple of 128, r1 <= m)", r0, r1);
+  if (ck.st == PB_OK && !corr && n < 2) ck.st = fail(PB_ERR_INVALID_ARG, "covariance needs n >= 2");
+  if (ck.st == PB_OK && !(float_n > 0.f)) ck.st = fail(PB_ERR_INVALID_ARG, "float_n must be > 0");
+  if (ck.st == PB_OK && !corr && float_n == 1.0f) ck.st = fail(PB_ERR_INVALID_ARG, "float_n - 1 == 0");
+  ck.cols4(m, "data/out");
+  ck.arr(data, n, m, false, "data");
+  ck.arr(out_blk, r1 - r0, m, true, corr ? "corr" : "cov");
+  ck.arr(mean, 1, m, true, "mean", false);
+  if (corr) ck.arr(stddev, 1, m, true, "stddev", false);
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  ws_stat_rows(need, m, n, r0, r1);
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  Carve c(ws, ws_bytes);
+  WsStatRows w = ws_stat_rows(c, m, n, r0, r1);
+  cudaStream_t st = S(s);
+  int L = 0;
+  PB_CUDA(launch_stats_split(data, n, m, (double)float_n, (double)eps, corr, w.xt.hi, w.xt.lo, w.xt.ld, mean,
+                             corr ? stddev : nullptr, st));
+  ++L;
+  GemmDesc d;  // rows [r0, r1) of X^T X over every column (both triangles: no mirror across ranks)
+  d.M = r1; d.N = m; d.K = n;
+  d.a[0] = w.xt.op(); d.b[0] = w.xt.op();
+  d.flags = EPI_OUT | (corr ? EPI_DIAG_ONE : 0u);
+  d.alpha = corr ? 1.0f : (float)(1.0 / ((double)float_n - 1.0));
+  d.out = out_blk; d.ldo = m; d.out_row0 = r0;
+  d.tm0 = r0 / 128; d.tm1 = (r1 + 127) / 128;
+  w.sk.attach(d);
+  PB_CUDA(launch_umma_gemm(d, st, &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_covariance_rows(int m, int n, float float_n, int r0, int r1, const float* data, float* cov_blk,
+                             float* mean, void* ws, size_t ws_bytes, pb_stream s) {
+  return stat_rows_core(false, m, n, float_n, 0.f, r0, r1, data, cov_blk, mean, nullptr, ws, ws_bytes, s);
+}
+
+pb_status pb_correlation_rows(int m, int n, float float_n, float eps, int r0, int r1, const float* data,
+                              float* corr_blk, float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s) {
+  return stat_rows_core(true, m, n, float_n, eps, r0, r1, data, corr_blk, mean, stddev, ws, ws_bytes, s);
 }
 
 pb_status pb_covariance(int m, int n, float float_n, const float* data, float* cov, float* mean, void* ws,

@@ -20,7 +20,7 @@ import paper_2312_13170_b200 as pb  # noqa: E402
 import pbgen  # noqa: E402
 
 dev = torch.device("cuda", 0)
-MM, SY, MV = 4096, 8192, 32768
+MM, SY, MV, ST = 4096, 8192, 32768, 2048
 
 
 def g(r, c, s):
@@ -54,8 +54,23 @@ def main():
     Amv = g(MV, MV, 1)
     Bmv = g(MV // 2, MV, 2)  # gesummv's B block (the largest block needed is half)
     x = g(1, MV, 6).view(-1)
+    data = g(ST, ST, 5)
     for G in (1, 2, 4, 8):
         res = {}
+        # covariance / correlation: G = 1 is the single-GPU call (banded, triangle + mirror);
+        # G > 1 a rank's row band of the replicated-data path (pb_<k>_rows)
+        cov, mean, sd = torch.empty(ST, ST, device=dev), torch.empty(ST, device=dev), torch.empty(ST, device=dev)
+        if G == 1:
+            wss = pb.workspace("covariance", (ST, ST), dev)
+            res["covariance"] = timed(lambda: pb.pb_covariance(ST, ST, float(ST), data, cov, mean, ws=wss))
+            res["correlation"] = timed(lambda: pb.pb_correlation(ST, ST, float(ST), 0.1, data, cov, mean, sd, ws=wss))
+        else:
+            b, e = pb.pb_row_partition(ST, G, 0, 0, 128)
+            wsr = pb.workspace("covariance_rows", (ST, ST, b, e), dev)
+            res["covariance"] = timed(lambda: pb.pb_covariance_rows(ST, ST, float(ST), b, e, data, cov[:e - b], mean,
+                                                                    ws=wsr))
+            res["correlation"] = timed(lambda: pb.pb_correlation_rows(ST, ST, float(ST), 0.1, b, e, data, cov[:e - b],
+                                                                      mean, sd, ws=wsr))
         r0, r1 = pb.pb_row_partition(MM, G, 0, 0, 128)  # uniform blocks: rank 0 is representative
         rows = r1 - r0
         tmp, D2 = torch.empty(rows, MM, device=dev), Dmm[:rows].clone()

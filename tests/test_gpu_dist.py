@@ -280,7 +280,7 @@ def test_bench_two_ranks_share_gpu(transport):
         env["PB_TRANSPORT"] = "local"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "3",
-           "--no-cpu", "--no-e2e", "--kernels", "3mm,atax,bicg,mvt,gesummv"]
+           "--no-cpu", "--no-e2e", "--kernels", "3mm,covariance,correlation,atax,bicg,mvt,gesummv"]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")][-1])
@@ -365,3 +365,34 @@ def test_comm_and_peer_argument_errors():
         comm.close()
         p1.close()
         p2.close()
+
+
+@pytest.mark.parametrize("m,n,G", [(260, 300, 2), (516, 2048, 3), (2048, 2048, 8), (128, 3000, 1)])
+def test_cov_corr_row_bands(m, n, G):
+    """pb_covariance_rows / pb_correlation_rows (replicated data, output row blocks, no
+    exchange): the bands of every rank assemble the full result within the parity
+    tolerance; correlation's diagonal is exactly 1."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_13170_b200 as pb
+    from tests import parity as P
+    data = P.structured_data(n, m)
+    dd = P.dev(data)
+    for corr in (False, True):
+        full = np.zeros((m, m), np.float32)
+        for g in range(G):
+            r0, r1 = pb.pb_row_partition(m, G, g, False, 128)
+            if r1 <= r0:
+                continue
+            blk = torch.empty(r1 - r0, m, device="cuda")
+            if corr:
+                pb.pb_correlation_rows(m, n, float(n), 0.1, r0, r1, dd, blk)
+            else:
+                pb.pb_covariance_rows(m, n, float(n), r0, r1, dd, blk)
+            full[r0:r1] = P.host(blk)
+        if corr:
+            r, s = oracle.correlation(float(n), 0.1, data)[0], oracle.correlation(float(n), 0.1, data, absmode=True)[0]
+            assert np.all(np.diag(full) == 1.0)
+        else:
+            r, s = oracle.covariance(float(n), data)[0], oracle.covariance(float(n), data, absmode=True)[0]
+        assert P.cerr(full, r, s) <= P.TOL, (corr, P.cerr(full, r, s))
