@@ -376,6 +376,13 @@ pb_status pb_conv3d(int ni, int nj, int nk, const float* w, const float* A, floa
 pb_status pb_fdtd_2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                      size_t ws_bytes, pb_stream s);
 
+/* Stencil ablation (as pb_gemm_variant for GEMM): variant 0 = the SYCL-Bench kernel
+ * shape - one thread per output point, every tap a global load, no staging;
+ * variant 1 = pb_conv2d / pb_conv3d. Same arguments and semantics. */
+pb_status pb_conv2d_variant(int variant, int ni, int nj, const float* w, const float* A, float* B, pb_stream s);
+pb_status pb_conv3d_variant(int variant, int ni, int nj, int nk, const float* w, const float* A, float* B,
+                            pb_stream s);
+
 /* gramschmidt (R22) — PolyBench/C 4.2 kernel_gramschmidt (the SYCL-Bench
  * "Gramschmidt" of PAPER.md:524; PAPER.md:551 notes its candidate loop sits in a
  * divergent region). Modified Gram-Schmidt, for k < n:

@@ -23,7 +23,7 @@ __all__ = [
     "pb_comm_destroy", "pb_gemm_dist", "pb_2mm_dist", "pb_3mm_dist", "pb_syrk_dist", "pb_syr2k_dist",
     "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist", "Peer", "pb_peer_create",
     "pb_comm_init_local", "pb_comm_attach_peer", "pb_conv2d", "pb_conv3d", "pb_fdtd_2d",
-    "pb_gramschmidt", "pb_covariance_rows", "pb_correlation_rows",
+    "pb_gramschmidt", "pb_covariance_rows", "pb_correlation_rows", "pb_conv2d_variant", "pb_conv3d_variant",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -63,6 +63,8 @@ ABI_FUNCTIONS = {
     "pb_gesummv_rows": ([_I, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_conv2d": ([_I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
     "pb_conv3d": ([_I, _I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
+    "pb_conv2d_variant": ([_I, _I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
+    "pb_conv3d_variant": ([_I, _I, _I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
     "pb_fdtd_2d": ([_I, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gramschmidt": ([_I, _I, _P, _P, _P, _P, _Z, _P], _I),
     "pb_covariance_rows": ([_I, _I, _F, _I, _I, _P, _P, _P, _P, _Z, _P], _I),
@@ -309,6 +311,16 @@ def pb_conv2d(ni, nj, w, A, B, stream=None):
 def pb_conv3d(ni, nj, nk, w, A, B, stream=None):
     """w: 27 weights (host), w[(di+1)*9 + (dj+1)*3 + (dk+1)]."""
     _check("pb_conv3d", lib().pb_conv3d(ni, nj, nk, _host_w(w, 27), _ptr(A), _ptr(B), _stream(stream, B)))
+
+
+def pb_conv2d_variant(variant, ni, nj, w, A, B, stream=None):
+    _check("pb_conv2d_variant", lib().pb_conv2d_variant(variant, ni, nj, _host_w(w, 9), _ptr(A), _ptr(B),
+                                                        _stream(stream, B)))
+
+
+def pb_conv3d_variant(variant, ni, nj, nk, w, A, B, stream=None):
+    _check("pb_conv3d_variant", lib().pb_conv3d_variant(variant, ni, nj, nk, _host_w(w, 27), _ptr(A), _ptr(B),
+                                                        _stream(stream, B)))
 
 
 def pb_fdtd_2d(tmax, nx, ny, ex, ey, hz, fict, ws=None, stream=None):

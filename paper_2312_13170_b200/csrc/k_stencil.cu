@@ -574,6 +574,43 @@ __global__ void __launch_bounds__(FT_THREADS, 1) fdtd_persist_kernel(float* __re
   }
 }
 
+
+// ---- ablation: the SYCL-Bench kernel shape (one work-item per output point, every
+// tap a global load, no staging: what the paper's loop internalization would have to
+// stage, PAPER.md:551 notes it did not apply to these). Weights from the parameter
+// block; same FMA order per point as the march kernel's rows (dj outer... per tap).
+__global__ void __launch_bounds__(256) conv2d_naive_kernel(const float* __restrict__ A, float* __restrict__ B, int ni,
+                                                           int nj, const __grid_constant__ W27x2 w) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = g / nj, j = g % nj;
+  if (i < 1 || i >= ni - 1 || j < 1 || j >= nj - 1) return;
+  float acc = 0.f;
+#pragma unroll
+  for (int di = -1; di <= 1; ++di)
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj) acc = fmaf(w.w[(di + 1) * 3 + (dj + 1)].x, A[(i + di) * nj + (j + dj)], acc);
+  B[i * nj + j] = acc;
+}
+
+__global__ void __launch_bounds__(256) conv3d_naive_kernel(const float* __restrict__ A, float* __restrict__ B, int ni,
+                                                           int nj, int nk, const __grid_constant__ W27x2 w) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long k = g % nk, j = (g / nk) % nj, i = g / ((long long)nk * nj);
+  if (i < 1 || i >= ni - 1 || j < 1 || j >= nj - 1 || k < 1 || k >= nk - 1) return;
+  const long long pl = (long long)nj * nk;
+  float acc = 0.f;
+#pragma unroll
+  for (int di = -1; di <= 1; ++di)
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj)
+#pragma unroll
+      for (int dk = -1; dk <= 1; ++dk) {
+        const float wv = w.w[(di + 1) * 9 + (dj + 1) * 3 + (dk + 1)].x;
+        if (wv != 0.f) acc = fmaf(wv, A[(i + di) * pl + (j + dj) * nk + (k + dk)], acc);
+      }
+  B[(i * nj + j) * nk + k] = acc;
+}
+
 }  // namespace
 
 cudaError_t launch_conv2d(const float* A, float* B, int ni, int nj, const float* w9, cudaStream_t s, int* launches) {
@@ -612,6 +649,19 @@ size_t fdtd_persist_ws(int nx, int ny) {
   return 2 * align_up(3 * (size_t)nx * ny * sizeof(float), 256) + align_up(tiles * sizeof(unsigned), 256);
 }
 }  // namespace
+
+cudaError_t launch_conv_naive(bool three_d, const float* A, float* B, int ni, int nj, int nk, const float* w,
+                              cudaStream_t s, int* launches) {
+  if (ni < 3 || nj < 3 || (three_d && nk < 3)) return cudaSuccess;
+  W27x2 wp = {};
+  for (int e = 0; e < (three_d ? 27 : 9); ++e) wp.w[e] = make_float2(w[e], w[e]);
+  const long long pts = (long long)ni * nj * (three_d ? nk : 1);
+  const unsigned grid = (unsigned)((pts + 255) / 256);
+  ++*launches;
+  if (three_d) conv3d_naive_kernel<<<grid, 256, 0, s>>>(A, B, ni, nj, nk, wp);
+  else conv2d_naive_kernel<<<grid, 256, 0, s>>>(A, B, ni, nj, wp);
+  return cudaGetLastError();
+}
 
 size_t fdtd_ws_bytes(int nx, int ny) {
   return std::max(3 * align_up((size_t)nx * ny * sizeof(float), 256), fdtd_persist_ws(nx, ny));

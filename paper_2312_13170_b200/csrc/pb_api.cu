@@ -801,6 +801,37 @@ pb_status pb_conv2d(int ni, int nj, const float* w, const float* A, float* B, pb
   return PB_OK;
 }
 
+pb_status pb_conv2d_variant(int variant, int ni, int nj, const float* w, const float* A, float* B, pb_stream s) {
+  if (variant == 1) return pb_conv2d(ni, nj, w, A, B, s);
+  if (variant != 0) return fail(PB_ERR_INVALID_ARG, "variant %d (0 = naive, 1 = production)", variant);
+  Check ck;
+  ck.dims({ni, nj});
+  ck.cols4(nj, "A/B");
+  if (ck.st == PB_OK && w == nullptr) ck.st = fail(PB_ERR_INVALID_ARG, "w is NULL");
+  ck.arr(A, ni, nj, false, "A"); ck.arr(B, ni, nj, true, "B");
+  PB_TRY(ck.finish());
+  int L = 0;
+  PB_CUDA(launch_conv_naive(false, A, B, ni, nj, 1, w, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
+pb_status pb_conv3d_variant(int variant, int ni, int nj, int nk, const float* w, const float* A, float* B,
+                            pb_stream s) {
+  if (variant == 1) return pb_conv3d(ni, nj, nk, w, A, B, s);
+  if (variant != 0) return fail(PB_ERR_INVALID_ARG, "variant %d (0 = naive, 1 = production)", variant);
+  Check ck;
+  ck.dims({ni, nj, nk});
+  ck.cols4(nk, "A/B");
+  if (ck.st == PB_OK && w == nullptr) ck.st = fail(PB_ERR_INVALID_ARG, "w is NULL");
+  ck.arr(A, (long long)ni * nj, nk, false, "A"); ck.arr(B, (long long)ni * nj, nk, true, "B");
+  PB_TRY(ck.finish());
+  int L = 0;
+  PB_CUDA(launch_conv_naive(true, A, B, ni, nj, nk, w, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
 pb_status pb_conv3d(int ni, int nj, int nk, const float* w, const float* A, float* B, pb_stream s) {
   Check ck;
   ck.dims({ni, nj, nk});

@@ -125,6 +125,9 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
 cudaError_t launch_conv2d(const float* A, float* B, int ni, int nj, const float* w9, cudaStream_t s, int* launches);
 cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, const float* w27, cudaStream_t s,
                           int* launches);
+// ablation: one thread per output point, every tap a global load (SYCL-Bench shape)
+cudaError_t launch_conv_naive(bool three_d, const float* A, float* B, int ni, int nj, int nk, const float* w,
+                              cudaStream_t s, int* launches);
 size_t fdtd_ws_bytes(int nx, int ny);
 cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                           cudaStream_t s, int* launches);

@@ -135,9 +135,37 @@ def gramschmidt(n, reps):
                 gflops=flops / med / 1e6, launches=pb.last_launch_count())
 
 
+def ablation():
+    """The paper's question for the stencils (loop internalization did
+    not apply to them): the SYCL-Bench kernel shape (variant 0: one thread per point,
+    every tap a global load) against the staged march kernel, and FDTD's per-step
+    launches against the persistent temporally blocked kernel (PB_FDTD_STEPS is read
+    once per process, so that pair is timed by scripts/fdtd_h.py in two processes)."""
+    out = []
+    for n in (4096, 16384):
+        A, B = gen((n, n), S["A"]), gen((n, n), S["B"])
+        t0, _ = timed(lambda: pb.pb_conv2d_variant(0, n, n, pbgen.CONV2D_W, A, B), 10)
+        t1, _ = timed(lambda: pb.pb_conv2d_variant(1, n, n, pbgen.CONV2D_W, A, B), 10)
+        out.append(dict(kernel="conv2d", n=n, naive_ms=t0, staged_ms=t1, speedup=t0 / t1))
+        del A, B
+    for n in (512, 1024):
+        A, B = gen((n, n, n), S["A"]), gen((n, n, n), S["B"])
+        t0, _ = timed(lambda: pb.pb_conv3d_variant(0, n, n, n, pbgen.conv3d_w27(), A, B), 5)
+        t1, _ = timed(lambda: pb.pb_conv3d_variant(1, n, n, n, pbgen.conv3d_w27(), A, B), 5)
+        out.append(dict(kernel="conv3d", n=n, naive_ms=t0, staged_ms=t1, speedup=t0 / t1))
+        del A, B
+    return out
+
+
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else None
     torch.cuda.set_device(0)
+    if len(sys.argv) > 2 and sys.argv[2] == "ablation":
+        res = ablation()
+        for r in res:
+            print(json.dumps(r))
+        json.dump({"ablation": res}, open(out, "w"), indent=1)
+        return
     res = [conv2d(4096, 30), conv2d(16384, 20), conv3d(1024, 10), conv3d(512, 20), fdtd(1024, 500, 10),
            gramschmidt(1024, 10), gramschmidt(2048, 5)]
     for r in res:

@@ -247,3 +247,23 @@ def test_conv_row_blocks_equal_whole(G):
         lo, hi = max(p0 - 1, 0), min(p1 + 1, n3)
         pb.pb_conv3d(hi - lo, nj3, nk3, pbgen.conv3d_w27(), A3[lo:hi], s3[lo:hi])
     assert np.array_equal(P.host(w3).view(np.uint32), P.host(s3).view(np.uint32))
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_conv_variants(variant):
+    """pb_conv2d_variant / pb_conv3d_variant (0: one thread per point, global loads; 1:
+    production) against the oracle, borders untouched."""
+    ni, nj = 67, 132
+    A, B0 = P.H(ni, nj, 1), P.H(ni, nj, 2)
+    dB = P.dev(B0)
+    pb.pb_conv2d_variant(variant, ni, nj, pbgen.CONV2D_W, P.dev(A), dB)
+    r, s = oracle.conv2d(pbgen.CONV2D_W, A, B0), oracle.conv2d(pbgen.CONV2D_W, A, B0, absmode=True)
+    g = P.host(dB)
+    assert P.cerr(g, r, s) <= P.TOL
+    n3 = (13, 11, 132)
+    A3 = P.H(n3[0] * n3[1], n3[2], 1).reshape(n3)
+    B3 = P.H(n3[0] * n3[1], n3[2], 2).reshape(n3)
+    dB3 = P.dev(B3)
+    pb.pb_conv3d_variant(variant, *n3, pbgen.conv3d_w27(), P.dev(A3), dB3)
+    r, s = oracle.conv3d(pbgen.conv3d_w27(), A3, B3), oracle.conv3d(pbgen.conv3d_w27(), A3, B3, absmode=True)
+    assert P.cerr(P.host(dB3), r, s) <= P.TOL
