@@ -398,6 +398,13 @@ pb_status pb_conv3d_variant(int variant, int ni, int nj, int nk, const float* w,
  * shared-memory path, else its columns stay in the (L2-resident) workspace. */
 pb_status pb_gramschmidt(int m, int n, float* A, float* R, float* Q, void* ws, size_t ws_bytes, pb_stream s);
 
+/* Gramschmidt ablation: variant 0 = the PolyBench-GPU / SYCL-Bench kernel shape (three
+ * launches per column: a single-thread norm, the column normalisation, one thread per
+ * trailing column looping over the rows; fp64 working arrays, same results within
+ * R22); variant 1 = pb_gramschmidt. Same arguments and workspace. */
+pb_status pb_gramschmidt_variant(int variant, int m, int n, float* A, float* R, float* Q, void* ws, size_t ws_bytes,
+                                 pb_stream s);
+
 /* Number of kernels launched by the last successful pb_* call on this thread. */
 int pb_last_launch_count(void);
 

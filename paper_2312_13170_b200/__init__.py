@@ -24,6 +24,7 @@ __all__ = [
     "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist", "Peer", "pb_peer_create",
     "pb_comm_init_local", "pb_comm_attach_peer", "pb_conv2d", "pb_conv3d", "pb_fdtd_2d",
     "pb_gramschmidt", "pb_covariance_rows", "pb_correlation_rows", "pb_conv2d_variant", "pb_conv3d_variant",
+    "pb_gramschmidt_variant",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -67,6 +68,7 @@ ABI_FUNCTIONS = {
     "pb_conv3d_variant": ([_I, _I, _I, _I, ctypes.POINTER(_F), _P, _P, _P], _I),
     "pb_fdtd_2d": ([_I, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gramschmidt": ([_I, _I, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_gramschmidt_variant": ([_I, _I, _I, _P, _P, _P, _P, _Z, _P], _I),
     "pb_covariance_rows": ([_I, _I, _F, _I, _I, _P, _P, _P, _P, _Z, _P], _I),
     "pb_correlation_rows": ([_I, _I, _F, _F, _I, _I, _P, _P, _P, _P, _P, _Z, _P], _I),
     # multi-GPU (NCCL inside libpb)
@@ -332,6 +334,12 @@ def pb_fdtd_2d(tmax, nx, ny, ex, ey, hz, fict, ws=None, stream=None):
 def pb_gramschmidt(m, n_, A, R, Q, ws=None, stream=None):
     p, n, keep = _ws(ws, "gramschmidt", (m, n_), A)
     _check("pb_gramschmidt", lib().pb_gramschmidt(m, n_, _ptr(A), _ptr(R), _ptr(Q), p, n, _stream(stream, A)))
+
+
+def pb_gramschmidt_variant(variant, m, n_, A, R, Q, ws=None, stream=None):
+    p, n, keep = _ws(ws, "gramschmidt", (m, n_), A)
+    _check("pb_gramschmidt_variant", lib().pb_gramschmidt_variant(variant, m, n_, _ptr(A), _ptr(R), _ptr(Q), p, n,
+                                                                  _stream(stream, A)))
 
 
 def pb_row_partition(rows, nranks, rank, triangular=False, align=1):

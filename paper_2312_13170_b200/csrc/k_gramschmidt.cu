@@ -294,11 +294,73 @@ int gs_sms() {
   return n;
 }
 
+
+// ---- ablation: the PolyBench-GPU / SYCL-Bench kernel shape --------------------------
+// Three launches per column k over fp64 row-major working arrays: a single work-item
+// computes the norm, m work-items normalise column k, and one work-item per column
+// j > k forms R[k][j] and updates column j (each looping over the m rows).
+__global__ void gsn_norm_kernel(const double* __restrict__ W, double* __restrict__ Rd, int m, int n, int k) {
+  double nrm = 0.0;
+  for (int i = 0; i < m; ++i) nrm += W[(size_t)i * n + k] * W[(size_t)i * n + k];
+  Rd[(size_t)k * n + k] = sqrt(nrm);
+}
+__global__ void gsn_q_kernel(const double* __restrict__ W, const double* __restrict__ Rd, double* __restrict__ Qd,
+                             int m, int n, int k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) Qd[(size_t)i * n + k] = W[(size_t)i * n + k] / Rd[(size_t)k * n + k];
+}
+__global__ void gsn_update_kernel(double* __restrict__ W, double* __restrict__ Rd, const double* __restrict__ Qd,
+                                  int m, int n, int k) {
+  const int j = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double r = 0.0;
+  for (int i = 0; i < m; ++i) r += Qd[(size_t)i * n + k] * W[(size_t)i * n + j];
+  Rd[(size_t)k * n + j] = r;
+  for (int i = 0; i < m; ++i) W[(size_t)i * n + j] -= Qd[(size_t)i * n + k] * r;
+}
+template <typename Tin, typename Tout>
+__global__ void gsn_copy_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, long long count) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < count) out[e] = (Tout)in[e];
+}
+// R (fp32) upper triangle from Rd: R[k][j] for j >= k
+__global__ void gsn_r_kernel(const double* __restrict__ Rd, float* __restrict__ R, int n) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < (long long)n * n && e % n >= e / n) R[e] = (float)Rd[e];
+}
+
 }  // namespace
 
 size_t gramschmidt_ws_bytes(int m, int n) {
   const size_t mat = align_up((size_t)m * n * sizeof(double), 256);
-  return 2 * mat + 256;
+  const size_t rn = align_up((size_t)n * n * sizeof(double), 256);
+  return 2 * mat + 256 + rn;  // + fp64 R for the ablation variant
+}
+
+cudaError_t launch_gramschmidt_naive(int m, int n, float* A, float* R, float* Q, void* ws, cudaStream_t s,
+                                     int* launches) {
+  const size_t mat = align_up((size_t)m * n * sizeof(double), 256);
+  double* W = static_cast<double*>(ws);
+  double* Qd = reinterpret_cast<double*>(static_cast<char*>(ws) + mat);
+  double* Rd = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * mat + 256);
+  const long long mn = (long long)m * n;
+  const unsigned gmn = (unsigned)((mn + 255) / 256);
+  gsn_copy_kernel<float, double><<<gmn, 256, 0, s>>>(A, W, mn);
+  int L = 1;
+  for (int k = 0; k < n; ++k) {
+    gsn_norm_kernel<<<1, 1, 0, s>>>(W, Rd, m, n, k);
+    gsn_q_kernel<<<(m + 255) / 256, 256, 0, s>>>(W, Rd, Qd, m, n, k);
+    L += 2;
+    if (k + 1 < n) {
+      gsn_update_kernel<<<(n - k - 1 + 255) / 256, 256, 0, s>>>(W, Rd, Qd, m, n, k);
+      ++L;
+    }
+  }
+  gsn_copy_kernel<double, float><<<gmn, 256, 0, s>>>(W, A, mn);
+  gsn_copy_kernel<double, float><<<gmn, 256, 0, s>>>(Qd, Q, mn);
+  gsn_r_kernel<<<(unsigned)(((long long)n * n + 255) / 256), 256, 0, s>>>(Rd, R, n);
+  *launches += L + 3;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_gramschmidt(int m, int n, float* A, float* R, float* Q, void* ws, cudaStream_t s, int* launches) {

@@ -865,6 +865,23 @@ pb_status pb_fdtd_2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, 
 }
 
 // ---- gramschmidt (reading R22) ---------------------------
+pb_status pb_gramschmidt_variant(int variant, int m, int n, float* A, float* R, float* Q, void* ws, size_t ws_bytes,
+                                 pb_stream s) {
+  if (variant == 1) return pb_gramschmidt(m, n, A, R, Q, ws, ws_bytes, s);
+  if (variant != 0) return fail(PB_ERR_INVALID_ARG, "variant %d (0 = naive, 1 = production)", variant);
+  Check ck;
+  ck.dims({m, n});
+  ck.arr(A, m, n, true, "A"); ck.arr(R, n, n, true, "R"); ck.arr(Q, m, n, true, "Q");
+  PB_TRY(ck.finish());
+  Carve need(nullptr, 0);
+  need.take<char>(gramschmidt_ws_bytes(m, n));
+  PB_TRY(check_ws(need, ws, ws_bytes));
+  int L = 0;
+  PB_CUDA(launch_gramschmidt_naive(m, n, A, R, Q, ws, S(s), &L));
+  g_launches = L;
+  return PB_OK;
+}
+
 pb_status pb_gramschmidt(int m, int n, float* A, float* R, float* Q, void* ws, size_t ws_bytes, pb_stream s) {
   Check ck;
   ck.dims({m, n});

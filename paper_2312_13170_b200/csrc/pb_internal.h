@@ -135,6 +135,9 @@ cudaError_t launch_fdtd2d(int tmax, int nx, int ny, float* ex, float* ey, float*
 // ---- gramschmidt (k_gramschmidt.cu): persistent modified Gram-Schmidt, fp64 state
 size_t gramschmidt_ws_bytes(int m, int n);
 cudaError_t launch_gramschmidt(int m, int n, float* A, float* R, float* Q, void* ws, cudaStream_t s, int* launches);
+// ablation: PolyBench-GPU shape (3 launches per column; fp64 working arrays)
+cudaError_t launch_gramschmidt_naive(int m, int n, float* A, float* R, float* Q, void* ws, cudaStream_t s,
+                                     int* launches);
 
 // ---- peer-memory collectives (k_peer.cu; host side in pb_dist.cu) ------------
 constexpr int PEER_MAXR = 8;            // ranks per peer group

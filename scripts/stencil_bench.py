@@ -154,6 +154,19 @@ def ablation():
         t1, _ = timed(lambda: pb.pb_conv3d_variant(1, n, n, n, pbgen.conv3d_w27(), A, B), 5)
         out.append(dict(kernel="conv3d", n=n, naive_ms=t0, staged_ms=t1, speedup=t0 / t1))
         del A, B
+    for n in (512, 1024):
+        A0 = gen((n, n), S["A"])
+        A = A0.clone()
+        R, Q = torch.zeros(n, n, device=dev), torch.zeros(n, n, device=dev)
+        ws = pb.workspace("gramschmidt", (n, n), dev)
+        res = []
+        for v in (0, 1):
+            def fn(v=v):
+                A.copy_(A0)
+                pb.pb_gramschmidt_variant(v, n, n, A, R, Q, ws)
+            res.append(timed(fn, 5)[0])
+        out.append(dict(kernel="gramschmidt", n=n, naive_ms=res[0], staged_ms=res[1], speedup=res[0] / res[1],
+                        naive_launches=3 * n + 3))
     return out
 
 

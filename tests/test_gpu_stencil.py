@@ -267,3 +267,20 @@ def test_conv_variants(variant):
     pb.pb_conv3d_variant(variant, *n3, pbgen.conv3d_w27(), P.dev(A3), dB3)
     r, s = oracle.conv3d(pbgen.conv3d_w27(), A3, B3), oracle.conv3d(pbgen.conv3d_w27(), A3, B3, absmode=True)
     assert P.cerr(P.host(dB3), r, s) <= P.TOL
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_gramschmidt_variants(variant):
+    """pb_gramschmidt_variant (0: PolyBench-GPU three-launches-per-column shape; 1:
+    production) against the oracle (reading R22)."""
+    m, n = 300, 149
+    A = P.H(m, n, 1)
+    dA, dR, dQ = P.dev(A), torch.zeros(n, n, device="cuda"), torch.zeros(m, n, device="cuda")
+    pb.pb_gramschmidt_variant(variant, m, n, dA, dR, dQ)
+    rA, rR, rQ = oracle.gramschmidt(A)
+    gA, gR, gQ = P.host(dA), P.host(dR), P.host(dQ)
+    cn = np.sqrt((A.astype(np.float64) ** 2).sum(0))
+    up = np.triu(np.ones((n, n), bool))
+    assert (np.abs(gQ - rQ) / np.abs(rQ).max(0)).max() <= P.TOL
+    assert (np.abs(gA - rA) / np.abs(rA).max(0)).max() <= P.TOL
+    assert (np.abs(gR - rR) / cn[None, :])[up].max() <= P.TOL
