@@ -3,14 +3,15 @@
 // definitions = readings R19-R21 in DESIGN.md).
 //
 // No contraction here, so no tensor cores: the convolutions are HBM streams and
-// FDTD at the paper's 1024^2 is an L2-resident time loop. Loop internalization's
-// role (stage what neighbouring work-items re-read through
-// local memory) is played by
+// FDTD at the paper's 1024^2 is an L2/shared-memory-resident time loop. Loop
+// internalization's role (stage what neighbouring work-items
+// re-read through local memory) is played by
 //   conv2d / conv3d: one "march" kernel. A CTA owns a tile of output columns (2-D:
-//           1024 columns of a row; 3-D: 8 rows x 128 columns of a plane) and marches
-//           along the slowest axis. Each plane (2-D: row) tile plus its halo is
-//           staged by 1-D bulk copies (the TMA engine) into a shared-memory ring
-//           STAGES ahead, so the bytes in flight do not depend on registers. Every
+//           1024 columns of a row; 3-D: 8 or 16 rows x 128 columns of a plane) and
+//           marches along the slowest axis. A producer warp stages each plane (2-D:
+//           row) tile plus its halo by 1-D bulk copies (the TMA engine) into a
+//           shared-memory ring STAGES ahead (full / empty mbarriers, no CTA barrier
+//           in the march), so the bytes in flight do not depend on registers. Every
 //           staged plane contributes to three output planes held in registers
 //           (register pipelining), so each tile is read from shared memory once.
 //           The FMAs are packed (fma.rn.f32x2: two outputs per instruction), and
@@ -18,13 +19,14 @@
 //           (the paper's host-to-device constant propagation: a
 //           filter known on the host specialises the device code); the weights'
 //           values stay runtime arguments.
-//   fdtd2d: one fused launch per time step. The three PolyBench sweeps are
-//           evaluated per point from the previous step's state; the two
-//           neighbour values the hz update needs (ex'[i][j+1], ey'[i+1][j]) are
-//           recomputed with the identical fp32 operations, so the result equals
-//           the sequential sweeps bitwise. State ping-pongs between the caller's
-//           arrays and the workspace (the sweeps' Jacobi structure needs the old
-//           neighbours).
+//   fdtd2d: a persistent cooperative kernel when every 64x128 tile fits on the GPU
+//           at once: each tile keeps its core plus an 8-wide halo of the three
+//           fields in shared memory, advances 8 steps, and exchanges only its
+//           outer band with its 8 neighbours through L2 (release/acquire epoch
+//           flags). Otherwise one fused launch per step, state ping-ponging through
+//           the workspace. In both, the hz update's two neighbour values
+//           (ex'[i][j+1], ey'[i+1][j]) are recomputed with the identical fp32
+//           operations, so the result equals the sequential sweeps bitwise.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
