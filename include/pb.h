@@ -371,8 +371,11 @@ pb_status pb_conv3d(int ni, int nj, int nk, const float* w, const float* A, floa
  * when tmax == 0). Every update is evaluated with the statement's fp32
  * operations in C order (no contraction), so the result is bitwise that of the
  * sequential PolyBench sweeps in fp32. ws: pb_workspace_size("fdtd_2d",
- * {nx, ny}) bytes (one ping-pong copy of the three fields). One kernel launch
- * per time step (+3 device copies when tmax is odd). */
+ * {nx, ny}) bytes. When every 64 x 128 tile fits on the GPU at once (nx * ny up to
+ * ~148 tiles), one persistent cooperative launch (state in shared memory, 8 steps
+ * per neighbour exchange through the workspace); otherwise one launch per time
+ * step with the fields ping-ponging through the workspace (+3 device copies when
+ * tmax is odd). */
 pb_status pb_fdtd_2d(int tmax, int nx, int ny, float* ex, float* ey, float* hz, const float* fict, void* ws,
                      size_t ws_bytes, pb_stream s);
 
