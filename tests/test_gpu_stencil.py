@@ -284,3 +284,25 @@ def test_gramschmidt_variants(variant):
     assert (np.abs(gQ - rQ) / np.abs(rQ).max(0)).max() <= P.TOL
     assert (np.abs(gA - rA) / np.abs(rA).max(0)).max() <= P.TOL
     assert (np.abs(gR - rR) / cn[None, :])[up].max() <= P.TOL
+
+
+def test_new_entry_points_reject_bad_arguments():
+    """Validation before any enqueue (include/pb.h conventions) for the entry points added
+    this round: aliasing, row-range rules, unknown variants."""
+    A = torch.zeros(256, 256, device="cuda")
+    R = torch.zeros(256, 256, device="cuda")
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_gramschmidt(256, 256, A, R, A)  # Q aliases A
+    assert e.value.status == 3
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_covariance_rows(256, 256, 256.0, 64, 256, A, R[:192])  # r0 not a multiple of 128
+    assert e.value.status == 1
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_correlation_rows(256, 256, 256.0, 0.1, 128, 300, A, R)  # r1 > m
+    assert e.value.status == 1
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_conv2d_variant(7, 256, 256, pbgen.CONV2D_W, A, R)
+    assert e.value.status == 1
+    with pytest.raises(pb.PBError) as e:
+        pb.pb_gramschmidt_variant(5, 256, 256, A, R, torch.zeros(256, 256, device="cuda"))
+    assert e.value.status == 1
