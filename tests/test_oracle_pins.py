@@ -415,3 +415,38 @@ def test_pins_catch_mutations():
     for k, refs in mutants.items():
         for m in refs:
             assert not close(m, good[k], 1e-6), k
+
+
+def test_hand_worked_goldens_all_kernels():
+    """Hand-worked PolyBench instances (tests/golden/polybench_hand.json, arithmetic in
+    each entry's 'how') for every kernel besides gemm's own golden."""
+    g = json.load(open(os.path.join(HERE, "golden", "polybench_hand.json")))
+    f32 = lambda v: np.array(v, np.float32)  # noqa: E731
+    ok = lambda a, b: np.allclose(np.asarray(a, np.float64), np.asarray(b, np.float64), rtol=0, atol=1e-12)  # noqa: E731
+    c = g["covariance"]
+    cov, mean = oracle.covariance(c["float_n"], f32(c["data"]))
+    assert ok(cov, c["cov"]) and ok(mean, c["mean"])
+    c = g["correlation"]
+    assert ok(oracle.correlation(c["float_n"], c["eps"], f32(c["data"]))[0], c["corr"])
+    c = g["atax"]
+    y, tmp = oracle.atax(f32(c["A"]), f32(c["x"]))
+    assert ok(y, c["y"]) and ok(tmp, c["tmp"])
+    c = g["bicg"]
+    s, q = oracle.bicg(f32(c["A"]), f32(c["p"]), f32(c["r"]))
+    assert ok(s, c["s"]) and ok(q, c["q"])
+    c = g["mvt"]
+    o1, o2 = oracle.mvt(f32(c["x1"]), f32(c["x2"]), f32(c["y_1"]), f32(c["y_2"]), f32(c["A"]))
+    assert ok(o1, c["x1_out"]) and ok(o2, c["x2_out"])
+    c = g["gesummv"]
+    tmp, y = oracle.gesummv(1.5, 1.2, f32(c["A"]), f32(c["B"]), f32(c["x"]))
+    assert ok(tmp, c["tmp"]) and ok(y, c["y"])
+    c = g["syrk"]
+    assert ok(oracle.syrk(1.5, 1.2, f32(c["C"]), f32(c["A"])), c["C_out"])
+    c = g["syr2k"]
+    assert ok(oracle.syr2k(1.5, 1.2, f32(c["C"]), f32(c["A"]), f32(c["B"])), c["C_out"])
+    c = g["2mm"]
+    tmp, D = oracle.mm2(1.5, 1.2, f32(c["A"]), f32(c["B"]), f32(c["C"]), f32(c["D"]))
+    assert ok(tmp, c["tmp"]) and ok(D, c["D_out"])
+    c = g["3mm"]
+    E, F, G = oracle.mm3(f32(c["A"]), f32(c["B"]), f32(c["C"]), f32(c["D"]))
+    assert ok(E, c["E"]) and ok(F, c["F"]) and ok(G, c["G"])
