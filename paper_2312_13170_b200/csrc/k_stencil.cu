@@ -633,13 +633,18 @@ cudaError_t launch_conv3d(const float* A, float* B, int ni, int nj, int nk, cons
   ++*launches;
   const uint32_t m = weight_mask(w27, 27);
   // Large grids: 16-row tiles, two output rows per warp (halo re-reads 18/16 instead of
-  // 10/8 rows; 1024^3: 1.60 -> 1.53 ms). Smaller ones keep 8-row tiles (more CTAs;
-  // 512^3: 0.209 vs 0.215 ms). PB_C3_RPW=1|2 overrides (tuning aid).
+  // 10/8 rows), 256 columns per tile when the rows are long enough (k-halo 8/256):
+  // 1024^3: 1.60 (8 x 128) -> 1.54 (16 x 128) -> 1.50 ms (16 x 256). Smaller grids keep
+  // 8-row tiles (more CTAs; 512^3: 0.209 vs 0.215 ms). PB_C3_RPW=1|2 overrides.
   static const int rpw_env = getenv("PB_C3_RPW") ? atoi(getenv("PB_C3_RPW")) : 0;
   const bool rpw2 = rpw_env ? rpw_env == 2 : (long long)ni * nj * nk >= (1ll << 28);
-  if ((m & ~MASK_PBGPU3D) == 0)
+  const bool wide = rpw2 && nk >= 256;
+  if ((m & ~MASK_PBGPU3D) == 0) {
+    if (wide) return launch_march<3, 16, 2, 2, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s);
     return rpw2 ? launch_march<3, 16, 1, 2, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s)
                 : launch_march<3, 8, 1, 1, MASK_PBGPU3D>(A, B, ni, nj, nk, w, s);
+  }
+  if (wide) return launch_march<3, 16, 2, 2, MASK_DENSE>(A, B, ni, nj, nk, w, s);
   return rpw2 ? launch_march<3, 16, 1, 2, MASK_DENSE>(A, B, ni, nj, nk, w, s)
               : launch_march<3, 8, 1, 1, MASK_DENSE>(A, B, ni, nj, nk, w, s);
 }
