@@ -40,4 +40,19 @@ for (m, n) in ((1024, 1024), (300, 149), (2048, 2048)):
         elif not all(np.array_equal(a, b) for a, b in zip(out, ref)):
             bad += 1
     print("gramschmidt", m, n, "ok" if bad == 0 else f"MISMATCH {bad}", flush=True)
+import pbgen  # noqa: E402
+for (ni, nj, nk) in ((1024, 1024, 1024), (257, 65, 516), (9, 130, 136)):
+    A = torch.empty(ni * nj, nk, device="cuda")
+    pbgen.gen_device(A, 1)
+    ref = None
+    for r in range(max(3, reps // 4)):
+        B = torch.zeros(ni * nj, nk, device="cuda")
+        pb.pb_conv3d(ni, nj, nk, pbgen.conv3d_w27(), A, B)
+        torch.cuda.synchronize()
+        h = torch.sum(B.view(torch.int32).to(torch.int64) * torch.arange(1, B.numel() + 1, device="cuda").view_as(B) % 1000003).item()
+        if ref is None:
+            ref = h
+        elif h != ref:
+            bad += 1
+    print("conv3d", ni, nj, nk, "ok" if bad == 0 else f"MISMATCH {bad}", flush=True)
 print("STRESS", "PASS" if bad == 0 else "FAIL")
