@@ -8,7 +8,7 @@ tail -5 gpurun_out/${TAG:-r06}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG:-r06}_smoke.log 2>&1; echo smoke rc=$?; tail -3 gpurun_out/${TAG:-r06}_smoke.log
 timeout 900 python bench.py > gpurun_out/${TAG:-r06}_bench_default.json 2> gpurun_out/${TAG:-r06}_bench.err; echo bench rc=$?
 tail -c 1500 gpurun_out/${TAG:-r06}_bench_default.json
-timeout 600 python scripts/stencil_bench.py gpurun_out/${TAG:-r06}_stencil.json > /dev/null 2>&1
+timeout 600 python -m tests.perf.stencil_bench gpurun_out/${TAG:-r06}_stencil.json > /dev/null 2>&1
 true
 for k in conv2d conv3d fdtd_2d gramschmidt; do
   case $k in conv2d|conv3d) re=march;; fdtd_2d) re=fdtd_persist;; gramschmidt) re=gs_kernel;; esac
