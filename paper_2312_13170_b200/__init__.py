@@ -128,11 +128,24 @@ def last_launch_count():
     return lib().pb_last_launch_count()
 
 
-def _ptr(t):
+def _ptr(t, numel=None, name="tensor"):
+    """Device pointer of a tensor argument (None -> NULL; an int is passed through as a
+    raw address). The C side can only check a pointer's start (alignment, device,
+    overlap), so the extent, dtype and layout are checked here: a CUDA, float32,
+    contiguous tensor with at least `numel` elements."""
     if t is None:
         return None
     if isinstance(t, int):
         return t
+    if not getattr(t, "is_cuda", False):
+        raise PBError("argument", 1, f"{name} must be a CUDA tensor")
+    import torch
+    if t.dtype != torch.float32:
+        raise PBError("argument", 1, f"{name} must be float32 (got {t.dtype})")
+    if not t.is_contiguous():
+        raise PBError("argument", 1, f"{name} must be contiguous (row-major, row pitch == #cols)")
+    if numel is not None and t.numel() < numel:
+        raise PBError("argument", 1, f"{name} has {t.numel()} elements, {numel} needed")
     return t.data_ptr()
 
 
@@ -165,136 +178,144 @@ def workspace(kernel: str, dims, device):
 
 
 _ws_cache = {}
+_ws_retired = []  # outgrown cached workspaces: never freed (a captured graph may still use them)
 
 
-def _ws(ws, kernel, dims, ref):
-    """Caller's workspace, or a per-device cached one (kept alive across calls so
-    asynchronous kernels never see it freed)."""
+def _ws(ws, kernel, dims, ref, stream=None):
+    """Caller's workspace, or a cached one per (device, stream): calls on different
+    streams never share a buffer (pb.h: such calls are independent). An outgrown
+    buffer is retired, not freed, so in-flight kernels and CUDA graphs captured
+    with it stay valid."""
     if ws is None:
         import torch
         need = max(workspace_size(kernel, dims), 256)
         device = ref.device if hasattr(ref, "device") else torch.device("cuda", torch.cuda.current_device())
-        cur = _ws_cache.get(device)
+        key = (device, _stream(stream, ref))
+        cur = _ws_cache.get(key)
         if cur is None or cur.numel() < need:
             if cur is not None:
-                torch.cuda.synchronize(device)  # the old buffer may still be in use
+                _ws_retired.append(cur)
             cur = torch.empty(need, dtype=torch.uint8, device=device)
-            _ws_cache[device] = cur
+            _ws_cache[key] = cur
         ws = cur
-    return _ptr(ws), (ws.numel() * ws.element_size() if hasattr(ws, "numel") else 1 << 62), ws
+    if hasattr(ws, "data_ptr"):
+        if not ws.is_cuda or not ws.is_contiguous():
+            raise PBError("argument", 1, "ws must be a contiguous CUDA tensor")
+        return ws.data_ptr(), ws.numel() * ws.element_size(), ws
+    return ws, 1 << 62, ws
 
 
 def pb_gemm(ni, nj, nk, alpha, beta, C, A, B, ws=None, stream=None):
-    p, n, keep = _ws(ws, "gemm", (ni, nj, nk), C)
-    _check("pb_gemm", lib().pb_gemm(ni, nj, nk, alpha, beta, _ptr(C), _ptr(A), _ptr(B), p, n, _stream(stream, C)))
+    p, n, keep = _ws(ws, "gemm", (ni, nj, nk), C, stream)
+    _check("pb_gemm", lib().pb_gemm(ni, nj, nk, alpha, beta, _ptr(C, ni*nj, "C"), _ptr(A, ni*nk, "A"), _ptr(B, nk*nj, "B"), p, n, _stream(stream, C)))
 
 
 def pb_gemm_variant(variant, ni, nj, nk, alpha, beta, C, A, B, ws=None, stream=None):
-    p, n, keep = _ws(ws, "gemm_variant", (ni, nj, nk), C)
-    _check("pb_gemm_variant", lib().pb_gemm_variant(variant, ni, nj, nk, alpha, beta, _ptr(C), _ptr(A), _ptr(B),
+    p, n, keep = _ws(ws, "gemm_variant", (ni, nj, nk), C, stream)
+    _check("pb_gemm_variant", lib().pb_gemm_variant(variant, ni, nj, nk, alpha, beta, _ptr(C, ni*nj, "C"), _ptr(A, ni*nk, "A"), _ptr(B, nk*nj, "B"),
                                                     p, n, _stream(stream, C)))
 
 
 def pb_2mm(ni, nj, nk, nl, alpha, beta, tmp, A, B, C, D, ws=None, stream=None):
-    p, n, keep = _ws(ws, "2mm", (ni, nj, nk, nl), D)
-    _check("pb_2mm", lib().pb_2mm(ni, nj, nk, nl, alpha, beta, _ptr(tmp), _ptr(A), _ptr(B), _ptr(C), _ptr(D),
+    p, n, keep = _ws(ws, "2mm", (ni, nj, nk, nl), D, stream)
+    _check("pb_2mm", lib().pb_2mm(ni, nj, nk, nl, alpha, beta, _ptr(tmp, ni*nj, "tmp"), _ptr(A, ni*nk, "A"), _ptr(B, nk*nj, "B"), _ptr(C, nj*nl, "C"), _ptr(D, ni*nl, "D"),
                                   p, n, _stream(stream, D)))
 
 
 def pb_3mm(ni, nj, nk, nl, nm, E, A, B, F, C, D, G, ws=None, stream=None):
-    p, n, keep = _ws(ws, "3mm", (ni, nj, nk, nl, nm), G)
-    _check("pb_3mm", lib().pb_3mm(ni, nj, nk, nl, nm, _ptr(E), _ptr(A), _ptr(B), _ptr(F), _ptr(C), _ptr(D),
-                                  _ptr(G), p, n, _stream(stream, G)))
+    p, n, keep = _ws(ws, "3mm", (ni, nj, nk, nl, nm), G, stream)
+    _check("pb_3mm", lib().pb_3mm(ni, nj, nk, nl, nm, _ptr(E, ni*nj, "E"), _ptr(A, ni*nk, "A"), _ptr(B, nk*nj, "B"), _ptr(F, nj*nl, "F"), _ptr(C, nj*nm, "C"), _ptr(D, nm*nl, "D"),
+                                  _ptr(G, ni*nl, "G"), p, n, _stream(stream, G)))
 
 
 def pb_syrk(n_, m, alpha, beta, C, A, ws=None, stream=None):
-    p, n, keep = _ws(ws, "syrk", (n_, m), C)
-    _check("pb_syrk", lib().pb_syrk(n_, m, alpha, beta, _ptr(C), _ptr(A), p, n, _stream(stream, C)))
+    p, n, keep = _ws(ws, "syrk", (n_, m), C, stream)
+    _check("pb_syrk", lib().pb_syrk(n_, m, alpha, beta, _ptr(C, n_*n_, "C"), _ptr(A, n_*m, "A"), p, n, _stream(stream, C)))
 
 
 def pb_syr2k(n_, m, alpha, beta, C, A, B, ws=None, stream=None):
-    p, n, keep = _ws(ws, "syr2k", (n_, m), C)
-    _check("pb_syr2k", lib().pb_syr2k(n_, m, alpha, beta, _ptr(C), _ptr(A), _ptr(B), p, n, _stream(stream, C)))
+    p, n, keep = _ws(ws, "syr2k", (n_, m), C, stream)
+    _check("pb_syr2k", lib().pb_syr2k(n_, m, alpha, beta, _ptr(C, n_*n_, "C"), _ptr(A, n_*m, "A"), _ptr(B, n_*m, "B"), p, n, _stream(stream, C)))
 
 
 def pb_syrk_full(n_, m, alpha, beta, C, A, ws=None, stream=None):
-    p, n, keep = _ws(ws, "syrk_full", (n_, m), C)
-    _check("pb_syrk_full", lib().pb_syrk_full(n_, m, alpha, beta, _ptr(C), _ptr(A), p, n, _stream(stream, C)))
+    p, n, keep = _ws(ws, "syrk_full", (n_, m), C, stream)
+    _check("pb_syrk_full", lib().pb_syrk_full(n_, m, alpha, beta, _ptr(C, n_*n_, "C"), _ptr(A, n_*m, "A"), p, n, _stream(stream, C)))
 
 
 def pb_syr2k_full(n_, m, alpha, beta, C, A, B, ws=None, stream=None):
-    p, n, keep = _ws(ws, "syr2k_full", (n_, m), C)
-    _check("pb_syr2k_full", lib().pb_syr2k_full(n_, m, alpha, beta, _ptr(C), _ptr(A), _ptr(B), p, n,
+    p, n, keep = _ws(ws, "syr2k_full", (n_, m), C, stream)
+    _check("pb_syr2k_full", lib().pb_syr2k_full(n_, m, alpha, beta, _ptr(C, n_*n_, "C"), _ptr(A, n_*m, "A"), _ptr(B, n_*m, "B"), p, n,
                                                 _stream(stream, C)))
 
 
 def pb_syrk_rows(n_, m, r0, r1, alpha, beta, C_blk, A, ws=None, stream=None):
-    p, n, keep = _ws(ws, "syrk_rows", (n_, m, r0, r1), A)
-    _check("pb_syrk_rows", lib().pb_syrk_rows(n_, m, r0, r1, alpha, beta, _ptr(C_blk), _ptr(A), p, n,
+    p, n, keep = _ws(ws, "syrk_rows", (n_, m, r0, r1), A, stream)
+    _check("pb_syrk_rows", lib().pb_syrk_rows(n_, m, r0, r1, alpha, beta, _ptr(C_blk, (r1-r0)*n_, "C_blk"), _ptr(A, r1*m, "A"), p, n,
                                               _stream(stream, A)))
 
 
 def pb_syr2k_rows(n_, m, r0, r1, alpha, beta, C_blk, A, B, ws=None, stream=None):
-    p, n, keep = _ws(ws, "syr2k_rows", (n_, m, r0, r1), A)
-    _check("pb_syr2k_rows", lib().pb_syr2k_rows(n_, m, r0, r1, alpha, beta, _ptr(C_blk), _ptr(A), _ptr(B), p, n,
+    p, n, keep = _ws(ws, "syr2k_rows", (n_, m, r0, r1), A, stream)
+    _check("pb_syr2k_rows", lib().pb_syr2k_rows(n_, m, r0, r1, alpha, beta, _ptr(C_blk, (r1-r0)*n_, "C_blk"), _ptr(A, r1*m, "A"), _ptr(B, r1*m, "B"), p, n,
                                                 _stream(stream, A)))
 
 
 def pb_covariance(m, n_, float_n, data, cov, mean=None, ws=None, stream=None):
-    p, n, keep = _ws(ws, "covariance", (m, n_), cov)
-    _check("pb_covariance", lib().pb_covariance(m, n_, float_n, _ptr(data), _ptr(cov), _ptr(mean), p, n,
+    p, n, keep = _ws(ws, "covariance", (m, n_), cov, stream)
+    _check("pb_covariance", lib().pb_covariance(m, n_, float_n, _ptr(data, n_*m, "data"), _ptr(cov, m*m, "cov"), _ptr(mean, m, "mean"), p, n,
                                                 _stream(stream, cov)))
 
 
 def pb_correlation(m, n_, float_n, eps, data, corr, mean=None, stddev=None, ws=None, stream=None):
-    p, n, keep = _ws(ws, "correlation", (m, n_), corr)
-    _check("pb_correlation", lib().pb_correlation(m, n_, float_n, eps, _ptr(data), _ptr(corr), _ptr(mean),
-                                                  _ptr(stddev), p, n, _stream(stream, corr)))
+    p, n, keep = _ws(ws, "correlation", (m, n_), corr, stream)
+    _check("pb_correlation", lib().pb_correlation(m, n_, float_n, eps, _ptr(data, n_*m, "data"), _ptr(corr, m*m, "corr"), _ptr(mean, m, "mean"),
+                                                  _ptr(stddev, m, "stddev"), p, n, _stream(stream, corr)))
 
 
 def pb_covariance_rows(m, n_, float_n, r0, r1, data, cov_blk, mean=None, ws=None, stream=None):
-    p, n, keep = _ws(ws, "covariance_rows", (m, n_, r0, r1), cov_blk)
-    _check("pb_covariance_rows", lib().pb_covariance_rows(m, n_, float_n, r0, r1, _ptr(data), _ptr(cov_blk),
-                                                          _ptr(mean), p, n, _stream(stream, cov_blk)))
+    p, n, keep = _ws(ws, "covariance_rows", (m, n_, r0, r1), cov_blk, stream)
+    _check("pb_covariance_rows", lib().pb_covariance_rows(m, n_, float_n, r0, r1, _ptr(data, n_*m, "data"), _ptr(cov_blk, (r1-r0)*m, "cov_blk"),
+                                                          _ptr(mean, m, "mean"), p, n, _stream(stream, cov_blk)))
 
 
 def pb_correlation_rows(m, n_, float_n, eps, r0, r1, data, corr_blk, mean=None, stddev=None, ws=None, stream=None):
-    p, n, keep = _ws(ws, "correlation_rows", (m, n_, r0, r1), corr_blk)
-    _check("pb_correlation_rows", lib().pb_correlation_rows(m, n_, float_n, eps, r0, r1, _ptr(data), _ptr(corr_blk),
-                                                            _ptr(mean), _ptr(stddev), p, n, _stream(stream, corr_blk)))
+    p, n, keep = _ws(ws, "correlation_rows", (m, n_, r0, r1), corr_blk, stream)
+    _check("pb_correlation_rows", lib().pb_correlation_rows(m, n_, float_n, eps, r0, r1, _ptr(data, n_*m, "data"), _ptr(corr_blk, (r1-r0)*m, "corr_blk"),
+                                                            _ptr(mean, m, "mean"), _ptr(stddev, m, "stddev"), p, n, _stream(stream, corr_blk)))
 
 
 def pb_atax(m, n_, A, x, y, tmp=None, ws=None, stream=None):
-    p, n, keep = _ws(ws, "atax", (m, n_), y)
-    _check("pb_atax", lib().pb_atax(m, n_, _ptr(A), _ptr(x), _ptr(y), _ptr(tmp), p, n, _stream(stream, y)))
+    p, n, keep = _ws(ws, "atax", (m, n_), y, stream)
+    _check("pb_atax", lib().pb_atax(m, n_, _ptr(A, m*n_, "A"), _ptr(x, n_, "x"), _ptr(y, n_, "y"), _ptr(tmp, m, "tmp"), p, n, _stream(stream, y)))
 
 
 def pb_bicg(m, n_, A, s, q, p_, r, ws=None, stream=None):
-    p, n, keep = _ws(ws, "bicg", (m, n_), q)
-    _check("pb_bicg", lib().pb_bicg(m, n_, _ptr(A), _ptr(s), _ptr(q), _ptr(p_), _ptr(r), p, n, _stream(stream, q)))
+    p, n, keep = _ws(ws, "bicg", (m, n_), q, stream)
+    _check("pb_bicg", lib().pb_bicg(m, n_, _ptr(A, n_*m, "A"), _ptr(s, m, "s"), _ptr(q, n_, "q"), _ptr(p_, m, "p_"), _ptr(r, n_, "r"), p, n, _stream(stream, q)))
 
 
 def pb_mvt(n_, x1, x2, y_1, y_2, A, ws=None, stream=None):
-    p, n, keep = _ws(ws, "mvt", (n_,), x1)
-    _check("pb_mvt", lib().pb_mvt(n_, _ptr(x1), _ptr(x2), _ptr(y_1), _ptr(y_2), _ptr(A), p, n, _stream(stream, x1)))
+    p, n, keep = _ws(ws, "mvt", (n_,), x1, stream)
+    _check("pb_mvt", lib().pb_mvt(n_, _ptr(x1, n_, "x1"), _ptr(x2, n_, "x2"), _ptr(y_1, n_, "y_1"), _ptr(y_2, n_, "y_2"), _ptr(A, n_*n_, "A"), p, n, _stream(stream, x1)))
 
 
 def pb_gesummv(n_, alpha, beta, A, B, tmp, x, y, ws=None, stream=None):
-    p, n, keep = _ws(ws, "gesummv", (n_,), y)
-    _check("pb_gesummv", lib().pb_gesummv(n_, alpha, beta, _ptr(A), _ptr(B), _ptr(tmp), _ptr(x), _ptr(y), p, n,
+    p, n, keep = _ws(ws, "gesummv", (n_,), y, stream)
+    _check("pb_gesummv", lib().pb_gesummv(n_, alpha, beta, _ptr(A, n_*n_, "A"), _ptr(B, n_*n_, "B"), _ptr(tmp, n_, "tmp"), _ptr(x, n_, "x"), _ptr(y, n_, "y"), p, n,
                                           _stream(stream, y)))
 
 
 def pb_gesummv_rows(rows, n_, alpha, beta, A_blk, B_blk, tmp_blk, x, y_blk, ws=None, stream=None):
-    p, n, keep = _ws(ws, "gesummv_rows", (rows, n_), A_blk)
-    _check("pb_gesummv_rows", lib().pb_gesummv_rows(rows, n_, alpha, beta, _ptr(A_blk), _ptr(B_blk), _ptr(tmp_blk),
-                                                    _ptr(x), _ptr(y_blk), p, n, _stream(stream, A_blk)))
+    p, n, keep = _ws(ws, "gesummv_rows", (rows, n_), A_blk, stream)
+    _check("pb_gesummv_rows", lib().pb_gesummv_rows(rows, n_, alpha, beta, _ptr(A_blk, rows*n_, "A_blk"), _ptr(B_blk, rows*n_, "B_blk"), _ptr(tmp_blk, rows, "tmp_blk"),
+                                                    _ptr(x, n_, "x"), _ptr(y_blk, rows, "y_blk"), p, n, _stream(stream, A_blk)))
 
 
 def pb_matvec_partial(rows, cols, A_blk, v, base_row, rowdot, w, base_col, colpart, ws=None, stream=None):
-    p, n, keep = _ws(ws, "matvec_partial", (rows, cols), A_blk)
-    _check("pb_matvec_partial", lib().pb_matvec_partial(rows, cols, _ptr(A_blk), _ptr(v), _ptr(base_row),
-                                                        _ptr(rowdot), _ptr(w), _ptr(base_col), _ptr(colpart),
+    p, n, keep = _ws(ws, "matvec_partial", (rows, cols), A_blk, stream)
+    _check("pb_matvec_partial", lib().pb_matvec_partial(rows, cols, _ptr(A_blk, rows*cols, "A_blk"), _ptr(v, cols, "v"), _ptr(base_row, rows, "base_row"),
+                                                        _ptr(rowdot, rows, "rowdot"), _ptr(w, rows, "w"), _ptr(base_col, cols, "base_col"), _ptr(colpart, cols, "colpart"),
                                                         p, n, _stream(stream, A_blk)))
 
 
@@ -307,38 +328,38 @@ def _host_w(w, n):
 
 def pb_conv2d(ni, nj, w, A, B, stream=None):
     """w: 9 weights (host), w[(di+1)*3 + (dj+1)]."""
-    _check("pb_conv2d", lib().pb_conv2d(ni, nj, _host_w(w, 9), _ptr(A), _ptr(B), _stream(stream, B)))
+    _check("pb_conv2d", lib().pb_conv2d(ni, nj, _host_w(w, 9), _ptr(A, ni*nj, "A"), _ptr(B, ni*nj, "B"), _stream(stream, B)))
 
 
 def pb_conv3d(ni, nj, nk, w, A, B, stream=None):
     """w: 27 weights (host), w[(di+1)*9 + (dj+1)*3 + (dk+1)]."""
-    _check("pb_conv3d", lib().pb_conv3d(ni, nj, nk, _host_w(w, 27), _ptr(A), _ptr(B), _stream(stream, B)))
+    _check("pb_conv3d", lib().pb_conv3d(ni, nj, nk, _host_w(w, 27), _ptr(A, ni*nj*nk, "A"), _ptr(B, ni*nj*nk, "B"), _stream(stream, B)))
 
 
 def pb_conv2d_variant(variant, ni, nj, w, A, B, stream=None):
-    _check("pb_conv2d_variant", lib().pb_conv2d_variant(variant, ni, nj, _host_w(w, 9), _ptr(A), _ptr(B),
+    _check("pb_conv2d_variant", lib().pb_conv2d_variant(variant, ni, nj, _host_w(w, 9), _ptr(A, ni*nj, "A"), _ptr(B, ni*nj, "B"),
                                                         _stream(stream, B)))
 
 
 def pb_conv3d_variant(variant, ni, nj, nk, w, A, B, stream=None):
-    _check("pb_conv3d_variant", lib().pb_conv3d_variant(variant, ni, nj, nk, _host_w(w, 27), _ptr(A), _ptr(B),
+    _check("pb_conv3d_variant", lib().pb_conv3d_variant(variant, ni, nj, nk, _host_w(w, 27), _ptr(A, ni*nj*nk, "A"), _ptr(B, ni*nj*nk, "B"),
                                                         _stream(stream, B)))
 
 
 def pb_fdtd_2d(tmax, nx, ny, ex, ey, hz, fict, ws=None, stream=None):
-    p, n, keep = _ws(ws, "fdtd_2d", (nx, ny), ex)
-    _check("pb_fdtd_2d", lib().pb_fdtd_2d(tmax, nx, ny, _ptr(ex), _ptr(ey), _ptr(hz), _ptr(fict), p, n,
+    p, n, keep = _ws(ws, "fdtd_2d", (nx, ny), ex, stream)
+    _check("pb_fdtd_2d", lib().pb_fdtd_2d(tmax, nx, ny, _ptr(ex, nx*ny, "ex"), _ptr(ey, nx*ny, "ey"), _ptr(hz, nx*ny, "hz"), _ptr(fict, max(tmax, 1), "fict"), p, n,
                                           _stream(stream, ex)))
 
 
 def pb_gramschmidt(m, n_, A, R, Q, ws=None, stream=None):
-    p, n, keep = _ws(ws, "gramschmidt", (m, n_), A)
-    _check("pb_gramschmidt", lib().pb_gramschmidt(m, n_, _ptr(A), _ptr(R), _ptr(Q), p, n, _stream(stream, A)))
+    p, n, keep = _ws(ws, "gramschmidt", (m, n_), A, stream)
+    _check("pb_gramschmidt", lib().pb_gramschmidt(m, n_, _ptr(A, m*n_, "A"), _ptr(R, n_*n_, "R"), _ptr(Q, m*n_, "Q"), p, n, _stream(stream, A)))
 
 
 def pb_gramschmidt_variant(variant, m, n_, A, R, Q, ws=None, stream=None):
-    p, n, keep = _ws(ws, "gramschmidt", (m, n_), A)
-    _check("pb_gramschmidt_variant", lib().pb_gramschmidt_variant(variant, m, n_, _ptr(A), _ptr(R), _ptr(Q), p, n,
+    p, n, keep = _ws(ws, "gramschmidt", (m, n_), A, stream)
+    _check("pb_gramschmidt_variant", lib().pb_gramschmidt_variant(variant, m, n_, _ptr(A, m*n_, "A"), _ptr(R, n_*n_, "R"), _ptr(Q, m*n_, "Q"), p, n,
                                                                   _stream(stream, A)))
 
 
@@ -386,62 +407,62 @@ def _first(*ts):
     return next(t for t in ts if t is not None and hasattr(t, "device"))
 
 
-def _dws(ws, name, dims, comm, *ts):
-    return _ws(ws, name + "_dist", tuple(dims) + (comm.nranks, comm.rank), _first(*ts))
+def _dws(ws, name, dims, comm, *ts, stream=None):
+    return _ws(ws, name + "_dist", tuple(dims) + (comm.nranks, comm.rank), _first(*ts), stream)
 
 
 def pb_gemm_dist(comm, ni, nj, nk, alpha, beta, C_blk, A_blk, B, ws=None, stream=None):
-    p, n, keep = _dws(ws, "gemm", (ni, nj, nk), comm, B)
-    _check("pb_gemm_dist", lib().pb_gemm_dist(comm.handle, ni, nj, nk, alpha, beta, _ptr(C_blk), _ptr(A_blk),
-                                              _ptr(B), p, n, _stream(stream, B)))
+    p, n, keep = _dws(ws, "gemm", (ni, nj, nk), comm, B, stream=stream)
+    _check("pb_gemm_dist", lib().pb_gemm_dist(comm.handle, ni, nj, nk, alpha, beta, _ptr(C_blk, None, "C_blk"), _ptr(A_blk, None, "A_blk"),
+                                              _ptr(B, None, "B"), p, n, _stream(stream, B)))
 
 
 def pb_2mm_dist(comm, ni, nj, nk, nl, alpha, beta, tmp_blk, A_blk, B, C, D_blk, ws=None, stream=None):
-    p, n, keep = _dws(ws, "2mm", (ni, nj, nk, nl), comm, B)
-    _check("pb_2mm_dist", lib().pb_2mm_dist(comm.handle, ni, nj, nk, nl, alpha, beta, _ptr(tmp_blk), _ptr(A_blk),
-                                            _ptr(B), _ptr(C), _ptr(D_blk), p, n, _stream(stream, B)))
+    p, n, keep = _dws(ws, "2mm", (ni, nj, nk, nl), comm, B, stream=stream)
+    _check("pb_2mm_dist", lib().pb_2mm_dist(comm.handle, ni, nj, nk, nl, alpha, beta, _ptr(tmp_blk, None, "tmp_blk"), _ptr(A_blk, None, "A_blk"),
+                                            _ptr(B, None, "B"), _ptr(C, None, "C"), _ptr(D_blk, None, "D_blk"), p, n, _stream(stream, B)))
 
 
 def pb_3mm_dist(comm, ni, nj, nk, nl, nm, E_blk, A_blk, B, F, C_blk, D, G_blk, ws=None, stream=None):
-    p, n, keep = _dws(ws, "3mm", (ni, nj, nk, nl, nm), comm, F)
-    _check("pb_3mm_dist", lib().pb_3mm_dist(comm.handle, ni, nj, nk, nl, nm, _ptr(E_blk), _ptr(A_blk), _ptr(B),
-                                            _ptr(F), _ptr(C_blk), _ptr(D), _ptr(G_blk), p, n, _stream(stream, F)))
+    p, n, keep = _dws(ws, "3mm", (ni, nj, nk, nl, nm), comm, F, stream=stream)
+    _check("pb_3mm_dist", lib().pb_3mm_dist(comm.handle, ni, nj, nk, nl, nm, _ptr(E_blk, None, "E_blk"), _ptr(A_blk, None, "A_blk"), _ptr(B, None, "B"),
+                                            _ptr(F, None, "F"), _ptr(C_blk, None, "C_blk"), _ptr(D, None, "D"), _ptr(G_blk, None, "G_blk"), p, n, _stream(stream, F)))
 
 
 def pb_syrk_dist(comm, n_, m, alpha, beta, C_blk, A, ws=None, stream=None):
-    p, n, keep = _dws(ws, "syrk", (n_, m), comm, A)
-    _check("pb_syrk_dist", lib().pb_syrk_dist(comm.handle, n_, m, alpha, beta, _ptr(C_blk), _ptr(A), p, n,
+    p, n, keep = _dws(ws, "syrk", (n_, m), comm, A, stream=stream)
+    _check("pb_syrk_dist", lib().pb_syrk_dist(comm.handle, n_, m, alpha, beta, _ptr(C_blk, None, "C_blk"), _ptr(A, None, "A"), p, n,
                                               _stream(stream, A)))
 
 
 def pb_syr2k_dist(comm, n_, m, alpha, beta, C_blk, A, B, ws=None, stream=None):
-    p, n, keep = _dws(ws, "syr2k", (n_, m), comm, A)
-    _check("pb_syr2k_dist", lib().pb_syr2k_dist(comm.handle, n_, m, alpha, beta, _ptr(C_blk), _ptr(A), _ptr(B),
+    p, n, keep = _dws(ws, "syr2k", (n_, m), comm, A, stream=stream)
+    _check("pb_syr2k_dist", lib().pb_syr2k_dist(comm.handle, n_, m, alpha, beta, _ptr(C_blk, None, "C_blk"), _ptr(A, None, "A"), _ptr(B, None, "B"),
                                                 p, n, _stream(stream, A)))
 
 
 def pb_atax_dist(comm, m, n_, A_blk, x, y_blk, tmp_blk=None, ws=None, stream=None):
-    p, n, keep = _dws(ws, "atax", (m, n_), comm, x)
-    _check("pb_atax_dist", lib().pb_atax_dist(comm.handle, m, n_, _ptr(A_blk), _ptr(x), _ptr(y_blk), _ptr(tmp_blk),
+    p, n, keep = _dws(ws, "atax", (m, n_), comm, x, stream=stream)
+    _check("pb_atax_dist", lib().pb_atax_dist(comm.handle, m, n_, _ptr(A_blk, None, "A_blk"), _ptr(x, None, "x"), _ptr(y_blk, None, "y_blk"), _ptr(tmp_blk, None, "tmp_blk"),
                                               p, n, _stream(stream, x)))
 
 
 def pb_bicg_dist(comm, m, n_, A_blk, s_blk, q_blk, p_, r_blk, ws=None, stream=None):
-    p, n, keep = _dws(ws, "bicg", (m, n_), comm, p_)
-    _check("pb_bicg_dist", lib().pb_bicg_dist(comm.handle, m, n_, _ptr(A_blk), _ptr(s_blk), _ptr(q_blk), _ptr(p_),
-                                              _ptr(r_blk), p, n, _stream(stream, p_)))
+    p, n, keep = _dws(ws, "bicg", (m, n_), comm, p_, stream=stream)
+    _check("pb_bicg_dist", lib().pb_bicg_dist(comm.handle, m, n_, _ptr(A_blk, None, "A_blk"), _ptr(s_blk, None, "s_blk"), _ptr(q_blk, None, "q_blk"), _ptr(p_, None, "p_"),
+                                              _ptr(r_blk, None, "r_blk"), p, n, _stream(stream, p_)))
 
 
 def pb_mvt_dist(comm, n_, x1_blk, x2_blk, y_1, y_2_blk, A_blk, ws=None, stream=None):
-    p, n, keep = _dws(ws, "mvt", (n_,), comm, y_1)
-    _check("pb_mvt_dist", lib().pb_mvt_dist(comm.handle, n_, _ptr(x1_blk), _ptr(x2_blk), _ptr(y_1), _ptr(y_2_blk),
-                                            _ptr(A_blk), p, n, _stream(stream, y_1)))
+    p, n, keep = _dws(ws, "mvt", (n_,), comm, y_1, stream=stream)
+    _check("pb_mvt_dist", lib().pb_mvt_dist(comm.handle, n_, _ptr(x1_blk, None, "x1_blk"), _ptr(x2_blk, None, "x2_blk"), _ptr(y_1, None, "y_1"), _ptr(y_2_blk, None, "y_2_blk"),
+                                            _ptr(A_blk, None, "A_blk"), p, n, _stream(stream, y_1)))
 
 
 def pb_gesummv_dist(comm, n_, alpha, beta, A_blk, B_blk, tmp_blk, x, y_blk, ws=None, stream=None):
-    p, n, keep = _dws(ws, "gesummv", (n_,), comm, x)
-    _check("pb_gesummv_dist", lib().pb_gesummv_dist(comm.handle, n_, alpha, beta, _ptr(A_blk), _ptr(B_blk),
-                                                    _ptr(tmp_blk), _ptr(x), _ptr(y_blk), p, n, _stream(stream, x)))
+    p, n, keep = _dws(ws, "gesummv", (n_,), comm, x, stream=stream)
+    _check("pb_gesummv_dist", lib().pb_gesummv_dist(comm.handle, n_, alpha, beta, _ptr(A_blk, None, "A_blk"), _ptr(B_blk, None, "B_blk"),
+                                                    _ptr(tmp_blk, None, "tmp_blk"), _ptr(x, None, "x"), _ptr(y_blk, None, "y_blk"), p, n, _stream(stream, x)))
 
 
 class Peer:
@@ -461,11 +482,11 @@ class Peer:
         return v.value
 
     def reduce_scatter(self, partial, out_blk, total, stream=None):
-        _check("pb_peer_reduce_scatter", lib().pb_peer_reduce_scatter(self.handle, _ptr(partial), _ptr(out_blk),
+        _check("pb_peer_reduce_scatter", lib().pb_peer_reduce_scatter(self.handle, _ptr(partial, None, "partial"), _ptr(out_blk, None, "out_blk"),
                                                                       total, _stream(stream, partial)))
 
     def all_gather(self, send_blk, recv, rows, cols, stream=None):
-        _check("pb_peer_all_gather", lib().pb_peer_all_gather(self.handle, _ptr(send_blk), _ptr(recv), rows, cols,
+        _check("pb_peer_all_gather", lib().pb_peer_all_gather(self.handle, _ptr(send_blk, None, "send_blk"), _ptr(recv, None, "recv"), rows, cols,
                                                               _stream(stream, recv)))
 
     def close(self):

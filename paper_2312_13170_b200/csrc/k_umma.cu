@@ -891,6 +891,7 @@ void timeline_umma(bool reset, unsigned long long* out4) {
 cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, const GramStats& st,
                                 cudaStream_t s, int* launches) {
   if (pl.split_tiles <= 0) return cudaSuccess;
+  if (pl.part_bytes > d.part_cap) return cudaErrorInvalidValue;
   if (st.nbands > MAXB) return cudaErrorInvalidValue;
   CombineStats cs;
   cs.band_mean = st.band_mean; cs.band_m2 = st.band_m2; cs.nbands = st.nbands; cs.n = st.n;
@@ -936,6 +937,9 @@ cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
   int ks = pl.ksplit;
   if (ks > 1 && (d.part == nullptr || d.counters == nullptr)) ks = 1;
   if ((d.flags & EPI_PARTIAL) && d.part == nullptr) return cudaErrorInvalidValue;
+  // the workspace reserved for partials / counters must hold what this plan writes
+  if ((ks > 1 || (d.flags & EPI_PARTIAL)) && (pl.part_bytes > d.part_cap || pl.counter_bytes > d.counter_cap))
+    return cudaErrorInvalidValue;
   if (pl.cfg == 3) return launch_cg<2, 256>(d, p, ks, pl.split_tiles, s, launches);
   if (pl.cfg == 2) return launch_cg<2, 128>(d, p, ks, pl.split_tiles, s, launches);
   return launch_cg<1, 128>(d, p, ks, pl.split_tiles, s, launches);

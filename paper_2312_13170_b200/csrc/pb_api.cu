@@ -68,7 +68,10 @@ SplitBuf take_split(Carve& c, int rows, int K) {
 struct SplitK {
   float* part = nullptr;
   unsigned* counters = nullptr;
-  void attach(GemmDesc& d) const { d.part = part; d.counters = counters; }
+  size_t part_bytes = 0, counter_bytes = 0;
+  void attach(GemmDesc& d) const {
+    d.part = part; d.counters = counters; d.part_cap = part_bytes; d.counter_cap = counter_bytes;
+  }
 };
 GemmDesc shape(int M, int N, int K, int npairs = 1, uint32_t flags = EPI_OUT, int tm0 = 0, int tm1 = -1) {
   GemmDesc d;
@@ -86,6 +89,8 @@ SplitK take_splitk(Carve& c, std::initializer_list<GemmDesc> gemms) {
   if (part) {
     k.part = c.take<float>(part / sizeof(float));
     k.counters = c.take<unsigned>(cnt / sizeof(unsigned));
+    k.part_bytes = part;
+    k.counter_bytes = cnt;
   }
   return k;
 }
@@ -122,7 +127,13 @@ WsStat ws_stat(Carve& c, int m, int n) {
   WsStat w;
   w.xt = take_split(c, m, n);
   const bool banded = banded_stats(n);
-  w.sk = take_splitk(c, {shape(m, m, n, 1, EPI_TRI | (banded ? EPI_PARTIAL : 0u))});
+  // The exact-mean path (n > MAX_BANDED) switches to EPI_PARTIAL when its plan splits K
+  // (stat_core), which re-plans with every tile through partials and possibly another
+  // tile shape: reserve the larger of the two plans.
+  if (banded)
+    w.sk = take_splitk(c, {shape(m, m, n, 1, EPI_TRI | EPI_PARTIAL)});
+  else
+    w.sk = take_splitk(c, {shape(m, m, n, 1, EPI_TRI), shape(m, m, n, 1, EPI_TRI | EPI_PARTIAL)});
   if (banded) {
     w.band_mean = c.take<double>((size_t)band_count(n) * m);
     w.band_m2 = c.take<double>((size_t)band_count(n) * m);

@@ -48,6 +48,7 @@ struct GemmDesc {
   int tm0 = 0, tm1 = -1;  // tile-row range in 128-row units (default all)
   float* part = nullptr;       // split-K partials (umma_plan(d).part_bytes)
   unsigned* counters = nullptr;  // split-K counters (umma_plan(d).counter_bytes)
+  size_t part_cap = 0, counter_cap = 0;  // bytes reserved at part / counters (checked at launch)
 };
 
 struct UmmaPlan {

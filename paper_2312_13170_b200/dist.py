@@ -15,15 +15,14 @@ steps the math needs:
                                     partial, so the sum is x2 + A^T y_2)
 
 Every arithmetic step runs in libpb through the C ABI (`K` below defaults to
-the binding; the CPU gloo tests inject an oracle-backed namespace to check
-the partition and collective logic without a GPU). Outputs stay row-sharded
-(reading R15).
+the binding; the CPU gloo tests inject an oracle-backed namespace, with
+host-staged stand-ins for the two collectives, to check the partition and
+collective logic without a GPU). Outputs stay row-sharded (reading R15).
 
 With an NCCL process group, `init_comm()` creates a libpb communicator and
 every call below goes to the C ABI's `pb_<k>_dist` entry points, which run the
 collectives with NCCL inside libpb (3mm's all-gather on the comm's side
-stream, overlapped with E = A B). Without one (gloo: the multi-rank tests on
-one GPU or on CPU), the same steps run here with torch.distributed.
+stream, overlapped with E = A B). A sharded call without one raises.
 """
 from __future__ import annotations
 
@@ -128,56 +127,16 @@ def partition(rows, world, rank, triangular=False, align=128, K=_pb):
     return K.pb_row_partition(rows, world, rank, triangular, align)
 
 
-def _staged():
-    """gloo carries CUDA tensors only through host copies (multi-rank tests on one
-    GPU); NCCL moves them device to device over NVLink."""
-    return dist.get_backend() != "nccl"
-
-
-def _all_gather_rows(full, local, world, bounds, async_op=False):
-    """full[rows] <- concat of every rank's `local` row block."""
-    sizes = [e - b for b, e in bounds]
-    if _staged() and full.is_cuda:
-        parts = [torch.empty((e - b,) + tuple(local.shape[1:]), dtype=local.dtype) for b, e in bounds]
-        _, rank = _world()
-        mx = max(sizes)
-        pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype)
-        pad[: sizes[rank]].copy_(local[: sizes[rank]].cpu())
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad)
-        for g, (b, e) in enumerate(bounds):
-            full[b:e].copy_(bufs[g][: e - b])
-        return None
-    if len(set(sizes)) == 1:
-        return dist.all_gather_into_tensor(full, local, async_op=async_op)
-    mx = max(sizes)  # uneven blocks: pad every block to the largest, gather, unpad
-    _, rank = _world()
-    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    pad[: sizes[rank]].copy_(local[: sizes[rank]])
-    big = torch.empty((world * mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(big, pad)
-    for g, (b, e) in enumerate(bounds):
-        full[b:e].copy_(big[g * mx: g * mx + (e - b)])
-    return None
-
-
-def _reduce_scatter_vec(out_local, partial, world, bounds):
-    """out_local <- (sum over ranks of partial)[bounds[rank]]."""
-    sizes = [e - b for b, e in bounds]
-    if _staged() and partial.is_cuda:
-        h = partial.cpu()
-        dist.all_reduce(h)
-        _, rank = _world()
-        b, e = bounds[rank]
-        out_local.copy_(h[b:e])
-        return
-    if len(set(sizes)) == 1 and sizes[0] * world == partial.numel():
-        dist.reduce_scatter_tensor(out_local, partial)
-    else:
-        dist.all_reduce(partial)
-        _, rank = _world()
-        b, e = bounds[rank]
-        out_local.copy_(partial[b:e])
+def _collectives(K):
+    """The exchange steps of a sharded call. With a libpb communicator they run inside
+    libpb (`pb_<k>_dist`: NCCL or the peer-memory kernels); a kernel namespace without
+    one must supply them (the CPU gloo tests inject host-staged stand-ins). The product
+    package performs no arithmetic outside libpb."""
+    ag = getattr(K, "all_gather_rows", None)
+    rs = getattr(K, "reduce_scatter_vec", None)
+    if ag is None or rs is None:
+        raise RuntimeError("sharded call without a libpb communicator: call dist.init_comm() first")
+    return ag, rs
 
 
 # --------------------------------------------------------------------- contractions
@@ -205,10 +164,11 @@ def mm3_rows(ctx, n, E, A, B, Fl, F, C, D, G, ws, K=_pb):
     if _COMM is not None and K is _pb:  # F rows -> all-gather (libpb side stream) || E -> G
         K.pb_3mm_dist(_COMM, n, n, n, n, n, E, A, B, F, C[f0:f1], D, G, ws=ws)
         return K.last_launch_count()
+    all_gather_rows, _ = _collectives(K)
     if f1 > f0:
         K.pb_gemm(f1 - f0, n, n, 1.0, 0.0, Fl, C[f0:f1], D, ws=ws)  # F[R'] = C[R'] D
         L += K.last_launch_count()
-    work = _all_gather_rows(F, Fl, world, bounds, async_op=True)
+    work = all_gather_rows(F, Fl, world, bounds)
     rows = A.shape[0]
     if rows:
         K.pb_gemm(rows, n, n, 1.0, 0.0, E, A, B, ws=ws)  # E[R] = A[R] B, overlaps the all-gather
@@ -270,24 +230,25 @@ def matvec(ctx, kernel, n, v, ws, alpha, beta, K=_pb):
         else:
             K.pb_gesummv_dist(c, n, alpha, beta, A, v["B"], v["tmp"][:rows], v["x"], v["yo"][r0:r1], ws=ws)
         return K.last_launch_count()
+    _, reduce_scatter_vec = _collectives(K)
     L = 0
     if kernel == "atax":  # tmp[R] = A[R] x ; y = sum_g A[R_g]^T tmp[R_g]
         part = v["yo"]
         K.pb_atax(rows, n, A, v["x"], part, v["tmp"][:rows], ws=ws)  # one pass over A[R]
         L += K.last_launch_count()
-        _reduce_scatter_vec(v["y"][r0:r1], part, world, bounds)
+        reduce_scatter_vec(v["y"][r0:r1], part, world, bounds)
     elif kernel == "bicg":  # q[R] = A[R] p ; s = sum_g A[R_g]^T r[R_g]
         part = v["yo"]
         K.pb_matvec_partial(rows, n, A, v["x"], None, v["q"][r0:r1], v["r"][r0:r1], None, part, ws=ws)
         L += K.last_launch_count()
-        _reduce_scatter_vec(v["s"][r0:r1], part, world, bounds)
+        reduce_scatter_vec(v["s"][r0:r1], part, world, bounds)
     elif kernel == "mvt":  # x1[R] += A[R] y_1 ; x2 = x2 + sum_g A[R_g]^T y_2[R_g]
         part = v["yo"]
         x1l = v["x1"][r0:r1]
         K.pb_matvec_partial(rows, n, A, v["x"], x1l, x1l, v["y2"][r0:r1], v["x2"] if rank == 0 else None, part,
                             ws=ws)
         L += K.last_launch_count()
-        _reduce_scatter_vec(v["x2"][r0:r1], part, world, bounds)
+        reduce_scatter_vec(v["x2"][r0:r1], part, world, bounds)
     else:  # gesummv: purely row-local
         K.pb_gesummv_rows(rows, n, alpha, beta, A, v["B"], v["tmp"][:rows], v["x"], v["yo"][r0:r1], ws=ws)
         L += K.last_launch_count()

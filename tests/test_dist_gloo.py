@@ -25,6 +25,27 @@ def _np(t):
     return t.detach().cpu().numpy()
 
 
+def host_all_gather_rows(full, local, world, bounds):
+    """full[rows] <- concat of every rank's `local` row block (gloo, host-staged; test only)."""
+    rank = dist.get_rank()
+    sizes = [e - b for b, e in bounds]
+    mx = max(sizes)
+    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype)
+    pad[: sizes[rank]].copy_(local[: sizes[rank]].cpu())
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad)
+    for g, (b, e) in enumerate(bounds):
+        full[b:e].copy_(bufs[g][: e - b])
+
+
+def host_reduce_scatter_vec(out_local, partial, world, bounds):
+    """out_local <- (sum over ranks of partial)[bounds[rank]] (gloo, host-staged; test only)."""
+    h = partial.cpu().clone()
+    dist.all_reduce(h)
+    b, e = bounds[dist.get_rank()]
+    out_local.copy_(h[b:e])
+
+
 def fake_kernels():
     """Oracle-backed CPU stand-ins with the binding's signatures (test only)."""
     K = types.SimpleNamespace()
@@ -82,6 +103,8 @@ def fake_kernels():
     K.pb_gemm = gemm
     K.pb_2mm = mm2
     K.pb_matvec_partial = matvec_partial
+    K.all_gather_rows = host_all_gather_rows
+    K.reduce_scatter_vec = host_reduce_scatter_vec
     K.pb_syrk_rows = lambda n, m, r0, r1, al, be, C, A, ws=None: syrk_rows(n, m, r0, r1, al, be, C, A)
     K.pb_syr2k_rows = lambda n, m, r0, r1, al, be, C, A, B, ws=None: syrk_rows(n, m, r0, r1, al, be, C, A, B=B)
     K.pb_gesummv_rows = gesummv_rows

@@ -43,6 +43,14 @@ def _worker(rank, world, port, q, backend="gloo"):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         if backend == "gloo-peer":  # local libpb comm: collectives = peer-memory kernels over CUDA IPC
             D.init_comm(transport="local", peer_bytes=4 << 20)
+    K = pb
+    if backend == "gloo":  # no libpb comm: the collectives are host-staged test stand-ins
+        import types
+
+        from tests.test_dist_gloo import host_all_gather_rows, host_reduce_scatter_vec
+        K = types.SimpleNamespace(**{a: getattr(pb, a) for a in dir(pb) if a.startswith("pb_")})
+        K.last_launch_count = pb.last_launch_count
+        K.all_gather_rows, K.reduce_scatter_vec = host_all_gather_rows, host_reduce_scatter_vec
     dev = torch.device("cuda", 0)
     H = lambda r, c, s, **kw: torch.from_numpy(pbgen.gen_host(r, c, s, **kw)).to(dev)  # noqa: E731
     res = {}
@@ -62,11 +70,11 @@ def _worker(rank, world, port, q, backend="gloo"):
                         need = max(need, pb.workspace_size(k + "_dist", tuple(d) + (world, rank)))
             return torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
         ws = wsz(("3mm", (n, n, n, n, n)))
-        D.mm3_rows(None, n, E, A[r0:r1].contiguous(), B, Fl, F, C, Dm, G, ws)
+        D.mm3_rows(None, n, E, A[r0:r1].contiguous(), B, Fl, F, C, Dm, G, ws, K=K)
         # 2mm: row-local
         tmp = torch.empty(r1 - r0, n, device=dev)
         D2 = Dm[r0:r1].clone()
-        D.mm2_rows(None, n, 1.5, 1.2, tmp, A[r0:r1].contiguous(), B, C, D2, wsz(("2mm", (n,) * 4)))
+        D.mm2_rows(None, n, 1.5, 1.2, tmp, A[r0:r1].contiguous(), B, C, D2, wsz(("2mm", (n,) * 4)), K=K)
         torch.cuda.synchronize()
         res["3mm"] = (r0, r1, G.cpu().numpy(), F.cpu().numpy())
         res["2mm"] = (r0, r1, D2.cpu().numpy())
@@ -77,8 +85,8 @@ def _worker(rank, world, port, q, backend="gloo"):
         Cf = H(n2, n2, 3, mode=pbgen.SYM)
         Cb, Cb2 = Cf[s0:s1].clone(), Cf[s0:s1].clone()
         wsy = wsz(("syr2k_rows", (n2, m2, 0, n2)), ("syr2k", (n2, m2)))
-        D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb, A2, wsy)
-        D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb2, A2, wsy, B=B2)
+        D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb, A2, wsy, K=K)
+        D.syrk_rows(None, n2, m2, 1.5, 1.2, Cb2, A2, wsy, B=B2, K=K)
         torch.cuda.synchronize()
         res["syrk"] = (s0, s1, Cb.cpu().numpy())
         res["syr2k"] = (s0, s1, Cb2.cpu().numpy())
@@ -93,7 +101,7 @@ def _worker(rank, world, port, q, backend="gloo"):
                      y2=vec["y2"].clone(), x1=vec["x1"].clone(), x2=vec["x2"].clone(),
                      y=torch.zeros(nv, device=dev), s=torch.zeros(nv, device=dev), q=torch.zeros(nv, device=dev),
                      yo=torch.zeros(nv, device=dev), tmp=torch.zeros(v1 - v0, device=dev))
-            D.matvec(None, kern, nv, v, wsm, 1.5, 1.2)
+            D.matvec(None, kern, nv, v, wsm, 1.5, 1.2, K=K)
             torch.cuda.synchronize()
             out = {"atax": v["y"], "bicg": v["s"], "mvt": v["x2"], "gesummv": v["yo"]}[kern]
             extra = {"bicg": v["q"], "mvt": v["x1"], "atax": v["tmp"], "gesummv": v["yo"]}[kern]
@@ -109,7 +117,8 @@ def _worker(rank, world, port, q, backend="gloo"):
 
 @pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1), ("gloo-peer", 2), ("nccl-peer", 1)])
 def test_dist_ranks_one_gpu_real_kernels(backend, world):
-    """gloo: two ranks share cuda:0 (host-staged torch collectives). nccl: one rank
+    """gloo: two ranks share cuda:0 (host-staged test stand-ins for the two
+    collectives, injected through the kernel namespace). nccl: one rank
     with PB_FORCE_DIST and a libpb communicator, i.e. the N>1 code path through
     the C ABI's pb_<k>_dist entry points (NCCL all-gather / reduce-scatter inside
     libpb, 3mm's side stream) end to end. gloo-peer: two processes on cuda:0 with
@@ -263,11 +272,11 @@ def test_peer_collectives_two_processes_one_gpu():
             assert np.array_equal(full.view(np.uint32), full_ref.view(np.uint32)), (it, r)
 
 
-@pytest.mark.parametrize("transport", ["gloo", "local"])
+@pytest.mark.parametrize("transport", ["local"])
 def test_bench_two_ranks_share_gpu(transport):
-    """bench.py under torchrun with 2 ranks on cuda:0 (PB_SHARE_GPU): host-staged
-    gloo collectives, or libpb's peer-memory kernels between the two processes
-    (PB_TRANSPORT=local). Checks the N=2 launch path end to end (timings are not
+    """bench.py under torchrun with 2 ranks on cuda:0 (PB_SHARE_GPU): libpb's
+    peer-memory kernels between the two processes (PB_TRANSPORT=local; the product
+    path has no host-staged collectives). Checks the N=2 launch path end to end (timings are not
     meaningful: the ranks share one GPU)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
