@@ -42,8 +42,63 @@
 
 #include "pb_device.cuh"
 #include "pb_internal.h"
+#include "pb_umma.cuh"
 
 namespace pb {
+// ---------------------------------------------------------------- host side (also used by k_gram.cu)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map: `inner` x `rows` (row pitch ld floats), box = box_inner x box_rows,
+// 128-B swizzle (box_inner == 32) or none. Out-of-bounds boxes are zero-filled on loads
+// and clipped on stores.
+bool make_map2d(CUtensorMap* m, const float* base, int inner, int rows, long long ld, int box_inner, int box_rows,
+                bool swizzle128) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// K-major operand (rows x K, pitch ld floats), box = 32 (K) x box_rows, 128-B swizzle.
+bool make_map(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_rows) {
+  return make_map2d(m, base, K, rows, ld, 32, box_rows, true);
+}
+
+int num_sms() {  // per device (cached)
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int n = cache[dev & 63].load(std::memory_order_relaxed);
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev & 63].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+
 namespace {
 
 __device__ int g_tl_on;                  // PB_TIMELINE (tuning only)
@@ -178,64 +233,6 @@ __device__ __forceinline__ Unit unit_of(const Params& p, long long u, int nkb_to
   r.kbA = (int)((long long)nkb_total * r.ks / S);
   r.kbB = (int)((long long)nkb_total * (r.ks + 1) / S);
   return r;
-}
-
-// ---- cta_group-specific PTX
-template <int CG>
-__device__ __forceinline__ void tmem_alloc_cg(uint32_t* dst, uint32_t ncols) {
-  if constexpr (CG == 1) {
-    tmem_alloc(dst, ncols);
-  } else {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-}
-template <int CG>
-__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) {
-  if constexpr (CG == 1)
-    tmem_dealloc(taddr, ncols);
-  else
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
-}
-template <int CG>
-__device__ __forceinline__ void mma_cg(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  if constexpr (CG == 1) {
-    mma_tf32(d, a, b, idesc, acc);
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-  }
-}
-// Commit this thread's MMAs to `bar` (CG=2: the barrier at the same offset in both CTAs).
-template <int CG>
-__device__ __forceinline__ void commit_cg(uint64_t* bar) {
-  if constexpr (CG == 1) {
-    mma_commit(bar);
-  } else {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"((uint16_t)3)
-        : "memory");
-  }
-}
-// TMA tile load; CG=2: completion is counted on the LEADER CTA's barrier.
-template <int CG>
-__device__ __forceinline__ void tma_load_cg(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1) {
-  if constexpr (CG == 1) {
-    tma_load_2d(m, bar, dst, c0, c1);
-  } else {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-        "%4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
-        : "memory");
-  }
 }
 
 template <int CG, int BN>
@@ -548,50 +545,6 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     tc_fence_after();
     tmem_dealloc_cg<CG>(tmem_base, TMEM_COLS);
   }
-}
-
-// ---------------------------------------------------------------- host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  }
-  return fn;
-}
-
-// K-major operand (rows x K, pitch ld floats), box = 32 (K) x box_rows, 128-B swizzle.
-bool make_map(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_rows) {
-  EncodeTiledFn enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-int num_sms() {  // per device (cached)
-  static std::atomic<int> cache[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int n = cache[dev & 63].load(std::memory_order_relaxed);
-  if (!n) {
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-    cache[dev & 63].store(n, std::memory_order_relaxed);
-  }
-  return n;
 }
 
 template <int CG, int BN>

@@ -125,6 +125,7 @@ inline bool banded_stats(int n) { return n <= MAX_BANDED; }
 struct WsStat { SplitBuf xt; SplitK sk; double* band_mean = nullptr; double* band_m2 = nullptr; };
 WsStat ws_stat(Carve& c, int m, int n) {
   WsStat w;
+  const size_t off0 = c.off;
   w.xt = take_split(c, m, n);
   const bool banded = banded_stats(n);
   // The exact-mean path (n > MAX_BANDED) switches to EPI_PARTIAL when its plan splits K
@@ -138,6 +139,9 @@ WsStat ws_stat(Carve& c, int m, int n) {
     w.band_mean = c.take<double>((size_t)band_count(n) * m);
     w.band_m2 = c.take<double>((size_t)band_count(n) * m);
   }
+  // the fused one-launch path (k_gram.cu) carves the same region its own way: reserve
+  // the larger of the two layouts
+  if (n <= MAX_BANDED && m <= 2048) c.off = std::max(c.off, align_up(off0, 256) + gram_fused_ws_bytes(m, n));
   return w;
 }
 // covariance/correlation row band [r0, r1) (multi-GPU: replicated data, output row
@@ -519,6 +523,14 @@ static pb_status stat_core(bool corr, int m, int n, float float_n, float eps, co
     cudaStreamSynchronize(st);
     timeline_stats(true, nullptr);
     timeline_umma(true, nullptr);
+  }
+  if (banded && gram_fused_ok(m, n) && !tl) {
+    // one launch: band statistics + centred split + Gram + split-K exchange + epilogue
+    char* wb = static_cast<char*>(ws) + align_up(0, 256);
+    PB_CUDA(launch_gram_fused(corr, m, n, (double)float_n, (double)eps, data, out, mean, corr ? stddev : nullptr, wb,
+                              st, &L));
+    g_launches = L;
+    return PB_OK;
   }
   GramStats gs;
   if (banded) {  // one pass: band-centred split + per-band column statistics

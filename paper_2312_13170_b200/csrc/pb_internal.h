@@ -59,6 +59,11 @@ struct UmmaPlan {
   size_t part_bytes = 0, counter_bytes = 0;
 };
 UmmaPlan umma_plan(const GemmDesc& d);
+// host helpers of k_umma.cu (tensor maps, SM count)
+bool make_map2d(CUtensorMap* m, const float* base, int inner, int rows, long long ld, int box_inner, int box_rows,
+                bool swizzle128);
+bool make_map(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_rows);
+int num_sms();
 cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches);
 // Statistics the Gram combine needs (nullptr band_mean: the operand was centred exactly).
 struct GramStats {
@@ -74,6 +79,13 @@ struct GramStats {
 // j <= i, mirrored to out[j][i]; diag_one -> out[i][i] = 1.
 cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag_one, const GramStats& st,
                                 cudaStream_t s, int* launches);
+
+// Fused covariance / correlation (k_gram.cu): prep + Gram + split-K exchange + epilogue
+// in one launch for n <= 2048, m <= 2048 (every unit co-resident).
+bool gram_fused_ok(int m, int n);
+size_t gram_fused_ws_bytes(int m, int n);
+cudaError_t launch_gram_fused(bool corr, int m, int n, double float_n, double eps, const float* data, float* out,
+                              float* mean, float* sd, void* ws, cudaStream_t s, int* launches);
 
 // ---- split / prep (k_split.cu) ----------------------------------------------
 // hi/lo split of a rows x cols matrix; same layout (ldo = ld of output).
