@@ -63,10 +63,10 @@ EncodeTiledFn get_encode() {
 }
 
 // 2-D fp32 tensor map: `inner` x `rows` (row pitch ld floats), box = box_inner x box_rows,
-// 128-B swizzle (box_inner == 32) or none. Out-of-bounds boxes are zero-filled on loads
+// 128-B swizzle (box_inner == 32) or none, unless `sw_override` names another mode. Out-of-bounds boxes are zero-filled on loads
 // and clipped on stores.
 bool make_map2d(CUtensorMap* m, const float* base, int inner, int rows, long long ld, int box_inner, int box_rows,
-                bool swizzle128) {
+                bool swizzle128, CUtensorMapSwizzle sw_override) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
@@ -75,8 +75,28 @@ bool make_map2d(CUtensorMap* m, const float* base, int inner, int rows, long lon
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   sw_override != CU_TENSOR_MAP_SWIZZLE_NONE ? sw_override
+                   : swizzle128                              ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                             : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// MN-major operand tiles of a row-major fp32 matrix (`inner` columns x `rows`, pitch ld
+// floats) as ONE 3-D box: {32 columns, box_rows rows, groups runs of 32 columns} lands in
+// smem as [group][row][32] (runs box_rows * 128 B apart). Needs inner % 32 == 0 (the run
+// dimension has no per-element bound).
+bool make_map_mn_runs(CUtensorMap* m, const float* base, int inner, int rows, long long ld, int box_rows, int groups,
+                      CUtensorMapSwizzle sw) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc || inner % 32) return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(inner / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, (cuuint32_t)groups};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

@@ -61,8 +61,11 @@ struct UmmaPlan {
 UmmaPlan umma_plan(const GemmDesc& d);
 // host helpers of k_umma.cu (tensor maps, SM count)
 bool make_map2d(CUtensorMap* m, const float* base, int inner, int rows, long long ld, int box_inner, int box_rows,
-                bool swizzle128);
+                bool swizzle128,
+                CUtensorMapSwizzle sw_override = CU_TENSOR_MAP_SWIZZLE_NONE);
 bool make_map(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_rows);
+bool make_map_mn_runs(CUtensorMap* m, const float* base, int inner, int rows, long long ld, int box_rows, int groups,
+                      CUtensorMapSwizzle sw);
 int num_sms();
 cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches);
 // Statistics the Gram combine needs (nullptr band_mean: the operand was centred exactly).

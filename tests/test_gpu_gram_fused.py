@@ -52,11 +52,11 @@ def test_fused_is_one_launch_and_deterministic():
     for _ in range(2):
         c = torch.empty(m, m, device="cuda")
         pb.pb_correlation(m, n, float(n), 0.1, data, c, None, None)
-        assert pb.last_launch_count() == 1
+        assert pb.last_launch_count() == 2  # flag zeroing + the fused kernel
         outs.append(P.host(c))
         c2 = torch.empty(m, m, device="cuda")
         pb.pb_covariance(m, n, float(n), data, c2, None)
-        assert pb.last_launch_count() == 1
+        assert pb.last_launch_count() == 2  # flag zeroing + the fused kernel
         outs.append(P.host(c2))
     assert np.array_equal(outs[0].view(np.uint32), outs[2].view(np.uint32))
     assert np.array_equal(outs[1].view(np.uint32), outs[3].view(np.uint32))
@@ -82,7 +82,30 @@ def test_fused_matches_three_launch_path():
         launches.append(int(r.stdout.strip().splitlines()[-1]))
         outs.append(np.load(path))
         os.unlink(path)
-    assert launches[0] == 1 and launches[1] == 3, launches
+    assert launches[0] == 2 and launches[1] == 3, launches
     a, b = outs
     scale = np.maximum(np.abs(b), 1e-3)
     assert np.max(np.abs(a - b) / scale) <= 2e-4
+
+
+@pytest.mark.parametrize("offset", [1000.0, -3.5e4])
+def test_fused_large_offset(offset):
+    """Columns whose mean dwarfs their spread (x = offset + U[0,1)): the band shifts (R18)
+    keep the Gram operand centred, so the componentwise gate still holds."""
+    import oracle
+    m, n = 516, 1000
+    data = P.H(n, m, P.S["data"], offset=offset)
+    fn = float(n)
+    d = P.dev(data)
+    cov, corr = torch.empty(m, m, device="cuda"), torch.empty(m, m, device="cuda")
+    mean, sd = torch.empty(m, device="cuda"), torch.empty(m, device="cuda")
+    pb.pb_covariance(m, n, fn, d, cov, mean)
+    assert pb.last_launch_count() == 2  # flag zeroing + the fused kernel
+    pb.pb_correlation(m, n, fn, 0.1, d, corr, None, sd)
+    c_r, mean_r = oracle.covariance(fn, data)
+    c_s, mean_s = oracle.covariance(fn, data, absmode=True)
+    k_r, _, sd_r = oracle.correlation(fn, 0.1, data)
+    k_s, _, _ = oracle.correlation(fn, 0.1, data, absmode=True)
+    errs = dict(cov=P.cerr(P.host(cov), c_r, c_s), mean=P.cerr(P.host(mean), mean_r, mean_s),
+                corr=P.cerr(P.host(corr), k_r, k_s), sd=P.cerr(P.host(sd), sd_r, sd_r))
+    assert max(errs.values()) <= P.TOL, errs
