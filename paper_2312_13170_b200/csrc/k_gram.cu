@@ -536,57 +536,60 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     if (et == 0) GTS(3);
     const uint32_t ta = ctl->tmem_base + ((uint32_t)(q * 32) << 16);
     // (b) split-K exchange: chunk c (CW columns) of the tile is finalised by unit ks == c.
-    // The other chunks go TMEM -> smem (their slots of the tile layout: [128 rows][32 cols]
-    // boxes, 128-B swizzle) -> L2 as one 1-D bulk copy each; the partners' copies of chunk ks
-    // come back into those slots.
+    // Each thread stores its row's part of the chunks it does not own straight from TMEM to
+    // an L2-resident partial tile ([column quad][128 rows] float4: a warp store covers 512
+    // contiguous bytes), loads its own chunk part from TMEM into registers, and after the
+    // partners' release flags adds their parts (ascending split index: a fixed order, so runs
+    // are bitwise reproducible) with coalesced loads. No smem staging, no bulk-copy round trip.
+    float acc[64];  // S > 1: this thread's own-chunk values (CW / 2 <= 64 columns), partners added
     if (p.S > 1) {
+      const int hw = CW / 2;
+      float4* const part4 = reinterpret_cast<float4*>(p.part);
+      const long long tile_f4 = 256 * 128 / 4;
+      float4* mine = part4 + (((long long)t * p.S + ks) * 2 + rank) * tile_f4;
       for (int cc = 0; cc < p.S; ++cc) {
         if (cc == ks) continue;
-        const int hw = CW / 2, f0 = cc * CW + ch * hw;
-        for (int c0 = f0; c0 < f0 + hw; c0 += 16) {
-          uint32_t r0[16], r1[16];
+        for (int c0 = cc * CW + ch * hw; c0 < cc * CW + ch * hw + hw; c0 += 16) {
+          uint32_t r0[16];
           tmem_ld16(ta + c0, r0);
-          if (nchunks > 1) tmem_ld16(ta + 256 + c0, r1);
           tmem_wait_ld();
-          uint8_t* bxp = smem + (c0 >> 5) * GEBOX;
 #pragma unroll
-          for (int qd = 0; qd < 4; ++qd) {
-            float v[4];
+          for (int qd = 0; qd < 4; ++qd)
+            __stcg(mine + ((c0 >> 2) + qd) * 128 + rl,
+                   make_float4(__uint_as_float(r0[4 * qd]), __uint_as_float(r0[4 * qd + 1]),
+                               __uint_as_float(r0[4 * qd + 2]), __uint_as_float(r0[4 * qd + 3])));
+        }
+      }
+      const int fo = ks * CW + ch * hw;  // this thread's own columns [fo, fo + hw)
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              v[e] = __uint_as_float(r0[4 * qd + e]) + (nchunks > 1 ? __uint_as_float(r1[4 * qd + e]) : 0.f);
-            st_sw(bxp, rl, ((c0 & 31) >> 2) + qd, make_float4(v[0], v[1], v[2], v[3]));
+      for (int j = 0; j < 4; ++j) {
+        if (16 * j < hw) {
+          uint32_t r0[16];
+          tmem_ld16(ta + fo + 16 * j, r0);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[16 * j + e] = __uint_as_float(r0[e]);
+        }
+      }
+      __threadfence();
+      epi_bar();
+      if (et == 0) st_rel(p.flags + p.nb * (p.mp / 32) + (t * p.S + ks) * 2 + rank, 1u);
+      if (warp == 2)
+        warp_wait_flags(lane < p.S && lane != ks ? p.flags + p.nb * (p.mp / 32) + (t * p.S + lane) * 2 + rank : nullptr,
+                        1u);
+      epi_bar();
+      if (et == 0) GTS(4);
+      for (int k = 0; k < p.S; ++k) {
+        if (k == ks) continue;
+        const float4* theirs = part4 + (((long long)t * p.S + k) * 2 + rank) * tile_f4;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (4 * j < hw) {
+            const float4 pv = __ldcg(theirs + ((fo >> 2) + j) * 128 + rl);
+            acc[4 * j] += pv.x; acc[4 * j + 1] += pv.y; acc[4 * j + 2] += pv.z; acc[4 * j + 3] += pv.w;
           }
         }
       }
-      fence_proxy_smem();
-      epi_bar();
-      if (et == 0) {
-        uint8_t* mine = reinterpret_cast<uint8_t*>(p.part) + (((long long)t * p.S + ks) * 2 + rank) * (256 * 128 * 4);
-        for (int cc = 0; cc < p.S; ++cc)
-          if (cc != ks) bulk_s2g(mine + cc * CB, smem + cc * CB, CB);
-        bulk_commit();
-        bulk_wait0();  // writes complete (and the smem of those chunks free)
-        fence_proxy_global();
-        __threadfence();
-        st_rel(p.flags + p.nb * (p.mp / 32) + (t * p.S + ks) * 2 + rank, 1u);
-      }
-      if (warp == 2) {
-        warp_wait_flags(lane < p.S && lane != ks ? p.flags + p.nb * (p.mp / 32) + (t * p.S + lane) * 2 + rank : nullptr,
-                        1u);
-        if (et == 0) {
-          GTS(4);
-          fence_proxy_global();
-          mbar_arrive_expect_tx(&ctl->xbar, (uint32_t)(p.S - 1) * CB);
-          for (int k = 0; k < p.S; ++k)
-            if (k != ks) {
-              const uint8_t* theirs =
-                  reinterpret_cast<const uint8_t*>(p.part) + (((long long)t * p.S + k) * 2 + rank) * (256 * 128 * 4);
-              bulk_g2s(smem + k * CB, theirs + ks * CB, CB, &ctl->xbar);
-            }
-        }
-      }
-      mbar_wait(&ctl->xbar, 0);
     }
     // (c) finalise chunk ks in sub-chunks of <= 128 columns: thread (row rl, half ch) takes
     // half of each sub-chunk's columns: own (TMEM) + partners (ascending k: a fixed order per
@@ -606,26 +609,27 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       const int kind = tm != tn || col0 + SW <= r0c ? 0 : col0 >= r0c + GSLAB ? 3 : (col0 == r0c && SW == GSLAB) ? 1 : 2;
       if (kind == 3) continue;  // above the diagonal: another block's mirror covers it
       const int hw = SW / 2, f0 = col0 + ch * hw;
-      for (int c0 = f0; c0 < f0 + hw; c0 += 16) {
-        uint32_t r0[16], r1[16];
-        tmem_ld16(ta + c0, r0);
-        if (nchunks > 1) tmem_ld16(ta + 256 + c0, r1);
-        tmem_wait_ld();
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int c0 = f0 + 16 * jj;
+        if (16 * jj >= hw) break;
+        float vals[16];
+        if (p.S > 1) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) vals[e] = acc[16 * jj + e];
+        } else {
+          uint32_t r0[16], r1[16];
+          tmem_ld16(ta + c0, r0);
+          if (nchunks > 1) tmem_ld16(ta + 256 + c0, r1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) vals[e] = __uint_as_float(r0[e]) + (nchunks > 1 ? __uint_as_float(r1[e]) : 0.f);
+        }
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
           const int col = c0 + 4 * qd;
-          const int rc = col - ks * CW;  // column within the chunk
           const int gq = (col & 31) >> 2;
-          float v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            v[e] = __uint_as_float(r0[4 * qd + e]) + (nchunks > 1 ? __uint_as_float(r1[4 * qd + e]) : 0.f);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (k >= p.S || k == ks) continue;
-            const float4 pv = ld_sw(smem + ((k * CW + rc) >> 5) * GEBOX, rl, gq);
-            v[0] += pv.x; v[1] += pv.y; v[2] += pv.z; v[3] += pv.w;
-          }
+          float v[4] = {vals[4 * qd], vals[4 * qd + 1], vals[4 * qd + 2], vals[4 * qd + 3]};
           const float4 ic = *reinterpret_cast<const float4*>(&st->inv[128 + col]);
           const float icv[4] = {ic.x, ic.y, ic.z, ic.w};
 #pragma unroll

@@ -210,9 +210,11 @@ def test_syrk_full(n, m, two):
 
 
 # ------------------------------------------------------------------ matrix-vector
-# single-pass cluster kernel: n >= 16384 and A >= 96 MB (e.g. (2000, 32764), (1537, 16388)); else two passes
+# single-pass cluster kernel: n >= 16384 and A >= 96 MB (e.g. (2000, 32764), (1537, 16388), (300, 32768));
+# else two passes (e.g. (6000, 4100): 98 MB of A with short rows)
 @pytest.mark.parametrize("m,n", [(1, 4), (7, 8), (257, 516), (1000, 2052), (4096, 4096), (3001, 5000),
-                                 (150, 32768), (5000, 1024), (148, 1028), (2000, 32764), (1537, 16388)])
+                                 (150, 32768), (5000, 1024), (148, 1028), (2000, 32764), (1537, 16388),
+                                 (6000, 4100), (300, 32768)])
 def test_atax(m, n):
     _ok(P.check_atax(m, n))
 
