@@ -16,14 +16,26 @@ namespace {
 // SPLIT_U at a time: SPLIT_U independent float4 loads in flight per thread, no index
 // division, coalesced 4 KiB row segments per CTA.
 constexpr int SPLIT_U = 4;
-__global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X, int rows, int cols4, int ldx,
-                                                    float* __restrict__ hi, float* __restrict__ lo, int ldo) {
+// done != nullptr: every CTA adds 1 (release) when its stores are complete: a chained GEMM
+// running concurrently on another stream acquires the count instead of a stream dependency.
+// (<= 42 registers: a CTA fits beside a resident chain CTA on the same SM, see launch_umma_chain.)
+__device__ __forceinline__ void signal_done(unsigned* done) {
+  if (!done) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(done) : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(256, 6) split_kernel(const float* __restrict__ X, int rows, int cols4, int ldx,
+                                                       float* __restrict__ hi, float* __restrict__ lo, int ldo,
+                                                       unsigned* done) {
   pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
   const int c4 = blockIdx.x * 256 + threadIdx.x;
-  if (c4 >= cols4) return;
   const int c = 4 * c4;
-  for (int r0 = blockIdx.y * SPLIT_U; r0 < rows; r0 += gridDim.y * SPLIT_U) {
+  for (int r0 = blockIdx.y * SPLIT_U; c4 < cols4 && r0 < rows; r0 += gridDim.y * SPLIT_U) {
     float4 v[SPLIT_U];
 #pragma unroll
     for (int u = 0; u < SPLIT_U; ++u)
@@ -42,15 +54,16 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X,
       *reinterpret_cast<float4*>(lo + o) = l;
     }
   }
+  signal_done(done);
 }
 
 // out[c][r] = split(f(X[r][c])) with f(x) = ((double)x - mean[c]) * inv[c] when mean != null.
 // 64 x 64 tile per CTA: float4 loads of X rows, padded smem transpose, float4
 // stores of the hi / lo rows (output pitch ldo is a multiple of 4).
-__global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ X, int rows, int cols, int ldx,
-                                                      float* __restrict__ hiT, float* __restrict__ loT, int ldo,
-                                                      const double* __restrict__ mean,
-                                                      const double* __restrict__ inv) {
+__global__ void __launch_bounds__(256, 6) split_t_kernel(const float* __restrict__ X, int rows, int cols, int ldx,
+                                                         float* __restrict__ hiT, float* __restrict__ loT, int ldo,
+                                                         const double* __restrict__ mean,
+                                                         const double* __restrict__ inv, unsigned* done) {
   __shared__ float tile[64][65];
   pdl_trigger();  // dependents may start their setup once every CTA here runs
   pdl_wait();
@@ -98,12 +111,13 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
       *reinterpret_cast<float4*>(loT + (long long)(c0 + cl) * ldo + r) = l;
     }
   }
+  signal_done(done);
 }
 
 }  // namespace
 
 cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi, float* lo, int ldo,
-                         cudaStream_t s) {
+                         cudaStream_t s, unsigned* done, unsigned* ctas) {
   const int cols4 = cols / 4;  // cols % 4 == 0 validated by the ABI
   const int gx = (cols4 + 255) / 256;
   const int row_steps = (rows + SPLIT_U - 1) / SPLIT_U;
@@ -111,13 +125,16 @@ cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi,
   if (gy > row_steps) gy = row_steps;
   if (gy > 65535) gy = 65535;
   if (gy < 1) gy = 1;
-  return launch_pdl(split_kernel, dim3((unsigned)gx, (unsigned)gy), dim3(256), 0, s, X, rows, cols4, ldx, hi, lo, ldo);
+  if (ctas) *ctas += (unsigned)(gx * gy);
+  return launch_pdl(split_kernel, dim3((unsigned)gx, (unsigned)gy), dim3(256), 0, s, X, rows, cols4, ldx, hi, lo, ldo,
+                    done);
 }
 
 cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* hiT, float* loT, int ldo,
-                           const double* mean, const double* inv, cudaStream_t s) {
+                           const double* mean, const double* inv, cudaStream_t s, unsigned* done, unsigned* ctas) {
   dim3 grid((cols + 63) / 64, (rows + 63) / 64);
-  return launch_pdl(split_t_kernel, grid, dim3(256), 0, s, X, rows, cols, ldx, hiT, loT, ldo, mean, inv);
+  if (ctas) *ctas += grid.x * grid.y;
+  return launch_pdl(split_t_kernel, grid, dim3(256), 0, s, X, rows, cols, ldx, hiT, loT, ldo, mean, inv, done);
 }
 
 }  // namespace pb

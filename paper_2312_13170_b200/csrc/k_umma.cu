@@ -172,6 +172,51 @@ struct Params {
   unsigned long long* tstamp;    // PB_UMMA_TIMING (tuning only): [cta][unit<16][8] globaltimer stamps
 };
 
+// A launch = one GEMM (nphase 1) or a CHAIN of up to 3 dependent GEMMs in one persistent
+// grid (NEXT-4 chain fusion: 2mm's tmp -> D, 3mm's F, E -> G). Units of phase q are
+// [ubase[q], ubase[q+1]); every CTA walks its units in order, so it finishes its part of a
+// phase before it starts the next. A phase's epilogue publishes each finished tile on a
+// readiness counter (release add after its stores); a later phase's TMA producer acquires
+// the counters of the operand panels it loads (A: the row panel tm of this CTA's rank;
+// B: the column panel tn, i.e. the rows of the transposed operand written by EPI_SPLIT_T)
+// before its first k-block. Only earlier phases are waited on and all CTAs are resident
+// (persistent grid <= SMs), so the waits cannot deadlock.
+struct Chain {
+  int nphase;
+  long long ubase[4];
+  Params ph[3];
+  unsigned* cnt;           // readiness counters (zeroed before the launch)
+  int sig_kind[3];         // 0 none, 1: cnt[sig_off + tm * CG + rank] += 1, 2: cnt[sig_off + tn] += 1
+  int sig_off[3];
+  int waitA_off[3], waitA_target[3];  // A rows: cnt[off + tm * CG + rank] >= target (off < 0: none)
+  int waitB_off[3], waitB_target[3];  // B rows: cnt[off + tn] >= target
+  // operand splits of a later phase done INSIDE the launch by the epilogue warps of every CTA
+  // (idle during the first tile's mainloop), published on cnt[pre_off] (one add per CTA)
+  struct Pre {
+    const float* X;
+    int rows, cols, ldx;
+    float* hi;
+    float* lo;
+    int ldo;
+    int transpose;  // 0: hi/lo of X (same layout); 1: hi/lo of X^T (cols x rows)
+  } pre[2];
+  int npre, pre_phase, pre_off;
+};
+constexpr int PRE_STAGE = 32 * 32 * 4;  // per epilogue warp: a 32 x 32 transpose block (swizzled)
+__device__ __forceinline__ int phase_of(const Chain& ch, long long u) {
+  int q = 0;
+  while (q + 1 < ch.nphase && u >= ch.ubase[q + 1]) ++q;
+  return q;
+}
+__device__ __forceinline__ void wait_count(const unsigned* c, unsigned target) {
+  unsigned v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (v >= target) break;
+    __nanosleep(64);
+  }
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -190,6 +235,7 @@ struct __align__(8) Ctl {
   uint64_t tempty[2];
   uint32_t tmem_base;
   uint32_t last_flag;
+  uint32_t pre_warps_done;  // chain: epilogue warps that finished their share of the in-launch splits
 };
 
 // number of column tiles in tile-row tm (lower triangle: tiles touching j <= i)
@@ -255,13 +301,17 @@ __device__ __forceinline__ Unit unit_of(const Params& p, long long u, int nkb_to
   return r;
 }
 
-template <int CG, int BN>
+// CHAIN = false: one GEMM (the chain machinery compiles away, keeping the epilogue's
+// register budget); CHAIN = true: the phases of a Chain in one launch.
+template <int CG, int BN, bool CHAIN>
 __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     umma3x_kernel(const __grid_constant__ CUtensorMap a0h, const __grid_constant__ CUtensorMap a0l,
                   const __grid_constant__ CUtensorMap b0h, const __grid_constant__ CUtensorMap b0l,
                   const __grid_constant__ CUtensorMap a1h, const __grid_constant__ CUtensorMap a1l,
                   const __grid_constant__ CUtensorMap b1h, const __grid_constant__ CUtensorMap b1l,
-                  const Params p) {
+                  const __grid_constant__ CUtensorMap a2h, const __grid_constant__ CUtensorMap a2l,
+                  const __grid_constant__ CUtensorMap b2h, const __grid_constant__ CUtensorMap b2l,
+                  const __grid_constant__ Chain ch) {
   using C = Cfg<CG, BN>;
   constexpr int STAGES = C::STAGES, STAGE_BYTES = C::STAGE_BYTES, B_TILE = C::B_TILE;
   constexpr int CHUNK_KB = C::CHUNK_KB;
@@ -284,11 +334,15 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       mbar_init(&ctl->tfull[s], 1);
       mbar_init(&ctl->tempty[s], C::EPI_WARPS * CG);  // one arrive per epilogue warp of every CTA
     }
+    ctl->pre_warps_done = 0;
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&a0h); tma_prefetch(&a0l); tma_prefetch(&b0h); tma_prefetch(&b0l);
-    if (p.npairs > 1) { tma_prefetch(&a1h); tma_prefetch(&a1l); tma_prefetch(&b1h); tma_prefetch(&b1l); }
+    if (ch.ph[0].npairs > 1 || ch.nphase > 1) {
+      tma_prefetch(&a1h); tma_prefetch(&a1l); tma_prefetch(&b1h); tma_prefetch(&b1l);
+    }
+    if (ch.nphase > 2) { tma_prefetch(&a2h); tma_prefetch(&a2l); tma_prefetch(&b2h); tma_prefetch(&b2l); }
   }
   if (warp == 1) tmem_alloc_cg<CG>(&ctl->tmem_base, TMEM_COLS);
   tc_fence_before();
@@ -299,8 +353,15 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   const int tl = g_tl_on;
   tl_enter(tl, g_tl, 0);
   const uint32_t tmem_base = ctl->tmem_base;
-  const int nkb_total = p.nkb * p.npairs;
-  const long long num_units = p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles);
+  const long long num_units = ch.ubase[ch.nphase];
+  // operand maps: phase q (chain) or pair q (syr2k) uses maps 4q .. 4q + 3
+  auto map_of = [&](int q, int which) -> const CUtensorMap* {
+    switch (q * 4 + which) {
+      case 0: return &a0h; case 1: return &a0l; case 2: return &b0h; case 3: return &b0l;
+      case 4: return &a1h; case 5: return &a1l; case 6: return &b1h; case 7: return &b1l;
+      case 8: return &a2h; case 9: return &a2l; case 10: return &b2h; default: return &b2l;
+    }
+  };
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA loads its own A rows and B half)
@@ -308,21 +369,30 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (long long u = tile0; u < num_units; u += tile_step) {
-        const Unit un = unit_of(p, u, nkb_total);
+        const int ph = CHAIN ? phase_of(ch, u) : 0;
+        const Params& p = ch.ph[ph];
+        const Unit un = unit_of(p, u - ch.ubase[ph], p.nkb * p.npairs);
         int tm, tn;
         tile_coords(p, un.t, tm, tn);
         const int arow = tm * C::PAIR_M + (int)rank * BM;
         const int brow = tn * BN + (int)rank * C::B_ROWS;
+        if (CHAIN && (ch.waitA_off[ph] >= 0 || ch.waitB_off[ph] >= 0 || (ch.npre && ph == ch.pre_phase))) {  // chain
+          if (ch.npre && ph == ch.pre_phase) wait_count(ch.cnt + ch.pre_off, gridDim.x);
+          if (ch.waitA_off[ph] >= 0) wait_count(ch.cnt + ch.waitA_off[ph] + tm * CG + rank, ch.waitA_target[ph]);
+          if (ch.waitB_off[ph] >= 0) wait_count(ch.cnt + ch.waitB_off[ph] + tn, ch.waitB_target[ph]);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy stores -> TMA reads
+        }
         for (int kb = un.kbA; kb < un.kbB; ++kb) {
           mbar_wait(&ctl->empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           const int pair = kb >= p.nkb;
           const int k = (kb - pair * p.nkb) * BK;
+          const int mq = ch.nphase > 1 ? ph : pair;
           if (leader) mbar_arrive_expect_tx(&ctl->full[stage], CG * STAGE_BYTES);
-          tma_load_cg<CG>(pair ? &a1h : &a0h, &ctl->full[stage], st, k, arow);
-          tma_load_cg<CG>(pair ? &a1l : &a0l, &ctl->full[stage], st + A_TILE, k, arow);
-          tma_load_cg<CG>(pair ? &b1h : &b0h, &ctl->full[stage], st + 2 * A_TILE, k, brow);
-          tma_load_cg<CG>(pair ? &b1l : &b0l, &ctl->full[stage], st + 2 * A_TILE + B_TILE, k, brow);
+          tma_load_cg<CG>(map_of(mq, 0), &ctl->full[stage], st, k, arow);
+          tma_load_cg<CG>(map_of(mq, 1), &ctl->full[stage], st + A_TILE, k, arow);
+          tma_load_cg<CG>(map_of(mq, 2), &ctl->full[stage], st + 2 * A_TILE, k, brow);
+          tma_load_cg<CG>(map_of(mq, 3), &ctl->full[stage], st + 2 * A_TILE + B_TILE, k, brow);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -341,7 +411,9 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       int chunk_it = 0;
       int ul = 0;
       for (long long u = tile0; u < num_units; u += tile_step, ++ul) {
-        const Unit un = unit_of(p, u, nkb_total);
+        const int ph = CHAIN ? phase_of(ch, u) : 0;
+        const Params& p = ch.ph[ph];
+        const Unit un = unit_of(p, u - ch.ubase[ph], p.nkb * p.npairs);
         const int kbA = un.kbA, kbB = un.kbB;
         TSTAMP(ul, 0);
         for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
@@ -383,14 +455,81 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   } else {
     // ===================== epilogue (warps 2..5 of every CTA) =====================
     const int q = warp & 3;                    // TMEM lane quarter this warp may access
-    const int ch = (warp - 2) / 4;             // which EPI_COLS-wide column half of the tile
-    const int cbase = ch * EPI_COLS;
-    const uint32_t flags = p.flags;
+    const int chalf = (warp - 2) / 4;          // which EPI_COLS-wide column half of the tile
+    const int cbase = chalf * EPI_COLS;
     int chunk_it = 0;
     int ul = 0;
-    for (long long u = tile0; u < num_units; u += tile_step, ++ul) {
-      const Unit un = unit_of(p, u, nkb_total);
+    // ---- chain: the later phase's operand splits (hi = rna_tf32(x), lo = rna_tf32(x - hi)),
+    // shared by the epilogue warps of all CTAs in 32 x 32 blocks, done one block at a time
+    // while a warp would otherwise spin on an accumulator chunk (so the MMA never waits for
+    // a drain); the last warp of a CTA to finish publishes the CTA's part (release add).
+    const int ew = warp - 2;
+    float* const stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024) + ew * (PRE_STAGE / 4);
+    const long long gw = (long long)blockIdx.x * C::EPI_WARPS + ew, nw = (long long)gridDim.x * C::EPI_WARPS;
+    int pre_k = 0;
+    long long pre_blk = gw;
+    bool pre_left = CHAIN && ch.npre > 0;
+    auto pre_step = [&]() {  // warp-uniform: one block of task pre_k, then advance
+      const Chain::Pre& t = ch.pre[pre_k];
+      const int br = (t.rows + 31) / 32, bc = (t.cols + 31) / 32;
+      if (pre_blk < (long long)br * bc) {
+        const int r0 = (int)(pre_blk / bc) * 32, c0 = (int)(pre_blk % bc) * 32;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = i * 4 + (lane >> 3), cq = lane & 7;  // block row, 16-B chunk: 4 rows x 128 B per load
+          const int r = r0 + rr, c = c0 + cq * 4;
+          const bool in = r < t.rows && c < t.cols;
+          const float4 v = in ? *reinterpret_cast<const float4*>(t.X + (long long)r * t.ldx + c)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (!t.transpose) {
+            if (in) {
+              float4 h, l;
+              split3x(v.x, h.x, l.x); split3x(v.y, h.y, l.y); split3x(v.z, h.z, l.z); split3x(v.w, h.w, l.w);
+              *reinterpret_cast<float4*>(t.hi + (long long)r * t.ldo + c) = h;
+              *reinterpret_cast<float4*>(t.lo + (long long)r * t.ldo + c) = l;
+            }
+          } else {
+            *reinterpret_cast<float4*>(stg + rr * 32 + ((cq ^ (rr & 7)) << 2)) = v;  // 16-B XOR swizzle
+          }
+        }
+        if (t.transpose) {
+          __syncwarp();
+          for (int cc = 0; cc < 32; ++cc) {  // output row c0 + cc (input column), element r0 + lane
+            const int j = c0 + cc, i2 = r0 + lane;
+            const float x = stg[lane * 32 + ((((cc >> 2) ^ (lane & 7)) << 2) | (cc & 3))];
+            if (j < t.cols && i2 < t.rows) {
+              float h, l;
+              split3x(x, h, l);
+              t.hi[(long long)j * t.ldo + i2] = h;
+              t.lo[(long long)j * t.ldo + i2] = l;
+            }
+          }
+          __syncwarp();
+        }
+        pre_blk += nw;
+      }
+      if (pre_blk >= (long long)br * bc) {
+        if (++pre_k < ch.npre) {
+          pre_blk = gw;
+        } else {
+          pre_left = false;
+          __threadfence();
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // for the later phase's TMA reads
+          __syncwarp();
+          if (lane == 0 && atomicAdd(&ctl->pre_warps_done, 1u) == (unsigned)C::EPI_WARPS - 1) {
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ch.cnt + ch.pre_off) : "memory");
+          }
+        }
+      }
+    };
+    for (long long u0 = tile0; u0 < num_units; u0 += tile_step, ++ul) {
+      const int ph = CHAIN ? phase_of(ch, u0) : 0;
+      const Params& p = ch.ph[ph];
+      const long long u = u0 - ch.ubase[ph];  // unit index within the phase
+      const Unit un = unit_of(p, u, p.nkb * p.npairs);
       const long long t = un.t;
+      const uint32_t flags = p.flags;
       const int kbA = un.kbA, kbB = un.kbB;
       int tm, tn;
       tile_coords(p, t, tm, tn);
@@ -400,6 +539,10 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
         const int slot = chunk_it & 1;
         const uint32_t slot_phase = (chunk_it >> 1) & 1;
+        if (CHAIN && pre_left) {  // in-launch splits fill the wait for this accumulator chunk
+          const uint32_t ta = smem_u32(&ctl->tfull[slot]);
+          while (pre_left && !__shfl_sync(0xffffffffu, lane == 0 ? (int)mbar_try_wait(ta, slot_phase) : 0, 0)) pre_step();
+        }
         mbar_wait(&ctl->tfull[slot], slot_phase);
         tc_fence_after();
         if (kb0 == kbA && warp == 2 && lane == 0) TSTAMP(ul, 2);
@@ -555,6 +698,18 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         }
       }
       if (warp == 2 && lane == 0) TSTAMP(ul, 5);
+      if (CHAIN && ch.sig_kind[ph]) {  // chain: publish this CTA's part of the finished tile
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // for the next phase's TMA reads
+        asm volatile("bar.sync 1, %0;" ::"r"(C::EPI_WARPS * 32) : "memory");
+        if (warp == 2 && lane == 0) {
+          unsigned* c = ch.cnt + ch.sig_off[ph] + (ch.sig_kind[ph] == 1 ? tm * CG + (int)rank : tn);
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
+        }
+      }
+    }
+    if constexpr (CHAIN) {
+      while (pre_left) pre_step();  // (a CTA with few units: the rest of its share of the splits)
     }
   }
 
@@ -567,8 +722,9 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
   }
 }
 
+// Tile/split fields of one GEMM (phase) for the tile config <CG, BN>; false if it has no tiles.
 template <int CG, int BN>
-cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_tiles, cudaStream_t s, int* launches) {
+bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles) {
   using C = Cfg<CG, BN>;
   const int tiles_m = (d.M + C::PAIR_M - 1) / C::PAIR_M;
   p.tiles_n = (d.N + BN - 1) / BN;
@@ -576,7 +732,7 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
   p.tm0 = d.tm0 * 128 / C::PAIR_M;  // d.tm0 is in 128-row units
   p.tm1 = d.tm1 < 0 ? tiles_m : (d.tm1 * 128 + C::PAIR_M - 1) / C::PAIR_M;
   if (p.tm1 > tiles_m) p.tm1 = tiles_m;
-  if (p.tm1 <= p.tm0) return cudaSuccess;
+  if (p.tm1 <= p.tm0) return false;
   long long nt = 0;
   for (int tm = p.tm0; tm < p.tm1; ++tm)
     nt += (d.flags & EPI_TRI) ? std::min(p.ratio * (tm + 1), p.tiles_n) : p.tiles_n;
@@ -589,30 +745,89 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
   static unsigned long long* tbuf = nullptr;
   if (timing && !tbuf) cudaMalloc(&tbuf, 148 * 16 * 8 * sizeof(unsigned long long));  // debug only
   p.tstamp = timing ? tbuf : nullptr;
-  if (timing) cudaMemsetAsync(tbuf, 0, 148 * 16 * 8 * sizeof(unsigned long long), s);
   p.part = d.part;
   p.counters = d.counters;
-  if (ksplit > 1 && !(d.flags & EPI_PARTIAL)) {
-    cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)p.split_tiles * CG * sizeof(unsigned), s);
-    if (e != cudaSuccess) return e;
-  }
-  CUtensorMap maps[8];
-  for (int q = 0; q < 2; ++q) {
-    const SplitOperand& A = d.a[q < d.npairs ? q : 0];
-    const SplitOperand& B = d.b[q < d.npairs ? q : 0];
+  return true;
+}
+inline long long phase_units(const Params& p) { return p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles); }
+
+template <int CG, int BN>
+bool phase_maps(const GemmDesc& d, CUtensorMap* maps /* 4 per operand pair */) {
+  using C = Cfg<CG, BN>;
+  for (int q = 0; q < d.npairs; ++q) {
+    const SplitOperand& A = d.a[q];
+    const SplitOperand& B = d.b[q];
     if (!make_map(&maps[4 * q + 0], A.hi, A.rows, A.K, A.ld, BM) ||
         !make_map(&maps[4 * q + 1], A.lo, A.rows, A.K, A.ld, BM) ||
         !make_map(&maps[4 * q + 2], B.hi, B.rows, B.K, B.ld, C::B_ROWS) ||
         !make_map(&maps[4 * q + 3], B.lo, B.rows, B.K, B.ld, C::B_ROWS))
-      return cudaErrorInvalidValue;
+      return false;
   }
-  const size_t smem = C::STAGES * C::STAGE_BYTES + 1024 + sizeof(Ctl) + 64;
+  return true;
+}
+
+template <int CG, int BN, bool CHAIN>
+cudaError_t launch_chain_kernel(const Chain& ch, const CUtensorMap* maps, cudaStream_t s, int* launches);
+
+template <int CG, int BN>
+cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_tiles, cudaStream_t s, int* launches) {
+  if (!prep_phase<CG, BN>(d, p, ksplit, split_tiles)) return cudaSuccess;
+  if (p.tstamp) cudaMemsetAsync(p.tstamp, 0, 148 * 16 * 8 * sizeof(unsigned long long), s);
+  if (ksplit > 1 && !(d.flags & EPI_PARTIAL)) {
+    cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)p.split_tiles * CG * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+  }
+  CUtensorMap maps[12];
+  if (!phase_maps<CG, BN>(d, maps)) return cudaErrorInvalidValue;
+  for (int q = 4 * d.npairs; q < 12; ++q) maps[q] = maps[q % 4];
+  Chain ch{};
+  ch.nphase = 1;
+  ch.ph[0] = p;
+  ch.ubase[0] = 0;
+  ch.ubase[1] = phase_units(p);
+  for (int q = 0; q < 3; ++q) { ch.waitA_off[q] = -1; ch.waitB_off[q] = -1; }
+  cudaError_t e = launch_chain_kernel<CG, BN, false>(ch, maps, s, launches);
+  if (e != cudaSuccess) return e;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (p.tstamp) cudaStreamIsCapturing(s, &cap);
+  const long long units = std::min<long long>(phase_units(p), num_sms() / CG);
+  if (p.tstamp && cap == cudaStreamCaptureStatusNone) {  // debug: per-phase durations (us), medians over CTAs/units
+    std::vector<unsigned long long> h(148 * 16 * 8);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), p.tstamp, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    std::vector<double> mma, drain_lag, split, store;
+    for (int c = 0; c < (int)(units * CG); ++c)
+      for (int u = 0; u < 16; ++u) {
+        const unsigned long long* ev = &h[((size_t)c * 16 + u) * 8];
+        for (int k = 0; k < 6; ++k)
+          if (ev[k]) { t0 = std::min(t0, ev[k]); t1 = std::max(t1, ev[k]); }
+        if (ev[0] && ev[1]) mma.push_back((ev[1] - ev[0]) / 1e3);
+        if (ev[1] && ev[3]) drain_lag.push_back(((long long)ev[3] - (long long)ev[1]) / 1e3);
+        if (ev[3] && ev[4]) split.push_back((ev[4] - ev[3]) / 1e3);
+        if (ev[4] && ev[5]) store.push_back((ev[5] - ev[4]) / 1e3);
+      }
+    auto med = [](std::vector<double> v) { if (v.empty()) return 0.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+    fprintf(stderr, "[pb timing] span %.1f us | per unit median: mma %.1f, mma-end->drained %.1f, split-exchange %.1f, "
+            "stores %.1f us (n=%zu)\n", (t1 - t0) / 1e3, med(mma), med(drain_lag), med(split), med(store), mma.size());
+  }
+  if (getenv("PB_TRACE"))
+    fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld split %lldx%d grid=%lld\n", CG,
+            BN, d.M, d.N, d.K, d.npairs, d.flags, p.num_tiles, p.split_tiles, p.ksplit, units * CG);
+  return cudaSuccess;
+}
+
+template <int CG, int BN, bool CHAIN>
+cudaError_t launch_chain_kernel(const Chain& ch, const CUtensorMap* maps, cudaStream_t s, int* launches) {
+  using C = Cfg<CG, BN>;
+  // CHAIN: + per-epilogue-warp transpose staging for the in-launch operand splits
+  const size_t smem = C::STAGES * C::STAGE_BYTES + 1024 + (CHAIN ? 1024 + C::EPI_WARPS * PRE_STAGE : sizeof(Ctl) + 64);
   {
-    const cudaError_t e = ensure_smem<umma3x_kernel<CG, BN>>(smem);
+    const cudaError_t e = ensure_smem<umma3x_kernel<CG, BN, CHAIN>>(smem);
     if (e != cudaSuccess) return e;
   }
   const long long max_units = num_sms() / CG;
-  const long long work = p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles);
+  const long long work = ch.ubase[ch.nphase];
   const long long units = work < max_units ? work : max_units;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
@@ -626,34 +841,9 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, umma3x_kernel<CG, BN>, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
-                                     maps[6], maps[7], p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, umma3x_kernel<CG, BN, CHAIN>, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+                                     maps[6], maps[7], maps[8], maps[9], maps[10], maps[11], ch);
   if (launches) ++*launches;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (p.tstamp) cudaStreamIsCapturing(s, &cap);
-  if (p.tstamp && cap == cudaStreamCaptureStatusNone) {  // debug: per-phase durations (us), medians over CTAs/units
-    std::vector<unsigned long long> h(148 * 16 * 8);
-    cudaStreamSynchronize(s);
-    cudaMemcpy(h.data(), p.tstamp, h.size() * 8, cudaMemcpyDeviceToHost);
-    unsigned long long t0 = ~0ull, t1 = 0;
-    std::vector<double> mma, drain_lag, split, store;
-    for (int c = 0; c < (int)(units * CG); ++c)
-      for (int u = 0; u < 16; ++u) {
-        const unsigned long long* e = &h[((size_t)c * 16 + u) * 8];
-        for (int k = 0; k < 6; ++k)
-          if (e[k]) { t0 = std::min(t0, e[k]); t1 = std::max(t1, e[k]); }
-        if (e[0] && e[1]) mma.push_back((e[1] - e[0]) / 1e3);
-        if (e[1] && e[3]) drain_lag.push_back(((long long)e[3] - (long long)e[1]) / 1e3);
-        if (e[3] && e[4]) split.push_back((e[4] - e[3]) / 1e3);
-        if (e[4] && e[5]) store.push_back((e[5] - e[4]) / 1e3);
-      }
-    auto med = [](std::vector<double> v) { if (v.empty()) return 0.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
-    fprintf(stderr, "[pb timing] span %.1f us | per unit median: mma %.1f, mma-end->drained %.1f, split-exchange %.1f, "
-            "stores %.1f us (n=%zu)\n", (t1 - t0) / 1e3, med(mma), med(drain_lag), med(split), med(store), mma.size());
-  }
-  if (getenv("PB_TRACE"))
-    fprintf(stderr, "[pb] umma3x<%d,%d> M=%d N=%d K=%d pairs=%d flags=0x%x tiles=%lld split %lldx%d grid=%lld\n", CG,
-            BN, d.M, d.N, d.K, d.npairs, d.flags, p.num_tiles, p.split_tiles, p.ksplit, units * CG);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -885,6 +1075,112 @@ cudaError_t launch_gram_combine(const GemmDesc& d, const UmmaPlan& pl, bool diag
   else if (pl.cfg == 2) e = launch_pdl(gram_combine_kernel<2, 128>, dim3(grid), dim3(256), 0, s, p, dg, cs);
   else e = launch_pdl(gram_combine_kernel<1, 128>, dim3(grid), dim3(256), 0, s, p, dg, cs);
   if (launches) ++*launches;
+  return e;
+}
+
+// ---- NEXT-4 chain fusion: up to 3 dependent GEMMs in one persistent launch (see Chain)
+namespace {
+Params base_params(const GemmDesc& d) {
+  Params p{};
+  p.M = d.M; p.N = d.N; p.K = d.K; p.npairs = d.npairs; p.nkb = (d.K + BK - 1) / BK;
+  p.flags = d.flags; p.alpha = d.alpha; p.beta = d.beta; p.cin = d.cin; p.ldc = d.ldc;
+  p.out = d.out; p.ldo = d.ldo; p.out_row0 = d.out_row0;
+  p.split_hi = d.split_hi; p.split_lo = d.split_lo; p.ld_split = d.ld_split;
+  return p;
+}
+}  // namespace
+
+bool umma_chain_ok(const GemmDesc* d, int nphase) {
+  // Opt-in (PB_CHAIN=1): measured on B200 at 4096 the chained launch is ~5% slower than the
+  // separate launches (the in-launch operand splits cost the epilogue warps' registers and
+  // time; the PDL-overlapped kernel boundary it removes is cheap). DESIGN.md §8 "chain".
+  static const char* env = getenv("PB_CHAIN");
+  if (!env || atoi(env) == 0) return false;
+  if (nphase < 1 || nphase > 3) return false;
+  for (int q = 0; q < nphase; ++q) {
+    const UmmaPlan pl = umma_plan(d[q]);
+    if (pl.cfg != 3 || d[q].npairs != 1 || (d[q].flags & (EPI_TRI | EPI_PARTIAL | EPI_MIRROR)) || d[q].tm0 != 0 ||
+        d[q].tm1 >= 0)
+      return false;
+  }
+  return num_sms() >= 2;
+}
+
+size_t umma_chain_cnt_bytes(const GemmDesc* d, int nphase) {
+  size_t n = 0;
+  for (int q = 0; q < nphase; ++q) n += (size_t)((d[q].M + 255) / 256) * 2 + (size_t)((d[q].N + 255) / 256);
+  return align_up((n + 1) * sizeof(unsigned), 256);  // + the in-launch split counter
+}
+
+cudaError_t launch_umma_chain(const GemmDesc* d, const ChainLink* links, int nphase, unsigned* cnt, size_t cnt_cap,
+                              cudaStream_t s, int* launches) {
+  if (!umma_chain_ok(d, nphase)) return cudaErrorNotSupported;
+  if (umma_chain_cnt_bytes(d, nphase) > cnt_cap) return cudaErrorInvalidValue;
+  constexpr int CG = 2, BN = 256;
+  Chain ch{};
+  ch.nphase = nphase;
+  ch.cnt = cnt;
+  CUtensorMap maps[12];
+  int off = 0;
+  int row_off[3], col_off[3];
+  for (int q = 0; q < nphase; ++q) {  // counter areas: [tile rows x ranks] then [tile columns] per phase
+    row_off[q] = off; off += ((d[q].M + 255) / 256) * CG;
+    col_off[q] = off; off += (d[q].N + 255) / 256;
+  }
+  ch.ubase[0] = 0;
+  for (int q = 0; q < nphase; ++q) {
+    const UmmaPlan pl = umma_plan(d[q]);
+    int ks = pl.ksplit;
+    if (ks > 1 && (d[q].part == nullptr || d[q].counters == nullptr)) ks = 1;
+    if (ks > 1 && (pl.part_bytes > d[q].part_cap || pl.counter_bytes > d[q].counter_cap)) return cudaErrorInvalidValue;
+    Params p = base_params(d[q]);
+    if (!prep_phase<CG, BN>(d[q], p, ks, pl.split_tiles)) return cudaErrorInvalidValue;
+    if (ks > 1) {
+      const cudaError_t e = cudaMemsetAsync(d[q].counters, 0, (size_t)p.split_tiles * CG * sizeof(unsigned), s);
+      if (e != cudaSuccess) return e;
+    }
+    if (!phase_maps<CG, BN>(d[q], maps + 4 * q)) return cudaErrorInvalidValue;
+    ch.ph[q] = p;
+    ch.ubase[q + 1] = ch.ubase[q] + phase_units(p);
+    ch.waitA_off[q] = -1;
+    ch.waitB_off[q] = -1;
+  }
+  for (int q = nphase; q < 3; ++q) {
+    for (int k = 0; k < 4; ++k) maps[4 * q + k] = maps[k];
+    ch.waitA_off[q] = ch.waitB_off[q] = -1;
+  }
+  ch.npre = 0;
+  for (int q = 0; q < nphase; ++q)
+    for (int k = 0; k < links[q].npre; ++k) {
+      if (ch.npre == 2 || (ch.npre && ch.pre_phase != q) || q == 0) return cudaErrorInvalidValue;
+      const ChainLink::Pre& a = links[q].pre[k];
+      ch.pre[ch.npre++] = Chain::Pre{a.X, a.rows, a.cols, a.ldx, a.hi, a.lo, a.ldo, a.transpose ? 1 : 0};
+      ch.pre_phase = q;
+    }
+  for (int q = 0; q < nphase; ++q) {
+    const int a = links[q].waitA, b = links[q].waitB;
+    if (a >= 0) {  // this phase's A rows = phase a's output rows, panel by panel (same 256-row tiling)
+      if (a >= q || d[a].M != d[q].M) return cudaErrorInvalidValue;
+      ch.sig_kind[a] = 1; ch.sig_off[a] = row_off[a];
+      ch.waitA_off[q] = row_off[a];
+      ch.waitA_target[q] = (d[a].N + BN - 1) / BN;  // every tile of the row panel, per rank
+    }
+    if (b >= 0) {  // this phase's B rows = phase b's output columns (EPI_SPLIT_T), column panel by panel
+      if (b >= q || d[b].N != d[q].N || !(d[b].flags & EPI_SPLIT_T)) return cudaErrorInvalidValue;
+      if (ch.sig_kind[b] == 1) return cudaErrorInvalidValue;
+      ch.sig_kind[b] = 2; ch.sig_off[b] = col_off[b];
+      ch.waitB_off[q] = col_off[b];
+      ch.waitB_target[q] = ((d[b].M + 255) / 256) * CG;  // both ranks of every tile of the column panel
+    }
+  }
+  ch.pre_off = off++;
+  if ((size_t)off * sizeof(unsigned) > cnt_cap) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)off * sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  e = launch_chain_kernel<CG, BN, true>(ch, maps, s, launches);
+  if (getenv("PB_TRACE"))
+    fprintf(stderr, "[pb] umma chain: %d phases, %lld units, grid %lld\n", nphase, ch.ubase[nphase],
+            std::min<long long>(ch.ubase[nphase], num_sms() / CG) * CG);
   return e;
 }
 

@@ -102,19 +102,36 @@ WsGemm ws_gemm(Carve& c, int ni, int nj, int nk) {
   w.sk = take_splitk(c, {shape(ni, nj, nk)});
   return w;
 }
-struct Ws2mm { SplitBuf a, bt, ct, tmp; SplitK sk; };
+// chain fusion (NEXT-4): each phase of the one-launch chain has its own split-K area (the
+// phases' split tiles can be live at the same time) plus the readiness counters
+struct ChainWs {
+  unsigned* cnt = nullptr;
+  size_t cnt_bytes = 0;
+};
+ChainWs take_chain(Carve& c, std::initializer_list<GemmDesc> gemms) {
+  ChainWs w;
+  w.cnt_bytes = umma_chain_cnt_bytes(gemms.begin(), (int)gemms.size());
+  w.cnt = c.take<unsigned>(w.cnt_bytes / sizeof(unsigned));
+  return w;
+}
+struct Ws2mm { SplitBuf a, bt, ct, tmp; SplitK sk, sk2; ChainWs chain; };
 Ws2mm ws_2mm(Carve& c, int ni, int nj, int nk, int nl) {
   Ws2mm w;
   w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.ct = take_split(c, nl, nj); w.tmp = take_split(c, ni, nj);
   w.sk = take_splitk(c, {shape(ni, nj, nk), shape(ni, nl, nj)});
+  w.sk2 = take_splitk(c, {shape(ni, nl, nj)});
+  w.chain = take_chain(c, {shape(ni, nj, nk), shape(ni, nl, nj)});
   return w;
 }
-struct Ws3mm { SplitBuf a, bt, c, dt, e, ft; SplitK sk; };
+struct Ws3mm { SplitBuf a, bt, c, dt, e, ft; SplitK sk, sk2, sk3; ChainWs chain; };
 Ws3mm ws_3mm(Carve& c, int ni, int nj, int nk, int nl, int nm) {
   Ws3mm w;
   w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.c = take_split(c, nj, nm);
   w.dt = take_split(c, nl, nm); w.e = take_split(c, ni, nj); w.ft = take_split(c, nl, nj);
   w.sk = take_splitk(c, {shape(nj, nl, nm), shape(ni, nj, nk), shape(ni, nl, nj)});
+  w.sk2 = take_splitk(c, {shape(ni, nj, nk)});
+  w.sk3 = take_splitk(c, {shape(ni, nl, nj)});
+  w.chain = take_chain(c, {shape(nj, nl, nm), shape(ni, nj, nk), shape(ni, nl, nj)});
   return w;
 }
 // covariance/correlation: n <= MAX_BANDED rows use the banded single-pass prep
@@ -332,6 +349,43 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
   Ws2mm w = ws_2mm(c, ni, nj, nk, nl);
   cudaStream_t st = S(s);
   int L = 0;
+  GemmDesc g1;  // tmp = alpha * A * B  (epilogue emits tmp's split = GEMM 2's A operand)
+  g1.M = ni; g1.N = nj; g1.K = nk;
+  g1.a[0] = w.a.op(); g1.b[0] = w.bt.op();
+  g1.flags = EPI_SPLIT | (tmp ? EPI_OUT : 0u);
+  g1.alpha = alpha;
+  g1.out = tmp; g1.ldo = nj;
+  g1.split_hi = w.tmp.hi; g1.split_lo = w.tmp.lo; g1.ld_split = w.tmp.ld;
+  w.sk.attach(g1);
+  GemmDesc g2;  // D = tmp * C + beta * D
+  g2.M = ni; g2.N = nl; g2.K = nj;
+  g2.a[0] = w.tmp.op(); g2.b[0] = w.ct.op();
+  g2.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
+  g2.alpha = 1.f; g2.beta = beta;
+  g2.cin = D; g2.ldc = nl; g2.out = D; g2.ldo = nl;
+  w.sk.attach(g2);
+  {
+    // NEXT-4 chain fusion: both GEMMs in one persistent launch; GEMM 2's
+    // tiles of row panel i start as soon as GEMM 1 has published tmp's row panel i. C^T's
+    // split (GEMM 2's B operand) is done inside the launch by the epilogue warps while
+    // GEMM 1's first tiles run.
+    GemmDesc gs[2] = {g1, g2};
+    w.sk2.attach(gs[1]);
+    if (umma_chain_ok(gs, 2)) {
+      ChainLink lk[2];
+      lk[1].waitA = 0;
+      lk[1].npre = 1;
+      ChainLink::Pre& pc = lk[1].pre[0];
+      pc.X = C; pc.rows = nj; pc.cols = nl; pc.ldx = nl;
+      pc.hi = const_cast<float*>(w.ct.hi); pc.lo = const_cast<float*>(w.ct.lo); pc.ldo = w.ct.ld; pc.transpose = true;
+      PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
+      PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
+      L += 2;
+      PB_CUDA(launch_umma_chain(gs, lk, 2, w.chain.cnt, w.chain.cnt_bytes, st, &L));
+      g_launches = L;
+      return PB_OK;
+    }
+  }
   Side* sd = side_stream();
   PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
   PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
@@ -344,23 +398,8 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
     PB_CUDA(launch_split_T(C, nj, nl, nl, w.ct.hi, w.ct.lo, w.ct.ld, nullptr, nullptr, st));
   }
   L += 3;
-  GemmDesc g1;  // tmp = alpha * A * B  (epilogue emits tmp's split = GEMM 2's A operand)
-  g1.M = ni; g1.N = nj; g1.K = nk;
-  g1.a[0] = w.a.op(); g1.b[0] = w.bt.op();
-  g1.flags = EPI_SPLIT | (tmp ? EPI_OUT : 0u);
-  g1.alpha = alpha;
-  g1.out = tmp; g1.ldo = nj;
-  g1.split_hi = w.tmp.hi; g1.split_lo = w.tmp.lo; g1.ld_split = w.tmp.ld;
-  w.sk.attach(g1);
   PB_CUDA(launch_umma_gemm(g1, st, &L));
   if (sd) PB_CUDA(cudaStreamWaitEvent(st, sd->join, 0));
-  GemmDesc g2;  // D = tmp * C + beta * D
-  g2.M = ni; g2.N = nl; g2.K = nj;
-  g2.a[0] = w.tmp.op(); g2.b[0] = w.ct.op();
-  g2.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
-  g2.alpha = 1.f; g2.beta = beta;
-  g2.cin = D; g2.ldc = nl; g2.out = D; g2.ldo = nl;
-  w.sk.attach(g2);
   PB_CUDA(launch_umma_gemm(g2, st, &L));
   g_launches = L;
   return PB_OK;
@@ -382,6 +421,53 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   Ws3mm w = ws_3mm(c, ni, nj, nk, nl, nm);
   cudaStream_t st = S(s);
   int L = 0;
+  GemmDesc gf;  // F = C * D; epilogue also emits F^T split (G's K-major B operand)
+  gf.M = nj; gf.N = nl; gf.K = nm;
+  gf.a[0] = w.c.op(); gf.b[0] = w.dt.op();
+  gf.flags = EPI_OUT | EPI_SPLIT_T;
+  gf.out = F; gf.ldo = nl;
+  gf.split_hi = w.ft.hi; gf.split_lo = w.ft.lo; gf.ld_split = w.ft.ld;
+  w.sk.attach(gf);
+  GemmDesc ge;  // E = A * B; epilogue also emits E split (G's A operand)
+  ge.M = ni; ge.N = nj; ge.K = nk;
+  ge.a[0] = w.a.op(); ge.b[0] = w.bt.op();
+  ge.flags = EPI_OUT | EPI_SPLIT;
+  ge.out = E; ge.ldo = nj;
+  ge.split_hi = w.e.hi; ge.split_lo = w.e.lo; ge.ld_split = w.e.ld;
+  w.sk.attach(ge);
+  GemmDesc gg;  // G = E * F
+  gg.M = ni; gg.N = nl; gg.K = nj;
+  gg.a[0] = w.e.op(); gg.b[0] = w.ft.op();
+  gg.flags = EPI_OUT;
+  gg.out = G; gg.ldo = nl;
+  w.sk.attach(gg);
+  {
+    // NEXT-4 chain fusion: F, E and G in one persistent launch. E's operand
+    // splits (A, B^T) are done inside the launch by the epilogue warps while F's first tiles
+    // run; G's tile (i, j) starts once E's row panel i and F's column panel j (F^T's rows)
+    // are published.
+    GemmDesc gs[3] = {gf, ge, gg};
+    w.sk2.attach(gs[1]);
+    w.sk3.attach(gs[2]);
+    if (umma_chain_ok(gs, 3)) {
+      ChainLink lk[3];
+      lk[2].waitA = 1;
+      lk[2].waitB = 0;
+      lk[1].npre = 2;
+      ChainLink::Pre& pa = lk[1].pre[0];
+      pa.X = A; pa.rows = ni; pa.cols = nk; pa.ldx = nk;
+      pa.hi = const_cast<float*>(w.a.hi); pa.lo = const_cast<float*>(w.a.lo); pa.ldo = w.a.ld; pa.transpose = false;
+      ChainLink::Pre& pbt = lk[1].pre[1];
+      pbt.X = B; pbt.rows = nk; pbt.cols = nj; pbt.ldx = nj;
+      pbt.hi = const_cast<float*>(w.bt.hi); pbt.lo = const_cast<float*>(w.bt.lo); pbt.ldo = w.bt.ld; pbt.transpose = true;
+      PB_CUDA(launch_split(C, nj, nm, nm, w.c.hi, w.c.lo, w.c.ld, st));
+      PB_CUDA(launch_split_T(D, nm, nl, nl, w.dt.hi, w.dt.lo, w.dt.ld, nullptr, nullptr, st));
+      L += 2;
+      PB_CUDA(launch_umma_chain(gs, lk, 3, w.chain.cnt, w.chain.cnt_bytes, st, &L));
+      g_launches = L;
+      return PB_OK;
+    }
+  }
   Side* sd = side_stream();
   cudaStream_t sab = st;
   PB_CUDA(launch_split(C, nj, nm, nm, w.c.hi, w.c.lo, w.c.ld, st));
@@ -395,29 +481,9 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, sab));
   if (sd) PB_CUDA(cudaEventRecord(sd->join, sd->s));
   L += 4;
-  GemmDesc gf;  // F = C * D; epilogue also emits F^T split (G's K-major B operand)
-  gf.M = nj; gf.N = nl; gf.K = nm;
-  gf.a[0] = w.c.op(); gf.b[0] = w.dt.op();
-  gf.flags = EPI_OUT | EPI_SPLIT_T;
-  gf.out = F; gf.ldo = nl;
-  gf.split_hi = w.ft.hi; gf.split_lo = w.ft.lo; gf.ld_split = w.ft.ld;
-  w.sk.attach(gf);
   PB_CUDA(launch_umma_gemm(gf, st, &L));
   if (sd) PB_CUDA(cudaStreamWaitEvent(st, sd->join, 0));
-  GemmDesc ge;  // E = A * B; epilogue also emits E split (G's A operand)
-  ge.M = ni; ge.N = nj; ge.K = nk;
-  ge.a[0] = w.a.op(); ge.b[0] = w.bt.op();
-  ge.flags = EPI_OUT | EPI_SPLIT;
-  ge.out = E; ge.ldo = nj;
-  ge.split_hi = w.e.hi; ge.split_lo = w.e.lo; ge.ld_split = w.e.ld;
-  w.sk.attach(ge);
   PB_CUDA(launch_umma_gemm(ge, st, &L));
-  GemmDesc gg;  // G = E * F
-  gg.M = ni; gg.N = nl; gg.K = nj;
-  gg.a[0] = w.e.op(); gg.b[0] = w.ft.op();
-  gg.flags = EPI_OUT;
-  gg.out = G; gg.ldo = nl;
-  w.sk.attach(gg);
   PB_CUDA(launch_umma_gemm(gg, st, &L));
   g_launches = L;
   return PB_OK;

@@ -59,6 +59,31 @@ struct UmmaPlan {
   size_t part_bytes = 0, counter_bytes = 0;
 };
 UmmaPlan umma_plan(const GemmDesc& d);
+// NEXT-4 chain fusion: phases 0..nphase-1 in ONE persistent launch (2-CTA 256x256 tiles).
+// Phase q waits for the row panels of phase links[q].waitA (its A operand = that phase's
+// split output, EPI_SPLIT) and/or the column panels of phase links[q].waitB (its B operand
+// = that phase's transposed split output, EPI_SPLIT_T). Every phase needs its own split-K
+// area (part / counters). cnt: readiness counters, umma_chain_cnt_bytes. Returns
+// cudaErrorNotSupported when the shapes do not fit one launch (callers launch separately).
+struct ChainLink {
+  int waitA = -1;
+  int waitB = -1;
+  // operand splits of this phase done inside the launch (by all CTAs' epilogue warps before
+  // their first epilogue): X (rows x cols, pitch ldx) -> hi/lo (transpose: of X^T), pitch ldo
+  struct Pre {
+    const float* X = nullptr;
+    int rows = 0, cols = 0, ldx = 0;
+    float* hi = nullptr;
+    float* lo = nullptr;
+    int ldo = 0;
+    bool transpose = false;
+  } pre[2];
+  int npre = 0;
+};
+bool umma_chain_ok(const GemmDesc* d, int nphase);
+size_t umma_chain_cnt_bytes(const GemmDesc* d, int nphase);
+cudaError_t launch_umma_chain(const GemmDesc* d, const ChainLink* links, int nphase, unsigned* cnt, size_t cnt_cap,
+                              cudaStream_t s, int* launches);
 // host helpers of k_umma.cu (tensor maps, SM count)
 bool make_map2d(CUtensorMap* m, const float* base, int inner, int rows, long long ld, int box_inner, int box_rows,
                 bool swizzle128,
@@ -92,13 +117,16 @@ cudaError_t launch_gram_fused(bool corr, int m, int n, double float_n, double ep
 
 // ---- split / prep (k_split.cu) ----------------------------------------------
 // hi/lo split of a rows x cols matrix; same layout (ldo = ld of output).
+// done != nullptr: each CTA adds 1 to *done when its part is stored (release); *ctas += grid size.
 cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi, float* lo, int ldo,
-                         cudaStream_t s);
+                         cudaStream_t s, unsigned* done = nullptr, unsigned* ctas = nullptr);
 // hi/lo split of the transpose: out (cols x rows), out pitch ldo (>= rows).
 // If mean != nullptr: value = (x - mean[col]) * inv[col] computed in double first
 // (inv == nullptr means 1).
 cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* hiT, float* loT, int ldo,
-                           const double* mean, const double* inv, cudaStream_t s);
+                           const double* mean, const double* inv, cudaStream_t s, unsigned* done = nullptr,
+                           unsigned* ctas = nullptr);
+
 
 // ---- column statistics (k_stats.cu) -----------------------------------------
 // Fused covariance/correlation prep: column mean (+ stddev, eps rule) and the

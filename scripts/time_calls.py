@@ -48,6 +48,12 @@ def main():
         ws = pb.workspace("2mm", (r, n, n, n), dev)
         f = lambda: pb.pb_2mm(r, n, n, n, 1.5, 1.2, tmp, A, B, C, Dm, ws=ws)  # noqa: E731
         flops = 4 * r * n * n
+    elif k == "3mm":
+        A, B, C, Dm = g(n, n, 1), g(n, n, 2), g(n, n, 3), g(n, n, 4)
+        E, F, Gm = (torch.empty(n, n, device=dev) for _ in range(3))
+        ws = pb.workspace("3mm", (n, n, n, n, n), dev)
+        f = lambda: pb.pb_3mm(n, n, n, n, n, E, A, B, F, C, Dm, Gm, ws=ws)  # noqa: E731
+        flops = 6 * n * n * n
     elif k == "syrk":
         A, C = g(n, n, 1), g(n, n, 3)
         ws = pb.workspace("syrk", (n, n), dev)
