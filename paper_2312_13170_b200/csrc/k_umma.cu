@@ -168,6 +168,10 @@ struct Params {
   long long split_tiles;         // tiles [0, split_tiles) are split; units of split tiles come first
   float* part;                   // split-K partial tiles [unit][CG][128][BN]
   unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
+  int streamk;                   // 1: stream-K schedule (pair p takes iterations [p I / P, (p+1) I / P))
+  long long sk_iters;            // I = num_tiles * k-blocks per tile
+  int sk_pairs;                  // P = CTA groups of the grid
+  int sk_maxseg;                 // partial slots per tile (max pairs sharing one tile)
   int dbg;                       // PB_UMMA_DEBUG (tuning only): 1 = skip partial exchange
   unsigned long long* tstamp;    // PB_UMMA_TIMING (tuning only): [cta][unit<16][8] globaltimer stamps
 };
@@ -282,6 +286,8 @@ struct Unit {
   long long t;
   int ks, kbA, kbB;
   bool split;
+  int nseg;        // units (K segments) that share tile t
+  long long slot;  // this unit's partial slot
 };
 __device__ __forceinline__ Unit unit_of(const Params& p, long long u, int nkb_total) {
   Unit r;
@@ -298,7 +304,62 @@ __device__ __forceinline__ Unit unit_of(const Params& p, long long u, int nkb_to
   const int S = r.split ? p.ksplit : 1;
   r.kbA = (int)((long long)nkb_total * r.ks / S);
   r.kbB = (int)((long long)nkb_total * (r.ks + 1) / S);
+  r.nseg = S;
+  r.slot = u;
   return r;
+}
+// partial slot of segment k2 of (split) tile t
+__device__ __forceinline__ long long slot_of(const Params& p, long long t, int k2) {
+  return p.streamk ? t * p.sk_maxseg + k2 : k2 * p.split_tiles + t;
+}
+
+// The units one CTA group works through, in order: round robin over [0, units) (every
+// launch; the phases of a chain one after the other), or, in stream-K mode (one GEMM),
+// the K segments covering this group's share of the flattened (tile, k-block) space:
+// group g takes iterations [g I / P, (g+1) I / P); tile t is shared by the groups
+// pair_of(t nkb) .. pair_of((t+1) nkb - 1), pair_of(i) = ((i + 1) P - 1) / I.
+struct UnitIter {
+  long long u, step, end;  // round robin
+  long long it, itend;     // stream-K
+  long long g;
+  bool sk;
+};
+__device__ __forceinline__ UnitIter iter_init(const Chain& ch, long long g, long long step) {
+  UnitIter r;
+  const Params& p = ch.ph[0];
+  r.sk = ch.nphase == 1 && p.streamk;
+  r.g = g;
+  r.u = g; r.step = step; r.end = ch.ubase[ch.nphase];
+  r.it = g * p.sk_iters / p.sk_pairs;
+  r.itend = (g + 1) * p.sk_iters / p.sk_pairs;
+  return r;
+}
+__device__ __forceinline__ bool iter_next(const Chain& ch, UnitIter& r, int& ph, long long& ul, Unit& un) {
+  if (r.sk) {
+    if (r.it >= r.itend) return false;
+    const Params& p = ch.ph[0];
+    const long long nkb = (long long)p.nkb * p.npairs, I = p.sk_iters, P = p.sk_pairs;
+    const long long t = r.it / nkb;
+    const int kbA = (int)(r.it - t * nkb);
+    const int kbB = (int)min(nkb, (long long)kbA + (r.itend - r.it));
+    const long long lo = ((t * nkb + 1) * P - 1) / I, hi = (((t + 1) * nkb) * P - 1) / I;
+    un.t = t; un.kbA = kbA; un.kbB = kbB;
+    un.nseg = (int)(hi - lo + 1);
+    un.ks = (int)(r.g - lo);
+    un.split = un.nseg > 1;
+    un.slot = t * p.sk_maxseg + un.ks;
+    ph = 0;
+    ul = un.slot;
+    r.it += kbB - kbA;
+    return true;
+  }
+  if (r.u >= r.end) return false;
+  ph = phase_of(ch, r.u);
+  const Params& p = ch.ph[ph];
+  ul = r.u - ch.ubase[ph];
+  un = unit_of(p, ul, p.nkb * p.npairs);
+  r.u += r.step;
+  return true;
 }
 
 // CHAIN = false: one GEMM (the chain machinery compiles away, keeping the epilogue's
@@ -368,10 +429,12 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (long long u = tile0; u < num_units; u += tile_step) {
-        const int ph = CHAIN ? phase_of(ch, u) : 0;
+      UnitIter ui = iter_init(ch, tile0, tile_step);
+      int ph;
+      long long uph;
+      Unit un;
+      while (iter_next(ch, ui, ph, uph, un)) {
         const Params& p = ch.ph[ph];
-        const Unit un = unit_of(p, u - ch.ubase[ph], p.nkb * p.npairs);
         int tm, tn;
         tile_coords(p, un.t, tm, tn);
         const int arow = tm * C::PAIR_M + (int)rank * BM;
@@ -410,10 +473,12 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       uint32_t phase = 0;
       int chunk_it = 0;
       int ul = 0;
-      for (long long u = tile0; u < num_units; u += tile_step, ++ul) {
-        const int ph = CHAIN ? phase_of(ch, u) : 0;
+      UnitIter ui = iter_init(ch, tile0, tile_step);
+      int ph;
+      long long uph;
+      Unit un;
+      for (; iter_next(ch, ui, ph, uph, un); ++ul) {
         const Params& p = ch.ph[ph];
-        const Unit un = unit_of(p, u - ch.ubase[ph], p.nkb * p.npairs);
         const int kbA = un.kbA, kbB = un.kbB;
         TSTAMP(ul, 0);
         for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
@@ -523,11 +588,12 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         }
       }
     };
-    for (long long u0 = tile0; u0 < num_units; u0 += tile_step, ++ul) {
-      const int ph = CHAIN ? phase_of(ch, u0) : 0;
+    UnitIter ui = iter_init(ch, tile0, tile_step);
+    int ph;
+    long long u;  // unit index within the phase
+    Unit un;
+    for (; iter_next(ch, ui, ph, u, un); ++ul) {
       const Params& p = ch.ph[ph];
-      const long long u = u0 - ch.ubase[ph];  // unit index within the phase
-      const Unit un = unit_of(p, u, p.nkb * p.npairs);
       const long long t = un.t;
       const uint32_t flags = p.flags;
       const int kbA = un.kbA, kbB = un.kbB;
@@ -576,19 +642,19 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       if (warp == 2 && lane == 0) TSTAMP(ul, 3);
       if (un.split && (flags & EPI_PARTIAL)) {  // partials only; launch_gram_combine finishes
         const int rl = q * 32 + lane;
-        float4* mine = reinterpret_cast<float4*>(p.part) + ((u * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
+        float4* mine = reinterpret_cast<float4*>(p.part) + ((un.slot * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
 #pragma unroll
         for (int c = 0; c < EPI_COLS; c += 4) mine[(c / 4) * BM] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
         continue;
       }
-      if (un.split && p.ksplit > 1 && p.dbg != 1) {
+      if (un.split && un.nseg > 1 && p.dbg != 1) {
         // Split-K: post this unit's partial tile, count arrivals; the LAST unit of
         // the tile to arrive sums all partials in split order (deterministic,
         // no waiting) and runs the epilogue; the others are done with the tile.
         // partial layout [unit][rank][col half][c/4][row 0..127][4]: lanes (rows) write
         // consecutive 16-byte pieces, every access is a coalesced 512-byte line set
         const int rl = q * 32 + lane;
-        float4* mine = reinterpret_cast<float4*>(p.part) + ((u * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
+        float4* mine = reinterpret_cast<float4*>(p.part) + ((un.slot * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
 #pragma unroll
         for (int c = 0; c < EPI_COLS; c += 4) mine[(c / 4) * BM] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
         __threadfence();
@@ -596,7 +662,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         if (warp == 2 && lane == 0) {
           unsigned* cnt = p.counters + t * CG + rank;
           const unsigned prev = atomicAdd(cnt, 1u);
-          const uint32_t last = prev == (unsigned)(p.ksplit - 1);
+          const uint32_t last = prev == (unsigned)(un.nseg - 1);
           if (last) atomicExch(cnt, 0u);
           ctl->last_flag = last;
         }
@@ -605,9 +671,9 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         __threadfence();
         // sum partials 0..ksplit-1 in order (own partial re-read from L2: same order
         // whichever unit arrives last)
-        for (int k2 = 0; k2 < p.ksplit; ++k2) {
+        for (int k2 = 0; k2 < un.nseg; ++k2) {
           const float4* o = reinterpret_cast<const float4*>(p.part) +
-                            (((k2 * p.split_tiles + t) * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
+                            ((slot_of(p, t, k2) * CG + rank) * (long long)BN + cbase) * (BM / 4) + rl;
 #pragma unroll
           for (int c = 0; c < EPI_COLS; c += 4) {
             const float4 v = __ldcg(o + (c / 4) * BM);
@@ -724,7 +790,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
 
 // Tile/split fields of one GEMM (phase) for the tile config <CG, BN>; false if it has no tiles.
 template <int CG, int BN>
-bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles) {
+bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles, const UmmaPlan* skp = nullptr) {
   using C = Cfg<CG, BN>;
   const int tiles_m = (d.M + C::PAIR_M - 1) / C::PAIR_M;
   p.tiles_n = (d.N + BN - 1) / BN;
@@ -747,9 +813,20 @@ bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles)
   p.tstamp = timing ? tbuf : nullptr;
   p.part = d.part;
   p.counters = d.counters;
+  p.streamk = 0;
+  p.sk_iters = 0; p.sk_pairs = 1; p.sk_maxseg = 1;
+  if (skp && skp->streamk) {
+    p.streamk = 1;
+    p.sk_pairs = num_sms() / CG;
+    p.sk_iters = nt * (long long)(p.nkb * p.npairs);
+    p.sk_maxseg = skp->maxseg;
+    p.split_tiles = nt;  // every tile may be split (its segment count decides)
+  }
   return true;
 }
-inline long long phase_units(const Params& p) { return p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles); }
+inline long long phase_units(const Params& p) {
+  return p.streamk ? p.sk_pairs : p.split_tiles * p.ksplit + (p.num_tiles - p.split_tiles);
+}
 
 template <int CG, int BN>
 bool phase_maps(const GemmDesc& d, CUtensorMap* maps /* 4 per operand pair */) {
@@ -770,10 +847,14 @@ template <int CG, int BN, bool CHAIN>
 cudaError_t launch_chain_kernel(const Chain& ch, const CUtensorMap* maps, cudaStream_t s, int* launches);
 
 template <int CG, int BN>
-cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_tiles, cudaStream_t s, int* launches) {
-  if (!prep_phase<CG, BN>(d, p, ksplit, split_tiles)) return cudaSuccess;
+cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_tiles, cudaStream_t s, int* launches,
+                      const UmmaPlan* skp = nullptr) {
+  if (!prep_phase<CG, BN>(d, p, ksplit, split_tiles, skp)) return cudaSuccess;
   if (p.tstamp) cudaMemsetAsync(p.tstamp, 0, 148 * 16 * 8 * sizeof(unsigned long long), s);
-  if (ksplit > 1 && !(d.flags & EPI_PARTIAL)) {
+  if (p.streamk) {
+    cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)p.num_tiles * CG * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+  } else if (ksplit > 1 && !(d.flags & EPI_PARTIAL)) {
     cudaError_t e = cudaMemsetAsync(d.counters, 0, (size_t)p.split_tiles * CG * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
   }
@@ -1099,7 +1180,7 @@ bool umma_chain_ok(const GemmDesc* d, int nphase) {
   if (nphase < 1 || nphase > 3) return false;
   for (int q = 0; q < nphase; ++q) {
     const UmmaPlan pl = umma_plan(d[q]);
-    if (pl.cfg != 3 || d[q].npairs != 1 || (d[q].flags & (EPI_TRI | EPI_PARTIAL | EPI_MIRROR)) || d[q].tm0 != 0 ||
+    if (pl.cfg != 3 || pl.streamk || d[q].npairs != 1 || (d[q].flags & (EPI_TRI | EPI_PARTIAL | EPI_MIRROR)) || d[q].tm0 != 0 ||
         d[q].tm1 >= 0)
       return false;
   }
@@ -1205,10 +1286,17 @@ cudaError_t launch_umma_gemm(const GemmDesc& d, cudaStream_t s, int* launches) {
   const UmmaPlan pl = umma_plan(d);
   int ks = pl.ksplit;
   if (ks > 1 && (d.part == nullptr || d.counters == nullptr)) ks = 1;
+  if (pl.streamk && ks == 1) return launch_cg<2, 256>(d, p, 1, 0, s, launches);  // no partials workspace
   if ((d.flags & EPI_PARTIAL) && d.part == nullptr) return cudaErrorInvalidValue;
   // the workspace reserved for partials / counters must hold what this plan writes
   if ((ks > 1 || (d.flags & EPI_PARTIAL)) && (pl.part_bytes > d.part_cap || pl.counter_bytes > d.counter_cap))
     return cudaErrorInvalidValue;
+  if (pl.streamk) {
+    if (!d.part || !d.counters) return cudaErrorInvalidValue;
+    if (pl.cfg == 3) return launch_cg<2, 256>(d, p, ks, pl.split_tiles, s, launches, &pl);
+    if (pl.cfg == 2) return launch_cg<2, 128>(d, p, ks, pl.split_tiles, s, launches, &pl);
+    return launch_cg<1, 128>(d, p, ks, pl.split_tiles, s, launches, &pl);
+  }
   if (pl.cfg == 3) return launch_cg<2, 256>(d, p, ks, pl.split_tiles, s, launches);
   if (pl.cfg == 2) return launch_cg<2, 128>(d, p, ks, pl.split_tiles, s, launches);
   return launch_cg<1, 128>(d, p, ks, pl.split_tiles, s, launches);
@@ -1248,6 +1336,29 @@ UmmaPlan plan_cfg(const GemmDesc& d, int cfg, int force_ks) {
   pl.split_tiles = R;
   pl.part_bytes = R > 0 ? (size_t)R * S * cg * 128 * bn * sizeof(float) : 0;
   pl.counter_bytes = (S > 1 && !(d.flags & EPI_PARTIAL)) ? (size_t)R * cg * sizeof(unsigned) : 0;
+  // Stream-K for shapes of at most two partial waves (e.g. a rank's 512 x 4096 x 4096 block
+  // of 2mm at 8 GPUs: 32 tiles for 74 SM pairs): every pair gets I / P of the I = tiles x
+  // k-blocks iterations, tiles shared by consecutive pairs are summed by the last arriver.
+  // Opt-in (PB_STREAMK=1): measured on B200 for 512 x 4096 x 4096 the pairs' MMA time drops
+  // from 74.7 to 47.5 us, but the shared tiles' partial exchange (~20 us, latency bound) and
+  // the exposed single-wave epilogue make the call slower (153.6 vs 143.6 us).
+  static const char* sk_env = getenv("PB_STREAMK");
+  const bool sk_on = sk_env && atoi(sk_env) != 0;
+  if (sk_on && cfg == 3 && !(d.flags & EPI_PARTIAL) && !force_ks && nt < 2 * units && nt % units != 0 &&
+      (long long)nt * nkb_total >= 8 * units) {
+    const long long I = nt * (long long)nkb_total, P = units;
+    int maxseg = 1;
+    for (long long t = 0; t < nt; ++t) {
+      const long long lo = ((t * nkb_total + 1) * P - 1) / I, hi = (((t + 1) * nkb_total) * P - 1) / I;
+      maxseg = std::max(maxseg, (int)(hi - lo + 1));
+    }
+    pl.streamk = 1;
+    pl.maxseg = maxseg;
+    pl.ksplit = maxseg;
+    pl.split_tiles = nt;
+    pl.part_bytes = (size_t)nt * maxseg * cg * 128 * bn * sizeof(float);
+    pl.counter_bytes = (size_t)nt * cg * sizeof(unsigned);
+  }
   return pl;
 }
 }  // namespace
@@ -1267,7 +1378,7 @@ UmmaPlan umma_plan(const GemmDesc& d) {
   // M = 512: 140 vs 147 us; gemm 1024^3: 46 vs 64 us; syrk 1024: 41 vs 67 us,
   // 2048: 68 vs 91 us; syr2k 1024: 50 vs 77 us, 2048: 119 vs 132 us. The Gram
   // (partials + combine) keeps 256x256 tiles (its 256x128 form measured slower).
-  if (cfg == 3 && !force_ks && pl.ksplit > 1 && pl.tiles < 74 && !(d.flags & EPI_PARTIAL)) {
+  if (cfg == 3 && !force_ks && !pl.streamk && pl.ksplit > 1 && pl.tiles < 74 && !(d.flags & EPI_PARTIAL)) {
     const UmmaPlan p2 = plan_cfg(d, 2, 0);
     if (p2.tiles <= 74) pl = p2;
   }

@@ -57,6 +57,8 @@ struct UmmaPlan {
   long long tiles = 0;
   long long split_tiles = 0;  // tiles [0, split_tiles) are split ksplit ways
   size_t part_bytes = 0, counter_bytes = 0;
+  int streamk = 0;  // 1: stream-K (every CTA group an equal share of all (tile, k-block) iterations)
+  int maxseg = 1;   // stream-K: most groups sharing one tile (partial slots per tile)
 };
 UmmaPlan umma_plan(const GemmDesc& d);
 // NEXT-4 chain fusion: phases 0..nphase-1 in ONE persistent launch (2-CTA 256x256 tiles).
