@@ -4,6 +4,8 @@ inputs. conv: componentwise 1e-4 (R8) and border entries untouched bitwise;
 fdtd: bitwise equal to the fp32 evaluation of the PolyBench statements and within
 1e-4 of max|state| of the fp64 oracle. Sizes span several tiles with ragged tails,
 the minimal interiors, and the paper's / bench sizes (sampled rows or planes)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -306,3 +308,21 @@ def test_new_entry_points_reject_bad_arguments():
     with pytest.raises(pb.PBError) as e:
         pb.pb_gramschmidt_variant(5, 256, 256, A, R, torch.zeros(256, 256, device="cuda"))
     assert e.value.status == 1
+
+
+def test_conv3d_large_grid_tile_paths_ragged():
+    """The 16-row conv3d tiles (16 x 256 when rows have >= 256 columns, else 16 x 128) are
+    taken for grids of >= 2^28 points; PB_C3_RPW=2 forces them on small ragged grids (rows
+    and columns not multiples of the tile, both weight masks) in a subprocess, since the
+    library reads the variable once per process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); from tests import parity as P; import pbgen;"
+            "rw = [((k * 7) %% 11 - 5) / 8.0 for k in range(27)];"
+            "res = [P.check_conv3d(20, 37, 260), P.check_conv3d(18, 35, 132), P.check_conv3d(19, 33, 300, rw),"
+            "       P.check_conv3d(17, 40, 140, rw)];"
+            "bad = [r for r in res if not r['ok']]; print('bad', bad); sys.exit(1 if bad else 0)" % root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, PB_C3_RPW="2"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
