@@ -372,6 +372,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
   cluster_sync_all();  // no CTA leaves while its peer may still touch its smem
 }
 
+// a*b + c on two lanes at once (fma.rn.f32x2: one packed FFMA2 issue for two RN FMAs)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
 // ------------------------------------------------------------------ atax, single pass, register rows
 // Variant of the kernel above: each thread copies ITS float4s of row b from the
 // smem stage into registers and the stage is handed back to the TMA engine at
@@ -446,15 +456,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
     }
     __syncthreads();  // every thread holds its part of row b: the stage can be refilled
     if (tid == 0 && b + AR_STAGES < nb) issue(b + AR_STAGES);
-    float p = 0.f;
+    // packed FMAs (two lanes per issue): the kernel's per-row instruction path is what the
+    // power-capped SM clock slows down in the suite (DESIGN.md §8 atax)
+    float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
 #pragma unroll
     for (int v = 0; v < AX_V; ++v) {
       const int idx = tid + v * AX_THREADS;
       if (idx < w4) {
         const float4 xv = xs4[idx];
-        p += cur[v].x * xv.x + cur[v].y * xv.y + cur[v].z * xv.z + cur[v].w * xv.w;
+        pa = ffma2(make_float2(cur[v].x, cur[v].y), make_float2(xv.x, xv.y), pa);
+        pb = ffma2(make_float2(cur[v].z, cur[v].w), make_float2(xv.z, xv.w), pb);
       }
     }
+    float p = (pa.x + pa.y) + (pb.x + pb.y);
     p = warp_sum(p);
     if (lane == 0) {
       volatile float* wr = ctl->wred[slot];
@@ -478,9 +492,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
       mbar_wait_cluster(&ctl->red[ps], (uint32_t)((b - 1) / AX_RED) & 1u);
       const float t = ctl->part[ps][0] + ctl->part[ps][1];
       if (tmp && rank == 0 && tid == 0) tmp[r0 + b - 1] = t;
+      const float2 t2 = make_float2(t, t);
 #pragma unroll
       for (int v = 0; v < AX_V; ++v) {
-        yacc[v].x += t * prev[v].x; yacc[v].y += t * prev[v].y; yacc[v].z += t * prev[v].z; yacc[v].w += t * prev[v].w;
+        const float2 lo = ffma2(t2, make_float2(prev[v].x, prev[v].y), make_float2(yacc[v].x, yacc[v].y));
+        const float2 hi = ffma2(t2, make_float2(prev[v].z, prev[v].w), make_float2(yacc[v].z, yacc[v].w));
+        yacc[v] = make_float4(lo.x, lo.y, hi.x, hi.y);
       }
     }
   };
@@ -497,9 +514,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
     mbar_wait_cluster(&ctl->red[ps], (uint32_t)(last / AX_RED) & 1u);
     const float t = ctl->part[ps][0] + ctl->part[ps][1];
     if (tmp && rank == 0 && tid == 0) tmp[r0 + last] = t;
+    const float2 t2 = make_float2(t, t);
 #pragma unroll
     for (int v = 0; v < AX_V; ++v) {
-      yacc[v].x += t * lr[v].x; yacc[v].y += t * lr[v].y; yacc[v].z += t * lr[v].z; yacc[v].w += t * lr[v].w;
+      const float2 lo = ffma2(t2, make_float2(lr[v].x, lr[v].y), make_float2(yacc[v].x, yacc[v].y));
+      const float2 hi = ffma2(t2, make_float2(lr[v].z, lr[v].w), make_float2(yacc[v].z, yacc[v].w));
+      yacc[v] = make_float4(lo.x, lo.y, hi.x, hi.y);
     }
   }
   float4* yp = reinterpret_cast<float4*>(ypart + (long long)cl * n + c0);
