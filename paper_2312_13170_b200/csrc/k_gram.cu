@@ -173,15 +173,6 @@ __device__ __forceinline__ float rna_tf32_int(float x) {
 __device__ __forceinline__ float4 f4sub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 
-// UMMA shared-memory descriptor of an MN-major tf32 operand. The only smem layout the
-// tensor core takes for MN-major 32-bit operands is the 128-B swizzle with 32-B atoms
-// (layout type 1, "128B_BASE32B"): 32-element (128-B) rows along M/N, the 32-B granules
-// of row r XOR-permuted by r mod 4; runs of 32 M/N elements `lbo` bytes apart, 4-row K
-// groups `sbo` bytes apart. TMA writes the same layout (CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
-__device__ __forceinline__ uint64_t umma_desc_mn_sw128b32(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
-}
 // byte offset of 16-B chunk c (0..7) of row r in that layout
 __device__ __forceinline__ uint32_t sw32_off(int r, int c) {
   return (uint32_t)(r * 128 + (((((c >> 1) ^ (r & 3)) << 1) | (c & 1)) << 4));

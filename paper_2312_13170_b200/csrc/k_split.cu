@@ -57,6 +57,28 @@ __global__ void __launch_bounds__(256, 6) split_kernel(const float* __restrict__
   signal_done(done);
 }
 
+// lo only (raw-hi split): lo[r][c] = lo_of_raw(X[r][c]); the GEMM reads X itself as hi.
+__global__ void __launch_bounds__(256, 6) split_lo_kernel(const float* __restrict__ X, int rows, int cols4, int ldx,
+                                                          float* __restrict__ lo, int ldo) {
+  pdl_trigger();  // dependents may start their setup once every CTA here runs
+  pdl_wait();
+  const int c4 = blockIdx.x * 256 + threadIdx.x;
+  const int c = 4 * c4;
+  for (int r0 = blockIdx.y * SPLIT_U; c4 < cols4 && r0 < rows; r0 += gridDim.y * SPLIT_U) {
+    float4 v[SPLIT_U];
+#pragma unroll
+    for (int u = 0; u < SPLIT_U; ++u)
+      v[u] = r0 + u < rows ? *reinterpret_cast<const float4*>(X + (long long)(r0 + u) * ldx + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < SPLIT_U; ++u) {
+      if (r0 + u >= rows) break;
+      const float4 l = make_float4(lo_of_raw(v[u].x), lo_of_raw(v[u].y), lo_of_raw(v[u].z), lo_of_raw(v[u].w));
+      *reinterpret_cast<float4*>(lo + (long long)(r0 + u) * ldo + c) = l;
+    }
+  }
+}
+
 // out[c][r] = split(f(X[r][c])) with f(x) = ((double)x - mean[c]) * inv[c] when mean != null.
 // 64 x 64 tile per CTA: float4 loads of X rows, padded smem transpose, float4
 // stores of the hi / lo rows (output pitch ldo is a multiple of 4).
@@ -128,6 +150,17 @@ cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi,
   if (ctas) *ctas += (unsigned)(gx * gy);
   return launch_pdl(split_kernel, dim3((unsigned)gx, (unsigned)gy), dim3(256), 0, s, X, rows, cols4, ldx, hi, lo, ldo,
                     done);
+}
+
+cudaError_t launch_split_lo(const float* X, int rows, int cols, int ldx, float* lo, int ldo, cudaStream_t s) {
+  const int cols4 = cols / 4;
+  const int gx = (cols4 + 255) / 256;
+  const int row_steps = (rows + SPLIT_U - 1) / SPLIT_U;
+  int gy = (148 * 8 + gx - 1) / gx;
+  if (gy > row_steps) gy = row_steps;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  return launch_pdl(split_lo_kernel, dim3((unsigned)gx, (unsigned)gy), dim3(256), 0, s, X, rows, cols4, ldx, lo, ldo);
 }
 
 cudaError_t launch_split_T(const float* X, int rows, int cols, int ldx, float* hiT, float* loT, int ldo,

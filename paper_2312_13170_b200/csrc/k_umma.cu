@@ -168,6 +168,7 @@ struct Params {
   long long split_tiles;         // tiles [0, split_tiles) are split; units of split tiles come first
   float* part;                   // split-K partial tiles [unit][CG][128][BN]
   unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
+  int b_mn;                      // 1: the B operand is MN-major (B[k][n] as stored), 32-column TMA runs
   int streamk;                   // 1: stream-K schedule (pair p takes iterations [p I / P, (p+1) I / P))
   long long sk_iters;            // I = num_tiles * k-blocks per tile
   int sk_pairs;                  // P = CTA groups of the grid
@@ -202,7 +203,7 @@ struct Chain {
     float* hi;
     float* lo;
     int ldo;
-    int transpose;  // 0: hi/lo of X (same layout); 1: hi/lo of X^T (cols x rows)
+    int transpose;  // 0: hi/lo of X (same layout); 1: hi/lo of X^T (cols x rows); 2: lo only (raw-hi)
   } pre[2];
   int npre, pre_phase, pre_off;
 };
@@ -454,8 +455,16 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&ctl->full[stage], CG * STAGE_BYTES);
           tma_load_cg<CG>(map_of(mq, 0), &ctl->full[stage], st, k, arow);
           tma_load_cg<CG>(map_of(mq, 1), &ctl->full[stage], st + A_TILE, k, arow);
-          tma_load_cg<CG>(map_of(mq, 2), &ctl->full[stage], st + 2 * A_TILE, k, brow);
-          tma_load_cg<CG>(map_of(mq, 3), &ctl->full[stage], st + 2 * A_TILE + B_TILE, k, brow);
+          if (p.b_mn) {  // B[k][n]: [32-column run][32 k rows][32] boxes, 128B_BASE32B layout
+#pragma unroll
+            for (int q = 0; q < C::B_ROWS / 32; ++q) {
+              tma_load_cg<CG>(map_of(mq, 2), &ctl->full[stage], st + 2 * A_TILE + q * 4096, brow + 32 * q, k);
+              tma_load_cg<CG>(map_of(mq, 3), &ctl->full[stage], st + 2 * A_TILE + B_TILE + q * 4096, brow + 32 * q, k);
+            }
+          } else {
+            tma_load_cg<CG>(map_of(mq, 2), &ctl->full[stage], st + 2 * A_TILE, k, brow);
+            tma_load_cg<CG>(map_of(mq, 3), &ctl->full[stage], st + 2 * A_TILE + B_TILE, k, brow);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -468,7 +477,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     // chunk runs in the other slot. The tensor-core accumulate truncates, so
     // this bounds the truncation bias to one chunk.
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(BM * CG, BN);
+      constexpr uint32_t idesc_k = idesc_tf32(BM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int chunk_it = 0;
@@ -480,6 +489,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       for (; iter_next(ch, ui, ph, uph, un); ++ul) {
         const Params& p = ch.ph[ph];
         const int kbA = un.kbA, kbB = un.kbB;
+        const uint32_t idesc = idesc_k | (p.b_mn ? (1u << 16) : 0u);  // B MN-major (bit 16)
         TSTAMP(ul, 0);
         for (int kb0 = kbA; kb0 < kbB; kb0 += CHUNK_KB, ++chunk_it) {
           const int slot = chunk_it & 1;
@@ -502,8 +512,10 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t ah = umma_desc_k_sw128(st + kk * 32);
               const uint64_t al = umma_desc_k_sw128(st + A_TILE + kk * 32);
-              const uint64_t bh = umma_desc_k_sw128(st + 2 * A_TILE + kk * 32);
-              const uint64_t bl = umma_desc_k_sw128(st + 2 * A_TILE + B_TILE + kk * 32);
+              const uint64_t bh = p.b_mn ? umma_desc_mn_sw128b32(st + 2 * A_TILE + kk * 1024, 4096, 512)
+                                         : umma_desc_k_sw128(st + 2 * A_TILE + kk * 32);
+              const uint64_t bl = p.b_mn ? umma_desc_mn_sw128b32(st + 2 * A_TILE + B_TILE + kk * 1024, 4096, 512)
+                                         : umma_desc_k_sw128(st + 2 * A_TILE + B_TILE + kk * 32);
               const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
               mma_cg<CG>(d_small, al, bh, idesc, accum);
               mma_cg<CG>(d_small, ah, bl, idesc, 1);
@@ -546,7 +558,11 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           const bool in = r < t.rows && c < t.cols;
           const float4 v = in ? *reinterpret_cast<const float4*>(t.X + (long long)r * t.ldx + c)
                               : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (!t.transpose) {
+          if (t.transpose == 2) {
+            if (in)
+              *reinterpret_cast<float4*>(t.lo + (long long)r * t.ldo + c) =
+                  make_float4(lo_of_raw(v.x), lo_of_raw(v.y), lo_of_raw(v.z), lo_of_raw(v.w));
+          } else if (!t.transpose) {
             if (in) {
               float4 h, l;
               split3x(v.x, h.x, l.x); split3x(v.y, h.y, l.y); split3x(v.z, h.z, l.z); split3x(v.w, h.w, l.w);
@@ -557,7 +573,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
             *reinterpret_cast<float4*>(stg + rr * 32 + ((cq ^ (rr & 7)) << 2)) = v;  // 16-B XOR swizzle
           }
         }
-        if (t.transpose) {
+        if (t.transpose == 1) {
           __syncwarp();
           for (int cc = 0; cc < 32; ++cc) {  // output row c0 + cc (input column), element r0 + lane
             const int j = c0 + cc, i2 = r0 + lane;
@@ -720,6 +736,13 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
               for (int e = 0; e < 16; e += 4)
                 if (j0 + e < p.N) store4(op + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
             }
+            if (flags & EPI_SPLIT_LO) {  // raw-hi split of the output: the next GEMM reads (out, lo)
+              float* lp = p.split_lo + (long long)i * p.ld_split + j0;
+#pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                if (j0 + e < p.N)
+                  store4(lp + e, lo_of_raw(v[e]), lo_of_raw(v[e + 1]), lo_of_raw(v[e + 2]), lo_of_raw(v[e + 3]));
+            }
             if (flags & EPI_SPLIT) {
               float* hp = p.split_hi + (long long)i * p.ld_split + j0;
               float* lp = p.split_lo + (long long)i * p.ld_split + j0;
@@ -813,6 +836,7 @@ bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles,
   p.tstamp = timing ? tbuf : nullptr;
   p.part = d.part;
   p.counters = d.counters;
+  p.b_mn = d.b[0].mn ? 1 : 0;
   p.streamk = 0;
   p.sk_iters = 0; p.sk_pairs = 1; p.sk_maxseg = 1;
   if (skp && skp->streamk) {
@@ -835,10 +859,16 @@ bool phase_maps(const GemmDesc& d, CUtensorMap* maps /* 4 per operand pair */) {
     const SplitOperand& A = d.a[q];
     const SplitOperand& B = d.b[q];
     if (!make_map(&maps[4 * q + 0], A.hi, A.rows, A.K, A.ld, BM) ||
-        !make_map(&maps[4 * q + 1], A.lo, A.rows, A.K, A.ld, BM) ||
-        !make_map(&maps[4 * q + 2], B.hi, B.rows, B.K, B.ld, C::B_ROWS) ||
-        !make_map(&maps[4 * q + 3], B.lo, B.rows, B.K, B.ld, C::B_ROWS))
+        !make_map(&maps[4 * q + 1], A.lo, A.rows, A.K, A.ld, BM))
       return false;
+    if (B.mn) {  // B[k][n] (K rows x rows columns): 32-column x 32-row boxes, 128B_BASE32B swizzle
+      if (!make_map2d(&maps[4 * q + 2], B.hi, B.rows, B.K, B.ld, 32, BK, true, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+          !make_map2d(&maps[4 * q + 3], B.lo, B.rows, B.K, B.ld, 32, BK, true, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+        return false;
+    } else if (!make_map(&maps[4 * q + 2], B.hi, B.rows, B.K, B.ld, C::B_ROWS) ||
+               !make_map(&maps[4 * q + 3], B.lo, B.rows, B.K, B.ld, C::B_ROWS)) {
+      return false;
+    }
   }
   return true;
 }
@@ -1235,7 +1265,7 @@ cudaError_t launch_umma_chain(const GemmDesc* d, const ChainLink* links, int nph
     for (int k = 0; k < links[q].npre; ++k) {
       if (ch.npre == 2 || (ch.npre && ch.pre_phase != q) || q == 0) return cudaErrorInvalidValue;
       const ChainLink::Pre& a = links[q].pre[k];
-      ch.pre[ch.npre++] = Chain::Pre{a.X, a.rows, a.cols, a.ldx, a.hi, a.lo, a.ldo, a.transpose ? 1 : 0};
+      ch.pre[ch.npre++] = Chain::Pre{a.X, a.rows, a.cols, a.ldx, a.hi, a.lo, a.ldo, a.lo_only ? 2 : a.transpose ? 1 : 0};
       ch.pre_phase = q;
     }
   for (int q = 0; q < nphase; ++q) {
@@ -1247,7 +1277,8 @@ cudaError_t launch_umma_chain(const GemmDesc* d, const ChainLink* links, int nph
       ch.waitA_target[q] = (d[a].N + BN - 1) / BN;  // every tile of the row panel, per rank
     }
     if (b >= 0) {  // this phase's B rows = phase b's output columns (EPI_SPLIT_T), column panel by panel
-      if (b >= q || d[b].N != d[q].N || !(d[b].flags & EPI_SPLIT_T)) return cudaErrorInvalidValue;
+      if (b >= q || d[b].N != d[q].N || !((d[b].flags & EPI_SPLIT_T) || ((d[b].flags & EPI_SPLIT_LO) && d[q].b[0].mn)))
+        return cudaErrorInvalidValue;
       if (ch.sig_kind[b] == 1) return cudaErrorInvalidValue;
       ch.sig_kind[b] = 2; ch.sig_off[b] = col_off[b];
       ch.waitB_off[q] = col_off[b];

@@ -54,6 +54,41 @@ struct SplitBuf {
     return o;
   }
 };
+// raw-hi operand: only the lo array is carved; op_raw(X) pairs it with the caller's X
+struct LoBuf {
+  float* lo;
+  int rows, K, ld;
+  SplitOperand op_raw(const float* X) const {
+    SplitOperand o;
+    o.hi = X; o.lo = lo; o.rows = rows; o.K = K; o.ld = ld;
+    return o;
+  }
+};
+LoBuf take_lo(Carve& c, int rows, int K) {
+  LoBuf b;
+  b.rows = rows;
+  b.K = K;
+  b.ld = round_up(K, 4);
+  b.lo = c.take<float>(fsz(rows, b.ld));
+  return b;
+}
+// MN-major B operand (B[k][n] as the caller stores it, K x N): lo of the same layout
+struct LoBufMN {
+  float* lo;
+  int N, K;
+  SplitOperand op_raw(const float* B) const {
+    SplitOperand o;
+    o.hi = B; o.lo = lo; o.rows = N; o.K = K; o.ld = N; o.mn = true;
+    return o;
+  }
+};
+LoBufMN take_lo_mn(Carve& c, int K, int N) {
+  LoBufMN b;
+  b.N = N;
+  b.K = K;
+  b.lo = c.take<float>(fsz(K, N));
+  return b;
+}
 SplitBuf take_split(Carve& c, int rows, int K) {
   SplitBuf b;
   b.rows = rows;
@@ -95,10 +130,10 @@ SplitK take_splitk(Carve& c, std::initializer_list<GemmDesc> gemms) {
   return k;
 }
 
-struct WsGemm { SplitBuf a, bt; SplitK sk; };
+struct WsGemm { LoBuf a; LoBufMN b; SplitK sk; };
 WsGemm ws_gemm(Carve& c, int ni, int nj, int nk) {
   WsGemm w;
-  w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk);
+  w.a = take_lo(c, ni, nk); w.b = take_lo_mn(c, nk, nj);
   w.sk = take_splitk(c, {shape(ni, nj, nk)});
   return w;
 }
@@ -114,20 +149,24 @@ ChainWs take_chain(Carve& c, std::initializer_list<GemmDesc> gemms) {
   w.cnt = c.take<unsigned>(w.cnt_bytes / sizeof(unsigned));
   return w;
 }
-struct Ws2mm { SplitBuf a, bt, ct, tmp; SplitK sk, sk2; ChainWs chain; };
+// raw-hi operands: A, tmp K-major (lo of the same layout), B, C MN-major (lo of B[k][n], C[k][n]);
+// tmp_out holds tmp when the caller passes none (GEMM 2 reads it as its hi operand)
+struct Ws2mm { LoBuf a, tmp; LoBufMN b, c; float* tmp_out; SplitK sk, sk2; ChainWs chain; };
 Ws2mm ws_2mm(Carve& c, int ni, int nj, int nk, int nl) {
   Ws2mm w;
-  w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.ct = take_split(c, nl, nj); w.tmp = take_split(c, ni, nj);
+  w.a = take_lo(c, ni, nk); w.b = take_lo_mn(c, nk, nj); w.c = take_lo_mn(c, nj, nl); w.tmp = take_lo(c, ni, nj);
+  w.tmp_out = c.take<float>(fsz(ni, nj));
   w.sk = take_splitk(c, {shape(ni, nj, nk), shape(ni, nl, nj)});
   w.sk2 = take_splitk(c, {shape(ni, nl, nj)});
   w.chain = take_chain(c, {shape(ni, nj, nk), shape(ni, nl, nj)});
   return w;
 }
-struct Ws3mm { SplitBuf a, bt, c, dt, e, ft; SplitK sk, sk2, sk3; ChainWs chain; };
+// raw-hi operands: A, C, E K-major; B, D, F MN-major (F = G's B operand as stored, no transpose)
+struct Ws3mm { LoBuf a, c, e; LoBufMN b, d, f; SplitK sk, sk2, sk3; ChainWs chain; };
 Ws3mm ws_3mm(Carve& c, int ni, int nj, int nk, int nl, int nm) {
   Ws3mm w;
-  w.a = take_split(c, ni, nk); w.bt = take_split(c, nj, nk); w.c = take_split(c, nj, nm);
-  w.dt = take_split(c, nl, nm); w.e = take_split(c, ni, nj); w.ft = take_split(c, nl, nj);
+  w.a = take_lo(c, ni, nk); w.b = take_lo_mn(c, nk, nj); w.c = take_lo(c, nj, nm);
+  w.d = take_lo_mn(c, nm, nl); w.e = take_lo(c, ni, nj); w.f = take_lo_mn(c, nj, nl);
   w.sk = take_splitk(c, {shape(nj, nl, nm), shape(ni, nj, nk), shape(ni, nl, nj)});
   w.sk2 = take_splitk(c, {shape(ni, nj, nk)});
   w.sk3 = take_splitk(c, {shape(ni, nl, nj)});
@@ -170,11 +209,11 @@ WsStatRows ws_stat_rows(Carve& c, int m, int n, int r0, int r1) {
   w.sk = take_splitk(c, {shape(r1, m, n, 1, EPI_OUT, r0 / 128, (r1 + 127) / 128)});
   return w;
 }
-struct WsSyrk { SplitBuf a, b; SplitK sk; };
+struct WsSyrk { LoBuf a, b; SplitK sk; };
 WsSyrk ws_syrk(Carve& c, int n, int m, int r0, int r1, bool two, bool full = false) {
   WsSyrk w;
-  w.a = take_split(c, r1, m);
-  if (two) w.b = take_split(c, r1, m);
+  w.a = take_lo(c, r1, m);
+  if (two) w.b = take_lo(c, r1, m);
   w.sk = take_splitk(c, {shape(r1, r1, m, two ? 2 : 1, full ? 0u : (uint32_t)EPI_TRI, r0 / 128, (r1 + 127) / 128)});
   return w;
 }
@@ -235,12 +274,13 @@ constexpr long long SMALL_GEMM_MACS = 1ll << 21;
 // core sequences (validated arguments) ---------------------------------------
 pb_status run_gemm(int ni, int nj, int nk, float alpha, float beta, float* C, const float* A, const float* B,
                    const WsGemm& w, cudaStream_t s, int* L) {
-  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, s));
-  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, s));
+  // raw-hi split: A and B are the hi operands as stored (B MN-major, no transpose): lo only
+  PB_CUDA(launch_split_lo(A, ni, nk, nk, w.a.lo, w.a.ld, s));
+  PB_CUDA(launch_split_lo(B, nk, nj, nj, w.b.lo, nj, s));
   *L += 2;
   GemmDesc d;
   d.M = ni; d.N = nj; d.K = nk;
-  d.a[0] = w.a.op(); d.b[0] = w.bt.op();
+  d.a[0] = w.a.op_raw(A); d.b[0] = w.b.op_raw(B);
   d.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
   d.alpha = alpha; d.beta = beta;
   d.cin = C; d.ldc = nj; d.out = C; d.ldo = nj;
@@ -349,26 +389,26 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
   Ws2mm w = ws_2mm(c, ni, nj, nk, nl);
   cudaStream_t st = S(s);
   int L = 0;
-  GemmDesc g1;  // tmp = alpha * A * B  (epilogue emits tmp's split = GEMM 2's A operand)
+  float* tmp_eff = tmp ? tmp : w.tmp_out;  // GEMM 2's hi operand
+  GemmDesc g1;  // tmp = alpha * A * B  (epilogue also emits lo of tmp: GEMM 2's A operand is (tmp, lo))
   g1.M = ni; g1.N = nj; g1.K = nk;
-  g1.a[0] = w.a.op(); g1.b[0] = w.bt.op();
-  g1.flags = EPI_SPLIT | (tmp ? EPI_OUT : 0u);
+  g1.a[0] = w.a.op_raw(A); g1.b[0] = w.b.op_raw(B);
+  g1.flags = EPI_OUT | EPI_SPLIT_LO;
   g1.alpha = alpha;
-  g1.out = tmp; g1.ldo = nj;
-  g1.split_hi = w.tmp.hi; g1.split_lo = w.tmp.lo; g1.ld_split = w.tmp.ld;
+  g1.out = tmp_eff; g1.ldo = nj;
+  g1.split_lo = w.tmp.lo; g1.ld_split = w.tmp.ld;
   w.sk.attach(g1);
   GemmDesc g2;  // D = tmp * C + beta * D
   g2.M = ni; g2.N = nl; g2.K = nj;
-  g2.a[0] = w.tmp.op(); g2.b[0] = w.ct.op();
+  g2.a[0] = w.tmp.op_raw(tmp_eff); g2.b[0] = w.c.op_raw(C);
   g2.flags = EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
   g2.alpha = 1.f; g2.beta = beta;
   g2.cin = D; g2.ldc = nl; g2.out = D; g2.ldo = nl;
   w.sk.attach(g2);
   {
-    // NEXT-4 chain fusion: both GEMMs in one persistent launch; GEMM 2's
-    // tiles of row panel i start as soon as GEMM 1 has published tmp's row panel i. C^T's
-    // split (GEMM 2's B operand) is done inside the launch by the epilogue warps while
-    // GEMM 1's first tiles run.
+    // NEXT-4 chain fusion (opt-in PB_CHAIN=1): both GEMMs in one persistent
+    // launch; GEMM 2's tiles of row panel i start as soon as GEMM 1 has published tmp's row
+    // panel i; C's lo split (GEMM 2's B operand) is done inside the launch.
     GemmDesc gs[2] = {g1, g2};
     w.sk2.attach(gs[1]);
     if (umma_chain_ok(gs, 2)) {
@@ -377,9 +417,9 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
       lk[1].npre = 1;
       ChainLink::Pre& pc = lk[1].pre[0];
       pc.X = C; pc.rows = nj; pc.cols = nl; pc.ldx = nl;
-      pc.hi = const_cast<float*>(w.ct.hi); pc.lo = const_cast<float*>(w.ct.lo); pc.ldo = w.ct.ld; pc.transpose = true;
-      PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
-      PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
+      pc.lo = w.c.lo; pc.ldo = nl; pc.lo_only = true;
+      PB_CUDA(launch_split_lo(A, ni, nk, nk, w.a.lo, w.a.ld, st));
+      PB_CUDA(launch_split_lo(B, nk, nj, nj, w.b.lo, nj, st));
       L += 2;
       PB_CUDA(launch_umma_chain(gs, lk, 2, w.chain.cnt, w.chain.cnt_bytes, st, &L));
       g_launches = L;
@@ -387,15 +427,16 @@ pb_status pb_2mm(int ni, int nj, int nk, int nl, float alpha, float beta, float*
     }
   }
   Side* sd = side_stream();
-  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, st));
-  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, st));
-  if (sd) {  // C^T's split (GEMM 2's B operand) starts with GEMM 1 and runs beside it
+  // raw-hi splits (lo only; B and C MN-major as stored, no transposes)
+  PB_CUDA(launch_split_lo(A, ni, nk, nk, w.a.lo, w.a.ld, st));
+  PB_CUDA(launch_split_lo(B, nk, nj, nj, w.b.lo, nj, st));
+  if (sd) {  // C's lo (GEMM 2's B operand) starts with GEMM 1 and runs beside it
     PB_CUDA(cudaEventRecord(sd->fork, st));
     PB_CUDA(cudaStreamWaitEvent(sd->s, sd->fork, 0));
-    PB_CUDA(launch_split_T(C, nj, nl, nl, w.ct.hi, w.ct.lo, w.ct.ld, nullptr, nullptr, sd->s));
+    PB_CUDA(launch_split_lo(C, nj, nl, nl, w.c.lo, nl, sd->s));
     PB_CUDA(cudaEventRecord(sd->join, sd->s));
   } else {
-    PB_CUDA(launch_split_T(C, nj, nl, nl, w.ct.hi, w.ct.lo, w.ct.ld, nullptr, nullptr, st));
+    PB_CUDA(launch_split_lo(C, nj, nl, nl, w.c.lo, nl, st));
   }
   L += 3;
   PB_CUDA(launch_umma_gemm(g1, st, &L));
@@ -421,31 +462,30 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   Ws3mm w = ws_3mm(c, ni, nj, nk, nl, nm);
   cudaStream_t st = S(s);
   int L = 0;
-  GemmDesc gf;  // F = C * D; epilogue also emits F^T split (G's K-major B operand)
+  GemmDesc gf;  // F = C * D; epilogue also emits lo of F (G's B operand is (F, lo), MN-major)
   gf.M = nj; gf.N = nl; gf.K = nm;
-  gf.a[0] = w.c.op(); gf.b[0] = w.dt.op();
-  gf.flags = EPI_OUT | EPI_SPLIT_T;
+  gf.a[0] = w.c.op_raw(C); gf.b[0] = w.d.op_raw(D);
+  gf.flags = EPI_OUT | EPI_SPLIT_LO;
   gf.out = F; gf.ldo = nl;
-  gf.split_hi = w.ft.hi; gf.split_lo = w.ft.lo; gf.ld_split = w.ft.ld;
+  gf.split_lo = w.f.lo; gf.ld_split = nl;
   w.sk.attach(gf);
-  GemmDesc ge;  // E = A * B; epilogue also emits E split (G's A operand)
+  GemmDesc ge;  // E = A * B; epilogue also emits lo of E (G's A operand is (E, lo))
   ge.M = ni; ge.N = nj; ge.K = nk;
-  ge.a[0] = w.a.op(); ge.b[0] = w.bt.op();
-  ge.flags = EPI_OUT | EPI_SPLIT;
+  ge.a[0] = w.a.op_raw(A); ge.b[0] = w.b.op_raw(B);
+  ge.flags = EPI_OUT | EPI_SPLIT_LO;
   ge.out = E; ge.ldo = nj;
-  ge.split_hi = w.e.hi; ge.split_lo = w.e.lo; ge.ld_split = w.e.ld;
+  ge.split_lo = w.e.lo; ge.ld_split = w.e.ld;
   w.sk.attach(ge);
   GemmDesc gg;  // G = E * F
   gg.M = ni; gg.N = nl; gg.K = nj;
-  gg.a[0] = w.e.op(); gg.b[0] = w.ft.op();
+  gg.a[0] = w.e.op_raw(E); gg.b[0] = w.f.op_raw(F);
   gg.flags = EPI_OUT;
   gg.out = G; gg.ldo = nl;
   w.sk.attach(gg);
   {
-    // NEXT-4 chain fusion: F, E and G in one persistent launch. E's operand
-    // splits (A, B^T) are done inside the launch by the epilogue warps while F's first tiles
-    // run; G's tile (i, j) starts once E's row panel i and F's column panel j (F^T's rows)
-    // are published.
+    // NEXT-4 chain fusion (opt-in PB_CHAIN=1): F, E and G in one persistent
+    // launch. E's operand splits (lo of A and B) are done inside the launch; G's tile (i, j)
+    // starts once E's row panel i and F's column panel j are published.
     GemmDesc gs[3] = {gf, ge, gg};
     w.sk2.attach(gs[1]);
     w.sk3.attach(gs[2]);
@@ -456,12 +496,12 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
       lk[1].npre = 2;
       ChainLink::Pre& pa = lk[1].pre[0];
       pa.X = A; pa.rows = ni; pa.cols = nk; pa.ldx = nk;
-      pa.hi = const_cast<float*>(w.a.hi); pa.lo = const_cast<float*>(w.a.lo); pa.ldo = w.a.ld; pa.transpose = false;
+      pa.lo = w.a.lo; pa.ldo = w.a.ld; pa.lo_only = true;
       ChainLink::Pre& pbt = lk[1].pre[1];
       pbt.X = B; pbt.rows = nk; pbt.cols = nj; pbt.ldx = nj;
-      pbt.hi = const_cast<float*>(w.bt.hi); pbt.lo = const_cast<float*>(w.bt.lo); pbt.ldo = w.bt.ld; pbt.transpose = true;
-      PB_CUDA(launch_split(C, nj, nm, nm, w.c.hi, w.c.lo, w.c.ld, st));
-      PB_CUDA(launch_split_T(D, nm, nl, nl, w.dt.hi, w.dt.lo, w.dt.ld, nullptr, nullptr, st));
+      pbt.lo = w.b.lo; pbt.ldo = nj; pbt.lo_only = true;
+      PB_CUDA(launch_split_lo(C, nj, nm, nm, w.c.lo, w.c.ld, st));
+      PB_CUDA(launch_split_lo(D, nm, nl, nl, w.d.lo, nl, st));
       L += 2;
       PB_CUDA(launch_umma_chain(gs, lk, 3, w.chain.cnt, w.chain.cnt_bytes, st, &L));
       g_launches = L;
@@ -470,15 +510,15 @@ pb_status pb_3mm(int ni, int nj, int nk, int nl, int nm, float* E, const float* 
   }
   Side* sd = side_stream();
   cudaStream_t sab = st;
-  PB_CUDA(launch_split(C, nj, nm, nm, w.c.hi, w.c.lo, w.c.ld, st));
-  PB_CUDA(launch_split_T(D, nm, nl, nl, w.dt.hi, w.dt.lo, w.dt.ld, nullptr, nullptr, st));
-  if (sd) {  // E's operands (A, B^T) are split beside GEMM F (fork: F's operands are ready)
+  PB_CUDA(launch_split_lo(C, nj, nm, nm, w.c.lo, w.c.ld, st));
+  PB_CUDA(launch_split_lo(D, nm, nl, nl, w.d.lo, nl, st));
+  if (sd) {  // E's operands (lo of A, B) are split beside GEMM F (fork: F's operands are ready)
     PB_CUDA(cudaEventRecord(sd->fork, st));
     PB_CUDA(cudaStreamWaitEvent(sd->s, sd->fork, 0));
     sab = sd->s;
   }
-  PB_CUDA(launch_split(A, ni, nk, nk, w.a.hi, w.a.lo, w.a.ld, sab));
-  PB_CUDA(launch_split_T(B, nk, nj, nj, w.bt.hi, w.bt.lo, w.bt.ld, nullptr, nullptr, sab));
+  PB_CUDA(launch_split_lo(A, ni, nk, nk, w.a.lo, w.a.ld, sab));
+  PB_CUDA(launch_split_lo(B, nk, nj, nj, w.b.lo, nj, sab));
   if (sd) PB_CUDA(cudaEventRecord(sd->join, sd->s));
   L += 4;
   PB_CUDA(launch_umma_gemm(gf, st, &L));
@@ -506,20 +546,21 @@ static pb_status syrk_core(int n, int m, int r0, int r1, float alpha, float beta
   PB_TRY(check_ws(need, ws, ws_bytes));
   Carve c(ws, ws_bytes);
   WsSyrk w = ws_syrk(c, n, m, r0, r1, B != nullptr, full);
-  SplitBuf sa = w.a, sb = w.b;
   cudaStream_t st = S(s);
   int L = 0;
-  PB_CUDA(launch_split(A, r1, m, m, sa.hi, sa.lo, sa.ld, st));
+  // raw-hi split (A and B are the hi operands, rows K-major as they are): lo only
+  PB_CUDA(launch_split_lo(A, r1, m, m, w.a.lo, w.a.ld, st));
   ++L;
-  if (B) { PB_CUDA(launch_split(B, r1, m, m, sb.hi, sb.lo, sb.ld, st)); ++L; }
+  if (B) { PB_CUDA(launch_split_lo(B, r1, m, m, w.b.lo, w.b.ld, st)); ++L; }
+  const SplitOperand oa = w.a.op_raw(A), ob = B ? w.b.op_raw(B) : SplitOperand{};
   GemmDesc d;
   d.M = r1; d.N = r1; d.K = m;
   if (B) {  // C[i][j] += A[j].B[i] + B[j].A[i]: pair 0 = (B rows i, A rows j), pair 1 = (A rows i, B rows j)
     d.npairs = 2;
-    d.a[0] = sb.op(); d.b[0] = sa.op();
-    d.a[1] = sa.op(); d.b[1] = sb.op();
+    d.a[0] = ob; d.b[0] = oa;
+    d.a[1] = oa; d.b[1] = ob;
   } else {
-    d.a[0] = sa.op(); d.b[0] = sa.op();
+    d.a[0] = oa; d.b[0] = oa;
   }
   d.flags = (full ? 0u : (uint32_t)EPI_TRI) | EPI_OUT | (beta != 0.f ? EPI_CIN : 0u);
   d.alpha = alpha; d.beta = beta;

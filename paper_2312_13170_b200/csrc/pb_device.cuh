@@ -174,6 +174,16 @@ __device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t smem_addr) {
   return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// UMMA shared-memory descriptor of an MN-major tf32 operand. The only smem layout the
+// tensor core takes for MN-major 32-bit operands is the 128-B swizzle with 32-B atoms
+// (layout type 1, "128B_BASE32B"): 32-element (128-B) rows along M/N, the 32-B granules
+// of row r XOR-permuted by r mod 4; runs of 32 M/N elements `lbo` bytes apart, 4-row K
+// groups `sbo` bytes apart. TMA writes the same layout (CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
+// (Measured on B200: with the ordinary 128-B swizzle an MN-major tf32 MMA reads zeros.)
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128b32(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
+}
 // Instruction descriptor, kind::tf32: D=F32, A=B=TF32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -190,6 +200,13 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ void split3x(float x, float& hi, float& lo) {
   hi = tf32_rna(x);
   lo = tf32_rna(__fsub_rn(x, hi));
+}
+// Raw-hi split: the tensor core reads a raw fp32 operand as tf32 by truncation (the low 13
+// mantissa bits ignored), so the fp32 array itself serves as hi and only
+// lo = rna_tf32(x - trunc_tf32(x)) (x - trunc is exact) has to be materialised.
+__device__ __forceinline__ float lo_of_raw(float x) {
+  const float t = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  return tf32_rna(__fsub_rn(x, t));
 }
 
 // ---------------------------------------------------------------- streaming loads

@@ -18,6 +18,9 @@ struct SplitOperand {
   int rows = 0;
   int K = 0;
   int ld = 0;
+  // mn = true (B operands only): hi / lo are stored K x rows row-major (pitch ld), i.e.
+  // MN-major (B[k][n] as the caller has it: no transpose); tiles go MN-major to the MMA.
+  bool mn = false;
 };
 
 enum : uint32_t {
@@ -29,6 +32,7 @@ enum : uint32_t {
   EPI_SPLIT = 1u << 5,     // write hi/lo split of v at [i][j] (next GEMM's K-major A operand)
   EPI_SPLIT_T = 1u << 6,   // write hi/lo split of v at [j][i] (next GEMM's K-major B operand)
   EPI_PARTIAL = 1u << 7,   // every tile only writes (per-split) partials; launch_gram_combine finishes
+  EPI_SPLIT_LO = 1u << 8,  // write lo_of_raw(v) at [i][j] (split_lo): the next GEMM's operand is (out, lo)
 };
 
 struct GemmDesc {
@@ -79,6 +83,7 @@ struct ChainLink {
     float* lo = nullptr;
     int ldo = 0;
     bool transpose = false;
+    bool lo_only = false;  // raw-hi split: write only lo (same layout as X; hi unused)
   } pre[2];
   int npre = 0;
 };
@@ -122,6 +127,8 @@ cudaError_t launch_gram_fused(bool corr, int m, int n, double float_n, double ep
 // done != nullptr: each CTA adds 1 to *done when its part is stored (release); *ctas += grid size.
 cudaError_t launch_split(const float* X, int rows, int cols, int ldx, float* hi, float* lo, int ldo,
                          cudaStream_t s, unsigned* done = nullptr, unsigned* ctas = nullptr);
+// raw-hi split: only lo of X (rows x cols, same layout, pitch ldo); X itself is the hi operand.
+cudaError_t launch_split_lo(const float* X, int rows, int cols, int ldx, float* lo, int ldo, cudaStream_t s);
 // hi/lo split of the transpose: out (cols x rows), out pitch ldo (>= rows).
 // If mean != nullptr: value = (x - mean[col]) * inv[col] computed in double first
 // (inv == nullptr means 1).
