@@ -47,9 +47,10 @@ def test_status_and_version():
 
 
 def test_workspace_sizes():
-    assert pb.workspace_size("gemm", (128, 128, 128)) == 4 * 128 * 128 * 4
-    assert pb.workspace_size("gemm", (7, 4, 5)) >= 2 * 4 * (7 * 8 + 4 * 8)
-    assert pb.workspace_size("syr2k", (8192, 8192)) >= 4 * 8192 * 8192 * 4  # + split-K partials
+    # raw-hi split: one lo array per operand (A, and B as stored)
+    assert pb.workspace_size("gemm", (128, 128, 128)) == 2 * 128 * 128 * 4
+    assert pb.workspace_size("gemm", (7, 4, 5)) >= 4 * (7 * 8 + 5 * 4)
+    assert pb.workspace_size("syr2k", (8192, 8192)) >= 2 * 8192 * 8192 * 4  # + split-K partials
     for k, d in [("2mm", (4, 4, 4, 4)), ("3mm", (4, 4, 4, 4, 4)), ("covariance", (8, 9)),
                  ("correlation", (8, 9)), ("atax", (5, 8)), ("bicg", (8, 5)), ("mvt", (8,)),
                  ("gesummv", (8,)), ("syrk_rows", (256, 8, 128, 256)), ("matvec_partial", (3, 8))]:
