@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
           }
         }
       }
+      if (et == 0) GTS(12);
     }
     // (c) finalise chunk ks in sub-chunks of <= 128 columns: thread (row rl, half ch) takes
     // half of each sub-chunk's columns: own (TMEM) + partners (ascending k: a fixed order per
@@ -852,10 +853,10 @@ cudaError_t launch_gram_fused(bool corr, int m, int n, double float_n, double ep
     const int G = 2 * f.T * f.S;
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < G; ++c) if (h[c * 16]) t0 = std::min(t0, h[c * 16]);
-    const char* names[12] = {"entry", "prep done", "first band ready", "MMA done", "partials in", "end",
+    const char* names[14] = {"entry", "prep done", "first band ready", "MMA done", "partials in", "end",
                              "var stats ready", "u0 loads in", "u0 shift", "u0 stores issued", "u0 published",
-                             "finalised"};
-    for (int k = 0; k < 12; ++k) {
+                             "finalised", "partner values in", "-"};
+    for (int k = 0; k < 13; ++k) {
       std::vector<double> v;
       for (int c = 0; c < G; ++c) if (h[c * 16 + k]) v.push_back((h[c * 16 + k] - t0) / 1e3);
       if (v.empty()) continue;
