@@ -427,3 +427,26 @@ def test_2mm_beta0_nan_not_read():
     pb.pb_2mm(ni, nj, nk, nl, 1.5, 0.0, None, P.dev(A), P.dev(B), P.dev(C), dD)
     (_, Dr), (_, Ds) = (oracle.mm2(1.5, 0.0, A, B, C, np.zeros((ni, nl), np.float32), absmode=a) for a in (False, True))
     assert P.cerr(P.host(dD), Dr, Ds) <= P.TOL
+
+
+@pytest.mark.parametrize("m,n", [(1024, 4096), (3072, 4096)])
+def test_cov_corr_exact_mean_path_workspace_bound(m, n):
+    """n > 2048 (exact-mean prep) with m large enough that the Gram plan splits K through
+    the partial buffer (the split-K area was once sized for the other
+    plan): the call gets a workspace of exactly pb_workspace_size bytes followed by a
+    sentinel region, which must come back untouched; results against the oracle."""
+    import oracle
+    data = P.H(n, m, P.S["data"])
+    for k in ("covariance", "correlation"):
+        need = pb.workspace_size(k, (m, n))
+        buf = torch.full((need + (1 << 20),), 0xAB, dtype=torch.uint8, device="cuda")
+        ws = buf[:need]
+        out = torch.empty(m, m, device="cuda")
+        if k == "covariance":
+            pb.pb_covariance(m, n, float(n), P.dev(data), out, None, ws=ws)
+            r, s = oracle.covariance(float(n), data)[0], oracle.covariance(float(n), data, absmode=True)[0]
+        else:
+            pb.pb_correlation(m, n, float(n), 0.1, P.dev(data), out, None, None, ws=ws)
+            r, s = oracle.correlation(float(n), 0.1, data)[0], oracle.correlation(float(n), 0.1, data, absmode=True)[0]
+        assert bool((P.host(buf[need:]) == 0xAB).all()), f"{k}: workspace overrun"
+        assert P.cerr(P.host(out), r, s) <= P.TOL, k
