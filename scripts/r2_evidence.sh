@@ -2,7 +2,7 @@
 # round-2 kernels, launch list of the bench step and ncu captures of the top kernels.
 set -x
 mkdir -p gpurun_out
-T=${TAG:-r2c}
+T=${TAG:-r2e}
 make -j8 > gpurun_out/${T}_make.log 2>&1 || tail -20 gpurun_out/${T}_make.log
 timeout 1500 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/${T}_pytest_gpu.log 2>&1; echo pytest rc=$?
 tail -3 gpurun_out/${T}_pytest_gpu.log
