@@ -123,13 +123,6 @@ __device__ __forceinline__ void warp_wait_flags(const unsigned* f, unsigned want
 }
 // generic-proxy global writes -> visible to async-proxy (TMA) reads
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1)
-               : "memory");
-}
 // 3-D tiled load, cta_group::2: completion counted on the LEADER CTA's barrier
 __device__ __forceinline__ void tma_load_3d_cg2(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2) {
   asm volatile(
@@ -144,9 +137,6 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 #define GTS(k)                                                                  \
   do {                                                                          \
     if (p.ts) p.ts[(unsigned long long)blockIdx.x * 16 + (k)] = gtimer_ns();    \

@@ -174,6 +174,7 @@ struct Params {
   int sk_pairs;                  // P = CTA groups of the grid
   int sk_maxseg;                 // partial slots per tile (max pairs sharing one tile)
   int dbg;                       // PB_UMMA_DEBUG (tuning only): 1 = skip partial exchange
+  int tma_epi;                   // 1: staged TMA-store epilogue (maps 8 = out, 9 = split_lo, 10 = cin)
   unsigned long long* tstamp;    // PB_UMMA_TIMING (tuning only): [cta][unit<16][8] globaltimer stamps
 };
 
@@ -241,6 +242,7 @@ struct __align__(8) Ctl {
   uint32_t tmem_base;
   uint32_t last_flag;
   uint32_t pre_warps_done;  // chain: epilogue warps that finished their share of the in-launch splits
+  uint64_t cbar[8];         // TMA-store epilogue: per epilogue warp, its C box loads
 };
 
 // number of column tiles in tile-row tm (lower triangle: tiles touching j <= i)
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       mbar_init(&ctl->tempty[s], C::EPI_WARPS * CG);  // one arrive per epilogue warp of every CTA
     }
     ctl->pre_warps_done = 0;
+    for (int w = 0; w < C::EPI_WARPS; ++w) mbar_init(&ctl->cbar[w], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -404,7 +407,9 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     if (ch.ph[0].npairs > 1 || ch.nphase > 1) {
       tma_prefetch(&a1h); tma_prefetch(&a1l); tma_prefetch(&b1h); tma_prefetch(&b1l);
     }
-    if (ch.nphase > 2) { tma_prefetch(&a2h); tma_prefetch(&a2l); tma_prefetch(&b2h); tma_prefetch(&b2l); }
+    if (ch.nphase > 2 || (!CHAIN && ch.ph[0].tma_epi)) {
+      tma_prefetch(&a2h); tma_prefetch(&a2l); tma_prefetch(&b2h); tma_prefetch(&b2l);
+    }
   }
   if (warp == 1) tmem_alloc_cg<CG>(&ctl->tmem_base, TMEM_COLS);
   tc_fence_before();
@@ -604,6 +609,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         }
       }
     };
+    uint32_t cpar = 0;  // TMA-store epilogue: parity of this warp's C-box barrier
     UnitIter ui = iter_init(ch, tile0, tile_step);
     int ph;
     long long u;  // unit index within the phase
@@ -707,6 +713,68 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       const bool row_ok = i < p.M;
       const bool diag_tile = (flags & EPI_TRI) && (tn * BN + BN - 1 > row0);  // tile crosses j > i
       const long long orow = (long long)(i - p.out_row0);
+      if (!CHAIN && p.tma_epi && !diag_tile) {
+        // Staged TMA-store epilogue (S4): this warp's 32 rows leave in 32 x 32 boxes. Per box:
+        // the C box arrives by TMA (EPI_CIN), every lane writes its row's 32 values into the
+        // 128-B-swizzled staging box (16-B piece c at c ^ (row & 7): conflict-free), and one
+        // lane stores the box with cp.async.bulk.tensor (out-of-range rows / columns clipped
+        // by the tensor map). EPI_SPLIT_LO reuses the box for lo once the out store has read it.
+        const int brow = row0 + q * 32;  // first row of this warp's block
+#pragma unroll
+        for (int cc = 0; cc < EPI_COLS / 32; ++cc) {
+          const int j0 = tn * BN + cbase + cc * 32;
+          if (j0 >= p.N) break;
+          if (lane == 0) bulk_wait_read0();  // the previous box's store has read the staging box
+          __syncwarp();
+          if (flags & EPI_CIN) {
+            if (lane == 0) {
+              mbar_arrive_expect_tx(&ctl->cbar[ew], 32 * 32 * 4);
+              tma_load_2d(map_of(2, 2), &ctl->cbar[ew], stg, j0, brow - p.out_row0);  // map 10: cin
+            }
+            mbar_wait(&ctl->cbar[ew], cpar);
+            cpar ^= 1u;
+          }
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            float4* sp = reinterpret_cast<float4*>(stg + lane * 32 + ((c4 ^ (lane & 7)) << 2));
+            const int e = cc * 32 + c4 * 4;
+            float4 w = make_float4(p.alpha * acc[e], p.alpha * acc[e + 1], p.alpha * acc[e + 2], p.alpha * acc[e + 3]);
+            if (flags & EPI_CIN) {
+              const float4 c = *sp;
+              w.x += p.beta * c.x; w.y += p.beta * c.y; w.z += p.beta * c.z; w.w += p.beta * c.w;
+            }
+            if (flags & EPI_DIAG_ONE) {
+              const int d = i - (j0 + c4 * 4);
+              if (d == 0) w.x = 1.f; else if (d == 1) w.y = 1.f; else if (d == 2) w.z = 1.f; else if (d == 3) w.w = 1.f;
+            }
+            *sp = w;
+          }
+          fence_proxy_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(map_of(2, 0), stg, j0, brow - p.out_row0);  // map 8: out
+            bulk_commit();
+          }
+          if (flags & EPI_SPLIT_LO) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              float4* sp = reinterpret_cast<float4*>(stg + lane * 32 + ((c4 ^ (lane & 7)) << 2));
+              const float4 w = *sp;
+              *sp = make_float4(lo_of_raw(w.x), lo_of_raw(w.y), lo_of_raw(w.z), lo_of_raw(w.w));
+            }
+            fence_proxy_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(map_of(2, 1), stg, j0, brow);  // map 9: split_lo (rows i, like EPI_SPLIT_LO)
+              bulk_commit();
+            }
+          }
+        }
+        if (warp == 2 && lane == 0) TSTAMP(ul, 5);
+        continue;
+      }
 #pragma unroll
       for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
         const int j0 = tn * BN + cbase + c0;
@@ -800,6 +868,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     if constexpr (CHAIN) {
       while (pre_left) pre_step();  // (a CTA with few units: the rest of its share of the splits)
     }
+    if (!CHAIN && lane == 0) bulk_wait0();  // this warp's TMA stores are complete
   }
 
   tc_fence_before();
@@ -837,6 +906,7 @@ bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles,
   p.part = d.part;
   p.counters = d.counters;
   p.b_mn = d.b[0].mn ? 1 : 0;
+  p.tma_epi = 0;
   p.streamk = 0;
   p.sk_iters = 0; p.sk_pairs = 1; p.sk_maxseg = 1;
   if (skp && skp->streamk) {
@@ -891,6 +961,21 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
   CUtensorMap maps[12];
   if (!phase_maps<CG, BN>(d, maps)) return cudaErrorInvalidValue;
   for (int q = 4 * d.npairs; q < 12; ++q) maps[q] = maps[q % 4];
+  // staged TMA-store epilogue (maps 8 = out, 9 = split_lo, 10 = cin; free in a one-GEMM launch,
+  // syr2k's second pair uses 4..7) when every output is a plain row-major store with 16-B rows
+  static const bool tma_off = getenv("PB_TMA_EPI") && atoi(getenv("PB_TMA_EPI")) == 0;
+  auto al16 = [](const void* x, long long ld) { return x && ((uintptr_t)x & 15) == 0 && ld % 4 == 0; };
+  if (!tma_off && (d.flags & EPI_OUT) && !(d.flags & (EPI_MIRROR | EPI_SPLIT | EPI_SPLIT_T | EPI_PARTIAL)) &&
+      d.M > d.out_row0 && al16(d.out, d.ldo) && (!(d.flags & EPI_CIN) || al16(d.cin, d.ldc)) &&
+      (!(d.flags & EPI_SPLIT_LO) || al16(d.split_lo, d.ld_split))) {
+    const bool ok = make_map2d(&maps[8], d.out, d.N, d.M - d.out_row0, d.ldo, 32, 32, true) &&
+                    (!(d.flags & EPI_SPLIT_LO) || make_map2d(&maps[9], d.split_lo, d.N, d.M, d.ld_split, 32, 32, true)) &&
+                    (!(d.flags & EPI_CIN) || make_map2d(&maps[10], d.cin, d.N, d.M - d.out_row0, d.ldc, 32, 32, true));
+    if (ok)
+      p.tma_epi = 1;
+    else
+      for (int q = 8; q < 12; ++q) maps[q] = maps[q % 4];
+  }
   Chain ch{};
   ch.nphase = 1;
   ch.ph[0] = p;
@@ -932,7 +1017,8 @@ template <int CG, int BN, bool CHAIN>
 cudaError_t launch_chain_kernel(const Chain& ch, const CUtensorMap* maps, cudaStream_t s, int* launches) {
   using C = Cfg<CG, BN>;
   // CHAIN: + per-epilogue-warp transpose staging for the in-launch operand splits
-  const size_t smem = C::STAGES * C::STAGE_BYTES + 1024 + (CHAIN ? 1024 + C::EPI_WARPS * PRE_STAGE : sizeof(Ctl) + 64);
+  // + Ctl (1 KB) + per-epilogue-warp 4 KB staging: the chain's transposes, else the TMA-store boxes
+  const size_t smem = C::STAGES * C::STAGE_BYTES + 1024 + 1024 + C::EPI_WARPS * PRE_STAGE;
   {
     const cudaError_t e = ensure_smem<umma3x_kernel<CG, BN, CHAIN>>(smem);
     if (e != cudaSuccess) return e;
