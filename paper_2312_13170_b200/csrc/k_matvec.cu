@@ -531,6 +531,182 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
   cluster_sync_all();
 }
 
+
+// ------------------------------------------------------------------ atax, single pass, x in TMEM
+// atax_reg_kernel with x held in tensor memory instead of shared memory. TMEM (256 KB per SM,
+// otherwise idle here) is read with tcgen05.ld straight into registers, so the per-row dot no
+// longer reads a 64 KB x slice through the shared-memory port (which also serves the TMA
+// writes and the stage copies: 192 -> 128 KB of smem traffic per row), and the freed 64 KB
+// holds a third stage. Thread (warp w, lane l) keeps its 32 x values in TMEM lane
+// 32 (w % 4) + l, columns 32 (w / 4) .. + 31 (a warp may only touch its lane quarter).
+// The CTA's partial dot is formed by the last warp to post (fence + counter, as in
+// atax_reg_kernel); the warp partials go through shared-memory atomics so the hand-off has
+// no plain racing accesses. (Posting every warp's partial into both CTAs with 2 x 16
+// cluster-barrier arrivals per row was measured slower: 844 vs 702 us.)
+constexpr int AT_STAGES = 3;
+constexpr uint32_t AT_TMEM_COLS = 128;
+
+struct __align__(16) AtCtl {
+  uint64_t full[AT_STAGES];
+  uint64_t red[AX_RED];
+  unsigned cnt[AX_RED];
+  float part[AX_RED][2];
+  unsigned wred[AX_RED][AX_THREADS / 32];  // warp partials (fp32 bits)
+  uint32_t tmem_base;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
+    atax_tm_kernel(const float* __restrict__ A, const float* __restrict__ x, int m, int n, int w0,
+                   float* __restrict__ tmp, float* __restrict__ ypart) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* stage_buf = reinterpret_cast<float*>(sm);  // AT_STAGES x AX_SLICE
+  AtCtl* ctl = reinterpret_cast<AtCtl*>(stage_buf + (size_t)AT_STAGES * AX_SLICE);
+  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = AX_THREADS / 32;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int c0 = rank ? w0 : 0;
+  const int w = rank ? n - w0 : w0;
+  const int w4 = w >> 2;
+  const int r0 = (int)((long long)m * cl / ncl), r1 = (int)((long long)m * (cl + 1) / ncl);
+  const int nb = r1 - r0;
+
+  if (tid == 0) {
+    for (int s = 0; s < AT_STAGES; ++s) mbar_init(&ctl->full[s], 1);
+    for (int s = 0; s < AX_RED; ++s) {
+      mbar_init(&ctl->red[s], 2);
+      ctl->cnt[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&ctl->tmem_base, AT_TMEM_COLS);
+  auto issue = [&](int b) {
+    const int s = b % AT_STAGES;
+    mbar_arrive_expect_tx(&ctl->full[s], (uint32_t)w * 4u);
+    if (w > 0) bulk_g2s(stage_buf + (size_t)s * AX_SLICE, A + (long long)(r0 + b) * n + c0, (uint32_t)w * 4u,
+                        &ctl->full[s]);
+  };
+  tc_fence_before();
+  cluster_sync_all();  // barriers exist in both CTAs; TMEM allocated
+  tc_fence_after();
+  if (tid == 0)
+    for (int b = 0; b < AT_STAGES && b < nb; ++b) issue(b);
+  const uint32_t tx = ctl->tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 32u;
+  {  // this thread's x float4s (idx = tid + v AX_THREADS, zero past the slice) -> TMEM
+    const float4* x4 = reinterpret_cast<const float4*>(x + c0);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t r[16];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int idx = tid + (h * 4 + v) * AX_THREADS;
+        const float4 xv = idx < w4 ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+        r[4 * v] = __float_as_uint(xv.x); r[4 * v + 1] = __float_as_uint(xv.y);
+        r[4 * v + 2] = __float_as_uint(xv.z); r[4 * v + 3] = __float_as_uint(xv.w);
+      }
+      tmem_st16(tx + 16u * h, r);
+    }
+    tmem_wait_st();
+  }
+  float4 yacc[AX_V];
+#pragma unroll
+  for (int v = 0; v < AX_V; ++v) yacc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t red0 = smem_u32(&ctl->red[0]);
+  const uint32_t part0 = smem_u32(&ctl->part[0][0]);
+
+  auto step = [&](int b, float4(&cur)[AX_V], float4(&prev)[AX_V]) {
+    const int s = b % AT_STAGES, slot = b % AX_RED;
+    mbar_wait(&ctl->full[s], (uint32_t)(b / AT_STAGES) & 1u);
+    const float4* row = reinterpret_cast<const float4*>(stage_buf + (size_t)s * AX_SLICE);
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const int idx = tid + v * AX_THREADS;
+      cur[v] = idx < w4 ? row[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();  // every thread holds its part of row b: the stage can be refilled
+    if (tid == 0 && b + AT_STAGES < nb) issue(b + AT_STAGES);
+    float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t xr[16];
+      tmem_ld16(tx + 16u * h, xr);
+      tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const float4 c = cur[h * 4 + v];
+        pa = ffma2(make_float2(c.x, c.y), make_float2(__uint_as_float(xr[4 * v]), __uint_as_float(xr[4 * v + 1])), pa);
+        pb = ffma2(make_float2(c.z, c.w), make_float2(__uint_as_float(xr[4 * v + 2]), __uint_as_float(xr[4 * v + 3])),
+                   pb);
+      }
+    }
+    float p = (pa.x + pa.y) + (pb.x + pb.y);
+    p = warp_sum(p);
+    if (lane == 0) {
+      unsigned* wr = ctl->wred[slot];
+      atomicExch(&wr[warp], __float_as_uint(p));  // (atomics: the hand-off below is fence + counter)
+      __threadfence_block();
+      if (atomicAdd(&ctl->cnt[slot], 1u) == NW - 1) {  // last warp forms the CTA partial
+        __threadfence_block();
+        atomicExch(&ctl->cnt[slot], 0u);
+        float q = 0.f;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) q += __uint_as_float(atomicAdd(&wr[k], 0u));
+        const uint32_t poff = (uint32_t)(slot * 2 + rank) * 4u, roff = (uint32_t)slot * 8u;
+        st_cluster_f32(map_peer(part0 + poff, rank), q);
+        st_cluster_f32(map_peer(part0 + poff, peer), q);
+        mbar_arrive_cluster(map_peer(red0 + roff, rank));
+        mbar_arrive_cluster(map_peer(red0 + roff, peer));
+      }
+    }
+    if (b >= 1) {  // axpy of row b-1 (its partials had the whole dot of row b to arrive)
+      const int ps = (b - 1) % AX_RED;
+      mbar_wait_cluster(&ctl->red[ps], (uint32_t)((b - 1) / AX_RED) & 1u);
+      const float t = ctl->part[ps][0] + ctl->part[ps][1];
+      if (tmp && rank == 0 && tid == 0) tmp[r0 + b - 1] = t;
+      const float2 t2 = make_float2(t, t);
+#pragma unroll
+      for (int v = 0; v < AX_V; ++v) {
+        const float2 lo = ffma2(t2, make_float2(prev[v].x, prev[v].y), make_float2(yacc[v].x, yacc[v].y));
+        const float2 hi = ffma2(t2, make_float2(prev[v].z, prev[v].w), make_float2(yacc[v].z, yacc[v].w));
+        yacc[v] = make_float4(lo.x, lo.y, hi.x, hi.y);
+      }
+    }
+  };
+  float4 ra[AX_V], rb[AX_V];
+  int b = 0;
+  for (; b + 1 < nb; b += 2) {
+    step(b, ra, rb);
+    step(b + 1, rb, ra);
+  }
+  if (b < nb) step(b, ra, rb);
+  if (nb > 0) {  // last row's axpy
+    const int last = nb - 1, ps = last % AX_RED;
+    float4(&lr)[AX_V] = (last & 1) ? rb : ra;
+    mbar_wait_cluster(&ctl->red[ps], (uint32_t)(last / AX_RED) & 1u);
+    const float t = ctl->part[ps][0] + ctl->part[ps][1];
+    if (tmp && rank == 0 && tid == 0) tmp[r0 + last] = t;
+    const float2 t2 = make_float2(t, t);
+#pragma unroll
+    for (int v = 0; v < AX_V; ++v) {
+      const float2 lo = ffma2(t2, make_float2(lr[v].x, lr[v].y), make_float2(yacc[v].x, yacc[v].y));
+      const float2 hi = ffma2(t2, make_float2(lr[v].z, lr[v].w), make_float2(yacc[v].z, yacc[v].w));
+      yacc[v] = make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
+  }
+  float4* yp = reinterpret_cast<float4*>(ypart + (long long)cl * n + c0);
+#pragma unroll
+  for (int v = 0; v < AX_V; ++v) {
+    const int idx = tid + v * AX_THREADS;
+    if (idx < w4) yp[idx] = yacc[v];
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(ctl->tmem_base, AT_TMEM_COLS);
+  }
+}
+
 }  // namespace
 
 size_t atax_ws_bytes(int m, int n) {
@@ -580,8 +756,15 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
     }
     const int w0 = ((n / 4 + 1) / 2) * 4;
     float* ypart = static_cast<float*>(ws);
-    static const int variant = getenv("PB_ATAX_VARIANT") ? atoi(getenv("PB_ATAX_VARIANT")) : 2;
-    if (variant == 2) {
+    static const int variant = getenv("PB_ATAX_VARIANT") ? atoi(getenv("PB_ATAX_VARIANT")) : 3;
+    if (variant == 3) {
+      const size_t smem3 = (size_t)AT_STAGES * AX_SLICE * 4 + sizeof(AtCtl);
+      {
+        const cudaError_t e = ensure_smem<atax_tm_kernel>(smem3);
+        if (e != cudaSuccess) return e;
+      }
+      atax_tm_kernel<<<2 * ncl, AX_THREADS, smem3, s>>>(A, x, m, n, w0, tmp, ypart);
+    } else if (variant == 2) {
       const size_t smem2 = (size_t)(1 + AR_STAGES) * AX_SLICE * 4 + sizeof(ArCtl);
       {
         const cudaError_t e = ensure_smem<atax_reg_kernel>(smem2);

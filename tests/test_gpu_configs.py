@@ -2,7 +2,8 @@
 the oracle: each case runs in a subprocess with the tuning environment set
 (PB_UMMA_TILE: 1 = 1-CTA 128x128, 2 = 2-CTA 256x128, 3 = 2-CTA 256x256;
 PB_UMMA_KSPLIT: forced split-K on every tile; PB_ATAX_VARIANT: 1 = smem rows,
-2 = register rows), since the library reads them once per process."""
+2 = register rows with x in smem, 3 (default) = register rows with x in TMEM; PB_TMA_EPI=0:
+the GEMM epilogue's per-thread row stores instead of the TMA-store boxes), since the library reads them once per process."""
 import os
 import subprocess
 import sys
@@ -18,6 +19,8 @@ CASES = [
     ({"PB_UMMA_TILE": "3", "PB_UMMA_KSPLIT": "3"}, "gemm or 2mm or 3mm or syrk or syr2k or cov or corr"),
     ({"PB_UMMA_TILE": "2", "PB_UMMA_KSPLIT": "2"}, "gemm or syr2k or cov"),
     ({"PB_ATAX_VARIANT": "1"}, "atax"),
+    ({"PB_ATAX_VARIANT": "2"}, "atax"),
+    ({"PB_TMA_EPI": "0"}, "gemm or 2mm or 3mm or syrk or syr2k"),
 ]
 
 
