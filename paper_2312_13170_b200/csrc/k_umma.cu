@@ -242,7 +242,7 @@ struct __align__(8) Ctl {
   uint32_t tmem_base;
   uint32_t last_flag;
   uint32_t pre_warps_done;  // chain: epilogue warps that finished their share of the in-launch splits
-  uint64_t cbar[8];         // TMA-store epilogue: per epilogue warp, its C box loads
+  uint64_t cbar[16];        // TMA-store epilogue: per epilogue warp, its two C-box buffers
 };
 
 // number of column tiles in tile-row tm (lower triangle: tiles touching j <= i)
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       mbar_init(&ctl->tempty[s], C::EPI_WARPS * CG);  // one arrive per epilogue warp of every CTA
     }
     ctl->pre_warps_done = 0;
-    for (int w = 0; w < C::EPI_WARPS; ++w) mbar_init(&ctl->cbar[w], 1);
+    for (int w = 0; w < 2 * C::EPI_WARPS; ++w) mbar_init(&ctl->cbar[w], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -609,7 +609,13 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         }
       }
     };
-    uint32_t cpar = 0;  // TMA-store epilogue: parity of this warp's C-box barrier
+    uint32_t cpar = 0;  // TMA-store epilogue: parities of this warp's two C-box barriers (bits 0, 1)
+    // (lane 0) request C box b (32 rows from brow, 16 columns) into staging buffer b & 1
+    auto load_c = [&](int b, int col0, int brow) {
+      uint64_t* bar = &ctl->cbar[2 * ew + (b & 1)];
+      mbar_arrive_expect_tx(bar, 32 * 16 * 4);
+      tma_load_2d(map_of(2, 2), bar, stg + (b & 1) * 512, col0 + cbase + b * 16, brow - ch.ph[0].out_row0);  // map 10
+    };
     UnitIter ui = iter_init(ch, tile0, tile_step);
     int ph;
     long long u;  // unit index within the phase
@@ -621,6 +627,18 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       const int kbA = un.kbA, kbB = un.kbB;
       int tm, tn;
       tile_coords(p, t, tm, tn);
+      bool cpre = false;  // TMA-store epilogue: C boxes 0 and 1 already requested
+      if (!CHAIN && p.tma_epi && (flags & EPI_CIN) && !un.split) {
+        const int r0 = tm * C::PAIR_M + (int)rank * BM;
+        if (!((flags & EPI_TRI) && (tn * BN + BN - 1 > r0))) {  // not a diagonal tile (row stores)
+          if (lane == 0) {
+            bulk_wait_read0();  // the previous tile's stores have read the buffers
+            if (tn * BN + cbase < p.N) load_c(0, tn * BN, r0 + q * 32);
+            if (tn * BN + cbase + 16 < p.N) load_c(1, tn * BN, r0 + q * 32);
+          }
+          cpre = true;
+        }
+      }
       float acc[EPI_COLS];  // this thread's row x column-half of the tile, fp32 registers
 #pragma unroll
       for (int c = 0; c < EPI_COLS; ++c) acc[c] = 0.f;
@@ -714,30 +732,40 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
       const bool diag_tile = (flags & EPI_TRI) && (tn * BN + BN - 1 > row0);  // tile crosses j > i
       const long long orow = (long long)(i - p.out_row0);
       if (!CHAIN && p.tma_epi && !diag_tile) {
-        // Staged TMA-store epilogue (S4): this warp's 32 rows leave in 32 x 32 boxes. Per box:
-        // the C box arrives by TMA (EPI_CIN), every lane writes its row's 32 values into the
-        // 128-B-swizzled staging box (16-B piece c at c ^ (row & 7): conflict-free), and one
-        // lane stores the box with cp.async.bulk.tensor (out-of-range rows / columns clipped
-        // by the tensor map). EPI_SPLIT_LO reuses the box for lo once the out store has read it.
+        // Staged TMA-store epilogue (S4): this warp's 32 rows leave in 32 x 16 boxes through
+        // two 2 KB staging buffers (64-B swizzle: 16-B piece c of row r at c ^ ((r >> 1) & 3),
+        // conflict-free). Per box: the C box arrives by TMA (EPI_CIN; boxes 0 and 1 are
+        // requested before the accumulator is drained, box b + 2 once box b's store has read
+        // its buffer), every lane writes its row's 16 values, and one lane stores the box with
+        // cp.async.bulk.tensor (ragged rows / columns clipped by the tensor map). EPI_SPLIT_LO
+        // reuses the buffer for lo once the out store has read it.
         const int brow = row0 + q * 32;  // first row of this warp's block
+        constexpr int NBOX = EPI_COLS / 16;
+        if ((flags & EPI_CIN) && !cpre && lane == 0) {
+          bulk_wait_read0();
+          if (tn * BN + cbase < p.N) load_c(0, tn * BN, brow);
+          if (tn * BN + cbase + 16 < p.N) load_c(1, tn * BN, brow);
+        }
 #pragma unroll
-        for (int cc = 0; cc < EPI_COLS / 32; ++cc) {
-          const int j0 = tn * BN + cbase + cc * 32;
+        for (int b = 0; b < NBOX; ++b) {
+          const int j0 = tn * BN + cbase + b * 16;
           if (j0 >= p.N) break;
-          if (lane == 0) bulk_wait_read0();  // the previous box's store has read the staging box
-          __syncwarp();
+          float* const buf = stg + (b & 1) * 512;
           if (flags & EPI_CIN) {
-            if (lane == 0) {
-              mbar_arrive_expect_tx(&ctl->cbar[ew], 32 * 32 * 4);
-              tma_load_2d(map_of(2, 2), &ctl->cbar[ew], stg, j0, brow - p.out_row0);  // map 10: cin
+            mbar_wait(&ctl->cbar[2 * ew + (b & 1)], (cpar >> (b & 1)) & 1u);
+            cpar ^= 1u << (b & 1);
+          } else {
+            if (lane == 0) {  // the buffer's previous store has read it
+              if (b == 0) bulk_wait_read0();
+              else if (b >= 2 && (flags & EPI_SPLIT_LO)) bulk_wait_read<2>();
+              else if (b >= 2) bulk_wait_read<1>();
             }
-            mbar_wait(&ctl->cbar[ew], cpar);
-            cpar ^= 1u;
+            __syncwarp();
           }
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            float4* sp = reinterpret_cast<float4*>(stg + lane * 32 + ((c4 ^ (lane & 7)) << 2));
-            const int e = cc * 32 + c4 * 4;
+          for (int c4 = 0; c4 < 4; ++c4) {
+            float4* sp = reinterpret_cast<float4*>(buf + lane * 16 + ((c4 ^ ((lane >> 1) & 3)) << 2));
+            const int e = b * 16 + c4 * 4;
             float4 w = make_float4(p.alpha * acc[e], p.alpha * acc[e + 1], p.alpha * acc[e + 2], p.alpha * acc[e + 3]);
             if (flags & EPI_CIN) {
               const float4 c = *sp;
@@ -752,24 +780,28 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           fence_proxy_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(map_of(2, 0), stg, j0, brow - p.out_row0);  // map 8: out
+            tma_store_2d(map_of(2, 0), buf, j0, brow - p.out_row0);  // map 8: out
             bulk_commit();
           }
           if (flags & EPI_SPLIT_LO) {
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              float4* sp = reinterpret_cast<float4*>(stg + lane * 32 + ((c4 ^ (lane & 7)) << 2));
+            for (int c4 = 0; c4 < 4; ++c4) {
+              float4* sp = reinterpret_cast<float4*>(buf + lane * 16 + ((c4 ^ ((lane >> 1) & 3)) << 2));
               const float4 w = *sp;
               *sp = make_float4(lo_of_raw(w.x), lo_of_raw(w.y), lo_of_raw(w.z), lo_of_raw(w.w));
             }
             fence_proxy_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(map_of(2, 1), stg, j0, brow);  // map 9: split_lo (rows i, like EPI_SPLIT_LO)
+              tma_store_2d(map_of(2, 1), buf, j0, brow);  // map 9: split_lo (rows i, like EPI_SPLIT_LO)
               bulk_commit();
             }
+          }
+          if ((flags & EPI_CIN) && b + 2 < NBOX && j0 + 32 < p.N && lane == 0) {
+            bulk_wait_read0();  // this box's store(s) have read the buffer
+            load_c(b + 2, tn * BN, brow);
           }
         }
         if (warp == 2 && lane == 0) TSTAMP(ul, 5);
@@ -968,9 +1000,10 @@ cudaError_t launch_cg(const GemmDesc& d, Params p, int ksplit, long long split_t
   if (!tma_off && (d.flags & EPI_OUT) && !(d.flags & (EPI_MIRROR | EPI_SPLIT | EPI_SPLIT_T | EPI_PARTIAL)) &&
       d.M > d.out_row0 && al16(d.out, d.ldo) && (!(d.flags & EPI_CIN) || al16(d.cin, d.ldc)) &&
       (!(d.flags & EPI_SPLIT_LO) || al16(d.split_lo, d.ld_split))) {
-    const bool ok = make_map2d(&maps[8], d.out, d.N, d.M - d.out_row0, d.ldo, 32, 32, true) &&
-                    (!(d.flags & EPI_SPLIT_LO) || make_map2d(&maps[9], d.split_lo, d.N, d.M, d.ld_split, 32, 32, true)) &&
-                    (!(d.flags & EPI_CIN) || make_map2d(&maps[10], d.cin, d.N, d.M - d.out_row0, d.ldc, 32, 32, true));
+    const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_64B;  // 32 x 16 boxes (64-B rows)
+    const bool ok = make_map2d(&maps[8], d.out, d.N, d.M - d.out_row0, d.ldo, 16, 32, false, sw) &&
+                    (!(d.flags & EPI_SPLIT_LO) || make_map2d(&maps[9], d.split_lo, d.N, d.M, d.ld_split, 16, 32, false, sw)) &&
+                    (!(d.flags & EPI_CIN) || make_map2d(&maps[10], d.cin, d.N, d.M - d.out_row0, d.ldc, 16, 32, false, sw));
     if (ok)
       p.tma_epi = 1;
     else
