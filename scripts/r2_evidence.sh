@@ -2,7 +2,7 @@
 # round-2 kernels, launch list of the bench step and ncu captures of the top kernels.
 set -x
 mkdir -p gpurun_out
-T=${TAG:-r2e}
+T=${TAG:-r2f}
 make -j8 > gpurun_out/${T}_make.log 2>&1 || tail -20 gpurun_out/${T}_make.log
 timeout 1500 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/${T}_pytest_gpu.log 2>&1; echo pytest rc=$?
 tail -3 gpurun_out/${T}_pytest_gpu.log
@@ -16,6 +16,8 @@ for tool in memcheck racecheck synccheck; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-next > /dev/null 2>&1; echo launches rc=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gram_fused -s 2 -c 1 -o gpurun_out/${T}_cov_gram -f python scripts/gram_timing.py > /dev/null 2>&1; echo ncu gram rc=$?
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:atax_reg -s 1 -c 1 -o gpurun_out/${T}_atax -f python scripts/time_calls.py atax 32768 2 > /dev/null 2>&1; echo ncu atax rc=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:atax_tm -s 1 -c 1 -o gpurun_out/${T}_atax -f python scripts/time_calls.py atax 32768 2 > /dev/null 2>&1; echo ncu atax rc=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:umma3x -c 1 -o gpurun_out/${T}_syr2k_gemm -f python scripts/time_calls.py syr2k 8192 2 > /dev/null 2>&1; echo ncu syr2k rc=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:umma3x -c 1 -o gpurun_out/${T}_2mm_gemm -f python scripts/time_calls.py 2mm 4096 2 > /dev/null 2>&1; echo ncu 2mm rc=$?
 timeout 900 python scripts/rank_shapes.py gpurun_out/${T}_rank_shapes.json > /dev/null 2>&1; echo rank rc=$?
 ls gpurun_out | grep ${T}
