@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   tc_fence_after();
   pdl_wait();  // data (and the zeroed flags) come from the preceding stream work
   const int slabA_ok = slabA < p.nslab, slabB_ok = slabB < p.nslab;
-  if (threadIdx.x == 0) GTS(0);
+  if (threadIdx.x == 0) {
+    GTS(0);
+    if (p.ts) p.ts[(unsigned long long)blockIdx.x * 16 + 14] = clock64();
+  }
 
   if (warp == 0) {
     // ============================ TMA producer (both CTAs) ============================
@@ -674,7 +677,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     }
   }
 
-  if (threadIdx.x == 64) GTS(5);
+  if (threadIdx.x == 64) {
+    GTS(5);
+    if (p.ts) p.ts[(unsigned long long)blockIdx.x * 16 + 15] = clock64();
+  }
   pdl_trigger();
   tc_fence_before();
   cluster_sync_all();
@@ -846,6 +852,16 @@ cudaError_t launch_gram_fused(bool corr, int m, int n, double float_n, double ep
     const char* names[14] = {"entry", "prep done", "first band ready", "MMA done", "partials in", "end",
                              "var stats ready", "u0 loads in", "u0 shift", "u0 stores issued", "u0 published",
                              "finalised", "partner values in", "-"};
+    {  // effective SM clock over [entry, end] (clock64 of threads 0 and 64 of one SM)
+      std::vector<double> mhz;
+      for (int c = 0; c < G; ++c)
+        if (h[c * 16 + 5] > h[c * 16] && h[c * 16 + 15] > h[c * 16 + 14])
+          mhz.push_back((double)(h[c * 16 + 15] - h[c * 16 + 14]) * 1e3 / (double)(h[c * 16 + 5] - h[c * 16]));
+      if (!mhz.empty()) {
+        std::sort(mhz.begin(), mhz.end());
+        fprintf(stderr, "[pb gram timing] SM clock        med %7.0f MHz\n", mhz[mhz.size() / 2]);
+      }
+    }
     for (int k = 0; k < 13; ++k) {
       std::vector<double> v;
       for (int c = 0; c < G; ++c) if (h[c * 16 + k]) v.push_back((h[c * 16 + k] - t0) / 1e3);

@@ -165,7 +165,8 @@ struct Params {
   int tm0, tm1, tiles_n, ratio;  // ratio = tile rows / BN (CG)
   long long num_tiles;
   int ksplit;                    // K splits of each split tile (split-K)
-  long long split_tiles;         // tiles [0, split_tiles) are split; units of split tiles come first
+  long long split_tiles;         // split tiles: [split_t0, split_t0 + split_tiles)
+  long long split_t0;            // 0: split tiles first (their units lead); num_tiles - split_tiles: last
   float* part;                   // split-K partial tiles [unit][CG][128][BN]
   unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
   int b_mn;                      // 1: the B operand is MN-major (B[k][n] as stored), 32-column TMA runs
@@ -282,9 +283,14 @@ __device__ __forceinline__ void store4(float* p, float a, float b, float c, floa
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
 }
 
-// Work unit u -> (tile, split, k-block range). Units [0, split_tiles*ksplit) are
-// the K-splits of the split tiles (split-major); the rest are whole tiles. Split
-// tiles go first so their fixup overlaps the whole tiles that follow.
+// Work unit u -> (tile, split, k-block range). Default (split_t0 = W = num_tiles -
+// split_tiles): units [0, W) are the whole tiles in raster order, then the K-splits of
+// the last split_tiles tiles (split-major). Every pair then runs whole tiles in lockstep
+// waves — the tiles of one wave stream the same A / B panel k-blocks at nearly the same
+// time, so L2 serves the re-reads (syr2k 8192: 8.3 GB of DRAM reads per launch instead of
+// 15.7 GB with split units first, whose 1/S-long units shift the waves against each other;
+// DESIGN.md §8) — and the split units fill the last partial wave. split_t0 = 0
+// (PB_SPLIT_FIRST=1, and every EPI_PARTIAL plan) puts the split units first instead.
 struct Unit {
   long long t;
   int ks, kbA, kbB;
@@ -295,25 +301,28 @@ struct Unit {
 __device__ __forceinline__ Unit unit_of(const Params& p, long long u, int nkb_total) {
   Unit r;
   const long long rs = p.split_tiles * p.ksplit;
-  if (u < rs) {
-    r.t = u % p.split_tiles;
-    r.ks = (int)(u / p.split_tiles);
+  const long long whole = p.num_tiles - p.split_tiles;
+  const long long v = p.split_t0 == 0 ? u : u - whole;  // index among the split units (if >= 0)
+  if (v >= 0 && v < rs) {
+    r.t = p.split_t0 + v % p.split_tiles;
+    r.ks = (int)(v / p.split_tiles);
     r.split = true;
+    r.slot = v;
   } else {
-    r.t = p.split_tiles + (u - rs);
+    r.t = p.split_t0 == 0 ? p.split_tiles + (u - rs) : u;
     r.ks = 0;
     r.split = false;
+    r.slot = u;
   }
   const int S = r.split ? p.ksplit : 1;
   r.kbA = (int)((long long)nkb_total * r.ks / S);
   r.kbB = (int)((long long)nkb_total * (r.ks + 1) / S);
   r.nseg = S;
-  r.slot = u;
   return r;
 }
 // partial slot of segment k2 of (split) tile t
 __device__ __forceinline__ long long slot_of(const Params& p, long long t, int k2) {
-  return p.streamk ? t * p.sk_maxseg + k2 : k2 * p.split_tiles + t;
+  return p.streamk ? t * p.sk_maxseg + k2 : k2 * p.split_tiles + (t - p.split_t0);
 }
 
 // The units one CTA group works through, in order: round robin over [0, units) (every
@@ -700,7 +709,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"r"(C::EPI_WARPS * 32) : "memory");
         if (warp == 2 && lane == 0) {
-          unsigned* cnt = p.counters + t * CG + rank;
+          unsigned* cnt = p.counters + (t - p.split_t0) * CG + rank;
           const unsigned prev = atomicAdd(cnt, 1u);
           const uint32_t last = prev == (unsigned)(un.nseg - 1);
           if (last) atomicExch(cnt, 0u);
@@ -929,6 +938,8 @@ bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles,
   p.num_tiles = nt;
   p.ksplit = ksplit;
   p.split_tiles = (ksplit > 1 || (d.flags & EPI_PARTIAL)) ? split_tiles : 0;
+  static const bool split_first = getenv("PB_SPLIT_FIRST") && atoi(getenv("PB_SPLIT_FIRST")) != 0;
+  p.split_t0 = (split_first || (d.flags & EPI_PARTIAL)) ? 0 : nt - p.split_tiles;
   static const int dbg = getenv("PB_UMMA_DEBUG") ? atoi(getenv("PB_UMMA_DEBUG")) : 0;
   p.dbg = dbg;
   static const bool timing = getenv("PB_UMMA_TIMING") != nullptr;
@@ -947,6 +958,7 @@ bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles,
     p.sk_iters = nt * (long long)(p.nkb * p.npairs);
     p.sk_maxseg = skp->maxseg;
     p.split_tiles = nt;  // every tile may be split (its segment count decides)
+    p.split_t0 = 0;
   }
   return true;
 }

@@ -8,8 +8,9 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
-h = rows[1]
-data = rows[2:]
+hi = next(i for i, r in enumerate(rows) if "Warp Stall Sampling (All Samples)" in r)
+h = rows[hi]
+data = [r for r in rows[hi + 1:] if len(r) == len(h)]
 i_s = h.index("Warp Stall Sampling (All Samples)")
 tot = sum(float(r[i_s] or 0) for r in data) or 1.0
 stall_cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]

@@ -9,11 +9,7 @@ tail -3 gpurun_out/${T}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo smoke rc=$?; tail -2 gpurun_out/${T}_smoke.log
 timeout 900 python bench.py > gpurun_out/${T}_bench_default.json 2> gpurun_out/${T}_bench.err; echo bench rc=$?
 tail -c 2500 gpurun_out/${T}_bench_default.json
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tests/perf/sanitize_r2.py > gpurun_out/${T}_sanitizer_${tool}.log 2>&1
-  PB_CHAIN=1 PB_STREAMK=1 timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tests/perf/sanitize_r2.py > gpurun_out/${T}_sanitizer_${tool}_opt.log 2>&1
-  tail -2 gpurun_out/${T}_sanitizer_${tool}.log; tail -2 gpurun_out/${T}_sanitizer_${tool}_opt.log
-done
+# compute-sanitizer is closed on this GPU pool (round 2): no sanitizer runs here
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-next > /dev/null 2>&1; echo launches rc=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gram_fused -s 2 -c 1 -o gpurun_out/${T}_cov_gram -f python scripts/gram_timing.py > /dev/null 2>&1; echo ncu gram rc=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:atax_tm -s 1 -c 1 -o gpurun_out/${T}_atax -f python scripts/time_calls.py atax 32768 2 > /dev/null 2>&1; echo ncu atax rc=$?
