@@ -126,7 +126,7 @@ __device__ unsigned long long g_tl[4];   // [umma entry, exit, combine entry, ex
 
 constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;
-constexpr int GROUP_M = 8;  // tile-rows per raster group (L2 reuse)
+constexpr int GROUP_M = 8;  // tile-rows per raster group (L2 reuse); PB_GROUP_M overrides (tuning)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int A_TILE = BM * BK * 4;  // 16 KiB
 constexpr int EPI_COLS = 128;        // accumulator columns (fp32 registers) per epilogue thread
@@ -166,6 +166,7 @@ struct Params {
   long long num_tiles;
   int ksplit;                    // K splits of each split tile (split-K)
   long long split_tiles;         // split tiles: [split_t0, split_t0 + split_tiles)
+  int group_m;                   // tile-rows per raster group (GROUP_M)
   long long split_t0;            // 0: split tiles first (their units lead); num_tiles - split_tiles: last
   float* part;                   // split-K partial tiles [unit][CG][128][BN]
   unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
@@ -259,7 +260,7 @@ __device__ __forceinline__ int row_tiles(const Params& p, int tm) {
 __device__ void tile_coords(const Params& p, long long t, int& tm, int& tn) {
   int g0 = p.tm0;
   for (;;) {
-    const int g1 = min(g0 + GROUP_M, p.tm1);
+    const int g1 = min(g0 + p.group_m, p.tm1);
     long long cnt = 0;
     for (int r = g0; r < g1; ++r) cnt += row_tiles(p, r);
     if (t < cnt || g1 >= p.tm1) {
@@ -940,6 +941,8 @@ bool prep_phase(const GemmDesc& d, Params& p, int ksplit, long long split_tiles,
   p.split_tiles = (ksplit > 1 || (d.flags & EPI_PARTIAL)) ? split_tiles : 0;
   static const bool split_first = getenv("PB_SPLIT_FIRST") && atoi(getenv("PB_SPLIT_FIRST")) != 0;
   p.split_t0 = (split_first || (d.flags & EPI_PARTIAL)) ? 0 : nt - p.split_tiles;
+  static const int gm = getenv("PB_GROUP_M") ? atoi(getenv("PB_GROUP_M")) : 0;
+  p.group_m = gm > 0 ? gm : GROUP_M;
   static const int dbg = getenv("PB_UMMA_DEBUG") ? atoi(getenv("PB_UMMA_DEBUG")) : 0;
   p.dbg = dbg;
   static const bool timing = getenv("PB_UMMA_TIMING") != nullptr;
@@ -1489,7 +1492,8 @@ UmmaPlan plan_cfg(const GemmDesc& d, int cfg, int force_ks) {
   // R = T mod units remainder tiles are split S ways (S <= units / R, <= 4, and
   // >= 8 k-blocks per split) so the last partial wave is ~full of 1/S-size units.
   long long R = nt < units ? nt : nt % units;
-  int S = R > 0 ? (int)std::min<long long>(4, units / R) : 1;
+  static const int smax = getenv("PB_KSPLIT_MAX") ? std::max(1, atoi(getenv("PB_KSPLIT_MAX"))) : 4;
+  int S = R > 0 ? (int)std::min<long long>(smax, units / R) : 1;
   while (S > 1 && nkb_total / S < 8) --S;
   if (force_ks >= 1 && force_ks <= 8 && nkb_total / force_ks >= 1) { S = force_ks; R = nt; }
   if (S <= 1) { S = 1; R = 0; }

@@ -847,9 +847,13 @@ pb_status pb_row_partition(int rows, int nranks, int rank, int triangular, int a
     // syrk/syr2k cost balance: rank g's cost = lower-triangle area of its rows
     // (r1^2 - r0^2)/2 + RHO * r1, the second term being the split of A[0:r1] (and
     // B) it needs. Measured on B200: 60.6 ps per triangle element (K = 8192) and
-    // 16.2 ns per split row -> RHO = 267 (both scale with K: independent of m).
+    // 16.2 ns per split row -> RHO = 267 (both scale with K: independent of m); with the
+    // lo-only split (~10 ns per row) the per-rank proxy (scripts/rank_shapes.py --only-syrk,
+    // PB_RHO sweep 120 / 165 / 210 / 267) is best at RHO = 210: G = 4 syrk 591 vs 660 us,
+    // G = 8 equal (424 us).
     // Equal cost C per rank: r1 = sqrt(r0^2 + 2 (C - RHO r1)) solved by bisection on C.
-    const double RHO = 267.0, n = rows;
+    static const double rho_env = getenv("PB_RHO") ? atof(getenv("PB_RHO")) : 0.0;  // tuning only
+    const double RHO = rho_env > 0.0 ? rho_env : 210.0, n = rows;
     auto last_bound = [&](double C, std::vector<double>* b) {
       double r0 = 0.0;
       if (b) b->assign(1, 0.0);

@@ -48,6 +48,9 @@ def timed(fn, reps=10):
 
 
 def main():
+    only_syrk = "--only-syrk" in sys.argv  # partition tuning: syrk / syr2k rows only
+    if only_syrk:
+        sys.argv.remove("--only-syrk")
     out = {}
     Amm, Bmm, Cmm, Dmm = g(MM, MM, 1), g(MM, MM, 2), g(MM, MM, 3), g(MM, MM, 4)
     Asy, Bsy = g(SY, SY, 1), g(SY, SY, 2)
@@ -57,6 +60,25 @@ def main():
     data = g(ST, ST, 5)
     for G in (1, 2, 4, 8):
         res = {}
+        if only_syrk:
+            for k in ("syrk", "syr2k"):
+                worst = 0.0
+                for gr in range(G):
+                    b, e = pb.pb_row_partition(SY, G, gr, 2, 256)
+                    if e <= b:
+                        continue
+                    Cb = torch.empty(e - b, SY, device=dev)
+                    wsy = pb.workspace(k + "_rows", (SY, SY, b, e), dev)
+                    if k == "syrk":
+                        f = lambda: pb.pb_syrk_rows(SY, SY, b, e, 1.5, 1.2, Cb, Asy, ws=wsy)  # noqa: E731
+                    else:
+                        f = lambda: pb.pb_syr2k_rows(SY, SY, b, e, 1.5, 1.2, Cb, Asy, Bsy, ws=wsy)  # noqa: E731
+                    worst = max(worst, timed(f, 5))
+                    del Cb
+                res[k] = worst
+            out[G] = {k: round(v * 1e3, 1) for k, v in res.items()}
+            print(G, out[G], flush=True)
+            continue
         # covariance / correlation: G = 1 is the single-GPU call (banded, triangle + mirror);
         # G > 1 a rank's row band of the replicated-data path (pb_<k>_rows)
         cov, mean, sd = torch.empty(ST, ST, device=dev), torch.empty(ST, device=dev), torch.empty(ST, device=dev)

@@ -124,12 +124,12 @@ def test_dist_workspace_sizes_cpu():
 
 def test_row_partition_syrk_cost_balance():
     """triangular = 2 (syrk/syr2k): blocks tile [0, n) in order, aligned, and the
-    max per-rank cost (triangle area + 267 * end, the split of A[0:end]) is lower
+    max per-rank cost (triangle area + 210 * end, the split of A[0:end]) is lower
     than with the pure area balance (triangular = 1)."""
     import paper_2312_13170_b200 as pb
 
     def cost(b, e):
-        return (e * e - b * b) / 2 + 267.0 * e
+        return (e * e - b * b) / 2 + 210.0 * e
     for n in (8192, 4096):
         for G in (2, 4, 8):
             worst = {}
