@@ -7,7 +7,7 @@ PKG       := paper_2312_13170_b200
 CSRC      := $(PKG)/csrc
 KSRC      := $(CSRC)/pb_api.cu $(CSRC)/k_umma.cu $(CSRC)/k_split.cu $(CSRC)/k_stats.cu \
              $(CSRC)/k_matvec.cu $(CSRC)/k_simt.cu $(CSRC)/pb_dist.cu $(CSRC)/k_peer.cu \
-             $(CSRC)/k_stencil.cu $(CSRC)/k_gramschmidt.cu $(CSRC)/k_gram.cu
+             $(CSRC)/k_stencil.cu $(CSRC)/k_gramschmidt.cu $(CSRC)/k_gram.cu $(CSRC)/k_covdist.cu
 KOBJ      := $(patsubst $(CSRC)/%.cu,build/%.o,$(KSRC))
 HDRS      := include/pb.h $(CSRC)/pb_internal.h $(CSRC)/pb_check.h $(CSRC)/pb_device.cuh $(CSRC)/pb_band_prep.cuh $(CSRC)/pb_umma.cuh
 

@@ -145,13 +145,22 @@ class Suite:
             n = GEMM_N
             t["gemm"] = dict(A=gen(n, n, S["A"]), B=gen(n, n, S["B"]), C=gen(n, n, S["C"]))
         if "covariance" in kernels or "correlation" in kernels:
-            # one GPU: the whole matrix (banded single-pass path); N > 1: the data
-            # replicated, each rank computes its output row band (no exchange)
+            # one GPU: the whole matrix (fused single-launch path); N > 1 with a libpb comm:
+            # the observations split (rank g holds data rows block(n, G, g, 0, 32) and returns
+            # output rows block(m, G, g, 0, 32); column-sum allreduce + partial-Gram
+            # reduce-scatter inside pb_<k>_dist); without one: the data replicated and each rank
+            # computes its output row band (pb_<k>_rows, no exchange)
             n = STAT_N
-            r0, r1 = pb.pb_row_partition(n, world, rank, False, 128) if world > 1 else (0, n)
+            self.stat_obs = D.comm() is not None and (world > 1 or bool(os.environ.get("PB_FORCE_DIST")))
+            if self.stat_obs:
+                o0, o1 = pb.pb_row_partition(n, world, rank, False, 32)
+                r0, r1 = pb.pb_row_partition(n, world, rank, False, 32)
+                data = gen(max(o1 - o0, 1), n, S["data"], row0=o0, ld=n)
+            else:
+                r0, r1 = pb.pb_row_partition(n, world, rank, False, 128) if world > 1 else (0, n)
+                data = gen(n, n, S["data"])
             self.stat_rows = (r0, r1)
-            t["stat"] = dict(data=gen(n, n, S["data"]), cov=e(max(r1 - r0, 1), n), corr=e(max(r1 - r0, 1), n),
-                             mean=e(n), sd=e(n))
+            t["stat"] = dict(data=data, cov=e(max(r1 - r0, 1), n), corr=e(max(r1 - r0, 1), n), mean=e(n), sd=e(n))
         if "2mm" in kernels or "3mm" in kernels:
             n = MM_N
             r0, r1 = pb.pb_row_partition(n, world, rank, False, 128)
@@ -201,6 +210,7 @@ class Suite:
             G = (self.world, self.rank)
             out += [("2mm_dist", (MM_N,) * 4 + G), ("3mm_dist", (MM_N,) * 5 + G), ("syr2k_dist", (SY_N, SY_N) + G),
                     ("atax_dist", (MV_N, MV_N) + G), ("bicg_dist", (MV_N, MV_N) + G), ("mvt_dist", (MV_N,) + G),
+                    ("covariance_dist", (STAT_N, STAT_N) + G), ("correlation_dist", (STAT_N, STAT_N) + G),
                     ("gesummv_dist", (MV_N,) + G)]
         return out
 
@@ -215,6 +225,9 @@ class Suite:
         elif k in ("covariance", "correlation"):
             s = t["stat"]
             r0, r1 = self.stat_rows
+            if self.stat_obs:
+                return D.stat_obs(self, k, STAT_N, STAT_N, float(STAT_N), EPS, s["data"], s["cov" if k == "covariance" else "corr"],
+                                  s["mean"], s["sd"], ws)
             if self.world == 1:
                 if k == "covariance":
                     pb.pb_covariance(STAT_N, STAT_N, float(STAT_N), s["data"], s["cov"], s["mean"], ws=ws)
@@ -512,9 +525,10 @@ def run_ours(args):
 def sharded_check(suite, kernels, dev):
     """N > 1: one post-timing check that the sharded path (row blocks + the exchange
     steps) reproduces the single-GPU libpb result, which the parity tests pin to the
-    oracle: atax's y (reduce-scatter of the transposed-product partials) and 3mm's G
-    (all-gather of F) are gathered on rank 0 and compared with rank 0's single-GPU
-    call on the full inputs. Not timed."""
+    oracle: atax's y (reduce-scatter of the transposed-product partials), 3mm's G
+    (all-gather of F) and the observations-split covariance (column-sum allreduce +
+    partial-Gram reduce-scatter) are gathered on rank 0 and compared with rank 0's
+    single-GPU call on the full inputs. Not timed."""
     import torch
     import torch.distributed as dist
 
@@ -563,6 +577,20 @@ def sharded_check(suite, kernels, dev):
             err = float(((G - Gr).abs() / Gr.abs().clamp_min(1e-30)).max())
             out["3mm_G_max_rel"] = err
             out["ok"] &= err <= 1e-4
+    if "covariance" in kernels and getattr(suite, "stat_obs", False):
+        # observations split: the reduce-scattered row bands against rank 0's single-GPU call
+        # (centred outputs have near-zero entries: normwise, max |diff| / max |cov|)
+        n = STAT_N
+        bounds = [pb.pb_row_partition(n, world, g, False, 32) for g in range(world)]
+        r0, r1 = bounds[rank]
+        cov = gather(suite.t["stat"]["cov"][: r1 - r0], n, bounds)
+        if rank == 0:
+            data = suite.gen(n, n, S["data"])
+            cr = torch.empty(n, n, device=dev)
+            pb.pb_covariance(n, n, float(n), data, cr, None)
+            err = float((cov - cr).abs().max() / cr.abs().max())
+            out["cov_max_abs_over_max"] = err
+            out["ok"] &= err <= 1e-5
     torch.cuda.synchronize(dev)
     flag = torch.tensor([1 if out["ok"] else 0], dtype=torch.int64,
                         device=dev if dist.get_backend() == "nccl" else "cpu")

@@ -323,6 +323,28 @@ pb_status pb_gesummv_dist(pb_comm* comm, int n, float alpha, float beta, const f
                           const float* B_blk, float* tmp_blk, const float* x, float* y_blk, void* ws,
                           size_t ws_bytes, pb_stream s);
 
+/* Covariance / correlation with the OBSERVATIONS split over ranks (SURVEY.md §8(e) /
+ * S17; BASELINE north_star: "an allreduce of column sums for covariance/correlation";
+ * definitions as pb_covariance / pb_correlation, PolyBench/C 4.2, readings R4-R6, R17).
+ * data_blk = this rank's observations: rows block(n, nranks, rank, tri 0, align 32) of
+ * data (n x m), i.e. (o1 - o0) x m. Steps: fp64 column sums S1, S2 of the block ->
+ * all-gather of every rank's sums, added in rank order on every rank (the allreduce; all
+ * ranks hold the same bits) -> mean = S1 / float_n, stddev from (S2 - 2 mean S1 + n mean^2)
+ * / float_n with the eps rule -> the centred (correlation: normalised) block, transposed ->
+ * its partial Gram on tcgen05 (pb_syrk_full, 3xTF32, full square) -> reduce-scatter of the
+ * m x m sum into row bands -> 1/(float_n - 1) (covariance) or diagonal := 1 (correlation).
+ * cov_blk / corr_blk: rows block(m, nranks, rank, tri 0, align 32) of the result (r1 - r0
+ * rows of m floats). mean / stddev: optional, FULL m vectors, written on every rank.
+ * The two triangles of the result are computed by different tiles and summed over ranks:
+ * symmetric to rounding, not bitwise (the single-GPU call mirrors, bitwise).
+ * Errors as pb_covariance; m % 4 == 0; workspace "covariance_dist" / "correlation_dist"
+ * {m, n, nranks, rank}. */
+pb_status pb_covariance_dist(pb_comm* comm, int m, int n, float float_n, const float* data_blk,
+                             float* cov_blk, float* mean, void* ws, size_t ws_bytes, pb_stream s);
+pb_status pb_correlation_dist(pb_comm* comm, int m, int n, float float_n, float eps,
+                              const float* data_blk, float* corr_blk, float* mean, float* stddev,
+                              void* ws, size_t ws_bytes, pb_stream s);
+
 /* ------------------------------------------------------------------------
  * Paper ablation: the GEMM of PAPER.md Listing 8
  * (variant 0: one thread per C[i][j], k-loop over global memory, C updated in

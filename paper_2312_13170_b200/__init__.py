@@ -24,7 +24,7 @@ __all__ = [
     "pb_atax_dist", "pb_bicg_dist", "pb_mvt_dist", "pb_gesummv_dist", "Peer", "pb_peer_create",
     "pb_comm_init_local", "pb_comm_attach_peer", "pb_conv2d", "pb_conv3d", "pb_fdtd_2d",
     "pb_gramschmidt", "pb_covariance_rows", "pb_correlation_rows", "pb_conv2d_variant", "pb_conv3d_variant",
-    "pb_gramschmidt_variant",
+    "pb_gramschmidt_variant", "pb_covariance_dist", "pb_correlation_dist",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -85,6 +85,8 @@ ABI_FUNCTIONS = {
     "pb_bicg_dist": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_mvt_dist": ([_P, _I, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
     "pb_gesummv_dist": ([_P, _I, _F, _F, _P, _P, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_covariance_dist": ([_P, _I, _I, _F, _P, _P, _P, _P, _Z, _P], _I),
+    "pb_correlation_dist": ([_P, _I, _I, _F, _F, _P, _P, _P, _P, _P, _Z, _P], _I),
     # peer-memory collectives (CUDA IPC symmetric buffers)
     "pb_peer_create": ([_I, _I, _Z, ctypes.POINTER(_P), _P], _I),
     "pb_peer_open": ([_P, _P], _I),
@@ -427,6 +429,21 @@ def pb_3mm_dist(comm, ni, nj, nk, nl, nm, E_blk, A_blk, B, F, C_blk, D, G_blk, w
     p, n, keep = _dws(ws, "3mm", (ni, nj, nk, nl, nm), comm, F, stream=stream)
     _check("pb_3mm_dist", lib().pb_3mm_dist(comm.handle, ni, nj, nk, nl, nm, _ptr(E_blk, None, "E_blk"), _ptr(A_blk, None, "A_blk"), _ptr(B, None, "B"),
                                             _ptr(F, None, "F"), _ptr(C_blk, None, "C_blk"), _ptr(D, None, "D"), _ptr(G_blk, None, "G_blk"), p, n, _stream(stream, F)))
+
+
+def pb_covariance_dist(comm, m, n_, float_n, data_blk, cov_blk, mean=None, ws=None, stream=None):
+    p, n, keep = _dws(ws, "covariance", (m, n_), comm, data_blk, cov_blk, mean, stream=stream)
+    _check("pb_covariance_dist", lib().pb_covariance_dist(comm.handle, m, n_, float_n, _ptr(data_blk, None, "data_blk"),
+                                                          _ptr(cov_blk, None, "cov_blk"), _ptr(mean, m, "mean"), p, n,
+                                                          _stream(stream, _first(data_blk, cov_blk, mean))))
+
+
+def pb_correlation_dist(comm, m, n_, float_n, eps, data_blk, corr_blk, mean=None, stddev=None, ws=None, stream=None):
+    p, n, keep = _dws(ws, "correlation", (m, n_), comm, data_blk, corr_blk, mean, stream=stream)
+    _check("pb_correlation_dist", lib().pb_correlation_dist(comm.handle, m, n_, float_n, eps, _ptr(data_blk, None, "data_blk"),
+                                                            _ptr(corr_blk, None, "corr_blk"), _ptr(mean, m, "mean"),
+                                                            _ptr(stddev, m, "stddev"), p, n,
+                                                            _stream(stream, _first(data_blk, corr_blk, mean))))
 
 
 def pb_syrk_dist(comm, n_, m, alpha, beta, C_blk, A, ws=None, stream=None):

@@ -103,6 +103,8 @@ inline cudaStream_t S(pb_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Partition conventions (include/pb.h).
 constexpr int ALIGN_MM = 128, ALIGN_SY = 256, ALIGN_MV = 4;
+// covariance / correlation with the observations split: observation blocks and output row bands
+constexpr int ALIGN_OBS = 32, ALIGN_ST = 32;
 
 struct Blk {
   int b = 0, e = 0;
@@ -148,6 +150,43 @@ DistWs dist_ws(void* ws, size_t ws_bytes, long long partial_len, long long base_
   return w;
 }
 
+// Workspace of pb_covariance_dist / pb_correlation_dist (m variables, n observations):
+// every rank's column sums [G][2][m] doubles (the all-gather buffer), the centred
+// transpose Yt (m x ldy, ldy = this rank's observations rounded up to 4), the partial
+// Gram P (m x m), then pb_syrk_full's own workspace.
+struct CovDistWs {
+  double* sums = nullptr;
+  float* Yt = nullptr;
+  float* P = nullptr;
+  void* gemm = nullptr;
+  size_t gemm_bytes = 0, total = 0;
+  int ldy = 0;
+  static CovDistWs carve(void* ws, long long m, long long n, int G, int g) {
+    CovDistWs w;
+    const Blk o = block((int)n, G, g, 0, ALIGN_OBS);
+    w.ldy = (o.n() + 3) / 4 * 4;
+    char* base = static_cast<char*>(ws);
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char* {
+      off = align_up(off, 256);
+      char* r = base ? base + off : nullptr;
+      off += bytes;
+      return r;
+    };
+    w.sums = reinterpret_cast<double*>(take((size_t)G * 2 * m * sizeof(double)));
+    if (w.ldy) {
+      w.Yt = reinterpret_cast<float*>(take((size_t)m * w.ldy * sizeof(float)));
+      w.P = reinterpret_cast<float*>(take((size_t)m * m * sizeof(float)));
+      w.gemm_bytes = ws_of("syrk_full", {m, w.ldy});
+      w.gemm = take(w.gemm_bytes);
+    } else {
+      w.P = reinterpret_cast<float*>(take((size_t)m * m * sizeof(float)));
+    }
+    w.total = align_up(off, 256);
+    return w;
+  }
+};
+
 size_t local_need(const std::string& k, const long long* d, int G, int g) {
   if (k == "gemm") {
     const Blk r = block(d[0], G, g, 0, ALIGN_MM);
@@ -184,6 +223,7 @@ size_t local_need(const std::string& k, const long long* d, int G, int g) {
     const Blk r = block(d[0], G, g, 0, ALIGN_MV);
     return r.n() ? ws_of("gesummv_rows", {r.n(), d[0]}) : 0;
   }
+  if (k == "covariance" || k == "correlation") return CovDistWs::carve(nullptr, d[0], d[1], G, g).total;
   return 0;
 }
 
@@ -196,29 +236,31 @@ pb_status peer_ready(const pb_peer* p) {
   return PB_OK;
 }
 
-pb_status peer_rs(pb_peer* P, const float* partial, float* dst, int total, int align, cudaStream_t s) {
+// dst (this rank's block) <- sum over ranks of partial. The blocks are row blocks
+// (partition tri 0 / align over `rows`) of a rows x cols array; vectors use cols = 1.
+pb_status peer_rs(pb_peer* P, const float* partial, float* dst, int rows, int cols, int align, cudaStream_t s) {
   PB_TRY(peer_ready(P));
   long long slot = 0;
   PeerPush push;
   Blk me;
   for (int g = 0; g < P->nranks; ++g) {
-    const Blk k = block(total, P->nranks, g, 0, align);
+    const Blk k = block(rows, P->nranks, g, 0, align);
     if (g == P->rank) me = k;
-    slot = std::max<long long>(slot, k.n());
+    slot = std::max<long long>(slot, (long long)k.n() * cols);
   }
   slot = (slot + 3) / 4 * 4;
   if ((size_t)slot * P->nranks * sizeof(float) > P->data_bytes)
     return fail(PB_ERR_WORKSPACE, "peer data region (%zu bytes) < %lld slots of %lld floats", P->data_bytes,
                 (long long)P->nranks, slot);
   for (int g = 0; g < P->nranks; ++g) {
-    const Blk k = block(total, P->nranks, g, 0, align);
-    push.src[g] = partial + k.b;
+    const Blk k = block(rows, P->nranks, g, 0, align);
+    push.src[g] = partial + (long long)k.b * cols;
     push.dst_off[g] = (long long)P->rank * slot;
-    push.count[g] = k.n();
+    push.count[g] = (long long)k.n() * cols;
   }
   PeerConsume con;
   con.out = dst;
-  con.count = me.n();
+  con.count = (long long)me.n() * cols;
   con.slot = slot;
   con.reduce = 1;
   PB_CU(launch_peer_push(P->view, push, s));
@@ -247,25 +289,27 @@ pb_status peer_ag(pb_peer* P, const float* send_blk, float* recv, int rows, int 
   return PB_OK;
 }
 
-// dst (this rank's block of a length-`total` vector, partition tri 0 / align 4)
-//   <- sum over ranks of partial[0, total)
-pb_status reduce_scatter(pb_comm* c, const float* partial, float* dst, int total, cudaStream_t s) {
-  if (c->peer) return peer_rs(c->peer, partial, dst, total, ALIGN_MV, s);
+// dst (this rank's row block, partition tri 0 / `align` over rows, of a rows x cols array)
+//   <- sum over ranks of partial[0, rows x cols). Vectors: cols = 1, align 4.
+pb_status reduce_scatter_rows(pb_comm* c, const float* partial, float* dst, int rows, int cols, int align,
+                              cudaStream_t s) {
+  if (c->peer) return peer_rs(c->peer, partial, dst, rows, cols, align, s);
   const Nccl& N = nccl();
   bool equal = true;
-  const Blk me = block(total, c->nranks, c->rank, 0, ALIGN_MV);
+  const Blk me = block(rows, c->nranks, c->rank, 0, align);
   for (int g = 0; g < c->nranks; ++g)
-    if (block(total, c->nranks, g, 0, ALIGN_MV).n() != me.n()) equal = false;
-  if (equal && (long long)me.n() * c->nranks == total) {
-    PB_NC(N.ReduceScatter(partial, dst, (size_t)me.n(), ncclFloat32, ncclSum, c->nc, s));
+    if (block(rows, c->nranks, g, 0, align).n() != me.n()) equal = false;
+  if (equal && (long long)me.n() * c->nranks == rows) {
+    PB_NC(N.ReduceScatter(partial, dst, (size_t)me.n() * cols, ncclFloat32, ncclSum, c->nc, s));
     return PB_OK;
   }
   PB_NC(N.GroupStart());  // uneven blocks: one reduce per root
   for (int g = 0; g < c->nranks; ++g) {
-    const Blk k = block(total, c->nranks, g, 0, ALIGN_MV);
+    const Blk k = block(rows, c->nranks, g, 0, align);
     if (!k.n()) continue;
-    float* recv = g == c->rank ? dst : const_cast<float*>(partial + k.b);  // only the root's is written
-    const ncclResult_t r = N.Reduce(partial + k.b, recv, (size_t)k.n(), ncclFloat32, ncclSum, g, c->nc, s);
+    const float* src = partial + (long long)k.b * cols;
+    float* recv = g == c->rank ? dst : const_cast<float*>(src);  // only the root's is written
+    const ncclResult_t r = N.Reduce(src, recv, (size_t)k.n() * cols, ncclFloat32, ncclSum, g, c->nc, s);
     if (r != ncclSuccess) {
       N.GroupEnd();
       return nc_check(r, "ncclReduce");
@@ -274,18 +318,21 @@ pb_status reduce_scatter(pb_comm* c, const float* partial, float* dst, int total
   PB_NC(N.GroupEnd());
   return PB_OK;
 }
+pb_status reduce_scatter(pb_comm* c, const float* partial, float* dst, int total, cudaStream_t s) {
+  return reduce_scatter_rows(c, partial, dst, total, 1, ALIGN_MV, s);
+}
 
 // Every rank's rows of F (rows x cols, partition tri 0 / align 128) -> the full F, in place.
-pb_status all_gather_rows(pb_comm* c, float* F, int rows, int cols, cudaStream_t s) {
+pb_status all_gather_rows(pb_comm* c, float* F, int rows, int cols, cudaStream_t s, int align = ALIGN_MM) {
   if (c->peer) {
-    const Blk me = block(rows, c->nranks, c->rank, 0, ALIGN_MM);
-    return peer_ag(c->peer, F + (size_t)me.b * cols, F, rows, cols, ALIGN_MM, s);
+    const Blk me = block(rows, c->nranks, c->rank, 0, align);
+    return peer_ag(c->peer, F + (size_t)me.b * cols, F, rows, cols, align, s);
   }
   const Nccl& N = nccl();
   bool equal = true;
-  const Blk me = block(rows, c->nranks, c->rank, 0, ALIGN_MM);
+  const Blk me = block(rows, c->nranks, c->rank, 0, align);
   for (int g = 0; g < c->nranks; ++g)
-    if (block(rows, c->nranks, g, 0, ALIGN_MM).n() != me.n()) equal = false;
+    if (block(rows, c->nranks, g, 0, align).n() != me.n()) equal = false;
   if (equal && (long long)me.n() * c->nranks == rows) {  // in place: send = recv + rank * count
     const size_t cnt = (size_t)me.n() * cols;
     PB_NC(N.AllGather(F + (size_t)me.b * cols, F, cnt, ncclFloat32, c->nc, s));
@@ -293,7 +340,7 @@ pb_status all_gather_rows(pb_comm* c, float* F, int rows, int cols, cudaStream_t
   }
   PB_NC(N.GroupStart());  // uneven blocks: one broadcast per owner
   for (int g = 0; g < c->nranks; ++g) {
-    const Blk k = block(rows, c->nranks, g, 0, ALIGN_MM);
+    const Blk k = block(rows, c->nranks, g, 0, align);
     if (!k.n()) continue;
     float* p = F + (size_t)k.b * cols;
     const ncclResult_t r = N.Broadcast(p, p, (size_t)k.n() * cols, ncclFloat32, g, c->nc, s);
@@ -321,7 +368,8 @@ namespace pb {
 pb_status dist_workspace_size(const std::string& name, const long long* d, int nd, size_t* bytes) {
   const std::string k = name.substr(0, name.size() - 5);
   const int nk = k == "gemm" ? 3 : k == "2mm" ? 4 : k == "3mm" ? 5 : (k == "syrk" || k == "syr2k") ? 2
-               : (k == "atax" || k == "bicg") ? 2 : (k == "mvt" || k == "gesummv") ? 1 : -1;
+               : (k == "atax" || k == "bicg") ? 2 : (k == "mvt" || k == "gesummv") ? 1
+               : (k == "covariance" || k == "correlation") ? 2 : -1;
   if (nk < 0 || nd != nk + 2) return fail(PB_ERR_INVALID_ARG, "unknown kernel '%s' or wrong dims (%d)", name.c_str(), nd);
   for (int i = 0; i < nk; ++i)
     if (d[i] <= 0 || d[i] > (1ll << 30)) return fail(PB_ERR_INVALID_ARG, "dimension %d is %lld", i, d[i]);
@@ -486,7 +534,7 @@ pb_status pb_peer_status(const pb_peer* p, unsigned* status) {
 pb_status pb_peer_reduce_scatter(pb_peer* p, const float* partial, float* out_blk, int total, pb_stream s) {
   if (total <= 0 || total % 4) return fail(PB_ERR_UNSUPPORTED, "total %d must be a positive multiple of 4", total);
   set_launches(2);
-  return peer_rs(p, partial, out_blk, total, ALIGN_MV, S(s));
+  return peer_rs(p, partial, out_blk, total, 1, ALIGN_MV, S(s));
 }
 
 pb_status pb_peer_all_gather(pb_peer* p, const float* send_blk, float* recv, int rows, int cols, pb_stream s) {
@@ -669,4 +717,81 @@ pb_status pb_mvt_dist(pb_comm* c, int n, float* x1_blk, float* x2_blk, const flo
   return PB_OK;
 }
 
+// ---- covariance / correlation: observations split (k_covdist.cu)
+// Rank g holds observations o = block(n, G, g, 0, 32) of data; it returns rows
+// block(m, G, g, 0, 32) of the m x m result, plus the full mean (and stddev) vectors.
+static pb_status covcorr_dist(bool corr, pb_comm* c, int m, int n, float float_n, float eps, const float* data_blk,
+                              float* out_blk, float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s) {
+  PB_TRY(comm_ok(c));
+  Check ck;
+  ck.dims({m, n});
+  if (ck.st == PB_OK && !corr && n < 2) ck.st = fail(PB_ERR_INVALID_ARG, "covariance needs n >= 2");
+  if (ck.st == PB_OK && !(float_n > 0.f)) ck.st = fail(PB_ERR_INVALID_ARG, "float_n must be > 0");
+  if (ck.st == PB_OK && !corr && float_n == 1.0f) ck.st = fail(PB_ERR_INVALID_ARG, "float_n - 1 == 0");
+  ck.cols4(m, "data/out");
+  const Blk o = block(n > 0 ? n : 1, c->nranks, c->rank, 0, ALIGN_OBS);
+  const Blk r = block(m > 0 ? m : 1, c->nranks, c->rank, 0, ALIGN_ST);
+  ck.arr(data_blk, o.n(), m, false, "data_blk", o.n() > 0);
+  ck.arr(out_blk, r.n(), m, true, corr ? "corr_blk" : "cov_blk", r.n() > 0);
+  ck.arr(mean, 1, m, true, "mean", false);
+  if (corr) ck.arr(stddev, 1, m, true, "stddev", false);
+  PB_TRY(ck.finish());
+  const CovDistWs need = CovDistWs::carve(nullptr, m, n, c->nranks, c->rank);
+  if (!ws) return fail(PB_ERR_WORKSPACE, "workspace is NULL (need %zu bytes)", need.total);
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(PB_ERR_WORKSPACE, "workspace not 256-byte aligned");
+  if (ws_bytes < need.total) return fail(PB_ERR_WORKSPACE, "workspace has %zu bytes, need %zu", ws_bytes, need.total);
+  const CovDistWs w = CovDistWs::carve(ws, m, n, c->nranks, c->rank);
+  const cudaStream_t st = S(s);
+  int L = 0;
+  // 1. this rank's column sums into its row of the gather buffer (4m floats per rank)
+  double* mine = w.sums + (size_t)c->rank * 2 * m;
+  if (o.n()) {
+    PB_CU(launch_obs_sums(data_blk, o.n(), m, mine, st));
+  } else {
+    PB_CU(cudaMemsetAsync(mine, 0, (size_t)2 * m * sizeof(double), st));
+  }
+  ++L;
+  // 2. "allreduce of column sums": gather every rank's sums (bit copies), summed in rank order
+  //    by every rank in step 3, so all ranks hold the same mean / stddev bits
+  PB_TRY(all_gather_rows(c, reinterpret_cast<float*>(w.sums), c->nranks, 4 * m, st, 1));
+  if (c->peer) L += 2;
+  // 3 + 4. statistics, centred transpose, local partial Gram P_g = Yt Yt^T (full square)
+  if (o.n()) {
+    PB_CU(launch_obs_center_t(corr, data_blk, o.n(), m, w.sums, c->nranks, n, (double)float_n, (double)eps, w.Yt,
+                              w.ldy, mean, stddev, st));
+    ++L;
+    PB_TRY(pb_syrk_full(m, w.ldy, 1.f, 0.f, w.P, w.Yt, w.gemm, w.gemm_bytes, s));
+    L += pb_last_launch_count();
+  } else {
+    // no observations here: P_g = 0; mean / stddev still come from the gathered sums
+    if (mean || stddev) {
+      PB_CU(launch_obs_center_t(corr, nullptr, 0, m, w.sums, c->nranks, n, (double)float_n, (double)eps, nullptr, 0,
+                                mean, stddev, st));
+      ++L;
+    }
+    PB_CU(cudaMemsetAsync(w.P, 0, (size_t)m * m * sizeof(float), st));
+  }
+  // 5. P = sum_g P_g, reduce-scattered into the output row bands
+  PB_TRY(reduce_scatter_rows(c, w.P, out_blk, m, m, ALIGN_ST, st));
+  if (c->peer) L += 2;
+  // 6. 1 / (float_n - 1) (covariance) or diagonal := 1 (correlation)
+  if (r.n()) {
+    PB_CU(launch_obs_finish(corr, out_blk, r.n(), m, r.b, (float)(1.0 / ((double)float_n - 1.0)), st));
+    ++L;
+  }
+  set_launches(L);
+  return PB_OK;
+}
+
+pb_status pb_covariance_dist(pb_comm* c, int m, int n, float float_n, const float* data_blk, float* cov_blk,
+                             float* mean, void* ws, size_t ws_bytes, pb_stream s) {
+  return covcorr_dist(false, c, m, n, float_n, 0.f, data_blk, cov_blk, mean, nullptr, ws, ws_bytes, s);
+}
+
+pb_status pb_correlation_dist(pb_comm* c, int m, int n, float float_n, float eps, const float* data_blk,
+                              float* corr_blk, float* mean, float* stddev, void* ws, size_t ws_bytes, pb_stream s) {
+  return covcorr_dist(true, c, m, n, float_n, eps, data_blk, corr_blk, mean, stddev, ws, ws_bytes, s);
+}
+
 }  // extern "C"
+

@@ -122,6 +122,16 @@ size_t gram_fused_ws_bytes(int m, int n);
 cudaError_t launch_gram_fused(bool corr, int m, int n, double float_n, double eps, const float* data, float* out,
                               float* mean, float* sd, void* ws, cudaStream_t s, int* launches);
 
+// Observation-split covariance / correlation steps (k_covdist.cu, driven by pb_dist.cu).
+// launch_obs_sums: out[0..m) = fp64 column sums of X (nl x m), out[m..2m) = sums of squares.
+cudaError_t launch_obs_sums(const float* X, int nl, int m, double* out, cudaStream_t s);
+// sums: nranks x [2][m] (rank order) -> mean / sd (optional outputs) and the centred (and for
+// correlation normalised) transpose Yt (m x ldy, zero for k >= nl).
+cudaError_t launch_obs_center_t(bool corr, const float* X, int nl, int m, const double* sums, int nranks, int n,
+                                double float_n, double eps, float* Yt, int ldy, float* mean, float* sd, cudaStream_t s);
+// in place on an output row band (rows [r0, r0 + rows)): cov *= alpha; corr: diagonal := 1.
+cudaError_t launch_obs_finish(bool corr, float* out, int rows, int m, int r0, float alpha, cudaStream_t s);
+
 // ---- split / prep (k_split.cu) ----------------------------------------------
 // hi/lo split of a rows x cols matrix; same layout (ldo = ld of output).
 // done != nullptr: each CTA adds 1 to *done when its part is stored (release); *ctas += grid size.

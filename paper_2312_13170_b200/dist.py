@@ -7,6 +7,9 @@ steps the math needs:
                                     computes them from its row block + replicated
                                     operands (2mm: tmp[R] = alpha A[R] B is exactly
                                     what D[R] = tmp[R] C + beta D[R] needs)
+  covariance, correlation           observations split: column sums ALL-GATHERed and summed in
+                                    rank order (the allreduce), local partial Gram, REDUCE-SCATTER
+                                    of the m x m sum into output row bands (stat_obs)
   3mm                               F = C D by row blocks, ALL-GATHER of F (async, overlapped
                                     with E[R] = A[R] B), then G[R] = E[R] F
   atax, bicg, mvt                   row dots local; the transposed product's per-rank
@@ -196,6 +199,22 @@ def syrk_rows(ctx, n, m, alpha, beta, C_blk, A, ws, B=None, K=_pb):
         K.pb_syrk_rows(n, m, r0, r1, alpha, beta, C_blk, A, ws=ws)
     else:
         K.pb_syr2k_rows(n, m, r0, r1, alpha, beta, C_blk, A, B, ws=ws)
+    return K.last_launch_count()
+
+
+# --------------------------------------------------------------------- covariance / correlation
+def stat_obs(ctx, kernel, m, n, float_n, eps, data_blk, out_blk, mean, sd, ws, K=_pb):
+    """covariance / correlation with the OBSERVATIONS split (north_star: "an allreduce of
+    column sums"): data_blk = this rank's observations block(n, G, g, 0, 32), out_blk =
+    rows block(m, G, g, 0, 32) of the result. Everything (column sums, their all-gather and
+    rank-order sum, centring, the tcgen05 partial Gram, the reduce-scatter of the m x m sum,
+    the scaling) runs in libpb (pb_<k>_dist); a sharded call needs init_comm()."""
+    if _COMM is None or K is not _pb:
+        raise RuntimeError("stat_obs needs a libpb communicator: call dist.init_comm() first")
+    if kernel == "covariance":
+        K.pb_covariance_dist(_COMM, m, n, float_n, data_blk, out_blk, mean, ws=ws)
+    else:
+        K.pb_correlation_dist(_COMM, m, n, float_n, eps, data_blk, out_blk, mean, sd, ws=ws)
     return K.last_launch_count()
 
 

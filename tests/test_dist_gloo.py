@@ -228,3 +228,80 @@ def test_dist_row_blocks_gloo(world):
         assert np.allclose(q[v0:v1], q_ref[v0:v1], rtol=1e-5)
         v0, v1, _, xx1 = out[r]["mvt"]
         assert np.allclose(xx1[v0:v1], x1_ref[v0:v1], rtol=1e-5)
+
+
+def _covobs_worker(rank, world, port, q):
+    """The observations-split covariance / correlation decomposition that
+    pb_<k>_dist implements (k_covdist.cu, pb_dist.cu), emulated with gloo
+    collectives on the host: the same partitions (libpb's pb_row_partition,
+    observations align 32, output rows align 32), fp64 column sums gathered and
+    added in rank order, local partial Grams of the centred block, a reduce-scatter
+    of the m x m sum into row bands (test only: the CUDA steps are checked against
+    the oracle on the GPU in tests/test_gpu_dist.py)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests import parity as P
+        m, n, eps = 36, 203, 0.1
+        data = P.structured_data(n, m)
+        o0, o1 = pb.pb_row_partition(n, world, rank, False, 32)
+        b0, b1 = pb.pb_row_partition(m, world, rank, False, 32)
+        X = data[o0:o1].astype(np.float64)
+        sums = torch.from_numpy(np.stack([X.sum(0), (X * X).sum(0)]))  # [2][m]
+        allsums = [torch.empty_like(sums) for _ in range(world)]
+        dist.all_gather(allsums, sums)
+        S1 = np.zeros(m)
+        S2 = np.zeros(m)
+        for g in range(world):  # rank order, as obs_center_t_kernel
+            S1 += allsums[g][0].numpy()
+            S2 += allsums[g][1].numpy()
+        res = {}
+        for corr in (False, True):
+            mean = S1 / n
+            inv = np.ones(m)
+            if corr:
+                sd = np.sqrt(np.maximum((S2 - 2 * mean * S1 + n * mean * mean) / n, 0.0))
+                sd[sd <= eps] = 1.0
+                inv = 1.0 / (np.sqrt(n) * sd)
+            Y = (X - mean) * inv
+            Pg = torch.from_numpy(Y.T @ Y)
+            dist.all_reduce(Pg)  # reduce-scatter = sum, then this rank's row band
+            band = Pg.numpy()[b0:b1].copy()
+            if corr:
+                for i in range(b0, b1):
+                    band[i - b0, i] = 1.0
+            else:
+                band /= n - 1
+            res[corr] = (b0, b1, band)
+        q.put((rank, res))
+    except Exception as e:
+        q.put((rank, {"error": repr(e)}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cov_corr_observation_split_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_covobs_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    from tests import parity as P
+    m, n = 36, 203
+    data = P.structured_data(n, m)
+    for corr in (False, True):
+        got = np.zeros((m, m))
+        for r in range(world):
+            assert "error" not in out[r], out[r]
+            b0, b1, band = out[r][corr]
+            got[b0:b1] = band
+        if corr:
+            ref, sc = oracle.correlation(float(n), 0.1, data)[0], oracle.correlation(float(n), 0.1, data, absmode=True)[0]
+        else:
+            ref, sc = oracle.covariance(float(n), data)[0], oracle.covariance(float(n), data, absmode=True)[0]
+        assert P.cerr(got, ref, sc) <= 1e-12, corr

@@ -106,6 +106,21 @@ def _worker(rank, world, port, q, backend="gloo"):
             out = {"atax": v["y"], "bicg": v["s"], "mvt": v["x2"], "gesummv": v["yo"]}[kern]
             extra = {"bicg": v["q"], "mvt": v["x1"], "atax": v["tmp"], "gesummv": v["yo"]}[kern]
             res[kern] = (v0, v1, out.cpu().numpy()[v0:v1], extra.cpu().numpy())
+        if D.comm() is not None:  # covariance / correlation, observations split (pb_<k>_dist)
+            ms, ns = 516, 700
+            data = P.structured_data(ns, ms)
+            o0, o1 = D.partition(ns, world, rank, False, 32)
+            b0, b1 = D.partition(ms, world, rank, False, 32)
+            dblk = torch.from_numpy(data[o0:o1].copy()).to(dev)
+            wsc = torch.empty(max(pb.workspace_size(k, (ms, ns, world, rank))
+                                  for k in ("covariance_dist", "correlation_dist")), dtype=torch.uint8, device=dev)
+            cb, kb = torch.empty(b1 - b0, ms, device=dev), torch.empty(b1 - b0, ms, device=dev)
+            mean, mean2, sd = (torch.empty(ms, device=dev) for _ in range(3))
+            D.stat_obs(None, "covariance", ms, ns, float(ns), 0.1, dblk, cb, mean, None, wsc)
+            D.stat_obs(None, "correlation", ms, ns, float(ns), 0.1, dblk, kb, mean2, sd, wsc)
+            torch.cuda.synchronize()
+            res["covcorr"] = (b0, b1, cb.cpu().numpy(), kb.cpu().numpy(), mean.cpu().numpy(), mean2.cpu().numpy(),
+                              sd.cpu().numpy())
         q.put((rank, res))
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, {"error": repr(e)}))
@@ -165,6 +180,23 @@ def test_dist_ranks_one_gpu_real_kernels(backend, world):
             s0, s1, blk = out[r][name]
             got[s0:s1] = blk
         assert P.cerr(got, ref, sc) <= P.TOL, name
+    if backend != "gloo":  # observations-split covariance / correlation (column-sum allreduce)
+        ms, ns = 516, 700
+        data = P.structured_data(ns, ms)
+        cov_r, mean_r = oracle.covariance(float(ns), data)
+        cov_s, mean_s = oracle.covariance(float(ns), data, absmode=True)
+        corr_r, _, sd_r = oracle.correlation(float(ns), 0.1, data)
+        corr_s, _, sd_s = oracle.correlation(float(ns), 0.1, data, absmode=True)
+        cov, corr = np.zeros((ms, ms)), np.zeros((ms, ms))
+        for r in range(world):
+            b0, b1, cb, kb, mean, mean2, sd = out[r]["covcorr"]
+            cov[b0:b1], corr[b0:b1] = cb, kb
+            assert P.cerr(mean, mean_r, mean_s) <= P.TOL and np.array_equal(mean, mean2)
+            assert P.cerr(sd, sd_r, sd_s) <= P.TOL
+            assert np.array_equal(mean, out[0]["covcorr"][4])  # every rank holds the same statistics
+        assert P.cerr(cov, cov_r, cov_s) <= P.TOL, P.cerr(cov, cov_r, cov_s)
+        assert P.cerr(corr, corr_r, corr_s) <= P.TOL, P.cerr(corr, corr_r, corr_s)
+        assert np.all(np.diag(corr) == 1.0) and np.all(cov[0] == 0.0)  # R6; constant column 0
     nv = 2048
     Av, Bv = pbgen.gen_host(nv, nv, 1), pbgen.gen_host(nv, nv, 2)
     x, rr, y2, x1, x2 = (pbgen.gen_host(1, nv, s)[0] for s in (6, 7, 7, 8, 9))
