@@ -166,8 +166,8 @@ struct Params {
   long long num_tiles;
   int ksplit;                    // K splits of each split tile (split-K)
   long long split_tiles;         // split tiles: [split_t0, split_t0 + split_tiles)
-  int group_m;                   // tile-rows per raster group (GROUP_M)
-  long long split_t0;            // 0: split tiles first (their units lead); num_tiles - split_tiles: last
+  int group_m = GROUP_M;         // tile-rows per raster group (PB_GROUP_M)
+  long long split_t0 = 0;        // 0: split tiles first (their units lead); num_tiles - split_tiles: last
   float* part;                   // split-K partial tiles [unit][CG][128][BN]
   unsigned* counters;            // split-K arrival counters [tile][CG], zero before launch
   int b_mn;                      // 1: the B operand is MN-major (B[k][n] as stored), 32-column TMA runs
@@ -260,7 +260,7 @@ __device__ __forceinline__ int row_tiles(const Params& p, int tm) {
 __device__ void tile_coords(const Params& p, long long t, int& tm, int& tn) {
   int g0 = p.tm0;
   for (;;) {
-    const int g1 = min(g0 + p.group_m, p.tm1);
+    const int g1 = min(g0 + (p.group_m > 0 ? p.group_m : GROUP_M), p.tm1);
     long long cnt = 0;
     for (int r = g0; r < g1; ++r) cnt += row_tiles(p, r);
     if (t < cnt || g1 >= p.tm1) {

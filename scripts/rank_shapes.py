@@ -87,6 +87,17 @@ def main():
             res["covariance"] = timed(lambda: pb.pb_covariance(ST, ST, float(ST), data, cov, mean, ws=wss))
             res["correlation"] = timed(lambda: pb.pb_correlation(ST, ST, float(ST), 0.1, data, cov, mean, sd, ws=wss))
         else:
+            # observations split (pb_<k>_dist, bench's N > 1 path): the rank's Gram of its
+            # observation block, m x m full square over K = n / G (pb_syrk_full on the centred
+            # transpose); the column-sum / centring / scaling kernels (~5 us) and the two
+            # collectives (8 KB all-gather, 16 MiB reduce-scatter) are not included
+            o0, o1 = pb.pb_row_partition(ST, G, 0, 0, 32)
+            nl = (o1 - o0 + 3) // 4 * 4
+            Yt = g(ST, nl, 5)
+            P_ = torch.empty(ST, ST, device=dev)
+            wso = pb.workspace("syrk_full", (ST, nl), dev)
+            res["covariance_obs_gram"] = timed(lambda: pb.pb_syrk_full(ST, nl, 1.0, 0.0, P_, Yt, ws=wso))
+            del Yt, P_
             b, e = pb.pb_row_partition(ST, G, 0, 0, 128)
             wsr = pb.workspace("covariance_rows", (ST, ST, b, e), dev)
             res["covariance"] = timed(lambda: pb.pb_covariance_rows(ST, ST, float(ST), b, e, data, cov[:e - b], mean,

@@ -121,6 +121,19 @@ def _worker(rank, world, port, q, backend="gloo"):
             torch.cuda.synchronize()
             res["covcorr"] = (b0, b1, cb.cpu().numpy(), kb.cpu().numpy(), mean.cpu().numpy(), mean2.cpu().numpy(),
                               sd.cpu().numpy())
+            # tiny: at world 3 the last rank has no observations and no output rows
+            mt, nt = 36, 40
+            data = P.structured_data(nt, mt)
+            o0, o1 = D.partition(nt, world, rank, False, 32)
+            b0, b1 = D.partition(mt, world, rank, False, 32)
+            dblk = torch.from_numpy(data[o0:o1].copy()).to(dev) if o1 > o0 else None
+            wst = torch.empty(max(pb.workspace_size(k, (mt, nt, world, rank))
+                                  for k in ("covariance_dist", "correlation_dist")), dtype=torch.uint8, device=dev)
+            cb = torch.empty(b1 - b0, mt, device=dev) if b1 > b0 else None
+            mean, sd = torch.empty(mt, device=dev), torch.empty(mt, device=dev)
+            D.stat_obs(None, "correlation", mt, nt, float(nt), 0.1, dblk, cb, mean, sd, wst)
+            torch.cuda.synchronize()
+            res["covcorr_tiny"] = (b0, b1, None if cb is None else cb.cpu().numpy(), mean.cpu().numpy())
         q.put((rank, res))
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, {"error": repr(e)}))
@@ -130,7 +143,8 @@ def _worker(rank, world, port, q, backend="gloo"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1), ("gloo-peer", 2), ("nccl-peer", 1)])
+@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1), ("gloo-peer", 2), ("nccl-peer", 1),
+                                           ("gloo-peer", 3)])
 def test_dist_ranks_one_gpu_real_kernels(backend, world):
     """gloo: two ranks share cuda:0 (host-staged test stand-ins for the two
     collectives, injected through the kernel namespace). nccl: one rank
@@ -197,6 +211,17 @@ def test_dist_ranks_one_gpu_real_kernels(backend, world):
         assert P.cerr(cov, cov_r, cov_s) <= P.TOL, P.cerr(cov, cov_r, cov_s)
         assert P.cerr(corr, corr_r, corr_s) <= P.TOL, P.cerr(corr, corr_r, corr_s)
         assert np.all(np.diag(corr) == 1.0) and np.all(cov[0] == 0.0)  # R6; constant column 0
+        mt, nt = 36, 40
+        data = P.structured_data(nt, mt)
+        cr, mr, _ = oracle.correlation(float(nt), 0.1, data)
+        cs, ms_, _ = oracle.correlation(float(nt), 0.1, data, absmode=True)
+        got = np.zeros((mt, mt))
+        for r in range(world):
+            b0, b1, blk, mean = out[r]["covcorr_tiny"]
+            if b1 > b0:
+                got[b0:b1] = blk
+            assert P.cerr(mean, mr, ms_) <= P.TOL
+        assert P.cerr(got, cr, cs) <= P.TOL
     nv = 2048
     Av, Bv = pbgen.gen_host(nv, nv, 1), pbgen.gen_host(nv, nv, 2)
     x, rr, y2, x1, x2 = (pbgen.gen_host(1, nv, s)[0] for s in (6, 7, 7, 8, 9))
@@ -327,6 +352,8 @@ def test_bench_two_ranks_share_gpu(transport):
     line = json.loads([ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
     assert (line["config"]["transport"] or "").startswith("peer") == (transport == "local")
+    chk = line["sharded_check"]  # atax y, 3mm G and the observations-split covariance vs one-GPU calls
+    assert chk["ok"] and "cov_max_abs_over_max" in chk, chk
 
 
 def test_peer_collectives_graph_replay():
