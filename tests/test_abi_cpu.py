@@ -116,6 +116,19 @@ def test_dist_workspace_sizes_cpu():
     assert pb.workspace_size("3mm_dist", (4096,) * 5 + (4, 3)) >= pb.workspace_size("gemm", (1024, 4096, 4096))
     r0, r1 = pb.pb_row_partition(8192, 4, 3, 2, 256)
     assert pb.workspace_size("syr2k_dist", (8192, 8192, 4, 3)) == pb.workspace_size("syr2k_rows", (8192, 8192, r0, r1))
+    # covariance / correlation, observations split: the rank's sums gather buffer [G][2][m]
+    # doubles + its centred transpose (m x ceil4(obs)) + the m x m partial Gram + pb_syrk_full's
+    m, nobs = 2048, 2048
+    for G in (1, 2, 8):
+        for g in range(G):
+            o0, o1 = pb.pb_row_partition(nobs, G, g, False, 32)
+            nl = (o1 - o0 + 3) // 4 * 4
+            need = pb.workspace_size("covariance_dist", (m, nobs, G, g))
+            assert need == pb.workspace_size("correlation_dist", (m, nobs, G, g))
+            assert need >= G * 2 * m * 8 + m * nl * 4 + m * m * 4 + pb.workspace_size("syrk_full", (m, nl))
+    for bad in [("covariance_dist", (m, nobs, 2, 2)), ("covariance_dist", (m, nobs)), ("correlation_dist", (0, 4, 1, 0))]:
+        with pytest.raises(pb.PBError):
+            pb.workspace_size(*bad)
     for bad in [("atax_dist", (n, n, 2, 2)), ("atax_dist", (n, n, 0, 0)), ("atax_dist", (n, n)),
                 ("nope_dist", (1, 1, 1)), ("gemm_dist", (0, 4, 4, 1, 0))]:
         with pytest.raises(pb.PBError):
