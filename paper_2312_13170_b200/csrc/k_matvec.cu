@@ -557,7 +557,7 @@ struct __align__(16) AtCtl {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
     atax_tm_kernel(const float* __restrict__ A, const float* __restrict__ x, int m, int n, int w0,
-                   float* __restrict__ tmp, float* __restrict__ ypart) {
+                   float* __restrict__ tmp, float* __restrict__ ypart, int chunks) {
   extern __shared__ __align__(128) uint8_t sm[];
   float* stage_buf = reinterpret_cast<float*>(sm);  // AT_STAGES x AX_SLICE
   AtCtl* ctl = reinterpret_cast<AtCtl*>(stage_buf + (size_t)AT_STAGES * AX_SLICE);
@@ -580,11 +580,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AX_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&ctl->tmem_base, AT_TMEM_COLS);
+  // a row slice arrives as `chunks` bulk copies (16-B multiples) on one barrier (PB_ATAX_CHUNKS)
+  const uint32_t cbytes = (((uint32_t)w * 4u + (uint32_t)chunks - 1u) / (uint32_t)chunks + 15u) & ~15u;
   auto issue = [&](int b) {
     const int s = b % AT_STAGES;
     mbar_arrive_expect_tx(&ctl->full[s], (uint32_t)w * 4u);
-    if (w > 0) bulk_g2s(stage_buf + (size_t)s * AX_SLICE, A + (long long)(r0 + b) * n + c0, (uint32_t)w * 4u,
-                        &ctl->full[s]);
+    const char* src = reinterpret_cast<const char*>(A + (long long)(r0 + b) * n + c0);
+    char* dst = reinterpret_cast<char*>(stage_buf + (size_t)s * AX_SLICE);
+    for (uint32_t off = 0; off < (uint32_t)w * 4u; off += cbytes) {
+      const uint32_t len = min(cbytes, (uint32_t)w * 4u - off);
+      bulk_g2s(dst + off, src + off, len, &ctl->full[s]);
+    }
   };
   tc_fence_before();
   cluster_sync_all();  // barriers exist in both CTAs; TMEM allocated
@@ -763,7 +769,8 @@ cudaError_t launch_atax(const float* A, const float* x, int m, int n, float* y, 
         const cudaError_t e = ensure_smem<atax_tm_kernel>(smem3);
         if (e != cudaSuccess) return e;
       }
-      atax_tm_kernel<<<2 * ncl, AX_THREADS, smem3, s>>>(A, x, m, n, w0, tmp, ypart);
+      static const int chunks = getenv("PB_ATAX_CHUNKS") ? std::max(1, std::min(64, atoi(getenv("PB_ATAX_CHUNKS")))) : 1;
+      atax_tm_kernel<<<2 * ncl, AX_THREADS, smem3, s>>>(A, x, m, n, w0, tmp, ypart, chunks);
     } else if (variant == 2) {
       const size_t smem2 = (size_t)(1 + AR_STAGES) * AX_SLICE * 4 + sizeof(ArCtl);
       {
