@@ -134,6 +134,16 @@ def _worker(rank, world, port, q, backend="gloo"):
             D.stat_obs(None, "correlation", mt, nt, float(nt), 0.1, dblk, cb, mean, sd, wst)
             torch.cuda.synchronize()
             res["covcorr_tiny"] = (b0, b1, None if cb is None else cb.cpu().numpy(), mean.cpu().numpy())
+            # PolyBench-GPU's constants: FLOAT_N = 3214212.01 (not the observation count), eps = 0.005
+            FN = 3214212.01
+            cb2 = torch.empty(b1 - b0, mt, device=dev) if b1 > b0 else None
+            kb2 = torch.empty(b1 - b0, mt, device=dev) if b1 > b0 else None
+            mean3, sd3 = torch.empty(mt, device=dev), torch.empty(mt, device=dev)
+            D.stat_obs(None, "covariance", mt, nt, FN, 0.005, dblk, cb2, mean3, None, wst)
+            D.stat_obs(None, "correlation", mt, nt, FN, 0.005, dblk, kb2, mean3, sd3, wst)
+            torch.cuda.synchronize()
+            res["covcorr_fn"] = (b0, b1, None if cb2 is None else cb2.cpu().numpy(),
+                                 None if kb2 is None else kb2.cpu().numpy(), mean3.cpu().numpy(), sd3.cpu().numpy())
         q.put((rank, res))
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, {"error": repr(e)}))
@@ -222,6 +232,18 @@ def test_dist_ranks_one_gpu_real_kernels(backend, world):
                 got[b0:b1] = blk
             assert P.cerr(mean, mr, ms_) <= P.TOL
         assert P.cerr(got, cr, cs) <= P.TOL
+        FN = 3214212.01
+        cv_r, mean_r = oracle.covariance(FN, data)
+        cv_s, mean_s = oracle.covariance(FN, data, absmode=True)
+        co_r, _, sd_r = oracle.correlation(FN, 0.005, data)
+        co_s, _, sd_s = oracle.correlation(FN, 0.005, data, absmode=True)
+        gcv, gco = np.zeros((mt, mt)), np.zeros((mt, mt))
+        for r in range(world):
+            b0, b1, cb2, kb2, mean3, sd3 = out[r]["covcorr_fn"]
+            if b1 > b0:
+                gcv[b0:b1], gco[b0:b1] = cb2, kb2
+            assert P.cerr(mean3, mean_r, mean_s) <= P.TOL and P.cerr(sd3, sd_r, sd_s) <= P.TOL
+        assert P.cerr(gcv, cv_r, cv_s) <= P.TOL and P.cerr(gco, co_r, co_s) <= P.TOL
     nv = 2048
     Av, Bv = pbgen.gen_host(nv, nv, 1), pbgen.gen_host(nv, nv, 2)
     x, rr, y2, x1, x2 = (pbgen.gen_host(1, nv, s)[0] for s in (6, 7, 7, 8, 9))
