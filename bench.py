@@ -954,6 +954,10 @@ def run_reference(args):
     if rank != 0:
         return
     kernels = KERNELS if args.kernels == "all" else args.kernels.split(",")
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:
+        # torchrun sets OMP_NUM_THREADS=1 for every worker; rank 0 runs alone here, so the
+        # oracle gets the host's cores as at N = 1 (set before its OpenMP runtime loads)
+        os.environ["OMP_NUM_THREADS"] = str(cpu_threads())
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
     fns = oracle_sample_fns(kernels)
     for _ in range(args.warmup):
