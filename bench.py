@@ -929,6 +929,8 @@ def cpu_threads():
 
 def cpu_baseline(kernels, budget_s=20.0):
     """The oracle timed on this host's cores: sample steps repeated for ~budget_s."""
+    if "TORCHELASTIC_RUN_ID" in os.environ:  # torchrun's OMP_NUM_THREADS=1 is for the GPU ranks
+        os.environ["OMP_NUM_THREADS"] = str(cpu_threads())
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
     fns = oracle_sample_fns(kernels)
     oracle_sample_step(fns)  # first run discarded (page faults, thread start-up)
