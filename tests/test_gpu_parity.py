@@ -85,6 +85,23 @@ def test_gemm_run_to_run_deterministic_P32():
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
+def test_gemm_mixed_whole_and_split_tiles_deterministic():
+    """A plan with whole tiles AND split-K units (2560 x 2048: 80 tiles of 256 x 256 for 74 SM
+    pairs -> 74 whole tiles first, then the 6 remainder tiles split along K, summed by the
+    last arriver in split order): parity with the oracle and bitwise run-to-run equality."""
+    M, N, K = 2560, 2048, 512
+    A, B, C0 = P.H(M, K, 1), P.H(K, N, 2), P.H(M, N, 3)
+    dA, dB = P.dev(A), P.dev(B)
+    outs = []
+    for _ in range(3):
+        C = P.dev(C0)
+        pb.pb_gemm(M, N, K, 1.5, 1.2, C, dA, dB)
+        outs.append(P.host(C))
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+    r = oracle.gemm(1.5, 1.2, C0, A, B)
+    assert P.cerr(outs[0], r, np.abs(r)) <= P.TOL  # non-negative inputs: the scale is |r| (R8)
+
+
 def test_gemm_precision_discriminator_P34():
     """centred inputs U[-1/2,1/2): 3xTF32 must stay at fp32-level error
     (<= 2e-6 of |A||B|), which a silent 1xTF32 path (~1e-5) would fail."""
