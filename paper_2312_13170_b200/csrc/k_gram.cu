@@ -73,6 +73,7 @@ struct GramArgs {
   float inv_sqrt_fn;  // 1 / sqrt(float_n)
   float eps;
   float fn;           // float_n
+  int xbulk;          // split-K partner values by bulk copy into smem (PB_GRAM_XBULK, default 1)
   uint32_t lbo, sbo;  // MN-major UMMA descriptor strides (bytes)
   int mp;             // row pitch of xh / xl (floats, m rounded up to 32)
   float* xh;          // n x mp: hi of the band-shifted data y = (x - x0_b) - d_b (row-major, like data)
@@ -563,14 +564,46 @@ __global__ void __launch_bounds__(GTHREADS, 1)
                         1u);
       epi_bar();
       if (et == 0) GTS(4);
-      for (int k = 0; k < p.S; ++k) {
-        if (k == ks) continue;
-        const float4* theirs = part4 + (((long long)t * p.S + k) * 2 + rank) * tile_f4;
+      if (p.xbulk) {
+        // the partners' posts of this unit's chunk (S - 1 contiguous [CW / 4 quads][128 rows]
+        // float4 runs) come in as bulk copies (TMA engine) into the free ring space behind the
+        // direct boxes, then every thread reads its values from shared memory; the sum order
+        // (own, then partners in ascending split index) is the same as the direct loads'.
+        const uint32_t run = (uint32_t)CW * 128u * 4u;
+        float4* xs = reinterpret_cast<float4*>(smem + (CW < 128 ? CW : 128) / 32 * GEBOX);
+        if (et == 0) {
+          fence_proxy_global();  // the partners' generic-proxy stores -> these async-proxy reads
+          mbar_arrive_expect_tx(&ctl->xbar, run * (uint32_t)(p.S - 1));
+          for (int k = 0, slot = 0; k < p.S; ++k) {
+            if (k == ks) continue;
+            const float4* theirs = part4 + (((long long)t * p.S + k) * 2 + rank) * tile_f4 + (ks * CW / 4) * 128;
+            bulk_g2s(xs + (size_t)slot * (CW / 4) * 128, theirs, run, &ctl->xbar);
+            ++slot;
+          }
+        }
+        mbar_wait(&ctl->xbar, 0);
+        for (int k = 0, slot = 0; k < p.S; ++k) {
+          if (k == ks) continue;
+          const float4* theirs = xs + (size_t)slot * (CW / 4) * 128;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (4 * j < hw) {
-            const float4 pv = __ldcg(theirs + ((fo >> 2) + j) * 128 + rl);
-            acc[4 * j] += pv.x; acc[4 * j + 1] += pv.y; acc[4 * j + 2] += pv.z; acc[4 * j + 3] += pv.w;
+          for (int j = 0; j < 16; ++j) {
+            if (4 * j < hw) {
+              const float4 pv = theirs[((fo - ks * CW) >> 2) * 128 + j * 128 + rl];
+              acc[4 * j] += pv.x; acc[4 * j + 1] += pv.y; acc[4 * j + 2] += pv.z; acc[4 * j + 3] += pv.w;
+            }
+          }
+          ++slot;
+        }
+      } else {
+        for (int k = 0; k < p.S; ++k) {
+          if (k == ks) continue;
+          const float4* theirs = part4 + (((long long)t * p.S + k) * 2 + rank) * tile_f4;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (4 * j < hw) {
+              const float4 pv = __ldcg(theirs + ((fo >> 2) + j) * 128 + rl);
+              acc[4 * j] += pv.x; acc[4 * j + 1] += pv.y; acc[4 * j + 2] += pv.z; acc[4 * j + 3] += pv.w;
+            }
           }
         }
       }
@@ -788,6 +821,8 @@ cudaError_t launch_gram_fused(bool corr, int m, int n, double float_n, double ep
   a.inv_sqrt_fn = (float)(1.0 / sqrt(float_n));
   a.eps = (float)eps;
   a.fn = (float)float_n;
+  static const int xbulk = getenv("PB_GRAM_XBULK") ? atoi(getenv("PB_GRAM_XBULK")) : 1;
+  a.xbulk = xbulk != 0;
   // MN-major operand boxes: 32-variable runs GBOX apart, 4-observation groups 512 B apart
   static const bool swap = getenv("PB_GRAM_MNSWAP") != nullptr;  // tuning / bring-up only
   a.lbo = swap ? 512u : (uint32_t)GBOX;
