@@ -228,8 +228,14 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   }
   if (warp == 1) tmem_alloc_cg<2>(&ctl->tmem_base, GTMEM);
   tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
+  // Cluster barrier split in arrive / wait: the producer and MMA warps wait here (barriers
+  // and TMEM of both CTAs ready); the epilogue warps start phase 0 at once (it touches no
+  // mbarrier, no TMEM and nothing of the peer CTA) and wait before phase 2.
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  if (warp < 2) {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+  }
   pdl_wait();  // data (and the zeroed flags) come from the preceding stream work
   const int slabA_ok = slabA < p.nslab, slabB_ok = slabB < p.nslab;
   if (threadIdx.x == 0) {
@@ -442,6 +448,8 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       }
     }
     if (et == 0) GTS(1);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // (arrived before phase 0)
+    tc_fence_after();
 
     // ============================ phase 2: epilogue ============================
     const int q = warp & 3, ch = (warp - 2) >> 2;
